@@ -1,0 +1,166 @@
+/*
+ * dp_b200.h — C ABI of the B200-native ShardTensor domain-parallel hot path.
+ *
+ * Every entry point is `extern "C"`, takes plain pointers / sizes / strides,
+ * returns DP_OK (0) or a DP_ERR_* code, never throws, never allocates (the
+ * caller passes any workspace), and enqueues its kernels on the caller's
+ * `stream` (a cudaStream_t passed as void*).  dp_last_error() returns the
+ * calling thread's last message.  There is no CPU implementation behind any
+ * of these symbols.
+ *
+ * Reference interfaces each group replaces (the reference is pure Python;
+ * these are the NumPy regions its operator API bottoms out in — SURVEY.md
+ * §2.1 / §8(b)):
+ *
+ *   dp_copy_strided        domainpar/mesh.py:370-386   halo face slicing +
+ *                                                     np.concatenate;
+ *                          domainpar/sharding.py:375-383 redistribute column
+ *                                                     slice; mesh.py:302
+ *                                                     varlen concat
+ *   dp_accumulate_strided  (no reference function)    reverse-halo gradient
+ *                                                     accumulate, SURVEY A9
+ *   dp_conv_fwd            domainpar/ops.py:397-413 + dense.py:174-214
+ *                                                     trim/pad + dense.conv
+ *   dp_conv_dgrad,         (no reference function)    conv backward, A9
+ *   dp_conv_wgrad
+ *   dp_attn_fwd_update     domainpar/ops.py:199-211,272-275  scores +
+ *                                                     RingSoftmaxState.update
+ *   dp_attn_finalize       domainpar/ops.py:213-214,278   acc / l
+ *   dp_attn_bwd_*          (no reference function)    ring attention bwd
+ */
+#ifndef DP_B200_H
+#define DP_B200_H
+
+#include <stdint.h>
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DP_ABI_VERSION 1
+
+/* return codes */
+#define DP_OK 0
+#define DP_ERR_INVALID 1      /* bad argument (shape, stride, null pointer) */
+#define DP_ERR_UNSUPPORTED 2  /* configuration outside the kernel envelope  */
+#define DP_ERR_CUDA 3         /* CUDA runtime / launch failure              */
+
+/* element types */
+#define DP_F32 0
+#define DP_F64 1
+#define DP_BF16 2
+
+/* algorithm selectors for the conv / attention entry points */
+#define DP_ALGO_AUTO 0     /* tcgen05 path when eligible, else SIMT          */
+#define DP_ALGO_SIMT 1     /* direct CUDA-core kernels (any dtype / stride)  */
+#define DP_ALGO_TC 2       /* tcgen05 + TMA path; DP_ERR_UNSUPPORTED if not  */
+
+int dp_abi_version(void);
+const char *dp_last_error(void);
+/* Kernels this library has launched in this process (monotonic). */
+uint64_t dp_launch_count(void);
+/* SM count and compute capability of the current device. */
+int dp_device_info(int *sm_count, int *cc_major, int *cc_minor);
+
+/* ---- data movement (halo / varlen pack, unpack, accumulate) ------------ */
+
+/* dst[i] = src[i] over an `ndim`-D index space (ndim <= 8); strides are in
+ * elements; elem_bytes in {1,2,4,8,16}.  Dimensions are collapsed and the
+ * innermost run is moved with 16-byte vectors when alignment allows. */
+int dp_copy_strided(int ndim, const int64_t *shape, void *dst, const int64_t *dst_strides,
+                    const void *src, const int64_t *src_strides, int elem_bytes, void *stream);
+
+/* dst[i] += src[i] (dtype DP_F32 / DP_F64 / DP_BF16 with fp32 add). */
+int dp_accumulate_strided(int ndim, const int64_t *shape, void *dst,
+                          const int64_t *dst_strides, const void *src,
+                          const int64_t *src_strides, int dtype, void *stream);
+
+/* ---- halo convolution --------------------------------------------------- */
+
+/* Geometry of one rank's share of a (possibly sharded) convolution.
+ * The input along spatial dim `shard` is the *virtual* block
+ *     [zeros | main (in_ext[shard] rows) | right halo (halo rows) | zeros]
+ * and output row o of every spatial dim i reads virtual rows
+ *     base[i] + o*stride[i] + t,  t in [0, kernel[i])
+ * (unsharded dims: base = -padding; virtual rows outside [0, in_ext) are
+ * zero).  This is the reference's trimmed + zero-padded extended block
+ * (domainpar/ops.py:397-413) without materialising it. */
+typedef struct dp_conv_geom {
+    int32_t nsp;            /* spatial dims, 1..3 */
+    int32_t shard;          /* spatial index extended by `halo`, or -1 */
+    int64_t batch, c_in, c_out;
+    int64_t in_ext[3];      /* main-block spatial extents */
+    int64_t halo;           /* right-halo rows on `shard` */
+    int64_t out_ext[3];     /* this rank's output spatial extents */
+    int32_t kernel[3];
+    int32_t stride[3];
+    int64_t base[3];
+    int64_t xs[5];          /* element strides [b, c, s0, s1, s2] of the main block */
+    int64_t hs[5];          /* ... of the halo block (ignored when halo == 0) */
+    int64_t ys[5];          /* ... of the output */
+} dp_conv_geom;
+
+/* y = conv(x_virtual, w); w is contiguous [c_out, c_in, k0(, k1(, k2))] in
+ * the activation dtype; accumulation is fp32 (fp64 for DP_F64). */
+int dp_conv_fwd(const dp_conv_geom *g, int dtype, int algo, const void *x, const void *x_halo,
+                const void *w, void *y, void *stream);
+
+/* dx_virtual = conv^T(dy, w) over virtual rows [0, in_ext + halo) of the
+ * sharded dim: rows [0, in_ext) land in dx (strides g->xs), rows
+ * [in_ext, in_ext + halo) in dx_halo (strides g->hs) — the block that is
+ * sent back to the next rank and accumulated there.  dy uses
+ * strides g->ys.  Overwrites dx / dx_halo. */
+int dp_conv_dgrad(const dp_conv_geom *g, int dtype, int algo, const void *dy, const void *w,
+                  void *dx, void *dx_halo, void *stream);
+
+/* dw (fp32 for DP_F32/DP_BF16, fp64 for DP_F64; contiguous [c_out, c_in,
+ * k...]) = sum over batch and output positions of dy * x_virtual.  The
+ * result is this rank's partial; the caller all-reduces it over the
+ * sharding group.  `workspace` must hold dp_conv_wgrad_workspace() bytes. */
+int64_t dp_conv_wgrad_workspace(const dp_conv_geom *g, int dtype, int algo);
+int dp_conv_wgrad(const dp_conv_geom *g, int dtype, int algo, const void *x, const void *x_halo,
+                  const void *dy, void *dw, void *workspace, int64_t workspace_bytes,
+                  void *stream);
+
+/* ---- ring attention blocks ------------------------------------------------ */
+
+/* Shapes: q [sq, h, d], k/v [sk, h, d] with element strides (row, head)
+ * and unit stride on d.  State: m, l [sq, h] and acc [sq, h, d] contiguous,
+ * fp32 (fp64 for DP_F64).  One call folds one K/V block into the running
+ * online-softmax state exactly as RingSoftmaxState.update
+ * (domainpar/ops.py:199-211): m' = max(m, rowmax(s)), c = exp(m - m'),
+ * l' = l*c + sum(exp(s - m')), acc' = acc*c + exp(s - m') @ v with
+ * s = (q @ k^T) * scale.  sk == 0 is a no-op. */
+typedef struct dp_attn_geom {
+    int64_t sq, sk, heads, dim;
+    int64_t q_rs, q_hs;     /* q row / head strides (elements) */
+    int64_t k_rs, k_hs;
+    int64_t v_rs, v_hs;
+    int64_t o_rs, o_hs;     /* output / dO strides */
+    double scale;
+} dp_attn_geom;
+
+int dp_attn_fwd_update(const dp_attn_geom *g, int dtype, int algo, const void *q, const void *k,
+                       const void *v, void *m, void *l, void *acc, void *stream);
+
+/* out = acc / l cast to dtype; lse = m + log(l) (fp32/fp64) for backward. */
+int dp_attn_finalize(const dp_attn_geom *g, int dtype, const void *m, const void *l,
+                     const void *acc, void *out, void *lse, void *stream);
+
+/* delta[i,h] = sum_d dO[i,h,d] * O[i,h,d] (fp32/fp64). */
+int dp_attn_bwd_preprocess(const dp_attn_geom *g, int dtype, const void *o, const void *dout,
+                           void *delta, void *stream);
+
+/* Fold one K/V block into the gradients: with P = exp(s - lse),
+ * dV += P^T dO, dS = P * (dO V^T - delta), dQ += scale dS K,
+ * dK += scale dS^T Q.  dq [sq,h,d], dk/dv [sk,h,d] are contiguous fp32
+ * (fp64) accumulators. */
+int dp_attn_bwd_update(const dp_attn_geom *g, int dtype, int algo, const void *q, const void *k,
+                       const void *v, const void *dout, const void *lse, const void *delta,
+                       void *dq, void *dk, void *dv, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DP_B200_H */

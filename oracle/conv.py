@@ -1,0 +1,104 @@
+"""Convolution restated from the reference (TEST INFRASTRUCTURE).
+
+conv()       domainpar/dense.py:174-214 — np.pad + sliding_window_view +
+             einsum, with the reference's einsum specs for 1-D/2-D; the 3-D
+             spec 'bcpqrklm,dcklm->bdpqr' extends the same construction (the
+             reference rejects 3-D, dense.py:181-185).
+conv_grads() the adjoint: dX by scattering dY*W back over every window
+             position, dW by contracting the windows with dY.  No reference
+             function exists (no autograd); pinned by central
+             finite differences in tests/test_oracle.py.
+halo_conv_members()  per-member outputs of the sharded algorithm
+             (domainpar/ops.py:363-422) on the gathered input.
+"""
+
+import numpy as np
+from numpy.lib.stride_tricks import sliding_window_view
+
+from .plan import conv_out, member_plans
+
+_SPECS = {1: "bcok,dck->bdo", 2: "bcpqkl,dckl->bdpq", 3: "bcpqrklm,dcklm->bdpqr"}
+
+
+def _norm(n, v):
+    return (v,) * n if isinstance(v, int) else tuple(v)
+
+
+def conv(x, w, stride=1, padding=0):
+    n = w.ndim - 2
+    batched = x.ndim == n + 2
+    xb = x if batched else x[None]
+    strides, pads = _norm(n, stride), _norm(n, padding)
+    for g, k, s, p in zip(xb.shape[2:], w.shape[2:], strides, pads):
+        conv_out(g, k, s, p)
+    xp = np.pad(xb, [(0, 0), (0, 0)] + [(p, p) for p in pads])
+    win = sliding_window_view(xp, w.shape[2:], axis=tuple(range(2, 2 + n)))
+    win = win[(slice(None), slice(None)) + tuple(slice(None, None, s) for s in strides)]
+    out = np.ascontiguousarray(np.einsum(_SPECS[n], win, w), dtype=x.dtype)
+    return out if batched else out[0]
+
+
+def conv_grads(x, w, dy, stride=1, padding=0):
+    """(dx, dw) of y = conv(x, w) given dy, in float64."""
+    n = w.ndim - 2
+    batched = x.ndim == n + 2
+    xb = (x if batched else x[None]).astype(np.float64)
+    dyb = (dy if batched else dy[None]).astype(np.float64)
+    w64 = w.astype(np.float64)
+    strides, pads = _norm(n, stride), _norm(n, padding)
+    xp = np.pad(xb, [(0, 0), (0, 0)] + [(p, p) for p in pads])
+    dxp = np.zeros_like(xp)
+    dw = np.zeros_like(w64)
+    outs = dyb.shape[2:]
+    for tap in np.ndindex(*w.shape[2:]):
+        sl = (slice(None), slice(None)) + tuple(
+            slice(t, t + s * (o - 1) + 1, s) for t, s, o in zip(tap, strides, outs))
+        xs = xp[sl]                                     # [b, ci, *out]
+        wt = w64[(slice(None), slice(None)) + tap]      # [co, ci]
+        nb, no = dyb.shape[:2]
+        dyf = dyb.reshape(nb, no, -1)
+        dxp[sl] += np.einsum("bop,oc->bcp", dyf, wt).reshape(xs.shape)
+        dw[(slice(None), slice(None)) + tap] = np.einsum("bop,bcp->oc", dyf,
+                                                         xs.reshape(nb, xs.shape[1], -1))
+    crop = (slice(None), slice(None)) + tuple(slice(p, p + g) for p, g in zip(pads, xb.shape[2:]))
+    dx = dxp[crop]
+    return (dx if batched else dx[0]), dw
+
+
+def halo_conv_members(x, w, extents, shard_dim, stride=1, padding=0):
+    """Per-member local outputs of the sharded conv (ops.py:363-422) computed
+    the reference's way: extended block = local + right-halo rows, trimmed
+    to [max(w_min,0), min(w_max,G)), zero-padded, dense conv with the
+    sharded padding materialised.  Returns (outputs, out_extents)."""
+    n = w.ndim - 2
+    first = x.ndim - n
+    sp = shard_dim - first
+    strides, pads = _norm(n, stride), _norm(n, padding)
+    g_in = x.shape[shard_dim]
+    k, s, p = w.shape[2 + sp], strides[sp], pads[sp]
+    plans = member_plans(extents, g_in, k, s, p)
+    bounds = np.concatenate([[0], np.cumsum(extents)]).astype(int)
+    outs = []
+    for m, (j_lo, j_hi, w_min, w_max, lw, rw) in enumerate(plans):
+        a, b = bounds[m], bounds[m + 1]
+        if j_hi == j_lo:
+            shape = list(x.shape)
+            shape[shard_dim] = 0
+            shape[first - 1] = w.shape[0]
+            for i in range(n):
+                if i != sp:
+                    shape[first + i] = conv_out(x.shape[first + i], w.shape[2 + i], strides[i],
+                                                pads[i])
+            outs.append(np.zeros(shape, dtype=x.dtype))
+            continue
+        lo, hi = max(w_min, 0), min(w_max, g_in)
+        idx = [slice(None)] * x.ndim
+        idx[shard_dim] = slice(lo, hi)
+        block = x[tuple(idx)]
+        pad = [(0, 0)] * x.ndim
+        pad[shard_dim] = (max(0, -w_min), max(0, w_max - g_in))
+        block = np.pad(block, pad)
+        lp = list(pads)
+        lp[sp] = 0
+        outs.append(conv(block, w, strides, tuple(lp)))
+    return outs, [pl[1] - pl[0] for pl in plans]

@@ -1,0 +1,105 @@
+// C-ABI entry points for convolution and attention: validate, pick the
+// algorithm (tcgen05 path when eligible, CUDA-core path otherwise), launch.
+#include "common.cuh"
+
+namespace dp {
+int conv_fwd_simt_launch(const dp_conv_geom *, int, const void *, const void *, const void *,
+                         void *, cudaStream_t);
+int conv_dgrad_simt_launch(const dp_conv_geom *, int, const void *, const void *, void *, void *,
+                           cudaStream_t);
+int64_t conv_wgrad_simt_workspace(const dp_conv_geom *, int);
+int conv_wgrad_simt_launch(const dp_conv_geom *, int, const void *, const void *, const void *,
+                           void *, void *, int64_t, cudaStream_t);
+int attn_fwd_update_simt_launch(const dp_attn_geom *, int, const void *, const void *,
+                                const void *, void *, void *, void *, cudaStream_t);
+int attn_bwd_update_simt_launch(const dp_attn_geom *, int, const void *, const void *,
+                                const void *, const void *, const void *, const void *, void *,
+                                void *, void *, cudaStream_t);
+// tcgen05 paths (conv_tc.cu / attn_tc.cu); return DP_ERR_UNSUPPORTED when the
+// configuration is outside their envelope.
+int conv_tc_eligible(const dp_conv_geom *, int dtype, int which);
+int conv_fwd_tc_launch(const dp_conv_geom *, const void *, const void *, const void *, void *,
+                       cudaStream_t);
+int conv_dgrad_tc_launch(const dp_conv_geom *, const void *, const void *, void *, void *,
+                         cudaStream_t);
+int64_t conv_wgrad_tc_workspace(const dp_conv_geom *);
+int conv_wgrad_tc_launch(const dp_conv_geom *, const void *, const void *, const void *, void *,
+                         void *, int64_t, cudaStream_t);
+int attn_tc_eligible(const dp_attn_geom *, int dtype);
+int attn_fwd_update_tc_launch(const dp_attn_geom *, const void *, const void *, const void *,
+                              void *, void *, void *, cudaStream_t);
+int attn_bwd_update_tc_launch(const dp_attn_geom *, const void *, const void *, const void *,
+                              const void *, const void *, const void *, void *, void *, void *,
+                              cudaStream_t);
+}  // namespace dp
+
+using namespace dp;
+
+static int pick(int algo, int eligible, const char *what) {
+    if (algo == DP_ALGO_SIMT) return DP_ALGO_SIMT;
+    if (algo == DP_ALGO_TC) {
+        if (!eligible) {
+            set_error("%s: configuration outside the tcgen05 envelope", what);
+            return -1;
+        }
+        return DP_ALGO_TC;
+    }
+    return eligible ? DP_ALGO_TC : DP_ALGO_SIMT;
+}
+
+extern "C" int dp_conv_fwd(const dp_conv_geom *g, int dtype, int algo, const void *x,
+                           const void *xh, const void *w, void *y, void *stream) {
+    int a = pick(algo, conv_tc_eligible(g, dtype, 0), "dp_conv_fwd");
+    if (a < 0) return DP_ERR_UNSUPPORTED;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (a == DP_ALGO_TC) return conv_fwd_tc_launch(g, x, xh, w, y, st);
+    return conv_fwd_simt_launch(g, dtype, x, xh, w, y, st);
+}
+
+extern "C" int dp_conv_dgrad(const dp_conv_geom *g, int dtype, int algo, const void *dy,
+                             const void *w, void *dx, void *dxh, void *stream) {
+    int a = pick(algo, conv_tc_eligible(g, dtype, 1), "dp_conv_dgrad");
+    if (a < 0) return DP_ERR_UNSUPPORTED;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (a == DP_ALGO_TC) return conv_dgrad_tc_launch(g, dy, w, dx, dxh, st);
+    return conv_dgrad_simt_launch(g, dtype, dy, w, dx, dxh, st);
+}
+
+extern "C" int64_t dp_conv_wgrad_workspace(const dp_conv_geom *g, int dtype, int algo) {
+    int a = pick(algo, conv_tc_eligible(g, dtype, 2), "dp_conv_wgrad");
+    if (a < 0) return -1;
+    if (a == DP_ALGO_TC) return conv_wgrad_tc_workspace(g);
+    return conv_wgrad_simt_workspace(g, dtype);
+}
+
+extern "C" int dp_conv_wgrad(const dp_conv_geom *g, int dtype, int algo, const void *x,
+                             const void *xh, const void *dy, void *dw, void *ws, int64_t ws_bytes,
+                             void *stream) {
+    int a = pick(algo, conv_tc_eligible(g, dtype, 2), "dp_conv_wgrad");
+    if (a < 0) return DP_ERR_UNSUPPORTED;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (a == DP_ALGO_TC) return conv_wgrad_tc_launch(g, x, xh, dy, dw, ws, ws_bytes, st);
+    return conv_wgrad_simt_launch(g, dtype, x, xh, dy, dw, ws, ws_bytes, st);
+}
+
+extern "C" int dp_attn_fwd_update(const dp_attn_geom *g, int dtype, int algo, const void *q,
+                                  const void *k, const void *v, void *m, void *l, void *acc,
+                                  void *stream) {
+    int a = pick(algo, attn_tc_eligible(g, dtype), "dp_attn_fwd_update");
+    if (a < 0) return DP_ERR_UNSUPPORTED;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (a == DP_ALGO_TC) return attn_fwd_update_tc_launch(g, q, k, v, m, l, acc, st);
+    return attn_fwd_update_simt_launch(g, dtype, q, k, v, m, l, acc, st);
+}
+
+extern "C" int dp_attn_bwd_update(const dp_attn_geom *g, int dtype, int algo, const void *q,
+                                  const void *k, const void *v, const void *dout,
+                                  const void *lse, const void *delta, void *dq, void *dk,
+                                  void *dv, void *stream) {
+    int a = pick(algo, attn_tc_eligible(g, dtype), "dp_attn_bwd_update");
+    if (a < 0) return DP_ERR_UNSUPPORTED;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (a == DP_ALGO_TC)
+        return attn_bwd_update_tc_launch(g, q, k, v, dout, lse, delta, dq, dk, dv, st);
+    return attn_bwd_update_simt_launch(g, dtype, q, k, v, dout, lse, delta, dq, dk, dv, st);
+}

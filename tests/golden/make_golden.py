@@ -1,0 +1,237 @@
+"""Generate the golden fixtures by running the REAL reference (`domainpar`
+from /root/reference/pkg/src) in this container.  The reference cannot
+travel to the GPU box, so its outputs are committed here as small fixtures:
+
+  plans.json        per-member (out_extent, left_width, right_width) of
+                    halo_conv captured from the reference's own halo_exchange
+                    calls, for KAT and random configurations; default_chunk
+                    KATs; debug_line strings
+  conv_cases.npz    halo_conv inputs and the reference's gathered outputs
+  ring_cases.npz    ring_attention inputs and the reference's outputs
+  redist_cases.npz  redistribute inputs and the reference's per-rank blocks
+
+Run:  python tests/golden/make_golden.py   (needs /root/reference)
+"""
+
+from __future__ import annotations
+
+import json
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, "/root/reference/pkg/src")
+
+import domainpar  # noqa: E402
+from domainpar import ops as rops  # noqa: E402
+from domainpar.mesh import spawn_mesh  # noqa: E402
+from domainpar.sharding import (Replicate, Shard, ShardTensor, default_chunk, replicated,  # noqa: E402
+                                redistribute, scatter_global)
+from domainpar.verify import random_partition  # noqa: E402
+
+
+def capture_plan(extents, g_in, k, s, p):
+    """Run the reference halo_conv on a 1-channel 1-D input and record what
+    each rank asked halo_exchange for, plus the output shard shapes."""
+    calls = {}
+    real = rops.halo_exchange
+
+    def spy(group, local, dim, lw, rw):
+        calls[group.ctx.rank_id] = (int(lw), int(rw))
+        return real(group, local, dim, lw, rw)
+
+    x = np.arange(g_in, dtype=np.float64).reshape(1, g_in)
+    w = np.ones((1, 1, k))
+
+    def prog(ctx):
+        st = ShardTensor(x[:, sum(extents[:ctx.rank_id]):sum(extents[:ctx.rank_id + 1])],
+                         (1, g_in), ctx, (Shard(1),), {0: tuple(extents)})
+        out = rops.halo_conv(st, w, stride=s, padding=p)
+        return out.shard_shapes[0]
+
+    rops.halo_exchange = spy
+    try:
+        res = spawn_mesh((len(extents),), ("domain",), prog)
+        err = None
+    except Exception as e:  # noqa: BLE001 - recorded as an expected failure
+        res, err = None, str(e)
+    finally:
+        rops.halo_exchange = real
+    if err is not None:
+        return {"extents": extents, "g_in": g_in, "k": k, "s": s, "p": p, "error": err}
+    return {"extents": extents, "g_in": g_in, "k": k, "s": s, "p": p,
+            "out_extents": list(res[0]), "widths": [list(calls[r]) for r in range(len(extents))]}
+
+
+def make_plans():
+    rng = np.random.default_rng(2605)
+    cases = []
+    kats = [([512, 512], 1024, 3, 1, 1),            # cfg1 -> (513, 511)
+            ([32] * 8, 256, 3, 1, 1),               # cfg2 layer 1
+            ([33] + [32] * 6 + [31], 256, 3, 1, 1),  # cfg2 layer 2 (drifted)
+            ([5, 5], 10, 3, 2, 1),                  # acceptance (3, 2)
+            ([4, 5], 9, 1, 3, 0),                   # (2, 1)
+            ([3, 0, 2], 5, 1, 1, 0),                # empty shard
+            ([5, 4, 3], 12, 3, 2, 1),
+            ([4, 4], 8, 5, 1, 4),
+            ([3, 1, 2], 6, 3, 1, 0)]                # multi-hop -> HaloError
+    for e, g, k, s, p in kats:
+        cases.append(capture_plan(list(e), g, k, s, p))
+    while len(cases) < 260:
+        r = int(rng.integers(1, 9))
+        k = int(rng.choice([1, 3, 5, 7]))
+        s = int(rng.integers(1, 4))
+        p = int(rng.integers(0, k // 2 + 2))
+        g = int(rng.integers(max(1, k - 2 * p), 40))
+        if (g + 2 * p - k) // s + 1 < 1:
+            continue
+        ext = [int(v) for v in random_partition(rng, g, r, min_part=0)]
+        cases.append(capture_plan(ext, g, k, s, p))
+    chunks = [[e, m, default_chunk(e, m)] for e, m in
+              [(10, 4), (5, 4), (0, 3), (7, 1), (3, 5), (8, 2), (17, 5), (9, 4), (6, 4),
+               (1024, 2), (256, 8), (65536, 8), (65536, 3)]]
+
+    def dl(ctx):
+        root = ctx.rank_id == 0
+        st = scatter_global(ctx, np.zeros((5, 3)) if root else None, (Shard(0),), {0: (3, 0, 2)})
+        rep = replicated(ctx, np.arange(4.0))
+        return st.debug_line(), rep.debug_line()
+
+    lines = spawn_mesh((3,), ("domain",), dl)
+
+    def dl2(ctx):
+        root = ctx.rank_id == 0
+        st = scatter_global(ctx, np.zeros((4, 6)) if root else None, (Shard(0), Shard(1)))
+        return st.debug_line()
+
+    lines2 = spawn_mesh((2, 3), ("a", "b"), dl2)
+    return {"halo_plans": cases, "default_chunk": chunks, "debug_lines": lines,
+            "debug_lines_2d": lines2}
+
+
+def make_conv_cases():
+    rng = np.random.default_rng(11)
+    specs = [
+        # (global shape, kernel shape tail, stride, padding, shard dim, extents, dtype)
+        ((2, 10), (3,), 2, 1, 1, (5, 5), np.float64),
+        ((1, 5), (1,), 1, 0, 1, (3, 0, 2), np.float32),
+        ((2, 3, 12, 7), (3, 5), (2, 1), (1, 2), 2, (5, 4, 3), np.float64),
+        ((1, 9), (1,), 3, 0, 1, (4, 5), np.float64),
+        ((2, 8), (5,), 1, 4, 1, (4, 4), np.float64),
+        ((1, 4, 16, 16), (3, 3), 1, 1, 2, (6, 5, 5), np.float32),
+        ((1, 4, 16, 16), (3, 3), 1, 1, 3, (3, 7, 6), np.float32),
+        ((2, 3, 20, 9), (5, 3), (1, 2), (2, 1), 2, (4, 7, 4, 5), np.float64),
+        ((3, 33), (3,), 1, 1, 1, (11, 11, 11), np.float32),
+        ((1, 8, 32, 24), (3, 3), 1, 1, 2, (8, 8, 8, 8), np.float32),
+        ((1, 8, 32, 24), (3, 3), 2, 1, 2, (10, 9, 7, 6), np.float32),
+        ((2, 16, 18, 10), (3, 3), 1, 0, 2, (7, 6, 5), np.float64),
+    ]
+    out = {}
+    for i, (shape, ktail, stride, pad, dim, ext, dt) in enumerate(specs):
+        n = len(ktail)
+        cin = shape[-n - 1]
+        cout = int(rng.integers(1, 5)) if cin < 8 else 8
+        x = rng.standard_normal(shape).astype(dt)
+        w = (rng.standard_normal((cout, cin) + ktail) * 0.5).astype(dt)
+
+        def prog(ctx, x=x, w=w, dim=dim, ext=ext, stride=stride, pad=pad):
+            st = scatter_global(ctx, x if ctx.rank_id == 0 else None, (Shard(dim),), {0: ext})
+            res = rops.halo_conv(st, w, stride=stride, padding=pad)
+            return res.full_tensor(), res.shard_shapes[0]
+
+        res = spawn_mesh((len(ext),), ("domain",), prog)
+        full, shapes = res[0]
+        dense = domainpar.conv(x, w, stride=stride, padding=pad)
+        assert np.array_equal(full, dense), i
+        out[f"c{i}_x"] = x
+        out[f"c{i}_w"] = w
+        out[f"c{i}_y"] = full
+        out[f"c{i}_meta"] = np.array(json.dumps({"stride": stride, "padding": pad, "dim": dim,
+                                                 "extents": list(ext),
+                                                 "out_extents": list(shapes)}))
+    out["count"] = np.array(len(specs))
+    return out
+
+
+def make_ring_cases():
+    rng = np.random.default_rng(7)
+    specs = [
+        (5, 11, 6, (2, 0, 3, 0), (4, 0, 5, 2), np.float64),
+        (4, 6, 4, (2, 2), (3, 3), np.float32),
+        (12, 12, 16, (5, 0, 4, 3), (5, 0, 4, 3), np.float64),
+        (12, 12, 16, (5, 0, 4, 3), (5, 0, 4, 3), np.float32),
+        (19, 17, 8, (3, 5, 4, 7), (9, 0, 0, 8), np.float64),
+        (64, 96, 32, (16, 16, 16, 16), (24, 24, 24, 24), np.float32),
+        (40, 40, 64, (5,) * 8, (5,) * 8, np.float32),
+    ]
+    out = {}
+    for i, (sq, sk, d, qe, ke, dt) in enumerate(specs):
+        q = rng.standard_normal((sq, d)).astype(dt)
+        k = rng.standard_normal((sk, d)).astype(dt)
+        v = rng.standard_normal((sk, d)).astype(dt)
+        if i == 1:
+            q = q * 100
+            k = k * 100
+
+        def prog(ctx, q=q, k=k, v=v, qe=qe, ke=ke):
+            root = ctx.rank_id == 0
+            qs = scatter_global(ctx, q if root else None, (Shard(0),), {0: qe})
+            ks = scatter_global(ctx, k if root else None, (Shard(0),), {0: ke})
+            vs = scatter_global(ctx, v if root else None, (Shard(0),), {0: ke})
+            return rops.ring_attention(qs, ks, vs).full_tensor()
+
+        full = spawn_mesh((len(qe),), ("domain",), prog)[0]
+        out[f"r{i}_q"], out[f"r{i}_k"], out[f"r{i}_v"], out[f"r{i}_o"] = q, k, v, full
+        out[f"r{i}_qe"] = np.array(qe)
+        out[f"r{i}_ke"] = np.array(ke)
+    out["count"] = np.array(len(specs))
+    return out
+
+
+def make_redist_cases():
+    rng = np.random.default_rng(3)
+    out = {}
+    cases = []
+    for r in (2, 3, 4, 5):
+        n = 13 + r
+        ext = tuple(int(v) for v in random_partition(rng, n, r, min_part=0))
+        cases.append(((n, n + 3), (Shard(0),), (Shard(1),), {0: ext}, (r,)))
+        cases.append(((n, n + 3), (Shard(0),), (Replicate(),), {0: ext}, (r,)))
+        cases.append(((n + 1, n), (Shard(1),), (Shard(0),), None, (r,)))
+    cases.append(((6, 8), (Shard(0), Shard(1)), (Shard(1), Shard(0)), None, (2, 2)))
+    cases.append(((6, 8), (Shard(0), Replicate()), (Shard(0), Shard(1)), {0: (5, 1)}, (2, 3)))
+    cases.append(((4, 3, 5), (Shard(2),), (Shard(0),), {0: (0, 5, 0)}, (3,)))
+    for i, (shape, old, new, shapes, mesh) in enumerate(cases):
+        g = rng.standard_normal(shape).astype(np.float32)
+        names = ("domain",) if len(mesh) == 1 else ("a", "b")
+
+        def prog(ctx, g=g, old=old, new=new, shapes=shapes):
+            st = scatter_global(ctx, g if ctx.rank_id == 0 else None, old, shapes)
+            r2 = redistribute(st, new)
+            return r2.local, {int(a): list(v) for a, v in r2.shard_shapes.items()}
+
+        res = spawn_mesh(mesh, names, prog)
+        out[f"d{i}_g"] = g
+        for rank, (loc, sh) in enumerate(res):
+            out[f"d{i}_local{rank}"] = loc
+        meta = {"mesh": list(mesh), "old": [repr(p) for p in old], "new": [repr(p) for p in new],
+                "shapes": None if shapes is None else {str(a): list(v) for a, v in shapes.items()},
+                "out_shapes": res[0][1]}
+        out[f"d{i}_meta"] = np.array(json.dumps(meta))
+    out["count"] = np.array(len(cases))
+    return out
+
+
+def main():
+    with open(os.path.join(HERE, "plans.json"), "w") as f:
+        json.dump(make_plans(), f, indent=0)
+    np.savez_compressed(os.path.join(HERE, "conv_cases.npz"), **make_conv_cases())
+    np.savez_compressed(os.path.join(HERE, "ring_cases.npz"), **make_ring_cases())
+    np.savez_compressed(os.path.join(HERE, "redist_cases.npz"), **make_redist_cases())
+    print("golden fixtures written to", HERE)
+
+
+if __name__ == "__main__":
+    main()
