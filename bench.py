@@ -1,0 +1,463 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 domain-parallel hot path (driver contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+
+Default workload = BASELINE.json configs[1] (cfg2): the UNet-style conv3d
+encoder block conv(16->32, 3^3) -> conv(32->32, 3^3), stride 1, padding 1,
+no bias/activation (the reference conv has neither), on a 1x16x256^3 bf16
+volume D-sharded over N GPUs (strong scaling).  One step = forward of both
+layers + backward (dgrad of both layers incl. the block input, wgrad of
+both, reverse halos, dW all-reduce) against a fixed synthetic upstream
+gradient.  Activations live channels-last (NDHWC) in HBM.
+
+Other configs (--config): cfg1 (conv2d fp32 parity anchor, R=2 semantics on
+N GPUs), cfg3 (ring attention 64k x 16 heads x 64, bf16), cfg4 (weak-scaling
+conv2d stack 64ch x4 on 2048^2 per GPU), cfg5 (uneven redistribute).
+
+Rank 0 prints ONE JSON line.  `value` = samples/s of the whole job with
+inputs resident in HBM (device time, CUDA events, max over ranks); `e2e` =
+the same through the public API with the input shard copied host->device
+(pinned) and dW read back device->host every step; `roofline` = the
+dominant kernel's achieved TFLOP/s (algorithmic FLOPs / measured launch
+time) vs the measured bf16 peak in MEASURED_PEAKS.json; `cpu_baseline` =
+the oracle port of the reference algorithm timed on a bounded sample on
+this host.  `--impl reference` times that CPU implementation as the
+reference arm (rank 0 only).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return p, "measured"
+    except OSError:
+        return PEAKS_FALLBACK, "fallback"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="cfg2", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--algo", default="auto", choices=["auto", "simt", "tc"])
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# clocks sampled during the timed region
+
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sms, maxes, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [s.strip() for s in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sms.append(float(parts[0]))
+                maxes.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[4:8]):
+                if val.lower() == "active":
+                    reasons.add(nm)
+        if not sms:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        sms.sort()
+        return {"sm_mhz": sms[len(sms) // 2], "sm_max_mhz": max(maxes),
+                "reasons": sorted(reasons), "samples": len(sms)}
+
+
+# ---------------------------------------------------------------------------
+# mesh
+
+
+def init(args):
+    import torch
+
+    import paper_2605_11111_b200 as dp
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        if args.gpus > 1:
+            raise SystemExit(f"--gpus {args.gpus} needs torchrun with {args.gpus} processes")
+    if world == 1 and "MASTER_PORT" not in os.environ:
+        import socket
+
+        with socket.socket() as s:
+            s.bind(("127.0.0.1", 0))
+            os.environ["MASTER_PORT"] = str(s.getsockname()[1])
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    ctx = dp.init_mesh((world,), ("domain",))
+    torch.cuda.set_device(ctx.device)
+    return ctx
+
+
+def max_over_ranks(ctx, value: float) -> float:
+    import torch
+    import torch.distributed as dist
+
+    if ctx.mesh.world_size == 1:
+        return value
+    t = torch.tensor([value], dtype=torch.float64, device=ctx.device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(ctx):
+    import torch
+    import torch.distributed as dist
+
+    if ctx.mesh.world_size > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+
+
+# ---------------------------------------------------------------------------
+# kernel-level timing (instrumented pass): events around every conv call
+
+
+class KernelTimer:
+    def __init__(self):
+        self.records = []  # (name, flops, start, end)
+        self.active = False
+
+    def wrap(self, kernels_mod):
+        import torch
+
+        timer = self
+        for name in ("conv_fwd", "conv_dgrad", "conv_wgrad"):
+            orig = getattr(kernels_mod, name)
+
+            def make(orig=orig, name=name):
+                def inner(*a, **kw):
+                    if not timer.active:
+                        return orig(*a, **kw)
+                    flops = conv_flops(name, a, kw)
+                    s = torch.cuda.Event(enable_timing=True)
+                    e = torch.cuda.Event(enable_timing=True)
+                    s.record()
+                    orig(*a, **kw)
+                    e.record()
+                    timer.records.append((name, flops, s, e))
+                return inner
+            setattr(kernels_mod, name, make())
+
+    def summary(self):
+        import torch
+
+        torch.cuda.synchronize()
+        out = {}
+        for name, flops, s, e in self.records:
+            d = out.setdefault(name, {"launches": 0, "ms": 0.0, "flops": 0.0})
+            d["launches"] += 1
+            d["ms"] += s.elapsed_time(e)
+            d["flops"] += flops
+        return out
+
+
+def conv_flops(name, a, kw):
+    """Algorithmic FLOPs of one conv call = 2 * C_in * C_out * taps * output
+    positions of the forward conv it belongs to (dgrad and wgrad count the
+    same MACs as the forward, the usual convention)."""
+    import math
+
+    if name == "conv_fwd":
+        x, _, w, y = a[:4]
+        pos = y.shape[0] * math.prod(y.shape[2:])
+    elif name == "conv_dgrad":
+        dy, w = a[0], a[1]
+        pos = dy.shape[0] * math.prod(dy.shape[2:])
+    else:
+        x, _, dy, w = a[0], a[1], a[2], a[3]
+        pos = dy.shape[0] * math.prod(dy.shape[2:])
+    return 2.0 * w.shape[0] * w.shape[1] * math.prod(w.shape[2:]) * pos
+
+
+# ---------------------------------------------------------------------------
+# workloads (ours)
+
+
+def setup_cfg2(ctx):
+    import torch
+
+    import paper_2605_11111_b200 as dp
+
+    G, C0, C1 = 256, 16, 32
+    R = ctx.mesh.world_size
+    me = ctx.rank_id
+    dev = ctx.device
+    ext = dp.default_chunk(G, R)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1234 + me)
+    fmt = torch.channels_last_3d
+    x = torch.randn((1, C0, ext[me], G, G), generator=gen, device=dev, dtype=torch.bfloat16)
+    x = x.contiguous(memory_format=fmt)
+    wg = torch.Generator(device=dev)
+    wg.manual_seed(7)  # identical weights on every rank (replicated)
+    w1 = (torch.randn((C1, C0, 3, 3, 3), generator=wg, device=dev) * 0.05).to(torch.bfloat16)
+    w2 = (torch.randn((C1, C1, 3, 3, 3), generator=wg, device=dev) * 0.05).to(torch.bfloat16)
+    p1 = dp.halo_conv_plan(ext, G, 3, 1, 1)
+    p2 = dp.halo_conv_plan(list(p1.out_extents), G, 3, 1, 1)
+    g = torch.randn((1, C1, p2.out_extents[me], G, G), generator=gen, device=dev,
+                    dtype=torch.bfloat16).contiguous(memory_format=fmt)
+    xst = dp.ShardTensor(x, (1, C0, G, G, G), ctx, (dp.Shard(2),), {0: tuple(ext)})
+
+    def step(xin=None):
+        st = xst if xin is None else dp.ShardTensor(xin, xst.global_shape, ctx, xst.placements,
+                                                    xst.shard_shapes)
+        y1, t1 = dp.halo_conv_forward(st, w1, 1, 1)
+        y2, t2 = dp.halo_conv_forward(y1, w2, 1, 1)
+        dy1, dw2 = dp.halo_conv_backward(t2, g)
+        dx, dw1 = dp.halo_conv_backward(t1, dy1)
+        return dw1, dw2
+
+    flops = 3 * 2.0 * (C0 * C1 + C1 * C1) * 27 * G ** 3  # fwd + dgrad + wgrad, both layers
+    info = {"workload": "cfg2: conv3d 3x3x3 UNet-style encoder block conv(16->32)->conv(32->32), "
+                        "s1 p1, no bias/activation, 1x16x256^3 bf16, D-sharded",
+            "global_batch": 1, "volume": [G, G, G], "channels": [C0, C1, C1],
+            "layout": "NDHWC (channels_last_3d)", "shard_extents": list(ext),
+            "parallelism": f"domain{R}",
+            "l2": "inputs larger than L2 (512 MiB activations per layer), no flush"}
+    return dict(step=step, x=x, flops=flops, info=info, scaling="strong", dtype="bf16",
+                unit="samples/s", samples_per_step=1)
+
+
+def cpu_sample_cfg2(threads: int):
+    """Oracle port of the reference algorithm on a bounded sample: the
+    block fwd+bwd on `threads` independent sub-volumes of 1 x 256 x 64
+    voxels (each 1/1024 of the volume), fp32, one per thread.  Returns
+    (seconds, fraction of one sample computed)."""
+    import numpy as np
+
+    from oracle import workloads
+
+    rng = np.random.default_rng(0)
+    w1 = (rng.standard_normal((32, 16, 3, 3, 3)) * 0.05).astype(np.float32)
+    w2 = (rng.standard_normal((32, 32, 3, 3, 3)) * 0.05).astype(np.float32)
+    jobs = []
+    for _ in range(threads):
+        x = rng.standard_normal((1, 16, 1, 256, 64)).astype(np.float32)
+        g = rng.standard_normal((1, 32, 1, 256, 64)).astype(np.float32)
+        jobs.append((x, g))
+    t0 = time.perf_counter()
+    if threads == 1:
+        workloads.conv_block_step(jobs[0][0], w1, w2, jobs[0][1])
+    else:
+        from concurrent.futures import ThreadPoolExecutor
+
+        with ThreadPoolExecutor(threads) as ex:
+            list(ex.map(lambda j: workloads.conv_block_step(j[0], w1, w2, j[1]), jobs))
+    dt = time.perf_counter() - t0
+    return dt, threads / 1024.0
+
+
+CONFIGS = {"cfg2": (setup_cfg2, cpu_sample_cfg2,
+                    "1 x 256 x 64 voxel sub-volumes (1/1024 of the 256^3 volume each), fp32, "
+                    "block fwd+bwd via the oracle port of dense.conv's einsum")}
+
+
+# ---------------------------------------------------------------------------
+
+
+def run_reference(args):
+    """The reference arm: the reference algorithm's CPU implementation (the
+    oracle port — the reference is Python and does not travel to this box)
+    on all host threads, bounded samples, same metric/unit/config."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    _, cpu_fn, sample_desc = CONFIGS[args.config]
+    for _ in range(max(0, min(args.warmup, 1))):
+        cpu_fn(cores)
+    times = []
+    frac = 1.0
+    for _ in range(max(1, min(args.steps, 2))):
+        dt, frac = cpu_fn(cores)
+        times.append(dt)
+    t = sum(times) / len(times)
+    value = frac / t  # samples per second
+    line = {"impl": "reference", "metric": "sharded fwd+bwd step latency & samples/s",
+            "value": value, "unit": "samples/s", "n_gpus": args.gpus, "steps": len(times),
+            "warmup": args.warmup, "ms_per_step": 1000.0 / value, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": args.config, "sample": sample_desc},
+            "cpu_baseline": {"value": value, "unit": "samples/s", "cores": cores,
+                             "kind": "port", "sample": f"{cores} x {sample_desc}"},
+            "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+
+    from paper_2605_11111_b200 import _lib, kernels
+
+    kernels.set_algo(args.algo)
+    ctx = init(args)
+    setup_fn, cpu_fn, sample_desc = CONFIGS[args.config]
+    W = setup_fn(ctx)
+    step = W["step"]
+    for _ in range(max(3, args.warmup)):
+        step()
+    barrier(ctx)
+
+    # --- timed region: device time, inputs resident in HBM ----------------
+    start = torch.cuda.Event(enable_timing=True)
+    end = torch.cuda.Event(enable_timing=True)
+    l0 = _lib.launch_count()
+    local_gpu = ctx.device.index if ctx.device.index is not None else 0
+    with ClockSampler(local_gpu) as clk:
+        barrier(ctx)
+        start.record()
+        for _ in range(args.steps):
+            step()
+        end.record()
+        barrier(ctx)
+    launches = _lib.launch_count() - l0
+    ms = max_over_ranks(ctx, start.elapsed_time(end) / args.steps)
+
+    # --- instrumented pass: per-kernel launch times --------------------------
+    timer = KernelTimer()
+    timer.wrap(kernels)
+    timer.active = True
+    for _ in range(max(1, min(args.steps, 3))):
+        step()
+    timer.active = False
+    ksum = timer.summary()
+
+    # --- e2e through the public API: pinned host input -> device, dW -> host
+    x = W["x"]
+    host = torch.empty_strided(x.shape, x.stride(), dtype=x.dtype, pin_memory=True)
+    host.copy_(x)
+    dev_in = torch.empty_strided(x.shape, x.stride(), dtype=x.dtype, device=x.device)
+    outs = step()
+    host_out = [torch.empty(o.shape, dtype=o.dtype, pin_memory=True) for o in outs]
+    d2h = sum(o.numel() * o.element_size() for o in outs)
+    barrier(ctx)
+    e_start = torch.cuda.Event(enable_timing=True)
+    e_end = torch.cuda.Event(enable_timing=True)
+    e2e_steps = max(1, min(args.steps, 5))
+    e_start.record()
+    for _ in range(e2e_steps):
+        dev_in.copy_(host, non_blocking=True)
+        outs = step(dev_in)
+        for h, o in zip(host_out, outs):
+            h.copy_(o, non_blocking=True)
+    e_end.record()
+    barrier(ctx)
+    e2e_ms = max_over_ranks(ctx, e_start.elapsed_time(e_end) / e2e_steps)
+
+    if ctx.rank_id != 0:
+        return
+    pk, pk_kind = peaks()
+    samples = W["samples_per_step"]
+    value = samples / (ms / 1000.0)
+    # dominant kernel
+    dom = max(ksum.items(), key=lambda kv: kv[1]["ms"]) if ksum else None
+    roof = None
+    if dom:
+        name, d = dom
+        avg_ms = d["ms"] / d["launches"]
+        ach = (d["flops"] / d["launches"]) / (avg_ms / 1000.0) / 1e12
+        peak = pk.get("bf16_tflops_sustained", PEAKS_FALLBACK["bf16_tflops_sustained"])
+        traffic = None
+        tpath = os.path.join(ROOT, "profiles", "traffic.json")
+        if os.path.exists(tpath):
+            with open(tpath) as f:
+                traffic = json.load(f).get(args.config, {}).get(name)
+        roof = {"bound": "tensor", "kernel": name, "achieved": ach, "peak": peak,
+                "unit": "TFLOP/s", "frac": ach / peak, "traffic": traffic,
+                "peak_kind": f"{pk_kind} bf16 sustained (kernel timed inside the step)",
+                "avg_launch_ms": avg_ms,
+                "flops_per_launch": d["flops"] / d["launches"]}
+    cpu = None
+    if not args.no_cpu_baseline and ctx.mesh.world_size == 1:
+        dt, frac = cpu_fn(1)
+        cpu = {"value": frac / dt, "unit": W["unit"], "cores": 1, "kind": "port",
+               "sample": sample_desc, "seconds": dt}
+    h2d = x.numel() * x.element_size()
+    line = {
+        "metric": "sharded fwd+bwd step latency & samples/s",
+        "value": value, "unit": W["unit"], "n_gpus": ctx.mesh.world_size, "steps": args.steps,
+        "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True,
+        "scaling": W["scaling"], "vs_baseline": None, "dtype": W["dtype"],
+        "data": "synthetic (torch.randn on device, fixed seeds)", "config": W["info"],
+        "roofline": roof, "cpu_baseline": cpu,
+        "e2e": {"value": samples / (e2e_ms / 1000.0), "unit": W["unit"], "ms_per_step": e2e_ms,
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "gpu_launches": launches // args.steps * args.steps,
+        "gpu_launches_per_step": launches / args.steps,
+        "clocks": clk.summary(),
+        "tflops_step": W["flops"] / (ms / 1000.0) / 1e12,
+        "kernels": {k: {"launches": v["launches"], "avg_ms": v["ms"] / v["launches"],
+                        "tflops": v["flops"] / (v["ms"] / 1000.0) / 1e12 if v["ms"] else None}
+                    for k, v in ksum.items()},
+    }
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -101,10 +101,19 @@ typedef struct dp_conv_geom {
     int64_t ys[5];          /* ... of the output */
 } dp_conv_geom;
 
+/* Workspace bytes the conv entry point `which` (DP_CONV_FWD / _DGRAD /
+ * _WGRAD) needs for this geometry and algorithm (weight images for the
+ * tcgen05 path, split-K partials for wgrad); -1 when `algo` cannot run it. */
+#define DP_CONV_FWD 0
+#define DP_CONV_DGRAD 1
+#define DP_CONV_WGRAD 2
+int64_t dp_conv_workspace(const dp_conv_geom *g, int dtype, int algo, int which);
+
 /* y = conv(x_virtual, w); w is contiguous [c_out, c_in, k0(, k1(, k2))] in
  * the activation dtype; accumulation is fp32 (fp64 for DP_F64). */
 int dp_conv_fwd(const dp_conv_geom *g, int dtype, int algo, const void *x, const void *x_halo,
-                const void *w, void *y, void *stream);
+                const void *w, void *y, void *workspace, int64_t workspace_bytes,
+                void *stream);
 
 /* dx_virtual = conv^T(dy, w) over virtual rows [0, in_ext + halo) of the
  * sharded dim: rows [0, in_ext) land in dx (strides g->xs), rows
@@ -112,13 +121,13 @@ int dp_conv_fwd(const dp_conv_geom *g, int dtype, int algo, const void *x, const
  * sent back to the next rank and accumulated there.  dy uses
  * strides g->ys.  Overwrites dx / dx_halo. */
 int dp_conv_dgrad(const dp_conv_geom *g, int dtype, int algo, const void *dy, const void *w,
-                  void *dx, void *dx_halo, void *stream);
+                  void *dx, void *dx_halo, void *workspace, int64_t workspace_bytes,
+                  void *stream);
 
 /* dw (fp32 for DP_F32/DP_BF16, fp64 for DP_F64; contiguous [c_out, c_in,
  * k...]) = sum over batch and output positions of dy * x_virtual.  The
  * result is this rank's partial; the caller all-reduces it over the
- * sharding group.  `workspace` must hold dp_conv_wgrad_workspace() bytes. */
-int64_t dp_conv_wgrad_workspace(const dp_conv_geom *g, int dtype, int algo);
+ * sharding group. */
 int dp_conv_wgrad(const dp_conv_geom *g, int dtype, int algo, const void *x, const void *x_halo,
                   const void *dy, void *dw, void *workspace, int64_t workspace_bytes,
                   void *stream);

@@ -19,6 +19,7 @@ LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
 DP_OK, DP_ERR_INVALID, DP_ERR_UNSUPPORTED, DP_ERR_CUDA = 0, 1, 2, 3
 DP_F32, DP_F64, DP_BF16 = 0, 1, 2
 ALGO_AUTO, ALGO_SIMT, ALGO_TC = 0, 1, 2
+CONV_FWD, CONV_DGRAD, CONV_WGRAD = 0, 1, 2
 
 _i64 = ctypes.c_int64
 _i32 = ctypes.c_int32
@@ -59,12 +60,12 @@ SIGNATURES = {
                                        ctypes.c_int, _vp]),
     "dp_accumulate_strided": (ctypes.c_int, [ctypes.c_int, _i64p, _vp, _i64p, _vp, _i64p,
                                              ctypes.c_int, _vp]),
+    "dp_conv_workspace": (ctypes.c_int64, [ctypes.POINTER(ConvGeom), ctypes.c_int, ctypes.c_int,
+                                           ctypes.c_int]),
     "dp_conv_fwd": (ctypes.c_int, [ctypes.POINTER(ConvGeom), ctypes.c_int, ctypes.c_int,
-                                   _vp, _vp, _vp, _vp, _vp]),
+                                   _vp, _vp, _vp, _vp, _vp, ctypes.c_int64, _vp]),
     "dp_conv_dgrad": (ctypes.c_int, [ctypes.POINTER(ConvGeom), ctypes.c_int, ctypes.c_int,
-                                     _vp, _vp, _vp, _vp, _vp]),
-    "dp_conv_wgrad_workspace": (ctypes.c_int64, [ctypes.POINTER(ConvGeom), ctypes.c_int,
-                                                 ctypes.c_int]),
+                                     _vp, _vp, _vp, _vp, _vp, ctypes.c_int64, _vp]),
     "dp_conv_wgrad": (ctypes.c_int, [ctypes.POINTER(ConvGeom), ctypes.c_int, ctypes.c_int,
                                      _vp, _vp, _vp, _vp, _vp, ctypes.c_int64, _vp]),
     "dp_attn_fwd_update": (ctypes.c_int, [ctypes.POINTER(AttnGeom), ctypes.c_int, ctypes.c_int,

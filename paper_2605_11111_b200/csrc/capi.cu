@@ -15,14 +15,13 @@ int attn_fwd_update_simt_launch(const dp_attn_geom *, int, const void *, const v
 int attn_bwd_update_simt_launch(const dp_attn_geom *, int, const void *, const void *,
                                 const void *, const void *, const void *, const void *, void *,
                                 void *, void *, cudaStream_t);
-// tcgen05 paths (conv_tc.cu / attn_tc.cu); return DP_ERR_UNSUPPORTED when the
-// configuration is outside their envelope.
+// tcgen05 paths (conv_tc.cu / attn_tc.cu)
 int conv_tc_eligible(const dp_conv_geom *, int dtype, int which);
+int64_t conv_tc_workspace(const dp_conv_geom *, int which);
 int conv_fwd_tc_launch(const dp_conv_geom *, const void *, const void *, const void *, void *,
-                       cudaStream_t);
+                       void *, int64_t, cudaStream_t);
 int conv_dgrad_tc_launch(const dp_conv_geom *, const void *, const void *, void *, void *,
-                         cudaStream_t);
-int64_t conv_wgrad_tc_workspace(const dp_conv_geom *);
+                         void *, int64_t, cudaStream_t);
 int conv_wgrad_tc_launch(const dp_conv_geom *, const void *, const void *, const void *, void *,
                          void *, int64_t, cudaStream_t);
 int attn_tc_eligible(const dp_attn_geom *, int dtype);
@@ -47,35 +46,37 @@ static int pick(int algo, int eligible, const char *what) {
     return eligible ? DP_ALGO_TC : DP_ALGO_SIMT;
 }
 
+extern "C" int64_t dp_conv_workspace(const dp_conv_geom *g, int dtype, int algo, int which) {
+    int a = pick(algo, conv_tc_eligible(g, dtype, which), "dp_conv_workspace");
+    if (a < 0) return -1;
+    if (a == DP_ALGO_TC) return conv_tc_workspace(g, which);
+    return which == DP_CONV_WGRAD ? conv_wgrad_simt_workspace(g, dtype) : 0;
+}
+
 extern "C" int dp_conv_fwd(const dp_conv_geom *g, int dtype, int algo, const void *x,
-                           const void *xh, const void *w, void *y, void *stream) {
-    int a = pick(algo, conv_tc_eligible(g, dtype, 0), "dp_conv_fwd");
+                           const void *xh, const void *w, void *y, void *ws, int64_t ws_bytes,
+                           void *stream) {
+    int a = pick(algo, conv_tc_eligible(g, dtype, DP_CONV_FWD), "dp_conv_fwd");
     if (a < 0) return DP_ERR_UNSUPPORTED;
     cudaStream_t st = (cudaStream_t)stream;
-    if (a == DP_ALGO_TC) return conv_fwd_tc_launch(g, x, xh, w, y, st);
+    if (a == DP_ALGO_TC) return conv_fwd_tc_launch(g, x, xh, w, y, ws, ws_bytes, st);
     return conv_fwd_simt_launch(g, dtype, x, xh, w, y, st);
 }
 
 extern "C" int dp_conv_dgrad(const dp_conv_geom *g, int dtype, int algo, const void *dy,
-                             const void *w, void *dx, void *dxh, void *stream) {
-    int a = pick(algo, conv_tc_eligible(g, dtype, 1), "dp_conv_dgrad");
+                             const void *w, void *dx, void *dxh, void *ws, int64_t ws_bytes,
+                             void *stream) {
+    int a = pick(algo, conv_tc_eligible(g, dtype, DP_CONV_DGRAD), "dp_conv_dgrad");
     if (a < 0) return DP_ERR_UNSUPPORTED;
     cudaStream_t st = (cudaStream_t)stream;
-    if (a == DP_ALGO_TC) return conv_dgrad_tc_launch(g, dy, w, dx, dxh, st);
+    if (a == DP_ALGO_TC) return conv_dgrad_tc_launch(g, dy, w, dx, dxh, ws, ws_bytes, st);
     return conv_dgrad_simt_launch(g, dtype, dy, w, dx, dxh, st);
-}
-
-extern "C" int64_t dp_conv_wgrad_workspace(const dp_conv_geom *g, int dtype, int algo) {
-    int a = pick(algo, conv_tc_eligible(g, dtype, 2), "dp_conv_wgrad");
-    if (a < 0) return -1;
-    if (a == DP_ALGO_TC) return conv_wgrad_tc_workspace(g);
-    return conv_wgrad_simt_workspace(g, dtype);
 }
 
 extern "C" int dp_conv_wgrad(const dp_conv_geom *g, int dtype, int algo, const void *x,
                              const void *xh, const void *dy, void *dw, void *ws, int64_t ws_bytes,
                              void *stream) {
-    int a = pick(algo, conv_tc_eligible(g, dtype, 2), "dp_conv_wgrad");
+    int a = pick(algo, conv_tc_eligible(g, dtype, DP_CONV_WGRAD), "dp_conv_wgrad");
     if (a < 0) return DP_ERR_UNSUPPORTED;
     cudaStream_t st = (cudaStream_t)stream;
     if (a == DP_ALGO_TC) return conv_wgrad_tc_launch(g, x, xh, dy, dw, ws, ws_bytes, st);

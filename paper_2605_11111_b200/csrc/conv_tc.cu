@@ -1,0 +1,880 @@
+// tcgen05 + TMA implicit-GEMM convolution (bf16 in, fp32 accumulate in TMEM)
+// for channels-last activations, stride 1 — the forward conv and, through a
+// flipped/transposed weight image, the data gradient.
+//
+// GEMM view: M = 128 output voxels along W (one TMEM lane each), N = C_out
+// (TMEM columns), K = taps x C_in (16 channels per tcgen05.mma).
+//
+// Geometry roles.  Spatial dims are mapped onto (P, Q, W):
+//   3-D (D,H,W): P = D, Q = H;   2-D (H,W): P = 1 (dummy), Q = H.
+// A work unit is a column (b, p_out, 128-voxel W tile) and a chunk of
+// output rows q_out in [q0, q1).  The unit streams INPUT rows q_in along Q;
+// one pipeline stage holds the KP input rows (kp = 0..KP-1) at one q_in
+// for all C_in, staged by TMA as 8-channel "chunk planes": plane = 130
+// voxels x 16 B, so shifting the UMMA A descriptor by 16 B shifts the
+// window by one voxel (the kw taps reuse the same smem; TMA zero-fills
+// every out-of-range voxel = the conv padding).  Each staged row feeds the
+// KQ output rows it contributes to (q_out = q_in - base_q - kq).  Their
+// fp32 accumulators sit in a ring of TMEM slots laid out in DECREASING
+// column order (slot(r) = (NSLOT-1 - r mod NSLOT) * N), so the KQ rows a
+// staged input row feeds are adjacent columns [row j | row j-1 | row j-2]:
+// ONE tcgen05.mma with N = KQ*C_out (B rows ordered (kq, c_out)) performs
+// all KQ tap contributions of a (kp, kw, 16-channel) step.  Slots are zeroed
+// by the epilogue when it drains them, so every MMA accumulates.  Input rows
+// are loaded once per unit instead of KQ times, and each A tile is read once
+// per KQ*C_out columns (3x fewer smem operand bytes and MMA issues than a
+// per-tap N = C_out GEMM).
+//
+// Virtual halo block: on the sharded dim (P for 3-D, Q for 2-D) input rows
+// [0, main) come from the local block's tensor map and [main, main+halo)
+// from the received halo's map; anything else is out of bounds -> zeros.
+// That is the reference's trimmed + zero-padded extended block
+// (domainpar/ops.py:397-413) without ever materialising it.
+//
+// Warp roles (192 threads, one CTA per SM, persistent over units):
+//   warp 0     TMA producer (one lane)          smem ring: full/empty mbarriers
+//   warp 1     tcgen05.mma issuer (one lane)    TMEM ring: tfull/tempty mbarriers
+//   warps 2-5  epilogue: tcgen05.ld -> bf16 -> 16-B global stores
+#include "tc_common.cuh"
+
+namespace dp {
+namespace {
+
+constexpr int kTileW = 128;
+constexpr int kThreads = 192;
+
+struct ConvTcParams {
+    int B, Cin, Cout;
+    int Pin, Qin, Win;        // main-block input extents (P, Q, W roles)
+    int Pout, Qout, Wout;     // output extents
+    int KP, KQ, KW;
+    int base_p, base_q, base_w;
+    int split;                // 0: halo on P, 1: halo on Q, -1: none
+    int halo;                 // halo rows on the split dim
+    __nv_bfloat16 *y, *y2;    // output / output rows >= ysplit on the split dim
+    int64_t ys[4], y2s[4];    // element strides (b, p, q, w); channel stride 1
+    int ysplit_dim, ysplit;   // -1: none
+    int n_wt, q_chunk, n_qc, n_units;
+    int nstage, plane;        // pipeline depth, bytes per chunk plane
+    int wimg_bytes;
+    const __nv_bfloat16 *wimg;
+};
+
+template <int N>
+__global__ void __launch_bounds__(kThreads, 1)
+conv_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap hmap,
+               const ConvTcParams p) {
+    using namespace tc;
+    extern __shared__ __align__(1024) uint8_t smem[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int C8 = p.Cin / 8, KC = p.Cin / 16;
+    constexpr int NSLOT = (512 / N) < 16 ? (512 / N) : 16;
+    const int BW = kTileW + p.KW - 1;
+    const uint32_t stage_bytes = (uint32_t)p.KP * C8 * p.plane;
+
+    uint8_t *wsm = smem;
+    uint8_t *stages = smem + ((p.wimg_bytes + 1023) & ~1023);
+    uint64_t *bars = reinterpret_cast<uint64_t *>(stages + (size_t)p.nstage * stage_bytes);
+    uint64_t *full = bars, *empty = bars + p.nstage;
+    uint64_t *tfull = empty + p.nstage, *tempty = tfull + NSLOT;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + NSLOT);
+
+    // weights: global image -> smem once per CTA (generic proxy), then fence
+    for (int i = threadIdx.x * 16; i < p.wimg_bytes; i += kThreads * 16)
+        *reinterpret_cast<int4 *>(wsm + i) =
+            *reinterpret_cast<const int4 *>(reinterpret_cast<const uint8_t *>(p.wimg) + i);
+    fence_async_smem();
+    if (warp == 0) {
+        if (lane == 0) {
+            for (int i = 0; i < p.nstage; ++i) {
+                mbar_init(&full[i], 1);
+                mbar_init(&empty[i], 1);
+            }
+            for (int i = 0; i < NSLOT; ++i) {
+                mbar_init(&tfull[i], 1);
+                mbar_init(&tempty[i], 128);
+            }
+            mbar_fence_init();
+            tma_prefetch(&xmap);
+            tma_prefetch(&hmap);
+        }
+        __syncwarp();
+        tmem_alloc(tmem_slot, 512);
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    if (warp >= 2) {
+        // every accumulator slot starts at zero (MMAs always accumulate)
+        const uint32_t lane_base = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+        uint32_t z[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) z[i] = 0u;
+        for (int c = 0; c < NSLOT * N; c += 16) tmem_st16(lane_base + c, z);
+        tmem_wait_st();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+
+    if (warp == 0) {
+        // ===================== TMA producer =====================
+        if (lane == 0) {
+            uint32_t it = 0;
+            for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
+                int r = u;
+                const int wt = r % p.n_wt; r /= p.n_wt;
+                const int qc = r % p.n_qc; r /= p.n_qc;
+                const int po = r % p.Pout;
+                const int b = r / p.Pout;
+                const int q0 = qc * p.q_chunk, q1 = min(p.Qout, q0 + p.q_chunk);
+                const int nrows = (q1 - q0) + p.KQ - 1;
+                const int wc = p.base_w + wt * kTileW;
+                for (int s = 0; s < nrows; ++s, ++it) {
+                    const uint32_t idx = it % p.nstage, ph = (it / p.nstage) & 1;
+                    mbar_wait(&empty[idx], ph ^ 1);
+                    mbar_expect_tx(&full[idx], (uint32_t)p.KP * C8 * BW * 16);
+                    uint8_t *dst = stages + (size_t)idx * stage_bytes;
+                    const int qv = p.base_q + q0 + s;
+                    for (int kp = 0; kp < p.KP; ++kp) {
+                        const int pv = p.base_p + po + kp;
+                        const CUtensorMap *map = &xmap;
+                        int pc = pv, qcrd = qv;
+                        if (p.split == 0 && pv >= p.Pin && pv < p.Pin + p.halo) {
+                            map = &hmap;
+                            pc = pv - p.Pin;
+                        } else if (p.split == 1 && qv >= p.Qin && qv < p.Qin + p.halo) {
+                            map = &hmap;
+                            qcrd = qv - p.Qin;
+                        }
+                        for (int c8 = 0; c8 < C8; ++c8)
+                            tma_load_5d(dst + (size_t)(kp * C8 + c8) * p.plane, map, &full[idx],
+                                        c8 * 8, wc, qcrd, pc, b);
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ===================== MMA issuer =====================
+        if (lane == 0) {
+            const uint32_t idesc_one = idesc_bf16(128, N);
+            const uint32_t idesc_all = idesc_bf16(128, N * p.KQ);
+            const uint32_t blk = (uint32_t)p.KQ * N * 32;   // bytes per (kp,kw,kc) B block
+            const uint64_t bdesc0 = sdesc(smem_u32(wsm), 128, 256);
+            const uint64_t adesc0 = sdesc(smem_u32(stages), p.plane, 128);
+            uint32_t it = 0, row_base = 0;
+            for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
+                int r = u / p.n_wt;
+                const int qc = r % p.n_qc;
+                const int q0 = qc * p.q_chunk, q1 = min(p.Qout, q0 + p.q_chunk);
+                const int nq = q1 - q0;
+                const int nrows = nq + p.KQ - 1;
+                for (int s = 0; s < nrows; ++s, ++it) {
+                    const uint32_t idx = it % p.nstage, ph = (it / p.nstage) & 1;
+                    if (s < nq) {
+                        // row s starts here: its slot must have been drained + zeroed
+                        const uint32_t row = row_base + s;
+                        mbar_wait(&tempty[row % NSLOT], ((row / NSLOT) & 1) ^ 1);
+                    }
+                    mbar_wait(&full[idx], ph);
+                    tc_fence_after();
+                    const uint64_t adesc = adesc0 + ((idx * stage_bytes) >> 4);
+                    const uint32_t top = row_base + s;  // row fed through kq = 0
+                    const bool merged = s >= p.KQ - 1 && s < nq &&
+                                        (int)(top % NSLOT) >= p.KQ - 1;
+                    if (merged) {
+                        const uint32_t d = tmem + (NSLOT - 1 - top % NSLOT) * N;
+                        for (int kp = 0; kp < p.KP; ++kp)
+                            for (int kw = 0; kw < p.KW; ++kw)
+                                for (int kc = 0; kc < KC; ++kc) {
+                                    const uint32_t aoff = (kp * C8 + 2 * kc) * p.plane + kw * 16;
+                                    const uint32_t boff = ((kp * p.KW + kw) * KC + kc) * blk;
+                                    mma_bf16(d, adesc + (aoff >> 4), bdesc0 + (boff >> 4),
+                                             idesc_all, 1u);
+                                }
+                    } else {
+                        for (int kq = 0; kq < p.KQ; ++kq) {
+                            const int j = s - kq;
+                            if (j < 0 || j >= nq) continue;
+                            const uint32_t row = row_base + j;
+                            const uint32_t d = tmem + (NSLOT - 1 - row % NSLOT) * N;
+                            for (int kp = 0; kp < p.KP; ++kp)
+                                for (int kw = 0; kw < p.KW; ++kw)
+                                    for (int kc = 0; kc < KC; ++kc) {
+                                        const uint32_t aoff =
+                                            (kp * C8 + 2 * kc) * p.plane + kw * 16;
+                                        const uint32_t boff =
+                                            ((kp * p.KW + kw) * KC + kc) * blk + kq * (N / 8) * 256;
+                                        mma_bf16(d, adesc + (aoff >> 4), bdesc0 + (boff >> 4),
+                                                 idesc_one, 1u);
+                                    }
+                        }
+                    }
+                    mma_commit(&empty[idx]);
+                    const int jd = s - (p.KQ - 1);
+                    if (jd >= 0 && jd < nq) mma_commit(&tfull[(row_base + jd) % NSLOT]);
+                }
+                row_base += nq;
+            }
+        }
+    } else {
+        // ===================== epilogue =====================
+        const int quarter = warp & 3;
+        const int m = quarter * 32 + lane;  // TMEM lane = voxel within the tile
+        const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
+        uint32_t z[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) z[i] = 0u;
+        uint32_t row_base = 0;
+        for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
+            int r = u;
+            const int wt = r % p.n_wt; r /= p.n_wt;
+            const int qc = r % p.n_qc; r /= p.n_qc;
+            const int po = r % p.Pout;
+            const int b = r / p.Pout;
+            const int q0 = qc * p.q_chunk, q1 = min(p.Qout, q0 + p.q_chunk);
+            const int w = wt * kTileW + m;
+            for (int j = 0; j < q1 - q0; ++j) {
+                const uint32_t row = row_base + j, slot = row % NSLOT;
+                mbar_wait(&tfull[slot], (row / NSLOT) & 1);
+                tc_fence_after();
+                const uint32_t col = lane_base + (NSLOT - 1 - slot) * N;
+                uint32_t v[N];
+#pragma unroll
+                for (int c = 0; c < N; c += 16) {
+                    uint32_t t[16];
+                    tmem_ld16(col + c, t);
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) v[c + i] = t[i];
+                }
+                tmem_wait_ld();
+#pragma unroll
+                for (int c = 0; c < N; c += 16) tmem_st16(col + c, z);
+                tmem_wait_st();
+                tc_fence_before();
+                mbar_arrive(&tempty[slot]);
+                if (w < p.Wout) {
+                    const int qo = q0 + j;
+                    __nv_bfloat16 *dst;
+                    if (p.ysplit_dim == 0 && po >= p.ysplit)
+                        dst = p.y2 + b * p.y2s[0] + (int64_t)(po - p.ysplit) * p.y2s[1] +
+                              (int64_t)qo * p.y2s[2] + (int64_t)w * p.y2s[3];
+                    else if (p.ysplit_dim == 1 && qo >= p.ysplit)
+                        dst = p.y2 + b * p.y2s[0] + (int64_t)po * p.y2s[1] +
+                              (int64_t)(qo - p.ysplit) * p.y2s[2] + (int64_t)w * p.y2s[3];
+                    else
+                        dst = p.y + b * p.ys[0] + (int64_t)po * p.ys[1] + (int64_t)qo * p.ys[2] +
+                              (int64_t)w * p.ys[3];
+#pragma unroll
+                    for (int c = 0; c < N; c += 8) {
+                        uint4 pk;
+                        pk.x = pack_bf16(__uint_as_float(v[c + 0]), __uint_as_float(v[c + 1]));
+                        pk.y = pack_bf16(__uint_as_float(v[c + 2]), __uint_as_float(v[c + 3]));
+                        pk.z = pack_bf16(__uint_as_float(v[c + 4]), __uint_as_float(v[c + 5]));
+                        pk.w = pack_bf16(__uint_as_float(v[c + 6]), __uint_as_float(v[c + 7]));
+                        *reinterpret_cast<uint4 *>(dst + c) = pk;
+                    }
+                }
+            }
+            row_base += q1 - q0;
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        tc_fence_after();
+        tmem_dealloc(tmem, 512);
+    }
+}
+
+// Weight smem image.  One block per (kp, kw, 16-channel kc) with KQ*N rows
+// n = kq*N + c_out (the merged-tap MMA's B operand), UMMA K-major canonical:
+// [n/8 group][k half][8 rows][8 k] bf16 -> SBO 256 B, LBO 128 B.
+// flip=1 builds the dgrad weights W'[n=ci][k=co][t] = W[co][ci][taps-1-t].
+__global__ void conv_tc_weight_image(const __nv_bfloat16 *__restrict__ w,
+                                     __nv_bfloat16 *__restrict__ img, int n_rows, int k_cols,
+                                     int KP, int KQ, int KW, int flip) {
+    const int KC = k_cols / 16;
+    const int taps = KP * KQ * KW;
+    const int NB = KQ * n_rows;  // rows per block
+    const int total = KP * KW * KC * NB * 16;
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
+        int r = e;
+        const int kk = r % 8; r /= 8;
+        const int nn = r % 8; r /= 8;
+        const int h = r % 2; r /= 2;
+        const int g = r % (NB / 8); r /= (NB / 8);
+        const int kc = r % KC; r /= KC;
+        const int kw = r % KW;
+        const int kp = r / KW;
+        const int nrow = g * 8 + nn;
+        const int kq = nrow / n_rows, n = nrow % n_rows;
+        const int k = kc * 16 + h * 8 + kk;
+        const int t = (kp * KQ + kq) * KW + kw;
+        __nv_bfloat16 v;
+        if (!flip)
+            v = w[((int64_t)n * k_cols + k) * taps + t];                  // W[co=n][ci=k][t]
+        else
+            v = w[((int64_t)k * n_rows + n) * taps + (taps - 1 - t)];    // W[co=k][ci=n][T-1-t]
+        img[e] = v;
+    }
+}
+
+// Map a dp_conv_geom onto the (P, Q, W) roles.  Returns false if the
+// configuration is outside this kernel's envelope.
+struct Roles {
+    int nsp;
+    int Pin, Qin, Win, Pout, Qout, Wout;
+    int KP, KQ, KW;
+    int base_p, base_q, base_w;
+    int split;
+    int64_t xs[4], hs[4], ys[4];  // (b, p, q, w) element strides
+};
+
+bool map_roles(const dp_conv_geom *g, bool dgrad, Roles &R) {
+    if (g->nsp != 2 && g->nsp != 3) return false;
+    for (int i = 0; i < g->nsp; ++i)
+        if (g->stride[i] != 1) return false;
+    if (!(g->shard == -1 || g->shard == 0)) return false;
+    R.nsp = g->nsp;
+    // "input" of the kernel: x (fwd) or dy (dgrad); "output": y (fwd) or dx (dgrad)
+    const int64_t *in_ext = dgrad ? g->out_ext : g->in_ext;
+    const int64_t *out_ext = dgrad ? g->in_ext : g->out_ext;
+    const int64_t *is = dgrad ? g->ys : g->xs;
+    const int64_t *os = dgrad ? g->xs : g->ys;
+    int k[3] = {g->kernel[0], g->kernel[1], g->kernel[2]};
+    int64_t base[3];
+    for (int i = 0; i < 3; ++i)
+        base[i] = dgrad ? -(g->base[i] + k[i] - 1) : g->base[i];
+    int64_t oext[3] = {out_ext[0], out_ext[1], out_ext[2]};
+    if (dgrad && g->shard == 0) oext[0] += g->halo;  // virtual rows [0, in + halo)
+    if (g->nsp == 3) {
+        R.Pin = (int)in_ext[0]; R.Qin = (int)in_ext[1]; R.Win = (int)in_ext[2];
+        R.Pout = (int)oext[0]; R.Qout = (int)oext[1]; R.Wout = (int)oext[2];
+        R.KP = k[0]; R.KQ = k[1]; R.KW = k[2];
+        R.base_p = (int)base[0]; R.base_q = (int)base[1]; R.base_w = (int)base[2];
+        R.split = g->shard == 0 ? 0 : -1;
+        for (int i = 0; i < 4; ++i) {
+            int src = i == 0 ? 0 : i + 1;
+            R.xs[i] = is[src];
+            R.hs[i] = g->hs[src];
+            R.ys[i] = os[src];
+        }
+    } else {
+        R.Pin = 1; R.Qin = (int)in_ext[0]; R.Win = (int)in_ext[1];
+        R.Pout = 1; R.Qout = (int)oext[0]; R.Wout = (int)oext[1];
+        R.KP = 1; R.KQ = k[0]; R.KW = k[1];
+        R.base_p = 0; R.base_q = (int)base[0]; R.base_w = (int)base[1];
+        R.split = g->shard == 0 ? 1 : -1;
+        R.xs[0] = is[0]; R.xs[1] = is[0]; R.xs[2] = is[2]; R.xs[3] = is[3];
+        R.hs[0] = g->hs[0]; R.hs[1] = g->hs[0]; R.hs[2] = g->hs[2]; R.hs[3] = g->hs[3];
+        R.ys[0] = os[0]; R.ys[1] = os[0]; R.ys[2] = os[2]; R.ys[3] = os[3];
+    }
+    return true;
+}
+
+int pick_n(int n) { return (n == 16 || n == 32 || n == 48 || n == 64 || n == 128) ? n : 0; }
+
+struct Plan {
+    Roles R;
+    int Cin, N;           // K channels, N channels of this conv
+    int plane, stage_bytes, wimg_bytes, nstage, smem;
+};
+
+bool make_plan(const dp_conv_geom *g, bool dgrad, Plan &pl) {
+    if (!map_roles(g, dgrad, pl.R)) return false;
+    pl.Cin = (int)(dgrad ? g->c_out : g->c_in);
+    pl.N = pick_n((int)(dgrad ? g->c_in : g->c_out));
+    if (!pl.N || pl.Cin % 16 || pl.Cin > 128) return false;
+    const Roles &R = pl.R;
+    if (R.KW > 15 || R.KQ > 7 || R.KP > 7) return false;
+    if (R.KQ * pl.N > 256) return false;                 // merged-tap MMA: N <= 256
+    if (R.KQ + 2 > ((512 / pl.N) < 16 ? (512 / pl.N) : 16)) return false;  // TMEM ring
+    // channel stride 1 on input and output, 16-B aligned row strides
+    const int64_t *is = dgrad ? g->ys : g->xs;
+    const int64_t *os = dgrad ? g->xs : g->ys;
+    if (is[1] != 1 || os[1] != 1) return false;
+    if (g->halo > 0 && g->hs[1] != 1) return false;
+    for (int i = 0; i < 4; ++i) {
+        if (R.xs[i] % 8 || R.ys[i] % 8) return false;
+        if (g->halo > 0 && R.hs[i] % 8) return false;
+    }
+    const int BW = kTileW + R.KW - 1;
+    pl.plane = ((BW * 16 + 127) / 128) * 128;
+    pl.stage_bytes = R.KP * (pl.Cin / 8) * pl.plane;
+    pl.wimg_bytes = R.KP * R.KQ * R.KW * pl.Cin * pl.N * 2;
+    const int budget = 220 * 1024;
+    const int fixed = ((pl.wimg_bytes + 1023) & ~1023) + 1024;
+    int ns = (budget - fixed) / pl.stage_bytes;
+    if (ns > 8) ns = 8;
+    if (ns < 2) return false;
+    pl.nstage = ns;
+    pl.smem = fixed + ns * pl.stage_bytes;
+    return true;
+}
+
+template <int N>
+int launch_n(const CUtensorMap &xm, const CUtensorMap &hm, const ConvTcParams &p, int grid,
+             int smem, cudaStream_t st) {
+    auto kern = conv_tc_kernel<N>;
+    DP_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    kern<<<grid, kThreads, smem, st>>>(xm, hm, p);
+    return launch_status("conv_tc_kernel");
+}
+
+int run_conv_tc(const dp_conv_geom *g, bool dgrad, const void *in, const void *in_halo,
+                const void *w, void *out, void *out2, void *ws, int64_t ws_bytes,
+                cudaStream_t st) {
+    Plan pl;
+    DP_REQUIRE(make_plan(g, dgrad, pl), DP_ERR_UNSUPPORTED, "conv_tc: outside the envelope");
+    const Roles &R = pl.R;
+    const int taps = R.KP * R.KQ * R.KW;
+    DP_REQUIRE(ws_bytes >= pl.wimg_bytes, DP_ERR_INVALID, "conv_tc: workspace too small");
+    int64_t outs = (int64_t)g->batch * R.Pout * R.Qout * R.Wout;
+    if (outs == 0) return DP_OK;
+    // weight image
+    {
+        int total = taps * pl.Cin * pl.N;
+        conv_tc_weight_image<<<grid_for(total, 256, 2), 256, 0, st>>>(
+            (const __nv_bfloat16 *)w, (__nv_bfloat16 *)ws, pl.N, pl.Cin, R.KP, R.KQ, R.KW,
+            dgrad ? 1 : 0);
+        int rc = launch_status("conv_tc_weight_image");
+        if (rc) return rc;
+    }
+    // tensor maps: dims {C, W, Q, P, B}
+    const int BW = kTileW + R.KW - 1;
+    uint32_t box[5] = {8, (uint32_t)BW, 1, 1, 1};
+    CUtensorMap xm, hm;
+    {
+        uint64_t dims[5] = {(uint64_t)pl.Cin, (uint64_t)R.Win, (uint64_t)R.Qin, (uint64_t)R.Pin,
+                            (uint64_t)g->batch};
+        uint64_t strides[4] = {(uint64_t)R.xs[3] * 2, (uint64_t)R.xs[2] * 2,
+                               (uint64_t)R.xs[1] * 2, (uint64_t)R.xs[0] * 2};
+        int rc = encode_tensor_map(&xm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void *>(in),
+                                   dims, strides, box);
+        if (rc) return rc;
+    }
+    hm = xm;
+    if (!dgrad && g->halo > 0) {
+        uint64_t dims[5] = {(uint64_t)pl.Cin, (uint64_t)R.Win,
+                            (uint64_t)(R.split == 1 ? g->halo : R.Qin),
+                            (uint64_t)(R.split == 0 ? g->halo : R.Pin), (uint64_t)g->batch};
+        uint64_t strides[4] = {(uint64_t)R.hs[3] * 2, (uint64_t)R.hs[2] * 2,
+                               (uint64_t)R.hs[1] * 2, (uint64_t)R.hs[0] * 2};
+        int rc = encode_tensor_map(&hm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5,
+                                   const_cast<void *>(in_halo), dims, strides, box);
+        if (rc) return rc;
+    }
+    ConvTcParams p;
+    memset(&p, 0, sizeof(p));
+    p.B = (int)g->batch;
+    p.Cin = pl.Cin;
+    p.Cout = pl.N;
+    p.Pin = R.Pin; p.Qin = R.Qin; p.Win = R.Win;
+    p.Pout = R.Pout; p.Qout = R.Qout; p.Wout = R.Wout;
+    p.KP = R.KP; p.KQ = R.KQ; p.KW = R.KW;
+    p.base_p = R.base_p; p.base_q = R.base_q; p.base_w = R.base_w;
+    p.split = dgrad ? -1 : (g->halo > 0 ? R.split : -1);
+    p.halo = dgrad ? 0 : (int)g->halo;
+    p.y = (__nv_bfloat16 *)out;
+    p.y2 = (__nv_bfloat16 *)(out2 ? out2 : out);
+    for (int i = 0; i < 4; ++i) {
+        p.ys[i] = R.ys[i];
+        p.y2s[i] = R.hs[i];
+    }
+    p.ysplit_dim = -1;
+    p.ysplit = 0;
+    if (dgrad && g->halo > 0 && g->shard == 0) {
+        p.ysplit_dim = R.split;                       // rows >= main extent -> dx_halo
+        p.ysplit = R.split == 0 ? (int)g->in_ext[0] : (int)g->in_ext[0];
+    }
+    p.n_wt = (R.Wout + kTileW - 1) / kTileW;
+    // choose the Q chunk so the unit count balances well over the SMs
+    const int sms = sm_count();
+    const int64_t cols = (int64_t)p.B * R.Pout * p.n_wt;
+    int best_chunk = R.Qout;
+    double best = -1;
+    for (int nq = 1; nq <= R.Qout && nq <= 64; ++nq) {
+        int chunk = (R.Qout + nq - 1) / nq;
+        int nqc = (R.Qout + chunk - 1) / chunk;
+        int64_t units = cols * nqc;
+        int64_t waves = (units + sms - 1) / sms;
+        double balance = (double)units / (double)(waves * sms);
+        double overhead = (double)(chunk + R.KQ - 1) / chunk;
+        double score = balance / overhead;
+        if (score > best + 1e-9) {
+            best = score;
+            best_chunk = chunk;
+        }
+    }
+    p.q_chunk = best_chunk;
+    p.n_qc = (R.Qout + best_chunk - 1) / best_chunk;
+    p.n_units = (int)(cols * p.n_qc);
+    p.nstage = pl.nstage;
+    p.plane = pl.plane;
+    p.wimg_bytes = pl.wimg_bytes;
+    p.wimg = (const __nv_bfloat16 *)ws;
+    int grid = p.n_units < sms ? p.n_units : sms;
+    switch (pl.N) {
+        case 16: return launch_n<16>(xm, hm, p, grid, pl.smem, st);
+        case 32: return launch_n<32>(xm, hm, p, grid, pl.smem, st);
+        case 48: return launch_n<48>(xm, hm, p, grid, pl.smem, st);
+        case 64: return launch_n<64>(xm, hm, p, grid, pl.smem, st);
+        default: return launch_n<128>(xm, hm, p, grid, pl.smem, st);
+    }
+}
+
+
+// ---------------------------------------------------------------------------
+// Weight gradient:
+//   dW[co][ci][kp][kq][kw] = sum_{b,po,qo,wo} dY[b,po,qo,wo,co] *
+//                            X_virtual[b, base_p+po+kp, base_q+qo+kq, base_w+wo+kw, ci]
+// Substituting w' = wo + kw: dW[..kw] = sum_w' X[base_w + w'] * dY[w' - kw].
+// One unit = one output row (b, po, qo) x a 128-wide w' tile.  Per unit the
+// stage holds (i) the KP*KQ input rows as 8-channel planes in (kp,kq,c8)
+// order and (ii) KW copies of the dY row, each TMA-loaded at w' - kw (zero
+// outside [0, Wout)), as planes in (kw, c8) order.  Then
+//   D[M = (kp,kq,ci)][N = (kw,co)] += A[M][K = w'] . B[K = w'][N]
+// with both operands MN-major straight out of the planes: ONE
+// tcgen05.mma (N = KW*C_out) per 16 voxels per 128-row M tile.  M is tiled
+// by 16 planes; a partial last tile computes garbage rows that are never
+// stored.  Every CTA accumulates all its units in TMEM; the partials
+// [cta][row][kw*co] go to the workspace and a deterministic reduction sums
+// them into dW.
+struct WgradTcParams {
+    int B, Cin, N;
+    int Pin, Qin, Win, Pout, Qout, Wout;
+    int KP, KQ, KW;
+    int base_p, base_q, base_w;
+    int split, halo;
+    int n_wt, n_units, n_mt, rows;   // rows = KP*KQ*Cin
+    int nstage, xplanes;
+    float *partial;                  // [grid][n_mt*128][KW*N]
+};
+
+constexpr int kPlane = kTileW * 16;  // 128 voxels x 8 channels x bf16
+
+template <int N>
+__global__ void __launch_bounds__(kThreads, 1)
+conv_wgrad_tc_kernel(const __grid_constant__ CUtensorMap xmap,
+                     const __grid_constant__ CUtensorMap hmap,
+                     const __grid_constant__ CUtensorMap dmap, const WgradTcParams p) {
+    using namespace tc;
+    extern __shared__ __align__(1024) uint8_t smem[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int C8 = p.Cin / 8;
+    const int NT = p.KW * N;  // MMA N
+    const uint32_t xbytes = (uint32_t)p.xplanes * kPlane;
+    const uint32_t stage_bytes = xbytes + (uint32_t)p.KW * (N / 8) * kPlane;
+    // garbage rows of a partial last M tile may read past the last stage
+    const int over = (p.n_mt * 16 - p.xplanes) * kPlane - p.KW * (N / 8) * kPlane;
+    const uint32_t tail = over > 0 ? (uint32_t)over : 0u;
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + (size_t)p.nstage * stage_bytes + tail);
+    uint64_t *full = bars, *empty = bars + p.nstage, *done = empty + p.nstage;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(done + 1);
+    uint32_t ncols = 32;
+    while (ncols < (uint32_t)(p.n_mt * NT)) ncols <<= 1;
+    if (warp == 0) {
+        if (lane == 0) {
+            for (int i = 0; i < p.nstage; ++i) {
+                mbar_init(&full[i], 1);
+                mbar_init(&empty[i], 1);
+            }
+            mbar_init(done, 1);
+            mbar_fence_init();
+            tma_prefetch(&xmap);
+            tma_prefetch(&hmap);
+            tma_prefetch(&dmap);
+        }
+        __syncwarp();
+        tmem_alloc(tmem_slot, ncols);
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            uint32_t it = 0;
+            for (int u = blockIdx.x; u < p.n_units; u += gridDim.x, ++it) {
+                int r = u;
+                const int wt = r % p.n_wt; r /= p.n_wt;
+                const int qo = r % p.Qout; r /= p.Qout;
+                const int po = r % p.Pout;
+                const int b = r / p.Pout;
+                const uint32_t idx = it % p.nstage, ph = (it / p.nstage) & 1;
+                mbar_wait(&empty[idx], ph ^ 1);
+                mbar_expect_tx(&full[idx], stage_bytes);
+                uint8_t *dst = smem + (size_t)idx * stage_bytes;
+                const int w0 = wt * kTileW;
+                for (int kp = 0; kp < p.KP; ++kp) {
+                    const int pv = p.base_p + po + kp;
+                    for (int kq = 0; kq < p.KQ; ++kq) {
+                        const int qv = p.base_q + qo + kq;
+                        const CUtensorMap *map = &xmap;
+                        int pc = pv, qc = qv;
+                        if (p.split == 0 && pv >= p.Pin && pv < p.Pin + p.halo) {
+                            map = &hmap;
+                            pc = pv - p.Pin;
+                        } else if (p.split == 1 && qv >= p.Qin && qv < p.Qin + p.halo) {
+                            map = &hmap;
+                            qc = qv - p.Qin;
+                        }
+                        for (int c8 = 0; c8 < C8; ++c8)
+                            tma_load_5d(dst + (size_t)((kp * p.KQ + kq) * C8 + c8) * kPlane, map,
+                                        &full[idx], c8 * 8, p.base_w + w0, qc, pc, b);
+                    }
+                }
+                for (int kw = 0; kw < p.KW; ++kw)
+                    for (int c8 = 0; c8 < N / 8; ++c8)
+                        tma_load_5d(dst + xbytes + (size_t)(kw * (N / 8) + c8) * kPlane, &dmap,
+                                    &full[idx], c8 * 8, w0 - kw, qo, po, b);
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            const uint32_t idesc = idesc_bf16(128, NT, 1, 1);
+            const uint64_t a0 = sdesc(smem_u32(smem), 128, kPlane);
+            const uint64_t b0 = sdesc(smem_u32(smem) + xbytes, 128, kPlane);
+            uint32_t it = 0;
+            for (int u = blockIdx.x; u < p.n_units; u += gridDim.x, ++it) {
+                const uint32_t idx = it % p.nstage, ph = (it / p.nstage) & 1;
+                mbar_wait(&full[idx], ph);
+                tc_fence_after();
+                const uint32_t so = (idx * stage_bytes) >> 4;
+                for (int mt = 0; mt < p.n_mt; ++mt)
+                    for (int ks = 0; ks < kTileW / 16; ++ks)
+                        mma_bf16(tmem + mt * NT, a0 + so + ((mt * 16 * kPlane + ks * 256) >> 4),
+                                 b0 + so + ((ks * 256) >> 4), idesc, (it | ks) != 0 ? 1u : 0u);
+                mma_commit(&empty[idx]);
+            }
+            mma_commit(done);
+        }
+    } else {
+        const int quarter = warp & 3;
+        const int m = quarter * 32 + lane;
+        mbar_wait(done, 0);
+        tc_fence_after();
+        for (int mt = 0; mt < p.n_mt; ++mt) {
+            float *dst = p.partial + ((size_t)blockIdx.x * p.n_mt * 128 + mt * 128 + m) * NT;
+            for (int c = 0; c < NT; c += 16) {
+                uint32_t t[16];
+                tmem_ld16(tmem + ((uint32_t)(quarter * 32) << 16) + mt * NT + c, t);
+                tmem_wait_ld();
+#pragma unroll
+                for (int i = 0; i < 16; i += 4)
+                    *reinterpret_cast<float4 *>(dst + c + i) =
+                        make_float4(__uint_as_float(t[i]), __uint_as_float(t[i + 1]),
+                                    __uint_as_float(t[i + 2]), __uint_as_float(t[i + 3]));
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        tc_fence_after();
+        tmem_dealloc(tmem, ncols);
+    }
+}
+
+// dw[co][ci][kp][kq][kw] = sum_cta partial[cta][row(kp,kq,ci)][kw*N + co]
+__global__ void wgrad_tc_reduce(const float *__restrict__ part, float *__restrict__ dw, int ctas,
+                                int rows_pad, int KP, int KQ, int KW, int Cin, int N) {
+    const int taps = KP * KQ * KW;
+    const int total = N * Cin * taps;
+    const int NT = KW * N;
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
+        int r = e;
+        const int kw = r % KW; r /= KW;
+        const int kq = r % KQ; r /= KQ;
+        const int kp = r % KP; r /= KP;
+        const int ci = r % Cin;
+        const int co = r / Cin;
+        const int row = (kp * KQ + kq) * Cin + ci;  // plane (kp,kq,ci/8) * 8 + ci%8
+        float s = 0.f;
+        for (int c = 0; c < ctas; ++c) s += part[((size_t)c * rows_pad + row) * NT + kw * N + co];
+        dw[e] = s;
+    }
+}
+
+struct WPlan {
+    Roles R;
+    int Cin, N, n_mt, rows, xplanes, stage_bytes, nstage, smem, grid;
+    int64_t n_units;
+};
+
+bool make_wplan(const dp_conv_geom *g, WPlan &pl) {
+    if (!map_roles(g, false, pl.R)) return false;
+    const Roles &R = pl.R;
+    pl.Cin = (int)g->c_in;
+    pl.N = pick_n((int)g->c_out);
+    if (!pl.N || pl.Cin % 8) return false;
+    if (R.KW * pl.N > 256) return false;
+    if (g->xs[1] != 1 || g->ys[1] != 1) return false;
+    if (g->halo > 0 && g->hs[1] != 1) return false;
+    for (int i = 0; i < 4; ++i) {
+        if (R.xs[i] % 8 || R.ys[i] % 8) return false;
+        if (g->halo > 0 && R.hs[i] % 8) return false;
+    }
+    pl.xplanes = R.KP * R.KQ * (pl.Cin / 8);
+    pl.rows = pl.xplanes * 8;
+    pl.n_mt = (pl.xplanes + 15) / 16;
+    if (pl.n_mt * R.KW * pl.N > 512) return false;
+    pl.stage_bytes = pl.xplanes * kPlane + R.KW * (pl.N / 8) * kPlane;
+    const int over = (pl.n_mt * 16 - pl.xplanes) * kPlane - R.KW * (pl.N / 8) * kPlane;
+    const int tail = over > 0 ? over : 0;
+    const int budget = 220 * 1024;
+    int ns = (budget - tail - 256) / pl.stage_bytes;
+    if (ns > 6) ns = 6;
+    if (ns < 2) return false;
+    pl.nstage = ns;
+    pl.smem = ns * pl.stage_bytes + tail + 256;
+    pl.n_units = (int64_t)g->batch * R.Pout * R.Qout * ((R.Wout + R.KW - 1 + kTileW - 1) / kTileW);
+    pl.grid = (int)(pl.n_units < sm_count() ? pl.n_units : sm_count());
+    if (pl.grid < 1) pl.grid = 1;
+    return true;
+}
+
+template <int N>
+int launch_wgrad_n(const CUtensorMap &xm, const CUtensorMap &hm, const CUtensorMap &dm,
+                   const WgradTcParams &p, int grid, int smem, cudaStream_t st) {
+    auto kern = conv_wgrad_tc_kernel<N>;
+    DP_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    kern<<<grid, kThreads, smem, st>>>(xm, hm, dm, p);
+    return launch_status("conv_wgrad_tc_kernel");
+}
+
+int run_wgrad_tc(const dp_conv_geom *g, const void *x, const void *xh, const void *dy, float *dw,
+                 void *ws, int64_t ws_bytes, cudaStream_t st) {
+    WPlan pl;
+    DP_REQUIRE(make_wplan(g, pl), DP_ERR_UNSUPPORTED, "conv_wgrad_tc: outside the envelope");
+    const Roles &R = pl.R;
+    const int64_t need = (int64_t)pl.grid * pl.n_mt * 128 * R.KW * pl.N * 4;
+    DP_REQUIRE(ws_bytes >= need, DP_ERR_INVALID, "conv_wgrad_tc: workspace too small");
+    (void)need;
+    const int taps = R.KP * R.KQ * R.KW;
+    if (pl.n_units == 0) {
+        DP_CUDA_CHECK(cudaMemsetAsync(dw, 0, (size_t)pl.N * pl.Cin * taps * 4, st));
+        return DP_OK;
+    }
+    uint32_t box[5] = {8, (uint32_t)kTileW, 1, 1, 1};
+    CUtensorMap xm, hm, dm;
+    {
+        uint64_t dims[5] = {(uint64_t)pl.Cin, (uint64_t)R.Win, (uint64_t)R.Qin, (uint64_t)R.Pin,
+                            (uint64_t)g->batch};
+        uint64_t strides[4] = {(uint64_t)R.xs[3] * 2, (uint64_t)R.xs[2] * 2,
+                               (uint64_t)R.xs[1] * 2, (uint64_t)R.xs[0] * 2};
+        int rc = encode_tensor_map(&xm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void *>(x),
+                                   dims, strides, box);
+        if (rc) return rc;
+    }
+    hm = xm;
+    if (g->halo > 0) {
+        uint64_t dims[5] = {(uint64_t)pl.Cin, (uint64_t)R.Win,
+                            (uint64_t)(R.split == 1 ? g->halo : R.Qin),
+                            (uint64_t)(R.split == 0 ? g->halo : R.Pin), (uint64_t)g->batch};
+        uint64_t strides[4] = {(uint64_t)R.hs[3] * 2, (uint64_t)R.hs[2] * 2,
+                               (uint64_t)R.hs[1] * 2, (uint64_t)R.hs[0] * 2};
+        int rc = encode_tensor_map(&hm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5,
+                                   const_cast<void *>(xh), dims, strides, box);
+        if (rc) return rc;
+    }
+    {
+        uint64_t dims[5] = {(uint64_t)pl.N, (uint64_t)R.Wout, (uint64_t)R.Qout, (uint64_t)R.Pout,
+                            (uint64_t)g->batch};
+        uint64_t strides[4] = {(uint64_t)R.ys[3] * 2, (uint64_t)R.ys[2] * 2,
+                               (uint64_t)R.ys[1] * 2, (uint64_t)R.ys[0] * 2};
+        uint32_t dbox[5] = {8, (uint32_t)kTileW, 1, 1, 1};
+        int rc = encode_tensor_map(&dm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void *>(dy),
+                                   dims, strides, dbox);
+        if (rc) return rc;
+    }
+    WgradTcParams p;
+    memset(&p, 0, sizeof(p));
+    p.B = (int)g->batch; p.Cin = pl.Cin; p.N = pl.N;
+    p.Pin = R.Pin; p.Qin = R.Qin; p.Win = R.Win;
+    p.Pout = R.Pout; p.Qout = R.Qout; p.Wout = R.Wout;
+    p.KP = R.KP; p.KQ = R.KQ; p.KW = R.KW;
+    p.base_p = R.base_p; p.base_q = R.base_q; p.base_w = R.base_w;
+    p.split = g->halo > 0 ? R.split : -1;
+    p.halo = (int)g->halo;
+    p.n_wt = (R.Wout + R.KW - 1 + kTileW - 1) / kTileW;
+    p.n_units = (int)pl.n_units;
+    p.n_mt = pl.n_mt; p.rows = pl.rows;
+    p.nstage = pl.nstage; p.xplanes = pl.xplanes;
+    p.partial = (float *)ws;
+    int rc;
+    switch (pl.N) {
+        case 16: rc = launch_wgrad_n<16>(xm, hm, dm, p, pl.grid, pl.smem, st); break;
+        case 32: rc = launch_wgrad_n<32>(xm, hm, dm, p, pl.grid, pl.smem, st); break;
+        case 48: rc = launch_wgrad_n<48>(xm, hm, dm, p, pl.grid, pl.smem, st); break;
+        default: rc = launch_wgrad_n<64>(xm, hm, dm, p, pl.grid, pl.smem, st); break;
+    }
+    if (rc) return rc;
+    const int total = pl.N * pl.Cin * taps;
+    wgrad_tc_reduce<<<grid_for(total, 256, 4), 256, 0, st>>>((const float *)ws, dw, pl.grid,
+                                                             pl.n_mt * 128, R.KP, R.KQ, R.KW,
+                                                             pl.Cin, pl.N);
+    return launch_status("wgrad_tc_reduce");
+}
+
+}  // namespace
+
+int encode_tensor_map(CUtensorMap *map, CUtensorMapDataType dtype, int rank, void *base,
+                      const uint64_t *dims, const uint64_t *strides_bytes, const uint32_t *box) {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q;
+        void *ptr = nullptr;
+        DP_CUDA_CHECK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q));
+        DP_REQUIRE(ptr && q == cudaDriverEntryPointSuccess, DP_ERR_CUDA,
+                   "cuTensorMapEncodeTiled unavailable");
+        fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+    }
+    uint32_t estr[5] = {1, 1, 1, 1, 1};
+    CUresult r = fn(map, dtype, rank, base, dims, strides_bytes, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    DP_REQUIRE(r == CUDA_SUCCESS, DP_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    return DP_OK;
+}
+
+int conv_tc_eligible(const dp_conv_geom *g, int dtype, int which) {
+    if (dtype != DP_BF16 || !g) return 0;
+    if (which == DP_CONV_WGRAD) {
+        WPlan wp;
+        return make_wplan(g, wp) ? 1 : 0;
+    }
+    Plan pl;
+    return make_plan(g, which == DP_CONV_DGRAD, pl) ? 1 : 0;
+}
+
+int64_t conv_tc_workspace(const dp_conv_geom *g, int which) {
+    if (which == DP_CONV_WGRAD) {
+        WPlan wp;
+        if (!make_wplan(g, wp)) return -1;
+        return (int64_t)wp.grid * wp.n_mt * 128 * wp.R.KW * wp.N * 4;
+    }
+    Plan pl;
+    if (!make_plan(g, which == DP_CONV_DGRAD, pl)) return -1;
+    return pl.wimg_bytes;
+}
+
+int conv_fwd_tc_launch(const dp_conv_geom *g, const void *x, const void *xh, const void *w, void *y,
+                       void *ws, int64_t ws_bytes, cudaStream_t st) {
+    return run_conv_tc(g, false, x, xh, w, y, nullptr, ws, ws_bytes, st);
+}
+
+int conv_dgrad_tc_launch(const dp_conv_geom *g, const void *dy, const void *w, void *dx, void *dxh,
+                         void *ws, int64_t ws_bytes, cudaStream_t st) {
+    return run_conv_tc(g, true, dy, nullptr, w, dx, dxh, ws, ws_bytes, st);
+}
+
+int conv_wgrad_tc_launch(const dp_conv_geom *g, const void *x, const void *xh, const void *dy,
+                         void *dw, void *ws, int64_t ws_bytes, cudaStream_t st) {
+    return run_wgrad_tc(g, x, xh, dy, (float *)dw, ws, ws_bytes, st);
+}
+
+}  // namespace dp

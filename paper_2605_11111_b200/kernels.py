@@ -144,12 +144,22 @@ def conv_geom(x: torch.Tensor, x_halo, y_shape, y_strides, c_out: int, kernel, s
     return g
 
 
+def _workspace(g, code, which, device):
+    nbytes = _lib.load().dp_conv_workspace(ctypes.byref(g), code, _algo, which)
+    if nbytes < 0:
+        _lib.check(_lib.DP_ERR_UNSUPPORTED, "dp_conv_workspace")
+    ws = torch.empty(max(int(nbytes), 16), dtype=torch.uint8, device=device)
+    return ws, int(ws.numel())
+
+
 def conv_fwd(x, x_halo, w, y, *, kernel, stride, base, shard, halo_rows) -> None:
     require_device("conv_fwd", x, x_halo, w, y)
     g = conv_geom(x, x_halo, y.shape, y.stride(), w.shape[0], kernel, stride, base, shard,
                   halo_rows)
-    rc = _lib.load().dp_conv_fwd(ctypes.byref(g), dtype_code(x), _algo, _ptr(x), _ptr(x_halo),
-                                 _ptr(w), _ptr(y), _stream(x))
+    code = dtype_code(x)
+    ws, nb = _workspace(g, code, _lib.CONV_FWD, x.device)
+    rc = _lib.load().dp_conv_fwd(ctypes.byref(g), code, _algo, _ptr(x), _ptr(x_halo), _ptr(w),
+                                 _ptr(y), _ptr(ws), nb, _stream(x))
     _lib.check(rc, "dp_conv_fwd")
 
 
@@ -157,8 +167,10 @@ def conv_dgrad(dy, w, dx, dx_halo, *, kernel, stride, base, shard, halo_rows) ->
     require_device("conv_dgrad", dy, w, dx, dx_halo)
     g = conv_geom(dx, dx_halo, dy.shape, dy.stride(), w.shape[0], kernel, stride, base, shard,
                   halo_rows)
-    rc = _lib.load().dp_conv_dgrad(ctypes.byref(g), dtype_code(dy), _algo, _ptr(dy), _ptr(w),
-                                   _ptr(dx), _ptr(dx_halo), _stream(dy))
+    code = dtype_code(dy)
+    ws, nb = _workspace(g, code, _lib.CONV_DGRAD, dy.device)
+    rc = _lib.load().dp_conv_dgrad(ctypes.byref(g), code, _algo, _ptr(dy), _ptr(w), _ptr(dx),
+                                   _ptr(dx_halo), _ptr(ws), nb, _stream(dy))
     _lib.check(rc, "dp_conv_dgrad")
 
 
@@ -167,14 +179,10 @@ def conv_wgrad(x, x_halo, dy, dw, *, kernel, stride, base, shard, halo_rows) -> 
     require_device("conv_wgrad", x, x_halo, dy, dw)
     g = conv_geom(x, x_halo, dy.shape, dy.stride(), dw.shape[0], kernel, stride, base, shard,
                   halo_rows)
-    lib = _lib.load()
     code = dtype_code(x)
-    nbytes = lib.dp_conv_wgrad_workspace(ctypes.byref(g), code, _algo)
-    if nbytes < 0:
-        _lib.check(_lib.DP_ERR_UNSUPPORTED, "dp_conv_wgrad_workspace")
-    ws = torch.empty(max(int(nbytes), 16), dtype=torch.uint8, device=x.device)
-    rc = lib.dp_conv_wgrad(ctypes.byref(g), code, _algo, _ptr(x), _ptr(x_halo), _ptr(dy),
-                           _ptr(dw), _ptr(ws), int(ws.numel()), _stream(x))
+    ws, nb = _workspace(g, code, _lib.CONV_WGRAD, x.device)
+    rc = _lib.load().dp_conv_wgrad(ctypes.byref(g), code, _algo, _ptr(x), _ptr(x_halo),
+                                   _ptr(dy), _ptr(dw), _ptr(ws), nb, _stream(x))
     _lib.check(rc, "dp_conv_wgrad")
 
 

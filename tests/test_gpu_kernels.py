@@ -144,3 +144,70 @@ def test_attention_block_fold_vs_oracle(dtype, sq, sk, h, d):
                      to_np(v).astype(np.float64))
     tol = {torch.float64: 1e-12, torch.float32: 1e-5, torch.bfloat16: 1.5e-2}[dtype]
     assert rel_err(to_np(out), want) < tol
+
+
+TC_CASES = [
+    # nsp, batch, cin, cout, spatial, k, pad, halo_rows (sharded virtual block)
+    (3, 1, 16, 32, (5, 7, 200), 3, 1, 0),
+    (3, 1, 32, 32, (4, 9, 130), 3, 1, 2),
+    (3, 2, 16, 16, (3, 5, 64), 3, 1, 1),
+    (2, 1, 64, 64, (40, 300), 3, 1, 2),
+    (2, 1, 32, 48, (9, 129), 3, 1, 0),
+    (2, 1, 16, 32, (12, 70), 5, 2, 4),
+    (3, 1, 16, 48, (3, 4, 128), 3, 1, 0),
+]
+
+
+@pytest.mark.parametrize("case", TC_CASES)
+def test_conv_tc_fwd_dgrad_vs_oracle(case):
+    """tcgen05 path forced (DP_ALGO_TC): forward and dgrad over the virtual
+    block [main | halo | zeros] on the sharded (outermost spatial) dim."""
+    k = kernels()
+    nsp, batch, cin, cout, sp, ks, pad, hrows = case
+    rng = np.random.default_rng(sum(sp) + cin)
+    fmt = torch.channels_last_3d if nsp == 3 else torch.channels_last
+    full_sp = (sp[0] + hrows,) + sp[1:]
+    xfull = torch.tensor(rng.standard_normal((batch, cin) + full_sp)).to(torch.bfloat16)
+    w = torch.tensor(rng.standard_normal((cout, cin) + (ks,) * nsp) * 0.1).to(torch.bfloat16)
+    x = xfull[:, :, :sp[0]].to(DEV).contiguous(memory_format=fmt)
+    xh = xfull[:, :, sp[0]:].to(DEV).contiguous(memory_format=fmt) if hrows else None
+    # a rank at the global start: outputs cover [0, sp0 + hrows - ks + 1 + pad) on dim 0
+    g_lo = -pad
+    n0 = sp[0] + hrows - ks + 1 + pad
+    out_sp = (n0,) + tuple(e + 2 * pad - ks + 1 for e in sp[1:])
+    y = torch.empty((batch, cout) + out_sp, dtype=torch.bfloat16, device=DEV,
+                    memory_format=fmt)
+    prev = k.set_algo("tc")
+    try:
+        base = [g_lo] + [-pad] * (nsp - 1)
+        k.conv_fwd(x, xh, w.to(DEV).contiguous(), y, kernel=(ks,) * nsp, stride=(1,) * nsp,
+                   base=base, shard=0, halo_rows=hrows)
+        # oracle: global conv over [main | halo] padded, rows [0, n0)
+        xr = to_np(xfull).astype(np.float64)
+        wr = to_np(w).astype(np.float64)
+        big = np.pad(xr, [(0, 0), (0, 0), (pad, 0)] + [(pad, pad)] * (nsp - 1))
+        want = oconv.conv(big, wr, 1, (0,) + (0,) * (nsp - 1))[:, :, :n0]
+        assert rel_err(to_np(y), want) < 1e-2
+        # dgrad of this virtual conv
+        dy = torch.tensor(rng.standard_normal(tuple(y.shape))).to(torch.bfloat16)
+        dyd = dy.to(DEV).contiguous(memory_format=fmt)
+        dx = torch.empty(x.shape, dtype=torch.bfloat16, device=DEV, memory_format=fmt)
+        dxh = torch.empty(xh.shape, dtype=torch.bfloat16, device=DEV,
+                          memory_format=fmt) if hrows else None
+        k.conv_dgrad(dyd, w.to(DEV).contiguous(), dx, dxh, kernel=(ks,) * nsp,
+                     stride=(1,) * nsp, base=base, shard=0, halo_rows=hrows)
+        gx, _ = oconv.conv_grads(big[:, :, :n0 + ks - 1], wr, to_np(dy).astype(np.float64), 1, 0)
+        gx = gx[:, :, pad:]  # drop the virtual zero rows at the global start
+        gx = gx[(slice(None), slice(None), slice(None)) + tuple(slice(pad, pad + e) for e in sp[1:])]
+        got = to_np(dx)
+        if hrows:
+            got = np.concatenate([got, to_np(dxh)], axis=2)
+        assert rel_err(got, gx[:, :, :got.shape[2]]) < 1e-2
+        # wgrad of the same virtual conv (fp32 partial, no all-reduce here)
+        dw = torch.empty(w.shape, dtype=torch.float32, device=DEV)
+        k.conv_wgrad(x, xh, dyd, dw, kernel=(ks,) * nsp, stride=(1,) * nsp, base=base, shard=0,
+                     halo_rows=hrows)
+        _, gw = oconv.conv_grads(big[:, :, :n0 + ks - 1], wr, to_np(dy).astype(np.float64), 1, 0)
+        assert rel_err(to_np(dw), gw) < 1e-3
+    finally:
+        k.set_algo(prev)
