@@ -43,6 +43,23 @@ namespace {
 constexpr int kTileW = 128;
 constexpr int kThreads = 192;
 
+// Channel blocking of the activation operand: one TMA box per (input row,
+// channel block) = BW voxels x cblk channels, i.e. a single contiguous run
+// of BW * cblk * 2 bytes in a channels-last tensor, landed with the matching
+// hardware swizzle (32/64/128 B rows).  The UMMA A operand is that box read
+// K-major-swizzled; the kw taps are descriptor shifts of one row
+// (rowbytes) — the swizzle is a function of the absolute smem address, so a
+// shifted start reads the same bytes TMA wrote.
+__host__ __device__ constexpr int chan_block(int c) {
+    return c == 16 ? 16 : c == 32 ? 32 : (c % 64 == 0 ? 64 : 16);
+}
+__host__ __device__ constexpr uint32_t swz_layout(int cblk) {  // UMMA layout_type field
+    return cblk == 16 ? 6u : cblk == 32 ? 4u : 2u;            // SW32 / SW64 / SW128
+}
+__host__ __device__ constexpr int box_bytes(int cblk, int kw) {
+    return (((kTileW + kw - 1) * cblk * 2) + 1023) / 1024 * 1024;
+}
+
 struct ConvTcParams {
     int B, Cin, Cout;
     int Pin, Qin, Win;        // main-block input extents (P, Q, W roles)
@@ -55,22 +72,37 @@ struct ConvTcParams {
     int64_t ys[4], y2s[4];    // element strides (b, p, q, w); channel stride 1
     int ysplit_dim, ysplit;   // -1: none
     int n_wt, q_chunk, n_qc, n_units;
-    int nstage, plane;        // pipeline depth, bytes per chunk plane
+    int nstage;               // pipeline depth
     int wimg_bytes;
     const __nv_bfloat16 *wimg;
+    int dbg;                  // profiling ablations (DP_CONV_DBG): 1 no stores, 2 no MMA, 4 no TMA
 };
 
-template <int N>
+// Template arguments KP_/KQ_/KW_/CIN_ = 0 select the runtime-shaped kernel;
+// non-zero values give the fully unrolled MMA issue the hot shapes use (a
+// runtime-bounded loop costs ~180 issue cycles per MMA vs ~56 of operand
+// time for N=96 — measured, scripts/umma_probe2.cu).
+template <int N, int KP_, int KQ_, int KW_, int CIN_>
 __global__ void __launch_bounds__(kThreads, 1)
 conv_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap hmap,
                const ConvTcParams p) {
     using namespace tc;
     extern __shared__ __align__(1024) uint8_t smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int C8 = p.Cin / 8, KC = p.Cin / 16;
+    constexpr bool kStatic = KP_ > 0;
+    const int KP = kStatic ? KP_ : p.KP;
+    const int KQ = kStatic ? KQ_ : p.KQ;
+    const int KW = kStatic ? KW_ : p.KW;
+    const int CIN = kStatic ? CIN_ : p.Cin;
+    const int CBLK = chan_block(CIN);
+    const int NBLK = CIN / CBLK;
+    const int KPB = CBLK / 16;               // 16-channel MMA steps per block row
+    const int KC = CIN / 16;
+    const int ROWB = CBLK * 2;               // bytes per voxel row of a box
+    const int BOXB = box_bytes(CBLK, KW);
     constexpr int NSLOT = (512 / N) < 16 ? (512 / N) : 16;
-    const int BW = kTileW + p.KW - 1;
-    const uint32_t stage_bytes = (uint32_t)p.KP * C8 * p.plane;
+    const int BW = kTileW + KW - 1;
+    const uint32_t stage_bytes = (uint32_t)(KP * NBLK * BOXB);
 
     uint8_t *wsm = smem;
     uint8_t *stages = smem + ((p.wimg_bytes + 1023) & ~1023);
@@ -119,104 +151,113 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
     tc_fence_after();
 
     if (warp == 0) {
-        // ===================== TMA producer =====================
-        if (lane == 0) {
-            uint32_t it = 0;
-            for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
-                int r = u;
-                const int wt = r % p.n_wt; r /= p.n_wt;
-                const int qc = r % p.n_qc; r /= p.n_qc;
-                const int po = r % p.Pout;
-                const int b = r / p.Pout;
-                const int q0 = qc * p.q_chunk, q1 = min(p.Qout, q0 + p.q_chunk);
-                const int nrows = (q1 - q0) + p.KQ - 1;
-                const int wc = p.base_w + wt * kTileW;
-                for (int s = 0; s < nrows; ++s, ++it) {
-                    const uint32_t idx = it % p.nstage, ph = (it / p.nstage) & 1;
-                    mbar_wait(&empty[idx], ph ^ 1);
-                    mbar_expect_tx(&full[idx], (uint32_t)p.KP * C8 * BW * 16);
-                    uint8_t *dst = stages + (size_t)idx * stage_bytes;
-                    const int qv = p.base_q + q0 + s;
-                    for (int kp = 0; kp < p.KP; ++kp) {
-                        const int pv = p.base_p + po + kp;
-                        const CUtensorMap *map = &xmap;
-                        int pc = pv, qcrd = qv;
-                        if (p.split == 0 && pv >= p.Pin && pv < p.Pin + p.halo) {
-                            map = &hmap;
-                            pc = pv - p.Pin;
-                        } else if (p.split == 1 && qv >= p.Qin && qv < p.Qin + p.halo) {
-                            map = &hmap;
-                            qcrd = qv - p.Qin;
-                        }
-                        for (int c8 = 0; c8 < C8; ++c8)
-                            tma_load_5d(dst + (size_t)(kp * C8 + c8) * p.plane, map, &full[idx],
-                                        c8 * 8, wc, qcrd, pc, b);
+        // ===================== TMA producer (whole warp, elected issue) =====================
+        uint32_t it = 0;
+        for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
+            int r = u;
+            const int wt = r % p.n_wt; r /= p.n_wt;
+            const int qc = r % p.n_qc; r /= p.n_qc;
+            const int po = r % p.Pout;
+            const int b = r / p.Pout;
+            const int q0 = qc * p.q_chunk, q1 = min(p.Qout, q0 + p.q_chunk);
+            const int nrows = (q1 - q0) + KQ - 1;
+            const int wc = p.base_w + wt * kTileW;
+            for (int s = 0; s < nrows; ++s, ++it) {
+                const uint32_t idx = it % p.nstage, ph = (it / p.nstage) & 1;
+                mbar_wait(&empty[idx], ph ^ 1);
+                if (p.dbg & 4) {
+                    if (lane == 0) mbar_arrive(&full[idx]);
+                    __syncwarp();
+                    continue;
+                }
+                mbar_expect_tx_e(&full[idx], (uint32_t)(KP * NBLK * BW * ROWB));
+                uint8_t *dst = stages + (size_t)idx * stage_bytes;
+                const int qv = p.base_q + q0 + s;
+                for (int kp = 0; kp < KP; ++kp) {
+                    const int pv = p.base_p + po + kp;
+                    const CUtensorMap *map = &xmap;
+                    int pc = pv, qcrd = qv;
+                    if (p.split == 0 && pv >= p.Pin && pv < p.Pin + p.halo) {
+                        map = &hmap;
+                        pc = pv - p.Pin;
+                    } else if (p.split == 1 && qv >= p.Qin && qv < p.Qin + p.halo) {
+                        map = &hmap;
+                        qcrd = qv - p.Qin;
                     }
+                    for (int cb = 0; cb < NBLK; ++cb)
+                        tma_load_5d_e(dst + (size_t)(kp * NBLK + cb) * BOXB, map, &full[idx],
+                                      cb * CBLK, wc, qcrd, pc, b);
                 }
             }
         }
     } else if (warp == 1) {
-        // ===================== MMA issuer =====================
-        if (lane == 0) {
-            const uint32_t idesc_one = idesc_bf16(128, N);
-            const uint32_t idesc_all = idesc_bf16(128, N * p.KQ);
-            const uint32_t blk = (uint32_t)p.KQ * N * 32;   // bytes per (kp,kw,kc) B block
-            const uint64_t bdesc0 = sdesc(smem_u32(wsm), 128, 256);
-            const uint64_t adesc0 = sdesc(smem_u32(stages), p.plane, 128);
-            uint32_t it = 0, row_base = 0;
-            for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
-                int r = u / p.n_wt;
-                const int qc = r % p.n_qc;
-                const int q0 = qc * p.q_chunk, q1 = min(p.Qout, q0 + p.q_chunk);
-                const int nq = q1 - q0;
-                const int nrows = nq + p.KQ - 1;
-                for (int s = 0; s < nrows; ++s, ++it) {
-                    const uint32_t idx = it % p.nstage, ph = (it / p.nstage) & 1;
-                    if (s < nq) {
-                        // row s starts here: its slot must have been drained + zeroed
-                        const uint32_t row = row_base + s;
-                        mbar_wait(&tempty[row % NSLOT], ((row / NSLOT) & 1) ^ 1);
-                    }
-                    mbar_wait(&full[idx], ph);
-                    tc_fence_after();
-                    const uint64_t adesc = adesc0 + ((idx * stage_bytes) >> 4);
-                    const uint32_t top = row_base + s;  // row fed through kq = 0
-                    const bool merged = s >= p.KQ - 1 && s < nq &&
-                                        (int)(top % NSLOT) >= p.KQ - 1;
-                    if (merged) {
-                        const uint32_t d = tmem + (NSLOT - 1 - top % NSLOT) * N;
-                        for (int kp = 0; kp < p.KP; ++kp)
-                            for (int kw = 0; kw < p.KW; ++kw)
-                                for (int kc = 0; kc < KC; ++kc) {
-                                    const uint32_t aoff = (kp * C8 + 2 * kc) * p.plane + kw * 16;
-                                    const uint32_t boff = ((kp * p.KW + kw) * KC + kc) * blk;
-                                    mma_bf16(d, adesc + (aoff >> 4), bdesc0 + (boff >> 4),
-                                             idesc_all, 1u);
-                                }
-                    } else {
-                        for (int kq = 0; kq < p.KQ; ++kq) {
-                            const int j = s - kq;
-                            if (j < 0 || j >= nq) continue;
-                            const uint32_t row = row_base + j;
-                            const uint32_t d = tmem + (NSLOT - 1 - row % NSLOT) * N;
-                            for (int kp = 0; kp < p.KP; ++kp)
-                                for (int kw = 0; kw < p.KW; ++kw)
-                                    for (int kc = 0; kc < KC; ++kc) {
-                                        const uint32_t aoff =
-                                            (kp * C8 + 2 * kc) * p.plane + kw * 16;
-                                        const uint32_t boff =
-                                            ((kp * p.KW + kw) * KC + kc) * blk + kq * (N / 8) * 256;
-                                        mma_bf16(d, adesc + (aoff >> 4), bdesc0 + (boff >> 4),
-                                                 idesc_one, 1u);
-                                    }
-                        }
-                    }
-                    mma_commit(&empty[idx]);
-                    const int jd = s - (p.KQ - 1);
-                    if (jd >= 0 && jd < nq) mma_commit(&tfull[(row_base + jd) % NSLOT]);
+        // ===================== MMA issuer (whole warp, elected issue) =====================
+        const uint32_t idesc_one = idesc_bf16(128, N);
+        const uint32_t idesc_all = idesc_bf16(128, N * KQ);
+        const uint32_t blk = (uint32_t)KQ * N * 32;   // bytes per (kp,kw,kc) B block
+        const uint64_t bdesc0 = sdesc(smem_u32(wsm), 128, 256);
+        const uint64_t adesc0 = sdesc_sw(smem_u32(stages), 8 * ROWB, swz_layout(CBLK));
+        uint32_t it = 0, row_base = 0;
+        for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
+            int r = u / p.n_wt;
+            const int qc = r % p.n_qc;
+            const int q0 = qc * p.q_chunk, q1 = min(p.Qout, q0 + p.q_chunk);
+            const int nq = q1 - q0;
+            const int nrows = nq + KQ - 1;
+            for (int s = 0; s < nrows; ++s, ++it) {
+                const uint32_t idx = it % p.nstage, ph = (it / p.nstage) & 1;
+                if (s < nq) {
+                    // row s starts here: its slot must have been drained + zeroed
+                    const uint32_t row = row_base + s;
+                    mbar_wait(&tempty[row % NSLOT], ((row / NSLOT) & 1) ^ 1);
                 }
-                row_base += nq;
+                mbar_wait(&full[idx], ph);
+                tc_fence_after();
+                const uint64_t adesc = adesc0 + ((idx * stage_bytes) >> 4);
+                const uint32_t top = row_base + s;  // row fed through kq = 0
+                const bool merged = s >= KQ - 1 && s < nq && (int)(top % NSLOT) >= KQ - 1;
+                if (p.dbg & 2) {
+                } else if (merged) {
+                    const uint32_t d = tmem + (NSLOT - 1 - top % NSLOT) * N;
+#pragma unroll
+                    for (int kp = 0; kp < KP; ++kp)
+#pragma unroll
+                        for (int kw = 0; kw < KW; ++kw)
+#pragma unroll
+                            for (int kc = 0; kc < KC; ++kc) {
+                                const uint32_t aoff = (kp * NBLK + kc / KPB) * BOXB + kw * ROWB +
+                                                      (kc % KPB) * 32;
+                                const uint32_t boff = ((kp * KW + kw) * KC + kc) * blk;
+                                mma_bf16_e(d, adesc + (aoff >> 4), bdesc0 + (boff >> 4),
+                                           idesc_all, 1u);
+                            }
+                } else {
+#pragma unroll
+                    for (int kq = 0; kq < KQ; ++kq) {
+                        const int j = s - kq;
+                        if (j < 0 || j >= nq) continue;
+                        const uint32_t row = row_base + j;
+                        const uint32_t d = tmem + (NSLOT - 1 - row % NSLOT) * N;
+#pragma unroll
+                        for (int kp = 0; kp < KP; ++kp)
+#pragma unroll
+                            for (int kw = 0; kw < KW; ++kw)
+#pragma unroll
+                                for (int kc = 0; kc < KC; ++kc) {
+                                    const uint32_t aoff = (kp * NBLK + kc / KPB) * BOXB +
+                                                          kw * ROWB + (kc % KPB) * 32;
+                                    const uint32_t boff =
+                                        ((kp * KW + kw) * KC + kc) * blk + kq * (N / 8) * 256;
+                                    mma_bf16_e(d, adesc + (aoff >> 4), bdesc0 + (boff >> 4),
+                                               idesc_one, 1u);
+                                }
+                    }
+                }
+                mma_commit_e(&empty[idx]);
+                const int jd = s - (KQ - 1);
+                if (jd >= 0 && jd < nq) mma_commit_e(&tfull[(row_base + jd) % NSLOT]);
             }
+            row_base += nq;
         }
     } else {
         // ===================== epilogue =====================
@@ -254,7 +295,7 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
                 tmem_wait_st();
                 tc_fence_before();
                 mbar_arrive(&tempty[slot]);
-                if (w < p.Wout) {
+                if (w < p.Wout && !(p.dbg & 1)) {
                     const int qo = q0 + j;
                     __nv_bfloat16 *dst;
                     if (p.ysplit_dim == 0 && po >= p.ysplit)
@@ -379,7 +420,7 @@ int pick_n(int n) { return (n == 16 || n == 32 || n == 48 || n == 64 || n == 128
 struct Plan {
     Roles R;
     int Cin, N;           // K channels, N channels of this conv
-    int plane, stage_bytes, wimg_bytes, nstage, smem;
+    int cblk, stage_bytes, wimg_bytes, nstage, smem;
 };
 
 bool make_plan(const dp_conv_geom *g, bool dgrad, Plan &pl) {
@@ -400,9 +441,8 @@ bool make_plan(const dp_conv_geom *g, bool dgrad, Plan &pl) {
         if (R.xs[i] % 8 || R.ys[i] % 8) return false;
         if (g->halo > 0 && R.hs[i] % 8) return false;
     }
-    const int BW = kTileW + R.KW - 1;
-    pl.plane = ((BW * 16 + 127) / 128) * 128;
-    pl.stage_bytes = R.KP * (pl.Cin / 8) * pl.plane;
+    pl.cblk = chan_block(pl.Cin);
+    pl.stage_bytes = R.KP * (pl.Cin / pl.cblk) * box_bytes(pl.cblk, R.KW);
     pl.wimg_bytes = R.KP * R.KQ * R.KW * pl.Cin * pl.N * 2;
     const int budget = 220 * 1024;
     const int fixed = ((pl.wimg_bytes + 1023) & ~1023) + 1024;
@@ -414,13 +454,27 @@ bool make_plan(const dp_conv_geom *g, bool dgrad, Plan &pl) {
     return true;
 }
 
-template <int N>
-int launch_n(const CUtensorMap &xm, const CUtensorMap &hm, const ConvTcParams &p, int grid,
+template <int N, int KP, int KQ, int KW, int CIN>
+int launch_k(const CUtensorMap &xm, const CUtensorMap &hm, const ConvTcParams &p, int grid,
              int smem, cudaStream_t st) {
-    auto kern = conv_tc_kernel<N>;
+    auto kern = conv_tc_kernel<N, KP, KQ, KW, CIN>;
     DP_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     kern<<<grid, kThreads, smem, st>>>(xm, hm, p);
     return launch_status("conv_tc_kernel");
+}
+
+// Hot shapes get a fully unrolled instantiation; everything else in the
+// envelope runs the runtime-shaped kernel.
+template <int N>
+int launch_n(const CUtensorMap &xm, const CUtensorMap &hm, const ConvTcParams &p, int grid,
+             int smem, cudaStream_t st) {
+    const bool k333 = p.KP == 3 && p.KQ == 3 && p.KW == 3;
+    const bool k133 = p.KP == 1 && p.KQ == 3 && p.KW == 3;
+    if (k333 && p.Cin == 16) return launch_k<N, 3, 3, 3, 16>(xm, hm, p, grid, smem, st);
+    if (k333 && p.Cin == 32) return launch_k<N, 3, 3, 3, 32>(xm, hm, p, grid, smem, st);
+    if (k133 && p.Cin == 32) return launch_k<N, 1, 3, 3, 32>(xm, hm, p, grid, smem, st);
+    if (k133 && p.Cin == 64) return launch_k<N, 1, 3, 3, 64>(xm, hm, p, grid, smem, st);
+    return launch_k<N, 0, 0, 0, 0>(xm, hm, p, grid, smem, st);
 }
 
 int run_conv_tc(const dp_conv_geom *g, bool dgrad, const void *in, const void *in_halo,
@@ -442,9 +496,12 @@ int run_conv_tc(const dp_conv_geom *g, bool dgrad, const void *in, const void *i
         int rc = launch_status("conv_tc_weight_image");
         if (rc) return rc;
     }
-    // tensor maps: dims {C, W, Q, P, B}
+    // tensor maps: dims {C, W, Q, P, B}; box = one channel block x BW voxels
     const int BW = kTileW + R.KW - 1;
-    uint32_t box[5] = {8, (uint32_t)BW, 1, 1, 1};
+    uint32_t box[5] = {(uint32_t)pl.cblk, (uint32_t)BW, 1, 1, 1};
+    const CUtensorMapSwizzle swz = pl.cblk == 16 ? CU_TENSOR_MAP_SWIZZLE_32B
+                                   : pl.cblk == 32 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                                   : CU_TENSOR_MAP_SWIZZLE_128B;
     CUtensorMap xm, hm;
     {
         uint64_t dims[5] = {(uint64_t)pl.Cin, (uint64_t)R.Win, (uint64_t)R.Qin, (uint64_t)R.Pin,
@@ -452,7 +509,7 @@ int run_conv_tc(const dp_conv_geom *g, bool dgrad, const void *in, const void *i
         uint64_t strides[4] = {(uint64_t)R.xs[3] * 2, (uint64_t)R.xs[2] * 2,
                                (uint64_t)R.xs[1] * 2, (uint64_t)R.xs[0] * 2};
         int rc = encode_tensor_map(&xm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void *>(in),
-                                   dims, strides, box);
+                                   dims, strides, box, swz);
         if (rc) return rc;
     }
     hm = xm;
@@ -463,7 +520,7 @@ int run_conv_tc(const dp_conv_geom *g, bool dgrad, const void *in, const void *i
         uint64_t strides[4] = {(uint64_t)R.hs[3] * 2, (uint64_t)R.hs[2] * 2,
                                (uint64_t)R.hs[1] * 2, (uint64_t)R.hs[0] * 2};
         int rc = encode_tensor_map(&hm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5,
-                                   const_cast<void *>(in_halo), dims, strides, box);
+                                   const_cast<void *>(in_halo), dims, strides, box, swz);
         if (rc) return rc;
     }
     ConvTcParams p;
@@ -512,9 +569,16 @@ int run_conv_tc(const dp_conv_geom *g, bool dgrad, const void *in, const void *i
     p.n_qc = (R.Qout + best_chunk - 1) / best_chunk;
     p.n_units = (int)(cols * p.n_qc);
     p.nstage = pl.nstage;
-    p.plane = pl.plane;
     p.wimg_bytes = pl.wimg_bytes;
     p.wimg = (const __nv_bfloat16 *)ws;
+    {
+        static int dbg = -1;
+        if (dbg < 0) {
+            const char *e = getenv("DP_CONV_DBG");
+            dbg = e ? atoi(e) : 0;
+        }
+        p.dbg = dbg;
+    }
     int grid = p.n_units < sms ? p.n_units : sms;
     switch (pl.N) {
         case 16: return launch_n<16>(xm, hm, p, grid, pl.smem, st);
@@ -596,7 +660,7 @@ conv_wgrad_tc_kernel(const __grid_constant__ CUtensorMap xmap,
     const uint32_t tmem = *tmem_slot;
 
     if (warp == 0) {
-        if (lane == 0) {
+        {
             uint32_t it = 0;
             for (int u = blockIdx.x; u < p.n_units; u += gridDim.x, ++it) {
                 int r = u;
@@ -606,7 +670,7 @@ conv_wgrad_tc_kernel(const __grid_constant__ CUtensorMap xmap,
                 const int b = r / p.Pout;
                 const uint32_t idx = it % p.nstage, ph = (it / p.nstage) & 1;
                 mbar_wait(&empty[idx], ph ^ 1);
-                mbar_expect_tx(&full[idx], stage_bytes);
+                mbar_expect_tx_e(&full[idx], stage_bytes);
                 uint8_t *dst = smem + (size_t)idx * stage_bytes;
                 const int w0 = wt * kTileW;
                 for (int kp = 0; kp < p.KP; ++kp) {
@@ -623,18 +687,18 @@ conv_wgrad_tc_kernel(const __grid_constant__ CUtensorMap xmap,
                             qc = qv - p.Qin;
                         }
                         for (int c8 = 0; c8 < C8; ++c8)
-                            tma_load_5d(dst + (size_t)((kp * p.KQ + kq) * C8 + c8) * kPlane, map,
-                                        &full[idx], c8 * 8, p.base_w + w0, qc, pc, b);
+                            tma_load_5d_e(dst + (size_t)((kp * p.KQ + kq) * C8 + c8) * kPlane, map,
+                                          &full[idx], c8 * 8, p.base_w + w0, qc, pc, b);
                     }
                 }
                 for (int kw = 0; kw < p.KW; ++kw)
                     for (int c8 = 0; c8 < N / 8; ++c8)
-                        tma_load_5d(dst + xbytes + (size_t)(kw * (N / 8) + c8) * kPlane, &dmap,
-                                    &full[idx], c8 * 8, w0 - kw, qo, po, b);
+                        tma_load_5d_e(dst + xbytes + (size_t)(kw * (N / 8) + c8) * kPlane, &dmap,
+                                      &full[idx], c8 * 8, w0 - kw, qo, po, b);
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
+        {
             const uint32_t idesc = idesc_bf16(128, NT, 1, 1);
             const uint64_t a0 = sdesc(smem_u32(smem), 128, kPlane);
             const uint64_t b0 = sdesc(smem_u32(smem) + xbytes, 128, kPlane);
@@ -646,11 +710,11 @@ conv_wgrad_tc_kernel(const __grid_constant__ CUtensorMap xmap,
                 const uint32_t so = (idx * stage_bytes) >> 4;
                 for (int mt = 0; mt < p.n_mt; ++mt)
                     for (int ks = 0; ks < kTileW / 16; ++ks)
-                        mma_bf16(tmem + mt * NT, a0 + so + ((mt * 16 * kPlane + ks * 256) >> 4),
-                                 b0 + so + ((ks * 256) >> 4), idesc, (it | ks) != 0 ? 1u : 0u);
-                mma_commit(&empty[idx]);
+                        mma_bf16_e(tmem + mt * NT, a0 + so + ((mt * 16 * kPlane + ks * 256) >> 4),
+                                   b0 + so + ((ks * 256) >> 4), idesc, (it | ks) != 0 ? 1u : 0u);
+                mma_commit_e(&empty[idx]);
             }
-            mma_commit(done);
+            mma_commit_e(done);
         }
     } else {
         const int quarter = warp & 3;
@@ -823,7 +887,8 @@ int run_wgrad_tc(const dp_conv_geom *g, const void *x, const void *xh, const voi
 }  // namespace
 
 int encode_tensor_map(CUtensorMap *map, CUtensorMapDataType dtype, int rank, void *base,
-                      const uint64_t *dims, const uint64_t *strides_bytes, const uint32_t *box) {
+                      const uint64_t *dims, const uint64_t *strides_bytes, const uint32_t *box,
+                      CUtensorMapSwizzle swizzle) {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
     if (!fn) {
         cudaDriverEntryPointQueryResult q;
@@ -835,7 +900,7 @@ int encode_tensor_map(CUtensorMap *map, CUtensorMapDataType dtype, int rank, voi
     }
     uint32_t estr[5] = {1, 1, 1, 1, 1};
     CUresult r = fn(map, dtype, rank, base, dims, strides_bytes, box, estr,
-                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle,
                     CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     DP_REQUIRE(r == CUDA_SUCCESS, DP_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
     return DP_OK;

@@ -93,6 +93,20 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t
     return d;
 }
 
+// K-major swizzled descriptor (layout 6 = SW32, 4 = SW64, 2 = SW128): 8-row
+// groups SBO bytes apart, LBO unused (1).  The swizzle XOR is applied to the
+// absolute shared address, so starts shifted by whole rows / 32-B K steps
+// inside a 1024-B aligned box address the bytes TMA wrote there.
+__device__ __forceinline__ uint64_t sdesc_sw(uint32_t saddr, uint32_t sbo, uint32_t layout) {
+    uint64_t d = 0;
+    d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFFu);
+    d |= static_cast<uint64_t>(1) << 16;
+    d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFFu) << 32;
+    d |= static_cast<uint64_t>(1) << 46;
+    d |= static_cast<uint64_t>(layout) << 61;
+    return d;
+}
+
 // Instruction descriptor for kind::f16: bf16 x bf16 -> fp32, M x N.
 // a_mn / b_mn select MN-major operands.
 __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, int a_mn = 0, int b_mn = 0) {
@@ -150,6 +164,58 @@ __device__ __forceinline__ void tmem_wait_ld() {
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+
+// ---- warp-uniform issue -------------------------------------------------------
+// The producer / MMA roles run their loops with the WHOLE warp converged so
+// descriptors and coordinates stay in uniform registers; one elected lane
+// issues the async op through a predicate inside the asm (no divergent
+// branch, no per-op R2UR waterfall).  Measured: per-op issue from a
+// lane-0-only branch cost ~60 cycles and made the N=96 conv MMAs 5x slower
+// than the operand-bandwidth floor (scripts/umma_probe.cu).
+__device__ __forceinline__ void mma_bf16_e(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
+                                           uint32_t accumulate) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p, e;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "elect.sync _|e, 0xffffffff;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+        "}\n" ::"r"(d_tmem),
+        "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void mma_commit_e(uint64_t *bar) {
+    asm volatile(
+        "{\n"
+        ".reg .pred e;\n"
+        "elect.sync _|e, 0xffffffff;\n"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n"
+        "}\n" ::"r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx_e(uint64_t *bar, uint32_t bytes) {
+    asm volatile(
+        "{\n"
+        ".reg .pred e;\n"
+        "elect.sync _|e, 0xffffffff;\n"
+        "@e mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(bytes)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_5d_e(void *dst, const CUtensorMap *map, uint64_t *bar,
+                                              int c0, int c1, int c2, int c3, int c4) {
+    asm volatile(
+        "{\n"
+        ".reg .pred e;\n"
+        "elect.sync _|e, 0xffffffff;\n"
+        "@e cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
+        "[%0], [%1, {%2, %3, %4, %5, %6}], [%7];\n"
+        "}\n" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4),
+        "r"(smem_u32(bar))
+        : "memory");
+}
+
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
     __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
     return *reinterpret_cast<uint32_t *>(&v);
@@ -160,6 +226,7 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
 // host: cuTensorMapEncodeTiled through the runtime's driver entry point
 // (no -lcuda link dependency).
 int encode_tensor_map(CUtensorMap *map, CUtensorMapDataType dtype, int rank, void *base,
-                      const uint64_t *dims, const uint64_t *strides_bytes, const uint32_t *box);
+                      const uint64_t *dims, const uint64_t *strides_bytes, const uint32_t *box,
+                      CUtensorMapSwizzle swizzle = CU_TENSOR_MAP_SWIZZLE_NONE);
 
 }  // namespace dp

@@ -1,0 +1,100 @@
+// Probe 2: the conv kernel's exact MMA stream (3 kp x 3 kw x 2 kc merged
+// N=96 MMAs per stage) with / without per-stage tcgen05.commit, to find what
+// throttles the conv MMA rate.
+#include <cstdio>
+#include <cstdint>
+#include <cuda_runtime.h>
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ uint64_t desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+    d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
+    d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+    d |= (uint64_t)1 << 46;
+    return d;
+}
+__device__ __forceinline__ void mma(uint32_t d, uint64_t a, uint64_t b, uint32_t id) {
+    asm volatile("{\n.reg .pred p, e;\nsetp.ne.b32 p, 1, 0;\nelect.sync _|e, 0xffffffff;\n"
+                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d), "l"(a), "l"(b), "r"(id));
+}
+__device__ __forceinline__ void commit(uint64_t *bar) {
+    asm volatile("{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void wait(uint64_t *bar, uint32_t ph) {
+    asm volatile("{\n.reg .pred P1;\nW:\nmbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n@P1 bra D;\nbra W;\nD:\n}\n" ::"r"(smem_u32(bar)), "r"(ph) : "memory");
+}
+__global__ void probe(int mode, int stages, uint32_t lboA, long long *out, int rnd, int KP, int KW, int KC, int C8) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    __shared__ uint32_t tslot;
+    __shared__ __align__(8) uint64_t bars[9];
+    for (int i = threadIdx.x * 16; i < 200 * 1024; i += blockDim.x * 16)
+        *reinterpret_cast<int4 *>(smem + i) = make_int4(0x3f803f80, 0x3f803f80, 0x3f803f80, 0x3f803f80);
+    if (rnd) {
+        uint32_t h = 0x9e3779b9u * (threadIdx.x + 1);
+        for (int i = threadIdx.x * 2; i < 200 * 1024; i += blockDim.x * 2) {
+            h ^= h << 13; h ^= h >> 17; h ^= h << 5;
+            // bf16 with random sign/mantissa, exponent around 1.0 (|x| in [0.5, 2))
+            uint16_t v = (uint16_t)((h & 0x8000u) | (0x3f00u + ((h >> 8) & 0xffu)));
+            *reinterpret_cast<uint16_t *>(smem + i) = v;
+        }
+    }
+    __syncthreads();
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    if (threadIdx.x < 32) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tslot)), "r"(512));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < 9; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&bars[i])), "r"(1));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    uint32_t tmem = tslot;
+    if (threadIdx.x < 32) {
+        const uint32_t id = (1u << 4) | (1u << 7) | (1u << 10) | ((96u >> 3) << 17) | ((128u >> 4) << 24);
+        const uint32_t plane = lboA;
+        const uint32_t stage_bytes = 12 * plane;  // 3 kp x 4 c8 planes
+        const uint64_t b0 = desc(smem_u32(smem) + 4 * stage_bytes, 128, 256);
+        const uint64_t a0 = desc(smem_u32(smem), plane, 128);
+        long long t0 = clock64();
+        for (int s = 0; s < stages; ++s) {
+            const int idx = s % 4;
+            const uint64_t ad = a0 + ((idx * stage_bytes) >> 4);
+            const uint32_t d = tmem + (13 - (s % 14)) * 32;
+            for (int kp = 0; kp < KP; ++kp)
+                for (int kw = 0; kw < KW; ++kw)
+                    for (int kc = 0; kc < KC; ++kc) {
+                        uint32_t aoff = (kp * C8 + 2 * kc) * plane + kw * 16;
+                        uint32_t boff = ((kp * KW + kw) * KC + kc) * 3072;
+                        mma(mode & 4 ? tmem : d, ad + (aoff >> 4), b0 + (boff >> 4), id);
+                    }
+            if (mode & 1) commit(&bars[idx]);
+            if (mode & 2) commit(&bars[6 + (s & 1)]);
+        }
+        commit(&bars[8]);
+        wait(&bars[8], 0);
+        long long t1 = clock64();
+        if (threadIdx.x == 0) out[blockIdx.x] = t1 - t0;
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (threadIdx.x < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+}
+int main() {
+    long long *d;
+    cudaMalloc(&d, 148 * sizeof(long long));
+    cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    const int stages = 512;
+    for (int rnd : {1}) for (int mode : {0, 3}) for (uint32_t lbo : {2176u}) {
+        probe<<<148, 128, 200 * 1024>>>(mode, stages, lbo, d, rnd, 3, 3, 2, 4);
+        cudaError_t e = cudaDeviceSynchronize();
+        if (e != cudaSuccess) { printf("mode %d: %s\n", mode, cudaGetErrorString(e)); return 1; }
+        long long h[148]; cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
+        long long mx = 0; for (int i = 0; i < 148; ++i) mx = h[i] > mx ? h[i] : mx;
+        printf("rnd %d mode %d (commit-stage %d, commit-row %d, fixedD %d) lbo %u: %.1f cyc/mma \n",
+               rnd, mode, mode & 1, (mode >> 1) & 1, (mode >> 2) & 1, lbo, (double)mx / (stages * 18));
+    }
+    return 0;
+}
