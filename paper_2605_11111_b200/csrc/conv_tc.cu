@@ -282,6 +282,7 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
                 tc_fence_after();
                 const uint32_t col = lane_base + (NSLOT - 1 - slot) * N;
                 uint32_t v[N];
+                if (!(p.dbg & 8)) {
 #pragma unroll
                 for (int c = 0; c < N; c += 16) {
                     uint32_t t[16];
@@ -293,6 +294,10 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
 #pragma unroll
                 for (int c = 0; c < N; c += 16) tmem_st16(col + c, z);
                 tmem_wait_st();
+                } else {
+#pragma unroll
+                    for (int i = 0; i < N; ++i) v[i] = 0u;
+                }
                 tc_fence_before();
                 mbar_arrive(&tempty[slot]);
                 if (w < p.Wout && !(p.dbg & 1)) {
@@ -595,31 +600,55 @@ int run_conv_tc(const dp_conv_geom *g, bool dgrad, const void *in, const void *i
 //   dW[co][ci][kp][kq][kw] = sum_{b,po,qo,wo} dY[b,po,qo,wo,co] *
 //                            X_virtual[b, base_p+po+kp, base_q+qo+kq, base_w+wo+kw, ci]
 // Substituting w' = wo + kw: dW[..kw] = sum_w' X[base_w + w'] * dY[w' - kw].
-// One unit = one output row (b, po, qo) x a 128-wide w' tile.  Per unit the
-// stage holds (i) the KP*KQ input rows as 8-channel planes in (kp,kq,c8)
-// order and (ii) KW copies of the dY row, each TMA-loaded at w' - kw (zero
-// outside [0, Wout)), as planes in (kw, c8) order.  Then
-//   D[M = (kp,kq,ci)][N = (kw,co)] += A[M][K = w'] . B[K = w'][N]
-// with both operands MN-major straight out of the planes: ONE
-// tcgen05.mma (N = KW*C_out) per 16 voxels per 128-row M tile.  M is tiled
-// by 16 planes; a partial last tile computes garbage rows that are never
-// stored.  Every CTA accumulates all its units in TMEM; the partials
-// [cta][row][kw*co] go to the workspace and a deterministic reduction sums
-// them into dW.
+//
+// A unit is a column (b, po, w' tile) and a chunk of output rows [q0, q1);
+// like the forward kernel it streams INPUT rows along Q.  Step s loads
+//   * input row q = base_q + q0 + s: KP x (channel blocks) boxes of
+//     KT*16 w' voxels, swizzled, into the X ring, and
+//   * (s < nq) dY row q0 + s as KW copies, each TMA-loaded at w' - kw (zero
+//     outside [0, Wout)), into the dY ring,
+// then for every kq with j = s - kq in [0, nq):
+//   D[kq][M = (kp,ci)][N = (kw,co)] += X_step(s)[K = w'] . dY_row(j)[K = w']
+// with both operands MN-major straight out of the TMA boxes (K = w' runs
+// down the swizzled rows).  Each X row is loaded once per unit (not KQ
+// times), each dY row KW times.  All units of a CTA accumulate into the same
+// TMEM tiles; the per-CTA partials [cta][kq][m][n] are summed into dW by a
+// deterministic reduction.  M tiles cover (kp, ci) rows 128 at a time; rows
+// past KP*Cin read the next boxes (garbage rows, never stored into dW).
 struct WgradTcParams {
-    int B, Cin, N;
+    int B, Cin, N;                   // N = Cout (dY channels)
     int Pin, Qin, Win, Pout, Qout, Wout;
     int KP, KQ, KW;
     int base_p, base_q, base_w;
     int split, halo;
-    int n_wt, n_units, n_mt, rows;   // rows = KP*KQ*Cin
-    int nstage, xplanes;
-    float *partial;                  // [grid][n_mt*128][KW*N]
+    int n_wt, n_qc, q_chunk, n_units, n_mt, kt;  // kt = 16-voxel K steps per w' tile
+    int nx, nd;                      // X ring / dY ring depth
+    int kq_lo, kq_hi;                // taps of this pass (TMEM holds (kq_hi-kq_lo) tiles)
+    float *partial;                  // [grid][KQ][n_mt*128][KW*N]
 };
 
-constexpr int kPlane = kTileW * 16;  // 128 voxels x 8 channels x bf16
+struct WLayout {
+    int cbx, nbx, boxx;              // X channel block, blocks, box bytes
+    int cbd, nbd, boxd;              // dY channel block, blocks, box bytes
+    int xslot, dslot, tail;          // ring slot bytes, garbage tail
+};
 
-template <int N>
+__host__ __device__ inline WLayout wlayout(int cin, int cout, int KP, int KW, int kt, int n_mt) {
+    WLayout L;
+    L.cbx = chan_block(cin);
+    L.nbx = cin / L.cbx;
+    L.boxx = (kt * 16 * L.cbx * 2 + 1023) / 1024 * 1024;
+    L.cbd = chan_block(cout);
+    L.nbd = cout / L.cbd;
+    L.boxd = (kt * 16 * L.cbd * 2 + 1023) / 1024 * 1024;
+    L.xslot = KP * L.nbx * L.boxx;
+    L.dslot = KW * L.nbd * L.boxd;
+    const int over = (n_mt * 128 / L.cbx - KP * L.nbx) * L.boxx;
+    L.tail = over > 0 ? over : 0;
+    return L;
+}
+
+template <int N, int KP_, int KQ_, int KW_, int CIN_>
 __global__ void __launch_bounds__(kThreads, 1)
 conv_wgrad_tc_kernel(const __grid_constant__ CUtensorMap xmap,
                      const __grid_constant__ CUtensorMap hmap,
@@ -627,23 +656,32 @@ conv_wgrad_tc_kernel(const __grid_constant__ CUtensorMap xmap,
     using namespace tc;
     extern __shared__ __align__(1024) uint8_t smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int C8 = p.Cin / 8;
-    const int NT = p.KW * N;  // MMA N
-    const uint32_t xbytes = (uint32_t)p.xplanes * kPlane;
-    const uint32_t stage_bytes = xbytes + (uint32_t)p.KW * (N / 8) * kPlane;
-    // garbage rows of a partial last M tile may read past the last stage
-    const int over = (p.n_mt * 16 - p.xplanes) * kPlane - p.KW * (N / 8) * kPlane;
-    const uint32_t tail = over > 0 ? (uint32_t)over : 0u;
-    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + (size_t)p.nstage * stage_bytes + tail);
-    uint64_t *full = bars, *empty = bars + p.nstage, *done = empty + p.nstage;
+    constexpr bool kStatic = KP_ > 0;
+    const int KP = kStatic ? KP_ : p.KP;
+    const int KQ = kStatic ? KQ_ : p.KQ;
+    const int KW = kStatic ? KW_ : p.KW;
+    const int CIN = kStatic ? CIN_ : p.Cin;
+    const int NMT = (KP * CIN + 127) / 128;
+    const WLayout L = wlayout(CIN, N, KP, KW, p.kt, NMT);
+    const int NT = KW * N;  // MMA N
+    uint8_t *xring = smem;
+    uint8_t *dring = smem + (size_t)p.nx * L.xslot + L.tail;
+    uint64_t *bars = reinterpret_cast<uint64_t *>(dring + (size_t)p.nd * L.dslot);
+    uint64_t *xfull = bars, *xempty = xfull + p.nx;
+    uint64_t *dfull = xempty + p.nx, *dempty = dfull + p.nd, *done = dempty + p.nd;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(done + 1);
+    const int NKQ = p.kq_hi - p.kq_lo;
     uint32_t ncols = 32;
-    while (ncols < (uint32_t)(p.n_mt * NT)) ncols <<= 1;
+    while (ncols < (uint32_t)(NKQ * NMT * NT)) ncols <<= 1;
     if (warp == 0) {
         if (lane == 0) {
-            for (int i = 0; i < p.nstage; ++i) {
-                mbar_init(&full[i], 1);
-                mbar_init(&empty[i], 1);
+            for (int i = 0; i < p.nx; ++i) {
+                mbar_init(&xfull[i], 1);
+                mbar_init(&xempty[i], 1);
+            }
+            for (int i = 0; i < p.nd; ++i) {
+                mbar_init(&dfull[i], 1);
+                mbar_init(&dempty[i], 1);
             }
             mbar_init(done, 1);
             mbar_fence_init();
@@ -658,80 +696,129 @@ conv_wgrad_tc_kernel(const __grid_constant__ CUtensorMap xmap,
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    const int WK = p.kt * 16;  // w' voxels per tile
 
     if (warp == 0) {
-        {
-            uint32_t it = 0;
-            for (int u = blockIdx.x; u < p.n_units; u += gridDim.x, ++it) {
-                int r = u;
-                const int wt = r % p.n_wt; r /= p.n_wt;
-                const int qo = r % p.Qout; r /= p.Qout;
-                const int po = r % p.Pout;
-                const int b = r / p.Pout;
-                const uint32_t idx = it % p.nstage, ph = (it / p.nstage) & 1;
-                mbar_wait(&empty[idx], ph ^ 1);
-                mbar_expect_tx_e(&full[idx], stage_bytes);
-                uint8_t *dst = smem + (size_t)idx * stage_bytes;
-                const int w0 = wt * kTileW;
-                for (int kp = 0; kp < p.KP; ++kp) {
-                    const int pv = p.base_p + po + kp;
-                    for (int kq = 0; kq < p.KQ; ++kq) {
-                        const int qv = p.base_q + qo + kq;
+        // ===================== TMA producer (whole warp, elected issue) =====================
+        uint32_t xi = 0, di = 0;
+        const uint32_t xbytes = (uint32_t)(KP * L.nbx * WK * L.cbx * 2);
+        const uint32_t dbytes = (uint32_t)(KW * L.nbd * WK * L.cbd * 2);
+        for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
+            int r = u;
+            const int wt = r % p.n_wt; r /= p.n_wt;
+            const int qc = r % p.n_qc; r /= p.n_qc;
+            const int po = r % p.Pout;
+            const int b = r / p.Pout;
+            const int q0 = qc * p.q_chunk, q1 = min(p.Qout, q0 + p.q_chunk);
+            const int nq = q1 - q0, nrows = nq + KQ - 1;
+            const int w0 = wt * WK;
+            for (int s = 0; s < nrows; ++s) {
+                {   // X: input row q = base_q + q0 + s, all kp
+                    const uint32_t idx = xi % p.nx, ph = (xi / p.nx) & 1;
+                    ++xi;
+                    mbar_wait(&xempty[idx], ph ^ 1);
+                    mbar_expect_tx_e(&xfull[idx], xbytes);
+                    uint8_t *dst = xring + (size_t)idx * L.xslot;
+                    const int qv = p.base_q + q0 + s;
+                    for (int kp = 0; kp < KP; ++kp) {
+                        const int pv = p.base_p + po + kp;
                         const CUtensorMap *map = &xmap;
-                        int pc = pv, qc = qv;
+                        int pc = pv, qcrd = qv;
                         if (p.split == 0 && pv >= p.Pin && pv < p.Pin + p.halo) {
                             map = &hmap;
                             pc = pv - p.Pin;
                         } else if (p.split == 1 && qv >= p.Qin && qv < p.Qin + p.halo) {
                             map = &hmap;
-                            qc = qv - p.Qin;
+                            qcrd = qv - p.Qin;
                         }
-                        for (int c8 = 0; c8 < C8; ++c8)
-                            tma_load_5d_e(dst + (size_t)((kp * p.KQ + kq) * C8 + c8) * kPlane, map,
-                                          &full[idx], c8 * 8, p.base_w + w0, qc, pc, b);
+                        for (int cb = 0; cb < L.nbx; ++cb)
+                            tma_load_5d_e(dst + (size_t)(kp * L.nbx + cb) * L.boxx, map,
+                                          &xfull[idx], cb * L.cbx, p.base_w + w0, qcrd, pc, b);
                     }
                 }
-                for (int kw = 0; kw < p.KW; ++kw)
-                    for (int c8 = 0; c8 < N / 8; ++c8)
-                        tma_load_5d_e(dst + xbytes + (size_t)(kw * (N / 8) + c8) * kPlane, &dmap,
-                                      &full[idx], c8 * 8, w0 - kw, qo, po, b);
+                if (s < nq) {  // dY row q0 + s, KW shifted copies
+                    const uint32_t idx = di % p.nd, ph = (di / p.nd) & 1;
+                    ++di;
+                    mbar_wait(&dempty[idx], ph ^ 1);
+                    mbar_expect_tx_e(&dfull[idx], dbytes);
+                    uint8_t *dst = dring + (size_t)idx * L.dslot;
+                    for (int kw = 0; kw < KW; ++kw)
+                        for (int cb = 0; cb < L.nbd; ++cb)
+                            tma_load_5d_e(dst + (size_t)(kw * L.nbd + cb) * L.boxd, &dmap,
+                                          &dfull[idx], cb * L.cbd, w0 - kw, q0 + s, po, b);
+                }
             }
         }
     } else if (warp == 1) {
-        {
-            const uint32_t idesc = idesc_bf16(128, NT, 1, 1);
-            const uint64_t a0 = sdesc(smem_u32(smem), 128, kPlane);
-            const uint64_t b0 = sdesc(smem_u32(smem) + xbytes, 128, kPlane);
-            uint32_t it = 0;
-            for (int u = blockIdx.x; u < p.n_units; u += gridDim.x, ++it) {
-                const uint32_t idx = it % p.nstage, ph = (it / p.nstage) & 1;
-                mbar_wait(&full[idx], ph);
+        // ===================== MMA issuer (whole warp, elected issue) =====================
+        const uint32_t idesc = idesc_bf16(128, NT, 1, 1);
+        const uint64_t a0 = sdesc_mn(smem_u32(xring), L.boxx, 8 * L.cbx * 2, swz_layout(L.cbx));
+        const uint64_t b0 = sdesc_mn(smem_u32(dring), L.boxd, 8 * L.cbd * 2, swz_layout(L.cbd));
+        const uint32_t astep = (16 * L.cbx * 2) >> 4;  // one K step = 16 w' rows
+        const uint32_t bstep = (16 * L.cbd * 2) >> 4;
+        const uint32_t mstep = (128 / L.cbx * L.boxx) >> 4;
+        uint32_t xi = 0, di = 0;   // X / dY ring counters (consumption order)
+        uint32_t fresh = (1u << (NKQ * NMT)) - 1u;  // accumulators not yet written
+        for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
+            int r = u / p.n_wt;
+            const int qc = r % p.n_qc;
+            const int q0 = qc * p.q_chunk, q1 = min(p.Qout, q0 + p.q_chunk);
+            const int nq = q1 - q0, nrows = nq + KQ - 1;
+            const uint32_t dbase = di;  // ring index of this unit's dY row 0
+            for (int s = 0; s < nrows; ++s) {
+                const uint32_t xidx = xi % p.nx, xph = (xi / p.nx) & 1;
+                ++xi;
+                if (s < nq) ++di;
+                mbar_wait(&xfull[xidx], xph);
+                if (s < nq) {
+                    const uint32_t j = dbase + s;
+                    mbar_wait(&dfull[j % p.nd], (j / p.nd) & 1);
+                }
                 tc_fence_after();
-                const uint32_t so = (idx * stage_bytes) >> 4;
-                for (int mt = 0; mt < p.n_mt; ++mt)
-                    for (int ks = 0; ks < kTileW / 16; ++ks)
-                        mma_bf16_e(tmem + mt * NT, a0 + so + ((mt * 16 * kPlane + ks * 256) >> 4),
-                                   b0 + so + ((ks * 256) >> 4), idesc, (it | ks) != 0 ? 1u : 0u);
-                mma_commit_e(&empty[idx]);
+                const uint64_t ax = a0 + ((xidx * L.xslot) >> 4);
+#pragma unroll
+                for (int kq = 0; kq < KQ; ++kq) {
+                    const int jr = s - kq;
+                    if (jr < 0 || jr >= nq || kq < p.kq_lo || kq >= p.kq_hi) continue;
+                    const uint32_t j = dbase + jr;
+                    const uint64_t bd = b0 + (((j % p.nd) * L.dslot) >> 4);
+                    const int t0 = (kq - p.kq_lo) * NMT;
+#pragma unroll
+                    for (int mt = 0; mt < NMT; ++mt) {
+                        const uint32_t d = tmem + (uint32_t)((t0 + mt) * NT);
+                        const uint32_t bit = 1u << (t0 + mt);
+                        uint32_t acc = (fresh & bit) ? 0u : 1u;
+                        fresh &= ~bit;
+                        for (int ks = 0; ks < p.kt; ++ks) {
+                            mma_bf16_e(d, ax + mt * mstep + ks * astep, bd + ks * bstep, idesc,
+                                       acc);
+                            acc = 1u;
+                        }
+                    }
+                    // dY row j is dead after this pass's last tap (always inside the unit)
+                    if (kq == p.kq_hi - 1) mma_commit_e(&dempty[j % p.nd]);
+                }
+                mma_commit_e(&xempty[xidx]);
             }
-            mma_commit_e(done);
         }
+        mma_commit_e(done);
     } else {
         const int quarter = warp & 3;
         const int m = quarter * 32 + lane;
         mbar_wait(done, 0);
         tc_fence_after();
-        for (int mt = 0; mt < p.n_mt; ++mt) {
-            float *dst = p.partial + ((size_t)blockIdx.x * p.n_mt * 128 + mt * 128 + m) * NT;
+        for (int t = 0; t < NKQ * NMT; ++t) {
+            float *dst = p.partial +
+                         ((size_t)(blockIdx.x * KQ * NMT + p.kq_lo * NMT + t) * 128 + m) * NT;
             for (int c = 0; c < NT; c += 16) {
-                uint32_t t[16];
-                tmem_ld16(tmem + ((uint32_t)(quarter * 32) << 16) + mt * NT + c, t);
+                uint32_t v[16];
+                tmem_ld16(tmem + ((uint32_t)(quarter * 32) << 16) + t * NT + c, v);
                 tmem_wait_ld();
 #pragma unroll
                 for (int i = 0; i < 16; i += 4)
                     *reinterpret_cast<float4 *>(dst + c + i) =
-                        make_float4(__uint_as_float(t[i]), __uint_as_float(t[i + 1]),
-                                    __uint_as_float(t[i + 2]), __uint_as_float(t[i + 3]));
+                        make_float4(__uint_as_float(v[i]), __uint_as_float(v[i + 1]),
+                                    __uint_as_float(v[i + 2]), __uint_as_float(v[i + 3]));
             }
         }
     }
@@ -743,9 +830,9 @@ conv_wgrad_tc_kernel(const __grid_constant__ CUtensorMap xmap,
     }
 }
 
-// dw[co][ci][kp][kq][kw] = sum_cta partial[cta][row(kp,kq,ci)][kw*N + co]
+// dw[co][ci][kp][kq][kw] = sum_cta partial[cta][kq][mt][m][kw*N + co], m = kp*Cin + ci
 __global__ void wgrad_tc_reduce(const float *__restrict__ part, float *__restrict__ dw, int ctas,
-                                int rows_pad, int KP, int KQ, int KW, int Cin, int N) {
+                                int n_mt, int KP, int KQ, int KW, int Cin, int N) {
     const int taps = KP * KQ * KW;
     const int total = N * Cin * taps;
     const int NT = KW * N;
@@ -756,16 +843,19 @@ __global__ void wgrad_tc_reduce(const float *__restrict__ part, float *__restric
         const int kp = r % KP; r /= KP;
         const int ci = r % Cin;
         const int co = r / Cin;
-        const int row = (kp * KQ + kq) * Cin + ci;  // plane (kp,kq,ci/8) * 8 + ci%8
+        const int row = kp * Cin + ci;
+        const size_t per_cta = (size_t)KQ * n_mt * 128 * NT;
+        const size_t off = ((size_t)kq * n_mt * 128 + row) * NT + kw * N + co;
         float s = 0.f;
-        for (int c = 0; c < ctas; ++c) s += part[((size_t)c * rows_pad + row) * NT + kw * N + co];
+        for (int c = 0; c < ctas; ++c) s += part[c * per_cta + off];
         dw[e] = s;
     }
 }
 
 struct WPlan {
     Roles R;
-    int Cin, N, n_mt, rows, xplanes, stage_bytes, nstage, smem, grid;
+    int Cin, N, n_mt, kt, n_wt, nx, nd, smem, grid, q_chunk, n_qc, kq_group;
+    WLayout L;
     int64_t n_units;
 };
 
@@ -774,7 +864,7 @@ bool make_wplan(const dp_conv_geom *g, WPlan &pl) {
     const Roles &R = pl.R;
     pl.Cin = (int)g->c_in;
     pl.N = pick_n((int)g->c_out);
-    if (!pl.N || pl.Cin % 8) return false;
+    if (!pl.N || pl.Cin % 16 || 128 % chan_block(pl.Cin) || pl.Cin > 128) return false;
     if (R.KW * pl.N > 256) return false;
     if (g->xs[1] != 1 || g->ys[1] != 1) return false;
     if (g->halo > 0 && g->hs[1] != 1) return false;
@@ -782,32 +872,75 @@ bool make_wplan(const dp_conv_geom *g, WPlan &pl) {
         if (R.xs[i] % 8 || R.ys[i] % 8) return false;
         if (g->halo > 0 && R.hs[i] % 8) return false;
     }
-    pl.xplanes = R.KP * R.KQ * (pl.Cin / 8);
-    pl.rows = pl.xplanes * 8;
-    pl.n_mt = (pl.xplanes + 15) / 16;
-    if (pl.n_mt * R.KW * pl.N > 512) return false;
-    pl.stage_bytes = pl.xplanes * kPlane + R.KW * (pl.N / 8) * kPlane;
-    const int over = (pl.n_mt * 16 - pl.xplanes) * kPlane - R.KW * (pl.N / 8) * kPlane;
-    const int tail = over > 0 ? over : 0;
-    const int budget = 220 * 1024;
-    int ns = (budget - tail - 256) / pl.stage_bytes;
-    if (ns > 6) ns = 6;
-    if (ns < 2) return false;
-    pl.nstage = ns;
-    pl.smem = ns * pl.stage_bytes + tail + 256;
-    pl.n_units = (int64_t)g->batch * R.Pout * R.Qout * ((R.Wout + R.KW - 1 + kTileW - 1) / kTileW);
-    pl.grid = (int)(pl.n_units < sm_count() ? pl.n_units : sm_count());
+    pl.n_mt = (R.KP * pl.Cin + 127) / 128;
+    // TMEM holds kq_group taps' accumulators at a time; more taps -> more passes
+    pl.kq_group = 512 / (pl.n_mt * R.KW * pl.N);
+    if (pl.kq_group < 1) return false;
+    if (pl.kq_group > R.KQ) pl.kq_group = R.KQ;
+    // w' tiles: K steps of 16 voxels, up to 16 steps (256-row boxes), balanced
+    const int wr = R.Wout + R.KW - 1;
+    const int steps = (wr + 15) / 16;
+    pl.n_wt = (steps + 15) / 16;
+    pl.kt = (steps + pl.n_wt - 1) / pl.n_wt;
+    // smem: X ring 2-3 slots, dY ring KQ+1.. slots
+    const int budget = 220 * 1024 - 512;
+    for (pl.kt = pl.kt; pl.kt >= 1; --pl.kt) {
+        pl.n_wt = (steps + pl.kt - 1) / pl.kt;
+        pl.L = wlayout(pl.Cin, pl.N, R.KP, R.KW, pl.kt, pl.n_mt);
+        pl.nx = 2;
+        pl.nd = R.KQ + 1;
+        const int need = pl.nx * pl.L.xslot + pl.L.tail + pl.nd * pl.L.dslot;
+        if (need <= budget) {
+            if (need + pl.L.xslot <= budget) ++pl.nx;
+            break;
+        }
+    }
+    if (pl.kt < 1) return false;
+    pl.smem = pl.nx * pl.L.xslot + pl.L.tail + pl.nd * pl.L.dslot + 512;
+    // q chunks: balance units over the SMs, amortise the KQ-1 extra rows
+    const int sms = sm_count();
+    const int64_t cols = (int64_t)g->batch * R.Pout * pl.n_wt;
+    int best_chunk = R.Qout;
+    double best = -1;
+    for (int nq = 1; nq <= R.Qout && nq <= 64; ++nq) {
+        const int chunk = (R.Qout + nq - 1) / nq;
+        const int nqc = (R.Qout + chunk - 1) / chunk;
+        const int64_t units = cols * nqc;
+        const int64_t waves = (units + sms - 1) / sms;
+        const double balance = (double)units / (double)(waves * sms);
+        const double overhead = (double)(chunk + R.KQ - 1) / chunk;
+        const double score = balance / overhead;
+        if (score > best + 1e-9) {
+            best = score;
+            best_chunk = chunk;
+        }
+    }
+    pl.q_chunk = best_chunk;
+    pl.n_qc = (R.Qout + best_chunk - 1) / best_chunk;
+    pl.n_units = cols * pl.n_qc;
+    pl.grid = (int)(pl.n_units < sms ? pl.n_units : sms);
     if (pl.grid < 1) pl.grid = 1;
     return true;
+}
+
+template <int N, int KP, int KQ, int KW, int CIN>
+int launch_wgrad_k(const CUtensorMap &xm, const CUtensorMap &hm, const CUtensorMap &dm,
+                   const WgradTcParams &p, int grid, int smem, cudaStream_t st) {
+    auto kern = conv_wgrad_tc_kernel<N, KP, KQ, KW, CIN>;
+    DP_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    kern<<<grid, kThreads, smem, st>>>(xm, hm, dm, p);
+    return launch_status("conv_wgrad_tc_kernel");
 }
 
 template <int N>
 int launch_wgrad_n(const CUtensorMap &xm, const CUtensorMap &hm, const CUtensorMap &dm,
                    const WgradTcParams &p, int grid, int smem, cudaStream_t st) {
-    auto kern = conv_wgrad_tc_kernel<N>;
-    DP_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    kern<<<grid, kThreads, smem, st>>>(xm, hm, dm, p);
-    return launch_status("conv_wgrad_tc_kernel");
+    const bool k333 = p.KP == 3 && p.KQ == 3 && p.KW == 3;
+    const bool k133 = p.KP == 1 && p.KQ == 3 && p.KW == 3;
+    if (k333 && p.Cin == 16) return launch_wgrad_k<N, 3, 3, 3, 16>(xm, hm, dm, p, grid, smem, st);
+    if (k333 && p.Cin == 32) return launch_wgrad_k<N, 3, 3, 3, 32>(xm, hm, dm, p, grid, smem, st);
+    if (k133 && p.Cin == 64) return launch_wgrad_k<N, 1, 3, 3, 64>(xm, hm, dm, p, grid, smem, st);
+    return launch_wgrad_k<N, 0, 0, 0, 0>(xm, hm, dm, p, grid, smem, st);
 }
 
 int run_wgrad_tc(const dp_conv_geom *g, const void *x, const void *xh, const void *dy, float *dw,
@@ -815,7 +948,7 @@ int run_wgrad_tc(const dp_conv_geom *g, const void *x, const void *xh, const voi
     WPlan pl;
     DP_REQUIRE(make_wplan(g, pl), DP_ERR_UNSUPPORTED, "conv_wgrad_tc: outside the envelope");
     const Roles &R = pl.R;
-    const int64_t need = (int64_t)pl.grid * pl.n_mt * 128 * R.KW * pl.N * 4;
+    const int64_t need = (int64_t)pl.grid * R.KQ * pl.n_mt * 128 * R.KW * pl.N * 4;
     DP_REQUIRE(ws_bytes >= need, DP_ERR_INVALID, "conv_wgrad_tc: workspace too small");
     (void)need;
     const int taps = R.KP * R.KQ * R.KW;
@@ -823,7 +956,13 @@ int run_wgrad_tc(const dp_conv_geom *g, const void *x, const void *xh, const voi
         DP_CUDA_CHECK(cudaMemsetAsync(dw, 0, (size_t)pl.N * pl.Cin * taps * 4, st));
         return DP_OK;
     }
-    uint32_t box[5] = {8, (uint32_t)kTileW, 1, 1, 1};
+    const WLayout &L = pl.L;
+    const uint32_t wk = (uint32_t)pl.kt * 16;
+    auto swz = [](int cb) {
+        return cb == 16 ? CU_TENSOR_MAP_SWIZZLE_32B
+                        : cb == 32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B;
+    };
+    uint32_t xbox[5] = {(uint32_t)L.cbx, wk, 1, 1, 1};
     CUtensorMap xm, hm, dm;
     {
         uint64_t dims[5] = {(uint64_t)pl.Cin, (uint64_t)R.Win, (uint64_t)R.Qin, (uint64_t)R.Pin,
@@ -831,7 +970,7 @@ int run_wgrad_tc(const dp_conv_geom *g, const void *x, const void *xh, const voi
         uint64_t strides[4] = {(uint64_t)R.xs[3] * 2, (uint64_t)R.xs[2] * 2,
                                (uint64_t)R.xs[1] * 2, (uint64_t)R.xs[0] * 2};
         int rc = encode_tensor_map(&xm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void *>(x),
-                                   dims, strides, box);
+                                   dims, strides, xbox, swz(L.cbx));
         if (rc) return rc;
     }
     hm = xm;
@@ -842,7 +981,7 @@ int run_wgrad_tc(const dp_conv_geom *g, const void *x, const void *xh, const voi
         uint64_t strides[4] = {(uint64_t)R.hs[3] * 2, (uint64_t)R.hs[2] * 2,
                                (uint64_t)R.hs[1] * 2, (uint64_t)R.hs[0] * 2};
         int rc = encode_tensor_map(&hm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5,
-                                   const_cast<void *>(xh), dims, strides, box);
+                                   const_cast<void *>(xh), dims, strides, xbox, swz(L.cbx));
         if (rc) return rc;
     }
     {
@@ -850,9 +989,9 @@ int run_wgrad_tc(const dp_conv_geom *g, const void *x, const void *xh, const voi
                             (uint64_t)g->batch};
         uint64_t strides[4] = {(uint64_t)R.ys[3] * 2, (uint64_t)R.ys[2] * 2,
                                (uint64_t)R.ys[1] * 2, (uint64_t)R.ys[0] * 2};
-        uint32_t dbox[5] = {8, (uint32_t)kTileW, 1, 1, 1};
+        uint32_t dbox[5] = {(uint32_t)L.cbd, wk, 1, 1, 1};
         int rc = encode_tensor_map(&dm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void *>(dy),
-                                   dims, strides, dbox);
+                                   dims, strides, dbox, swz(L.cbd));
         if (rc) return rc;
     }
     WgradTcParams p;
@@ -864,23 +1003,27 @@ int run_wgrad_tc(const dp_conv_geom *g, const void *x, const void *xh, const voi
     p.base_p = R.base_p; p.base_q = R.base_q; p.base_w = R.base_w;
     p.split = g->halo > 0 ? R.split : -1;
     p.halo = (int)g->halo;
-    p.n_wt = (R.Wout + R.KW - 1 + kTileW - 1) / kTileW;
+    p.n_wt = pl.n_wt; p.n_qc = pl.n_qc; p.q_chunk = pl.q_chunk;
     p.n_units = (int)pl.n_units;
-    p.n_mt = pl.n_mt; p.rows = pl.rows;
-    p.nstage = pl.nstage; p.xplanes = pl.xplanes;
+    p.n_mt = pl.n_mt; p.kt = pl.kt;
+    p.nx = pl.nx; p.nd = pl.nd;
     p.partial = (float *)ws;
-    int rc;
-    switch (pl.N) {
-        case 16: rc = launch_wgrad_n<16>(xm, hm, dm, p, pl.grid, pl.smem, st); break;
-        case 32: rc = launch_wgrad_n<32>(xm, hm, dm, p, pl.grid, pl.smem, st); break;
-        case 48: rc = launch_wgrad_n<48>(xm, hm, dm, p, pl.grid, pl.smem, st); break;
-        default: rc = launch_wgrad_n<64>(xm, hm, dm, p, pl.grid, pl.smem, st); break;
+    for (int lo = 0; lo < R.KQ; lo += pl.kq_group) {
+        p.kq_lo = lo;
+        p.kq_hi = lo + pl.kq_group < R.KQ ? lo + pl.kq_group : R.KQ;
+        int rc;
+        switch (pl.N) {
+            case 16: rc = launch_wgrad_n<16>(xm, hm, dm, p, pl.grid, pl.smem, st); break;
+            case 32: rc = launch_wgrad_n<32>(xm, hm, dm, p, pl.grid, pl.smem, st); break;
+            case 48: rc = launch_wgrad_n<48>(xm, hm, dm, p, pl.grid, pl.smem, st); break;
+            default: rc = launch_wgrad_n<64>(xm, hm, dm, p, pl.grid, pl.smem, st); break;
+        }
+        if (rc) return rc;
     }
-    if (rc) return rc;
     const int total = pl.N * pl.Cin * taps;
     wgrad_tc_reduce<<<grid_for(total, 256, 4), 256, 0, st>>>((const float *)ws, dw, pl.grid,
-                                                             pl.n_mt * 128, R.KP, R.KQ, R.KW,
-                                                             pl.Cin, pl.N);
+                                                             pl.n_mt, R.KP, R.KQ, R.KW, pl.Cin,
+                                                             pl.N);
     return launch_status("wgrad_tc_reduce");
 }
 
@@ -920,7 +1063,7 @@ int64_t conv_tc_workspace(const dp_conv_geom *g, int which) {
     if (which == DP_CONV_WGRAD) {
         WPlan wp;
         if (!make_wplan(g, wp)) return -1;
-        return (int64_t)wp.grid * wp.n_mt * 128 * wp.R.KW * wp.N * 4;
+        return (int64_t)wp.grid * wp.R.KQ * wp.n_mt * 128 * wp.R.KW * wp.N * 4;
     }
     Plan pl;
     if (!make_plan(g, which == DP_CONV_DGRAD, pl)) return -1;

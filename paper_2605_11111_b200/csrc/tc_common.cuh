@@ -107,6 +107,19 @@ __device__ __forceinline__ uint64_t sdesc_sw(uint32_t saddr, uint32_t sbo, uint3
     return d;
 }
 
+// MN-major swizzled descriptor: MN swizzle-atom groups LBO bytes apart,
+// 8-row K groups SBO bytes apart.
+__device__ __forceinline__ uint64_t sdesc_mn(uint32_t saddr, uint32_t lbo, uint32_t sbo,
+                                             uint32_t layout) {
+    uint64_t d = 0;
+    d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFFu);
+    d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFFu) << 16;
+    d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFFu) << 32;
+    d |= static_cast<uint64_t>(1) << 46;
+    d |= static_cast<uint64_t>(layout) << 61;
+    return d;
+}
+
 // Instruction descriptor for kind::f16: bf16 x bf16 -> fp32, M x N.
 // a_mn / b_mn select MN-major operands.
 __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, int a_mn = 0, int b_mn = 0) {
