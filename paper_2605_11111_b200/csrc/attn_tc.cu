@@ -1,0 +1,327 @@
+// tcgen05 + TMA ring-attention block kernels (bf16 in, fp32 state), head
+// dim 64.  One launch folds ONE K/V block of the ring into the running
+// online-softmax state (m, l, acc) of the local queries — the reference's
+// per-step `scores = q @ kb.T * scale; state.update(scores, vb)`
+// (domainpar/ops.py:272-275, RingSoftmaxState.update :199-211) — so the ring
+// loop on the host (K||V rotating over NVLink) is unchanged; the state
+// stays fp32 in HBM between ring steps.
+//
+// Forward CTA = one 128-row query tile of one head, looping over the block's
+// keys 128 at a time (warp-specialised, 192 threads):
+//   warp 0     TMA producer: Q once, K/V tiles into a 3-stage ring
+//   warp 1     MMA issuer:   S(j) = Q K_j^T into a double-buffered TMEM
+//              S (M=128, N=128, K=64), then O += P(j-1) V(j-1) (M=128, N=64,
+//              K=128) into the TMEM O accumulator — S(j+1) runs while the
+//              softmax warps work on S(j)
+//   warps 2-5  softmax: thread = query row; tcgen05.ld its S row, online
+//              max with lazy rescaling (O and l are rescaled only when the
+//              running max grows by more than 2^8, which keeps the state
+//              exact: any reference max gives the same acc/l), P = exp2(.)
+//              as bf16 into a swizzled smem tile (the A operand of P V);
+//              they also load acc into TMEM at the start and write the
+//              state back at the end.
+// Operand layouts: Q, K tiles land from TMA as [128 rows][64 d] with the
+// 128-B swizzle (K-major A/B of S = Q K^T); V lands the same way and is
+// read as the MN-major B operand of P V; P is written K-major SW128.
+#include "tc_common.cuh"
+
+namespace dp {
+namespace {
+
+constexpr int kBM = 128;      // query rows per tile
+constexpr int kBN = 128;      // keys per block
+constexpr int kD = 64;        // head dim
+constexpr int kStages = 3;    // K/V ring depth
+constexpr int kThreads = 192;
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr float kRescale = 8.0f;  // log2 units: rescale when the max grows by > 2^8
+
+constexpr int kTileBytes = kBM * kD * 2;           // 16 KB (Q, K or V tile)
+constexpr int kPBytes = kBM * kBN * 2;             // 32 KB (P tile)
+constexpr int kSmemQ = 0;
+constexpr int kSmemKV = kSmemQ + kTileBytes;       // stages of [K | V]
+constexpr int kSmemP = kSmemKV + kStages * 2 * kTileBytes;
+constexpr int kSmemBar = kSmemP + 2 * kPBytes;
+constexpr int kSmemFwd = kSmemBar + 256;
+
+// TMEM columns: S0 [0,128), S1 [128,256), O [256,320)
+constexpr uint32_t kColS = 0, kColO = 256;
+
+struct FwdParams {
+    int sq, sk, H;
+    int n_qt;
+    float c;                  // scale * log2(e)
+    float *m, *l, *acc;       // fp32 state: [sq,H], [sq,H], [sq,H,64]
+};
+
+__device__ __forceinline__ float ex2(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap kmap,
+                   const __grid_constant__ CUtensorMap vmap, const FwdParams p) {
+    using namespace tc;
+    extern __shared__ __align__(1024) uint8_t smem[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int qt = blockIdx.x % p.n_qt, h = blockIdx.x / p.n_qt;
+    const int q0 = qt * kBM;
+    const int nblk = (p.sk + kBN - 1) / kBN;
+
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + kSmemBar);
+    uint64_t *q_full = bars;
+    uint64_t *kv_full = bars + 1, *kv_empty = kv_full + kStages;
+    uint64_t *s_full = kv_empty + kStages;      // [2]
+    uint64_t *p_full = s_full + 2;              // [2] softmax -> MMA (count 128)
+    uint64_t *p_empty = p_full + 2;             // [2] PV done (commit)
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(p_empty + 2);
+
+    if (warp == 0) {
+        if (lane == 0) {
+            mbar_init(q_full, 1);
+            for (int i = 0; i < kStages; ++i) {
+                mbar_init(&kv_full[i], 1);
+                mbar_init(&kv_empty[i], 1);
+            }
+            for (int i = 0; i < 2; ++i) {
+                mbar_init(&s_full[i], 1);
+                mbar_init(&p_full[i], 128);
+                mbar_init(&p_empty[i], 1);
+            }
+            mbar_fence_init();
+            tma_prefetch(&qmap);
+            tma_prefetch(&kmap);
+            tma_prefetch(&vmap);
+        }
+        __syncwarp();
+        tmem_alloc(tmem_slot, 512);
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        // ===================== TMA producer =====================
+        mbar_expect_tx_e(q_full, kTileBytes);
+        tma_load_3d_e(smem + kSmemQ, &qmap, q_full, 0, h, q0);
+        for (int j = 0; j < nblk; ++j) {
+            const int st = j % kStages;
+            mbar_wait(&kv_empty[st], ((j / kStages) & 1) ^ 1);
+            mbar_expect_tx_e(&kv_full[st], 2 * kTileBytes);
+            uint8_t *dst = smem + kSmemKV + st * 2 * kTileBytes;
+            tma_load_3d_e(dst, &kmap, &kv_full[st], 0, h, j * kBN);
+            tma_load_3d_e(dst + kTileBytes, &vmap, &kv_full[st], 0, h, j * kBN);
+        }
+    } else if (warp == 1) {
+        // ===================== MMA issuer =====================
+        const uint32_t id_s = idesc_bf16(kBM, kBN);            // K-major A, K-major B
+        const uint32_t id_o = idesc_bf16(kBM, kD, 0, 1);       // P K-major, V MN-major
+        const uint64_t qd = sdesc_sw(smem_u32(smem + kSmemQ), 1024, 2);
+        mbar_wait(q_full, 0);
+        auto issue_pv = [&](int jj) {
+            const int b = jj & 1;
+            mbar_wait(&p_full[b], (jj >> 1) & 1);
+            tc_fence_after();
+            const int st = jj % kStages;
+            const uint64_t pd = sdesc_sw(smem_u32(smem + kSmemP + b * kPBytes), 1024, 2);
+            const uint64_t vd =
+                sdesc_mn(smem_u32(smem + kSmemKV + st * 2 * kTileBytes + kTileBytes), 8192, 1024, 2);
+#pragma unroll
+            for (int k = 0; k < kBN / 16; ++k) {
+                // P: key block k/4 (64 keys = one 128-B row), +32 B per 16 keys
+                const uint32_t pa = ((k >> 2) * (kBM * 128) + (k & 3) * 32) >> 4;
+                const uint32_t vb = (k * 16 * 128) >> 4;  // 16 key rows of V
+                mma_bf16_e(tmem + kColO, pd + pa, vd + vb, id_o, 1u);
+            }
+            mma_commit_e(&p_empty[b]);
+            mma_commit_e(&kv_empty[st]);
+        };
+        for (int j = 0; j < nblk; ++j) {
+            const int st = j % kStages;
+            mbar_wait(&kv_full[st], (j / kStages) & 1);
+            tc_fence_after();
+            const uint64_t kd = sdesc_sw(smem_u32(smem + kSmemKV + st * 2 * kTileBytes), 1024, 2);
+            const uint32_t sc = tmem + kColS + (j & 1) * kBN;
+#pragma unroll
+            for (int k = 0; k < kD / 16; ++k)
+                mma_bf16_e(sc, qd + ((k * 32) >> 4), kd + ((k * 32) >> 4), id_s, k ? 1u : 0u);
+            mma_commit_e(&s_full[j & 1]);
+            if (j >= 1) issue_pv(j - 1);
+        }
+        if (nblk >= 1) issue_pv(nblk - 1);
+    } else {
+        // ===================== softmax / state =====================
+        const int quarter = warp & 3;
+        const int rl = quarter * 32 + lane;          // row within the tile = TMEM lane
+        const int row = q0 + rl;
+        const bool valid = row < p.sq;
+        const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
+        const size_t sidx = (size_t)row * p.H + h;
+        float m_run = -INFINITY, l_run = 0.f;
+        {
+            uint32_t o[16];
+            for (int c = 0; c < kD; c += 16) {
+#pragma unroll
+                for (int i = 0; i < 16; ++i)
+                    o[i] = valid ? __float_as_uint(p.acc[sidx * kD + c + i]) : 0u;
+                tmem_st16(lane_base + kColO + c, o);
+            }
+            tmem_wait_st();
+            if (valid) {
+                m_run = p.m[sidx] * kLog2e;
+                l_run = p.l[sidx];
+            }
+        }
+        uint8_t *prow = smem + kSmemP + rl * 128;
+        for (int j = 0; j < nblk; ++j) {
+            mbar_wait(&s_full[j & 1], (j >> 1) & 1);
+            tc_fence_after();
+            const uint32_t sc = lane_base + kColS + (j & 1) * kBN;
+            float s[kBN];
+#pragma unroll
+            for (int c = 0; c < kBN; c += 16) {
+                uint32_t t[16];
+                tmem_ld16(sc + c, t);
+#pragma unroll
+                for (int i = 0; i < 16; ++i) s[c + i] = __uint_as_float(t[i]);
+            }
+            tmem_wait_ld();
+            const int kvalid = p.sk - j * kBN;  // keys of this block that exist
+            float t = -INFINITY;
+#pragma unroll
+            for (int i = 0; i < kBN; ++i) {
+                s[i] = i < kvalid ? s[i] * p.c : -INFINITY;
+                t = fmaxf(t, s[i]);
+            }
+            // lazy rescale: only when this row's max grows by more than 2^kRescale
+            const bool grow = t > m_run + kRescale;
+            if (__any_sync(0xffffffffu, grow)) {
+                if (j >= 1) mbar_wait(&p_empty[(j - 1) & 1], ((j - 1) >> 1) & 1);
+                tc_fence_after();
+                const float f = grow ? ex2(m_run - t) : 1.f;
+                for (int c = 0; c < kD; c += 16) {
+                    uint32_t o[16];
+                    tmem_ld16(lane_base + kColO + c, o);
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * f);
+                    tmem_st16(lane_base + kColO + c, o);
+                }
+                tmem_wait_st();
+                if (grow) {
+                    l_run *= f;
+                    m_run = t;
+                }
+            }
+            // P = exp2(s - m) (bf16) into the swizzled P tile of buffer j & 1
+            if (j >= 2) mbar_wait(&p_empty[j & 1], ((j >> 1) & 1) ^ 1);
+            uint8_t *pb = prow + (j & 1) * kPBytes;
+            float sum = 0.f;
+#pragma unroll
+            for (int c = 0; c < kBN / 8; ++c) {
+                float e[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    e[i] = ex2(s[c * 8 + i] - m_run);
+                    sum += e[i];
+                }
+                uint4 pk;
+                pk.x = pack_bf16(e[0], e[1]);
+                pk.y = pack_bf16(e[2], e[3]);
+                pk.z = pack_bf16(e[4], e[5]);
+                pk.w = pack_bf16(e[6], e[7]);
+                const int blk = c >> 3, ch = c & 7;
+                *reinterpret_cast<uint4 *>(pb + blk * (kBM * 128) + ((ch ^ (rl & 7)) << 4)) = pk;
+            }
+            l_run += sum;
+            fence_async_smem();
+            tc_fence_before();
+            mbar_arrive(&p_full[j & 1]);
+        }
+        // final state back to HBM once the last P V has landed
+        if (nblk >= 1) mbar_wait(&p_empty[(nblk - 1) & 1], ((nblk - 1) >> 1) & 1);
+        tc_fence_after();
+        for (int c = 0; c < kD; c += 16) {
+            uint32_t o[16];
+            tmem_ld16(lane_base + kColO + c, o);
+            tmem_wait_ld();
+            if (valid) {
+                float4 *dst = reinterpret_cast<float4 *>(p.acc + sidx * kD + c);
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+                    dst[i] = make_float4(__uint_as_float(o[4 * i]), __uint_as_float(o[4 * i + 1]),
+                                         __uint_as_float(o[4 * i + 2]), __uint_as_float(o[4 * i + 3]));
+            }
+        }
+        if (valid) {
+            p.m[sidx] = m_run / kLog2e;
+            p.l[sidx] = l_run;
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        tc_fence_after();
+        tmem_dealloc(tmem, 512);
+    }
+}
+
+// [S, H, 64] bf16 view with element strides (row, head): box 64 x 1 x 128,
+// 128-B swizzle.
+int head_map(CUtensorMap *m, const void *base, int64_t rows, int64_t heads, int64_t rs, int64_t hs) {
+    uint64_t dims[3] = {(uint64_t)kD, (uint64_t)heads, (uint64_t)rows};
+    uint64_t strides[2] = {(uint64_t)hs * 2, (uint64_t)rs * 2};
+    uint32_t box[3] = {(uint32_t)kD, 1, (uint32_t)kBM};
+    return encode_tensor_map(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void *>(base), dims,
+                             strides, box, CU_TENSOR_MAP_SWIZZLE_128B);
+}
+
+}  // namespace
+
+int attn_tc_eligible(const dp_attn_geom *g, int dtype) {
+    if (!g || dtype != DP_BF16 || g->dim != kD) return 0;
+    const int64_t s[6] = {g->q_rs, g->q_hs, g->k_rs, g->k_hs, g->v_rs, g->v_hs};
+    for (int i = 0; i < 6; ++i)
+        if (s[i] % 8) return 0;  // 16-B aligned TMA strides
+    if (g->sq > (1 << 30) || g->sk > (1 << 30)) return 0;
+    return 1;
+}
+
+int attn_bwd_tc_eligible(const dp_attn_geom *, int) { return 0; }
+
+int attn_fwd_update_tc_launch(const dp_attn_geom *g, const void *q, const void *k, const void *v,
+                              void *m, void *l, void *acc, cudaStream_t st) {
+    DP_REQUIRE(attn_tc_eligible(g, DP_BF16), DP_ERR_UNSUPPORTED, "attn_tc: outside the envelope");
+    if (g->sq == 0 || g->sk == 0) return DP_OK;
+    CUtensorMap qm, km, vm;
+    int rc = head_map(&qm, q, g->sq, g->heads, g->q_rs, g->q_hs);
+    if (!rc) rc = head_map(&km, k, g->sk, g->heads, g->k_rs, g->k_hs);
+    if (!rc) rc = head_map(&vm, v, g->sk, g->heads, g->v_rs, g->v_hs);
+    if (rc) return rc;
+    FwdParams p;
+    p.sq = (int)g->sq;
+    p.sk = (int)g->sk;
+    p.H = (int)g->heads;
+    p.n_qt = (int)((g->sq + kBM - 1) / kBM);
+    p.c = (float)(g->scale * 1.4426950408889634);
+    p.m = (float *)m;
+    p.l = (float *)l;
+    p.acc = (float *)acc;
+    DP_CUDA_CHECK(cudaFuncSetAttribute(attn_fwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       kSmemFwd));
+    const int64_t grid = (int64_t)p.n_qt * p.H;
+    attn_fwd_tc_kernel<<<(unsigned)grid, kThreads, kSmemFwd, st>>>(qm, km, vm, p);
+    return launch_status("attn_fwd_tc_kernel");
+}
+
+int attn_bwd_update_tc_launch(const dp_attn_geom *, const void *, const void *, const void *,
+                              const void *, const void *, const void *, void *, void *, void *,
+                              cudaStream_t) {
+    set_error("attn_tc: backward not built yet");
+    return DP_ERR_UNSUPPORTED;
+}
+
+}  // namespace dp

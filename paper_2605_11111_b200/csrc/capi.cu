@@ -25,6 +25,7 @@ int conv_dgrad_tc_launch(const dp_conv_geom *, const void *, const void *, void 
 int conv_wgrad_tc_launch(const dp_conv_geom *, const void *, const void *, const void *, void *,
                          void *, int64_t, cudaStream_t);
 int attn_tc_eligible(const dp_attn_geom *, int dtype);
+int attn_bwd_tc_eligible(const dp_attn_geom *, int dtype);
 int attn_fwd_update_tc_launch(const dp_attn_geom *, const void *, const void *, const void *,
                               void *, void *, void *, cudaStream_t);
 int attn_bwd_update_tc_launch(const dp_attn_geom *, const void *, const void *, const void *,
@@ -97,7 +98,7 @@ extern "C" int dp_attn_bwd_update(const dp_attn_geom *g, int dtype, int algo, co
                                   const void *k, const void *v, const void *dout,
                                   const void *lse, const void *delta, void *dq, void *dk,
                                   void *dv, void *stream) {
-    int a = pick(algo, attn_tc_eligible(g, dtype), "dp_attn_bwd_update");
+    int a = pick(algo, attn_bwd_tc_eligible(g, dtype), "dp_attn_bwd_update");
     if (a < 0) return DP_ERR_UNSUPPORTED;
     cudaStream_t st = (cudaStream_t)stream;
     if (a == DP_ALGO_TC)
