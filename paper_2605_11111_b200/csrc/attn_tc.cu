@@ -269,6 +269,291 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
     }
 }
 
+// ---------------------------------------------------------------------------
+// Backward block: with P = exp(s - lse), D = rowsum(dO * O) (from
+// dp_attn_bwd_preprocess):  dV += P^T dO,  dS = P (dO V^T - D),
+// dQ += scale dS K,  dK += scale dS^T Q  — the same math as the CUDA-core
+// kernels, for one K/V block of the ring.
+//
+// CTA = one 128-key tile of one head (K, V resident in smem; dK, dV
+// accumulate in TMEM over the whole query range), looping over 128-row
+// query blocks (Q, dO double-buffered by TMA).  320 threads:
+//   warp 0     TMA producer
+//   warp 1     MMA issuer: S^T = K Q^T and dP^T = V dO^T into TMEM; once the
+//              softmax warps have written P^T / dS^T (bf16, swizzled smem):
+//              dV += P^T dO, dK += dS^T Q (A = the key-major tiles), and
+//              dQ = dS K into a double-buffered TMEM tile (A = the SAME dS^T
+//              bytes read as an MN-major operand)
+//   warps 2-5  thread = key row: P^T = exp2(S^T c - LSE2), dS^T =
+//              scale P^T (dP^T - D) -> smem; at the end dK, dV += TMEM
+//   warps 6-9  thread = query row: dQ tile TMEM -> float4 atomics into dq
+// The next block's S^T / dP^T MMAs are issued before this block's gradient
+// MMAs, so the softmax warps overlap the tensor pipe.
+constexpr int kBwdThreads = 320;
+constexpr int kB_K = 0, kB_V = kTileBytes;
+constexpr int kB_QD = 2 * kTileBytes;                  // 2 stages of [Q | dO]
+constexpr int kB_PS = kB_QD + 2 * 2 * kTileBytes;      // 2 buffers of [P^T | dS^T]
+constexpr int kB_LD = kB_PS + 2 * 2 * kPBytes;         // lse2[2][128], delta[2][128]
+constexpr int kB_BAR = kB_LD + 4 * 128 * 4;
+constexpr int kSmemBwd = kB_BAR + 256;
+// TMEM columns: S^T [0,128), dP^T [128,256), dV [256,320), dK [320,384), dQ x2 [384,512)
+constexpr uint32_t kColST = 0, kColDP = 128, kColDV = 256, kColDK = 320, kColDQ = 384;
+
+struct BwdParams {
+    int sq, sk, H;
+    int n_kt;
+    float c;                  // scale * log2(e)
+    float scale;
+    const float *lse, *delta;  // [sq, H]
+    float *dq;                 // [sq, H, 64] (atomic +=)
+    float *dk, *dv;            // [sk, H, 64] (+=)
+};
+
+__device__ __forceinline__ void named_bar(int id, int n) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+__global__ void __launch_bounds__(kBwdThreads, 1)
+attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap kmap,
+                   const __grid_constant__ CUtensorMap vmap, const __grid_constant__ CUtensorMap dmap,
+                   const BwdParams p) {
+    using namespace tc;
+    extern __shared__ __align__(1024) uint8_t smem[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int kt = blockIdx.x % p.n_kt, h = blockIdx.x / p.n_kt;
+    const int k0 = kt * kBN;
+    const int nq = (p.sq + kBM - 1) / kBM;
+
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + kB_BAR);
+    uint64_t *kv_full = bars;
+    uint64_t *qd_full = bars + 1, *qd_empty = qd_full + 2;
+    uint64_t *s_full = qd_empty + 2, *s_free = s_full + 1;
+    uint64_t *p_full = s_free + 1, *p_empty = p_full + 2;
+    uint64_t *dq_full = p_empty + 2, *dq_empty = dq_full + 2;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(dq_empty + 2);
+    float *lse2_s = reinterpret_cast<float *>(smem + kB_LD);   // [2][128]
+    float *delta_s = lse2_s + 256;                             // [2][128]
+
+    if (warp == 0) {
+        if (lane == 0) {
+            mbar_init(kv_full, 1);
+            for (int i = 0; i < 2; ++i) {
+                mbar_init(&qd_full[i], 1);
+                mbar_init(&qd_empty[i], 1);
+                mbar_init(&p_full[i], 128);
+                mbar_init(&p_empty[i], 1);
+                mbar_init(&dq_full[i], 1);
+                mbar_init(&dq_empty[i], 128);
+            }
+            mbar_init(s_full, 1);
+            mbar_init(s_free, 128);
+            mbar_fence_init();
+            tma_prefetch(&qmap);
+            tma_prefetch(&kmap);
+            tma_prefetch(&vmap);
+            tma_prefetch(&dmap);
+        }
+        __syncwarp();
+        tmem_alloc(tmem_slot, 512);
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        // ===================== TMA producer =====================
+        mbar_expect_tx_e(kv_full, 2 * kTileBytes);
+        tma_load_3d_e(smem + kB_K, &kmap, kv_full, 0, h, k0);
+        tma_load_3d_e(smem + kB_V, &vmap, kv_full, 0, h, k0);
+        for (int i = 0; i < nq; ++i) {
+            const int st = i & 1;
+            mbar_wait(&qd_empty[st], ((i >> 1) & 1) ^ 1);
+            mbar_expect_tx_e(&qd_full[st], 2 * kTileBytes);
+            uint8_t *dst = smem + kB_QD + st * 2 * kTileBytes;
+            tma_load_3d_e(dst, &qmap, &qd_full[st], 0, h, i * kBM);
+            tma_load_3d_e(dst + kTileBytes, &dmap, &qd_full[st], 0, h, i * kBM);
+        }
+    } else if (warp == 1) {
+        // ===================== MMA issuer =====================
+        const uint32_t id_s = idesc_bf16(kBN, kBM);           // M = keys, N = queries
+        const uint32_t id_g = idesc_bf16(kBN, kD, 0, 1);      // dV / dK: A K-major, B MN-major
+        const uint32_t id_q = idesc_bf16(kBM, kD, 1, 1);      // dQ: A (dS) MN-major, B MN-major
+        const uint64_t kd = sdesc_sw(smem_u32(smem + kB_K), 1024, 2);
+        const uint64_t vd = sdesc_sw(smem_u32(smem + kB_V), 1024, 2);
+        const uint64_t kmn = sdesc_mn(smem_u32(smem + kB_K), 8192, 1024, 2);
+        mbar_wait(kv_full, 0);
+        auto issue_grads = [&](int j) {
+            const int b = j & 1;
+            mbar_wait(&p_full[b], (j >> 1) & 1);
+            tc_fence_after();
+            uint8_t *qdst = smem + kB_QD + b * 2 * kTileBytes;
+            uint8_t *ps = smem + kB_PS + b * 2 * kPBytes;
+            const uint64_t pt = sdesc_sw(smem_u32(ps), 1024, 2);
+            const uint64_t dst_k = sdesc_sw(smem_u32(ps + kPBytes), 1024, 2);
+            const uint64_t ds_mn = sdesc_mn(smem_u32(ps + kPBytes), kBM * 128, 1024, 2);
+            const uint64_t q_mn = sdesc_mn(smem_u32(qdst), 8192, 1024, 2);
+            const uint64_t do_mn = sdesc_mn(smem_u32(qdst + kTileBytes), 8192, 1024, 2);
+#pragma unroll
+            for (int k = 0; k < kBM / 16; ++k) {
+                const uint32_t a = ((k >> 2) * (kBN * 128) + (k & 3) * 32) >> 4;
+                const uint32_t bb = (k * 16 * 128) >> 4;
+                const uint32_t acc = (j > 0 || k > 0) ? 1u : 0u;
+                mma_bf16_e(tmem + kColDV, pt + a, do_mn + bb, id_g, acc);
+                mma_bf16_e(tmem + kColDK, dst_k + a, q_mn + bb, id_g, acc);
+            }
+            if (j >= 2) mbar_wait(&dq_empty[b], ((j >> 1) & 1) ^ 1);
+            tc_fence_after();
+#pragma unroll
+            for (int k = 0; k < kBN / 16; ++k) {
+                const uint32_t a = (k * 16 * 128) >> 4;     // 16 key rows of dS^T
+                mma_bf16_e(tmem + kColDQ + b * kD, ds_mn + a, kmn + a, id_q, k ? 1u : 0u);
+            }
+            mma_commit_e(&p_empty[b]);
+            mma_commit_e(&qd_empty[b]);
+            mma_commit_e(&dq_full[b]);
+        };
+        for (int i = 0; i < nq; ++i) {
+            const int st = i & 1;
+            mbar_wait(&qd_full[st], (i >> 1) & 1);
+            if (i >= 1) mbar_wait(s_free, (i - 1) & 1);
+            tc_fence_after();
+            uint8_t *qdst = smem + kB_QD + st * 2 * kTileBytes;
+            const uint64_t qk = sdesc_sw(smem_u32(qdst), 1024, 2);
+            const uint64_t dok = sdesc_sw(smem_u32(qdst + kTileBytes), 1024, 2);
+#pragma unroll
+            for (int k = 0; k < kD / 16; ++k) {
+                mma_bf16_e(tmem + kColST, kd + ((k * 32) >> 4), qk + ((k * 32) >> 4), id_s,
+                           k ? 1u : 0u);
+                mma_bf16_e(tmem + kColDP, vd + ((k * 32) >> 4), dok + ((k * 32) >> 4), id_s,
+                           k ? 1u : 0u);
+            }
+            mma_commit_e(s_full);
+            if (i >= 1) issue_grads(i - 1);
+        }
+        if (nq >= 1) issue_grads(nq - 1);
+    } else if (warp < 6) {
+        // ===================== P^T / dS^T (thread = key row) =====================
+        const int quarter = warp & 3;
+        const int rl = quarter * 32 + lane;
+        const int tid = threadIdx.x - 64;                 // 0..127
+        const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
+        for (int i = 0; i < nq; ++i) {
+            const int b = i & 1;
+            {
+                const int qrow = i * kBM + tid;
+                const bool qv = qrow < p.sq;
+                const size_t qi = (size_t)qrow * p.H + h;
+                lse2_s[b * 128 + tid] = qv ? p.lse[qi] * kLog2e : INFINITY;
+                delta_s[b * 128 + tid] = qv ? p.delta[qi] : 0.f;
+            }
+            named_bar(1, 128);
+            if (i >= 2) mbar_wait(&p_empty[b], ((i >> 1) & 1) ^ 1);
+            mbar_wait(s_full, i & 1);
+            tc_fence_after();
+            uint8_t *ps = smem + kB_PS + b * 2 * kPBytes + rl * 128;
+            const float *L2 = lse2_s + b * 128;
+            const float *Dl = delta_s + b * 128;
+#pragma unroll 1
+            for (int c0 = 0; c0 < kBM; c0 += 32) {
+                uint32_t sv[32], dv[32];
+                tmem_ld16(lane_base + kColST + c0, *reinterpret_cast<uint32_t(*)[16]>(sv));
+                tmem_ld16(lane_base + kColST + c0 + 16, *reinterpret_cast<uint32_t(*)[16]>(sv + 16));
+                tmem_ld16(lane_base + kColDP + c0, *reinterpret_cast<uint32_t(*)[16]>(dv));
+                tmem_ld16(lane_base + kColDP + c0 + 16, *reinterpret_cast<uint32_t(*)[16]>(dv + 16));
+                tmem_wait_ld();
+                if (c0 + 32 >= kBM) {
+                    tc_fence_before();
+                    mbar_arrive(s_free);   // S^T / dP^T TMEM may be overwritten
+                }
+#pragma unroll
+                for (int g = 0; g < 4; ++g) {
+                    float pe[8], de[8];
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) {
+                        const int qc = c0 + g * 8 + e;
+                        const float pv = ex2(__uint_as_float(sv[g * 8 + e]) * p.c - L2[qc]);
+                        pe[e] = pv;
+                        de[e] = p.scale * pv * (__uint_as_float(dv[g * 8 + e]) - Dl[qc]);
+                    }
+                    const int c = (c0 >> 3) + g;      // 16-B chunk index along q
+                    const int off = (c >> 3) * (kBN * 128) + (((c & 7) ^ (rl & 7)) << 4);
+                    uint4 pk, dk4;
+                    pk.x = pack_bf16(pe[0], pe[1]); pk.y = pack_bf16(pe[2], pe[3]);
+                    pk.z = pack_bf16(pe[4], pe[5]); pk.w = pack_bf16(pe[6], pe[7]);
+                    dk4.x = pack_bf16(de[0], de[1]); dk4.y = pack_bf16(de[2], de[3]);
+                    dk4.z = pack_bf16(de[4], de[5]); dk4.w = pack_bf16(de[6], de[7]);
+                    *reinterpret_cast<uint4 *>(ps + off) = pk;
+                    *reinterpret_cast<uint4 *>(ps + kPBytes + off) = dk4;
+                }
+            }
+            fence_async_smem();
+            tc_fence_before();
+            mbar_arrive(&p_full[b]);
+        }
+        // dK, dV (+=) once the last gradient MMAs have landed
+        if (nq >= 1) mbar_wait(&p_empty[(nq - 1) & 1], ((nq - 1) >> 1) & 1);
+        tc_fence_after();
+        const int key = k0 + rl;
+        const bool kv_ok = key < p.sk;
+        const size_t ki = ((size_t)key * p.H + h) * kD;
+        for (int c = 0; c < kD; c += 16) {
+            uint32_t a[16], bq[16];
+            tmem_ld16(lane_base + kColDV + c, a);
+            tmem_ld16(lane_base + kColDK + c, bq);
+            tmem_wait_ld();
+            if (kv_ok) {
+                float4 *pv = reinterpret_cast<float4 *>(p.dv + ki + c);
+                float4 *pk = reinterpret_cast<float4 *>(p.dk + ki + c);
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    float4 x = pv[e], y = pk[e];
+                    x.x += __uint_as_float(a[4 * e]); x.y += __uint_as_float(a[4 * e + 1]);
+                    x.z += __uint_as_float(a[4 * e + 2]); x.w += __uint_as_float(a[4 * e + 3]);
+                    y.x += __uint_as_float(bq[4 * e]); y.y += __uint_as_float(bq[4 * e + 1]);
+                    y.z += __uint_as_float(bq[4 * e + 2]); y.w += __uint_as_float(bq[4 * e + 3]);
+                    pv[e] = x;
+                    pk[e] = y;
+                }
+            }
+        }
+    } else {
+        // ===================== dQ epilogue (thread = query row) =====================
+        const int quarter = warp & 3;
+        const int rl = quarter * 32 + lane;
+        const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
+        for (int i = 0; i < nq; ++i) {
+            const int b = i & 1;
+            mbar_wait(&dq_full[b], (i >> 1) & 1);
+            tc_fence_after();
+            const int qrow = i * kBM + rl;
+            const bool qv = qrow < p.sq;
+            float *dst = p.dq + ((size_t)qrow * p.H + h) * kD;
+            for (int c = 0; c < kD; c += 16) {
+                uint32_t a[16];
+                tmem_ld16(lane_base + kColDQ + b * kD + c, a);
+                tmem_wait_ld();
+                if (qv) {
+#pragma unroll
+                    for (int e = 0; e < 4; ++e)
+                        atomicAdd(reinterpret_cast<float4 *>(dst + c) + e,
+                                  make_float4(__uint_as_float(a[4 * e]), __uint_as_float(a[4 * e + 1]),
+                                              __uint_as_float(a[4 * e + 2]),
+                                              __uint_as_float(a[4 * e + 3])));
+                }
+            }
+            tc_fence_before();
+            mbar_arrive(&dq_empty[b]);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        tc_fence_after();
+        tmem_dealloc(tmem, 512);
+    }
+}
+
 // [S, H, 64] bf16 view with element strides (row, head): box 64 x 1 x 128,
 // 128-B swizzle.
 int head_map(CUtensorMap *m, const void *base, int64_t rows, int64_t heads, int64_t rs, int64_t hs) {
@@ -289,8 +574,6 @@ int attn_tc_eligible(const dp_attn_geom *g, int dtype) {
     if (g->sq > (1 << 30) || g->sk > (1 << 30)) return 0;
     return 1;
 }
-
-int attn_bwd_tc_eligible(const dp_attn_geom *, int) { return 0; }
 
 int attn_fwd_update_tc_launch(const dp_attn_geom *g, const void *q, const void *k, const void *v,
                               void *m, void *l, void *acc, cudaStream_t st) {
@@ -317,11 +600,40 @@ int attn_fwd_update_tc_launch(const dp_attn_geom *g, const void *q, const void *
     return launch_status("attn_fwd_tc_kernel");
 }
 
-int attn_bwd_update_tc_launch(const dp_attn_geom *, const void *, const void *, const void *,
-                              const void *, const void *, const void *, void *, void *, void *,
-                              cudaStream_t) {
-    set_error("attn_tc: backward not built yet");
-    return DP_ERR_UNSUPPORTED;
+int attn_bwd_tc_eligible(const dp_attn_geom *g, int dtype) {
+    if (!attn_tc_eligible(g, dtype)) return 0;
+    return (g->o_rs % 8 == 0 && g->o_hs % 8 == 0) ? 1 : 0;
+}
+
+int attn_bwd_update_tc_launch(const dp_attn_geom *g, const void *q, const void *k, const void *v,
+                              const void *dout, const void *lse, const void *delta, void *dq,
+                              void *dk, void *dv, cudaStream_t st) {
+    DP_REQUIRE(attn_bwd_tc_eligible(g, DP_BF16), DP_ERR_UNSUPPORTED,
+               "attn_tc bwd: outside the envelope");
+    if (g->sq == 0 || g->sk == 0) return DP_OK;
+    CUtensorMap qm, km, vm, dm;
+    int rc = head_map(&qm, q, g->sq, g->heads, g->q_rs, g->q_hs);
+    if (!rc) rc = head_map(&km, k, g->sk, g->heads, g->k_rs, g->k_hs);
+    if (!rc) rc = head_map(&vm, v, g->sk, g->heads, g->v_rs, g->v_hs);
+    if (!rc) rc = head_map(&dm, dout, g->sq, g->heads, g->o_rs, g->o_hs);
+    if (rc) return rc;
+    BwdParams p;
+    p.sq = (int)g->sq;
+    p.sk = (int)g->sk;
+    p.H = (int)g->heads;
+    p.n_kt = (int)((g->sk + kBN - 1) / kBN);
+    p.c = (float)(g->scale * 1.4426950408889634);
+    p.scale = (float)g->scale;
+    p.lse = (const float *)lse;
+    p.delta = (const float *)delta;
+    p.dq = (float *)dq;
+    p.dk = (float *)dk;
+    p.dv = (float *)dv;
+    DP_CUDA_CHECK(cudaFuncSetAttribute(attn_bwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       kSmemBwd));
+    const int64_t grid = (int64_t)p.n_kt * p.H;
+    attn_bwd_tc_kernel<<<(unsigned)grid, kBwdThreads, kSmemBwd, st>>>(qm, km, vm, dm, p);
+    return launch_status("attn_bwd_tc_kernel");
 }
 
 }  // namespace dp

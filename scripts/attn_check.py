@@ -68,3 +68,55 @@ for (sq, sk) in ((8192, 8192), (16384, 16384), (65536, 65536)):
     ms = e0.elapsed_time(e1) / n
     fl = 4.0 * sq * sk * d * Hh
     print(f"fwd block sq={sq} sk={sk} H={Hh}: {ms:.3f} ms  {fl / ms / 1e9:.1f} TFLOP/s")
+
+# ---- backward: tcgen05 vs CUDA-core vs fp64 autograd ----
+S2, H2 = int(os.environ.get("BS", "700")), 2
+q2, k2, v2, do2 = (torch.randn(S2, H2, d, device=dev).to(torch.bfloat16) for _ in range(4))
+qd, kd, vd = (t.double().requires_grad_() for t in (q2, k2, v2))
+att = torch.softmax(torch.einsum("qhd,khd->hqk", qd, kd) * scale, -1)
+od = torch.einsum("hqk,khd->qhd", att, vd)
+od.backward(do2.double())
+
+
+def bwd(algo):
+    kernels.set_algo(algo)
+    out, lse = run(algo, q2, k2, v2)
+    delta = torch.empty((S2, H2), device=dev)
+    kernels.attn_bwd_preprocess(out, do2, delta)
+    dq = torch.zeros((S2, H2, d), device=dev)
+    dk = torch.zeros_like(dq)
+    dv = torch.zeros_like(dq)
+    cuts = [0, S2 // 3, S2]
+    for a, b in zip(cuts[:-1], cuts[1:]):
+        kernels.attn_bwd_update(q2, k2[a:b], v2[a:b], do2, lse, delta, dq, dk[a:b], dv[a:b], scale)
+    return dq, dk, dv
+
+
+for algo in ("tc", "simt"):
+    g = bwd(algo)
+    errs = [((a.double() - b.grad).abs().max() / b.grad.abs().max()).item()
+            for a, b in zip(g, (qd, kd, vd))]
+    print(f"bwd {algo}: rel err dq {errs[0]:.3e} dk {errs[1]:.3e} dv {errs[2]:.3e}")
+
+for (sq, sk) in ((8192, 8192), (65536, 65536)):
+    Hh = 16
+    qq, kk, vv, dd = (torch.randn(sq if i in (0, 3) else sk, Hh, d, device=dev).to(torch.bfloat16)
+                      for i in range(4))
+    lse = torch.randn(sq, Hh, device=dev) + 10
+    delta = torch.randn(sq, Hh, device=dev)
+    dq = torch.zeros((sq, Hh, d), device=dev)
+    dk = torch.zeros((sk, Hh, d), device=dev)
+    dv = torch.zeros_like(dk)
+    kernels.set_algo("tc")
+    kernels.attn_bwd_update(qq, kk, vv, dd, lse, delta, dq, dk, dv, scale)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    n = 2
+    e0.record()
+    for _ in range(n):
+        kernels.attn_bwd_update(qq, kk, vv, dd, lse, delta, dq, dk, dv, scale)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / n
+    fl = 2.5 * 4.0 * sq * sk * d * Hh
+    print(f"bwd block sq={sq} sk={sk} H={Hh}: {ms:.3f} ms  {fl / ms / 1e9:.1f} TFLOP/s")
