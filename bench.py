@@ -200,14 +200,15 @@ class KernelTimer:
         import torch
 
         timer = self
-        for name in ("conv_fwd", "conv_dgrad", "conv_wgrad"):
+        for name in ("conv_fwd", "conv_dgrad", "conv_wgrad", "attn_fwd_update",
+                     "attn_bwd_update"):
             orig = getattr(kernels_mod, name)
 
             def make(orig=orig, name=name):
                 def inner(*a, **kw):
                     if not timer.active:
                         return orig(*a, **kw)
-                    flops = conv_flops(name, a, kw)
+                    flops = kernel_work(name, a, kw)
                     s = torch.cuda.Event(enable_timing=True)
                     e = torch.cuda.Event(enable_timing=True)
                     s.record()
@@ -230,10 +231,12 @@ class KernelTimer:
         return out
 
 
-def conv_flops(name, a, kw):
-    """Algorithmic FLOPs of one conv call = 2 * C_in * C_out * taps * output
-    positions of the forward conv it belongs to (dgrad and wgrad count the
-    same MACs as the forward, the usual convention)."""
+def kernel_work(name, a, kw):
+    """Algorithmic work of one wrapped call: FLOPs for conv / attention
+    (conv: 2 * C_in * C_out * taps * output positions of the forward conv it
+    belongs to — dgrad and wgrad count the same MACs; attention fwd block:
+    4 * sq * sk * d * H; bwd block: 2.5x that, the 5-GEMM convention of
+    SURVEY 8(d))."""
     import math
 
     if name == "conv_fwd":
@@ -242,9 +245,14 @@ def conv_flops(name, a, kw):
     elif name == "conv_dgrad":
         dy, w = a[0], a[1]
         pos = dy.shape[0] * math.prod(dy.shape[2:])
-    else:
+    elif name == "conv_wgrad":
         x, _, dy, w = a[0], a[1], a[2], a[3]
         pos = dy.shape[0] * math.prod(dy.shape[2:])
+    else:  # attention blocks
+        q, k = a[0], a[1]
+        heads = q.shape[1] if q.dim() == 3 else 1
+        f = 4.0 * q.shape[0] * k.shape[0] * q.shape[-1] * heads
+        return f * (2.5 if name == "attn_bwd_update" else 1.0)
     return 2.0 * w.shape[0] * w.shape[1] * math.prod(w.shape[2:]) * pos
 
 
@@ -277,8 +285,8 @@ def setup_cfg2(ctx):
                     dtype=torch.bfloat16).contiguous(memory_format=fmt)
     xst = dp.ShardTensor(x, (1, C0, G, G, G), ctx, (dp.Shard(2),), {0: tuple(ext)})
 
-    def step(xin=None):
-        st = xst if xin is None else dp.ShardTensor(xin, xst.global_shape, ctx, xst.placements,
+    def step(ins=None):
+        st = xst if ins is None else dp.ShardTensor(ins[0], xst.global_shape, ctx, xst.placements,
                                                     xst.shard_shapes)
         y1, t1 = dp.halo_conv_forward(st, w1, 1, 1)
         y2, t2 = dp.halo_conv_forward(y1, w2, 1, 1)
@@ -293,7 +301,7 @@ def setup_cfg2(ctx):
             "layout": "NDHWC (channels_last_3d)", "shard_extents": list(ext),
             "parallelism": f"domain{R}",
             "l2": "inputs larger than L2 (512 MiB activations per layer), no flush"}
-    return dict(step=step, x=x, flops=flops, info=info, scaling="strong", dtype="bf16",
+    return dict(step=step, inputs=[x], flops=flops, info=info, scaling="strong", dtype="bf16",
                 unit="samples/s", samples_per_step=1)
 
 
@@ -326,9 +334,167 @@ def cpu_sample_cfg2(threads: int):
     return dt, threads / 1024.0
 
 
+def setup_cfg3(ctx):
+    """Ring attention, ViT-style 64k-token sequence, 16 heads, d = 64, bf16,
+    sequence-sharded (Shard(0), default_chunk) over the N ranks.  One step =
+    ring_attention forward + backward (R-1 K||V hops forward, R (K,V,dK,dV)
+    hops backward) against a fixed synthetic dO."""
+    import torch
+
+    import paper_2605_11111_b200 as dp
+
+    S, H, D = 65536, 16, 64
+    R = ctx.mesh.world_size
+    me = ctx.rank_id
+    dev = ctx.device
+    ext = dp.default_chunk(S, R)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(4321 + me)
+    q, k, v, do = (torch.randn((ext[me], H, D), generator=gen, device=dev,
+                               dtype=torch.bfloat16) for _ in range(4))
+    shards = {0: tuple(ext)}
+    kst = dp.ShardTensor(k, (S, H, D), ctx, (dp.Shard(0),), shards)
+    vst = dp.ShardTensor(v, (S, H, D), ctx, (dp.Shard(0),), shards)
+    qst = dp.ShardTensor(q, (S, H, D), ctx, (dp.Shard(0),), shards)
+
+    def step(ins=None):
+        if ins is None:
+            qs, ks, vs, g = qst, kst, vst, do
+        else:
+            qs, ks, vs = (dp.ShardTensor(t, (S, H, D), ctx, (dp.Shard(0),), shards)
+                          for t in ins[:3])
+            g = ins[3]
+        out, tape = dp.ring_attention_forward(qs, ks, vs)
+        dq, dk, dv = dp.ring_attention_backward(tape, g)
+        return dq.local, dk.local, dv.local
+
+    flops = 3.5 * 4.0 * S * S * D * H  # fwd + 2.5x bwd
+    info = {"workload": "cfg3: ring-attention SDPA, ViT-style 64k-token sequence, 16 heads, "
+                        "d=64, bf16, non-causal, scale 1/8, sequence-sharded",
+            "global_batch": 1, "seq_len": S, "heads": H, "head_dim": D,
+            "shard_extents": list(ext), "parallelism": f"ring{R}",
+            "l2": "inputs (q,k,v,dO 8 MiB/head-tile stream, 512 MiB total) exceed L2, no flush"}
+    return dict(step=step, inputs=[q, k, v, do], flops=flops, info=info, scaling="strong",
+                dtype="bf16", unit="samples/s", samples_per_step=1)
+
+
+def cpu_sample_cfg3(threads: int):
+    """Oracle port on a bounded sample: per thread one head's 128 query rows
+    against all 65536 keys, fwd + bwd in fp64 softmax (1/8192 of the cfg3
+    fwd+bwd work each)."""
+    import numpy as np
+
+    from oracle import workloads
+
+    rng = np.random.default_rng(0)
+    S, D, rows = 65536, 64, 128
+    k = rng.standard_normal((S, D)).astype(np.float32)
+    v = rng.standard_normal((S, D)).astype(np.float32)
+    jobs = [(rng.standard_normal((rows, D)).astype(np.float32),
+             rng.standard_normal((rows, D)).astype(np.float32)) for _ in range(threads)]
+    t0 = time.perf_counter()
+    if threads == 1:
+        workloads.attention_step(jobs[0][0], k, v, jobs[0][1])
+    else:
+        from concurrent.futures import ThreadPoolExecutor
+
+        with ThreadPoolExecutor(threads) as ex:
+            list(ex.map(lambda j: workloads.attention_step(j[0], k, v, j[1]), jobs))
+    dt = time.perf_counter() - t0
+    return dt, threads * rows / (S * 16.0)
+
+
+def setup_cfg4(ctx):
+    """Weak-scaling 2-D conv stack: 4 x conv(64->64, 3x3, s1, p1), 2048^2
+    per GPU (global [1, 64, 2048*R, 2048], Shard(2)), bf16 NHWC.  One step
+    = forward of the 4 layers + backward (dgrad incl. the stack input,
+    wgrad, reverse halos, dW all-reduces)."""
+    import torch
+
+    import paper_2605_11111_b200 as dp
+
+    C, L, Hper, W = 64, 4, 2048, 2048
+    R = ctx.mesh.world_size
+    me = ctx.rank_id
+    dev = ctx.device
+    G = Hper * R
+    ext = [Hper] * R
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(99 + me)
+    fmt = torch.channels_last
+    x = torch.randn((1, C, Hper, W), generator=gen, device=dev,
+                    dtype=torch.bfloat16).contiguous(memory_format=fmt)
+    wg = torch.Generator(device=dev)
+    wg.manual_seed(11)
+    ws = [(torch.randn((C, C, 3, 3), generator=wg, device=dev) * 0.05).to(torch.bfloat16)
+          for _ in range(L)]
+    plans = []
+    cur = ext
+    for _ in range(L):
+        pl = dp.halo_conv_plan(cur, G, 3, 1, 1)
+        plans.append(pl)
+        cur = list(pl.out_extents)
+    g = torch.randn((1, C, cur[me], W), generator=gen, device=dev,
+                    dtype=torch.bfloat16).contiguous(memory_format=fmt)
+    xst = dp.ShardTensor(x, (1, C, G, W), ctx, (dp.Shard(2),), {0: tuple(ext)})
+
+    def step(ins=None):
+        st = xst if ins is None else dp.ShardTensor(ins[0], xst.global_shape, ctx, xst.placements,
+                                                    xst.shard_shapes)
+        tapes = []
+        for w in ws:
+            st, t = dp.halo_conv_forward(st, w, 1, 1)
+            tapes.append(t)
+        dy = g
+        dws = []
+        for t in reversed(tapes):
+            dxs, dw = dp.halo_conv_backward(t, dy)
+            dy = dxs.local
+            dws.append(dw)
+        return dws
+
+    flops = 3 * L * 2.0 * C * C * 9 * Hper * W
+    info = {"workload": "cfg4: weak-scaling conv2d stack, 4 x conv(64->64, 3x3, s1 p1), "
+                        "2048^2 per GPU, bf16, H-sharded",
+            "global_batch": 1, "grid_per_gpu": [Hper, W], "channels": C, "layers": L,
+            "layout": "NHWC (channels_last)", "shard_extents": ext, "parallelism": f"domain{R}",
+            "l2": "inputs larger than L2 (512 MiB activations per layer), no flush"}
+    return dict(step=step, inputs=[x], flops=flops, info=info, scaling="weak", dtype="bf16",
+                unit="samples/s", samples_per_step=1)
+
+
+def cpu_sample_cfg4(threads: int):
+    """Oracle port on a bounded sample: per thread a 1 x 64 x 16 x 256 tile
+    through the 4-layer stack fwd+bwd (1/1024 of one GPU's 2048^2 step)."""
+    import numpy as np
+
+    from oracle import workloads
+
+    rng = np.random.default_rng(0)
+    ws = [(rng.standard_normal((64, 64, 3, 3)) * 0.05).astype(np.float32) for _ in range(4)]
+    jobs = [(rng.standard_normal((1, 64, 16, 256)).astype(np.float32),
+             rng.standard_normal((1, 64, 16, 256)).astype(np.float32)) for _ in range(threads)]
+    t0 = time.perf_counter()
+    if threads == 1:
+        workloads.conv_stack_step(jobs[0][0], ws, jobs[0][1])
+    else:
+        from concurrent.futures import ThreadPoolExecutor
+
+        with ThreadPoolExecutor(threads) as ex:
+            list(ex.map(lambda j: workloads.conv_stack_step(j[0], ws, j[1]), jobs))
+    dt = time.perf_counter() - t0
+    return dt, threads / 1024.0
+
+
 CONFIGS = {"cfg2": (setup_cfg2, cpu_sample_cfg2,
                     "1 x 256 x 64 voxel sub-volumes (1/1024 of the 256^3 volume each), fp32, "
-                    "block fwd+bwd via the oracle port of dense.conv's einsum")}
+                    "block fwd+bwd via the oracle port of dense.conv's einsum"),
+           "cfg3": (setup_cfg3, cpu_sample_cfg3,
+                    "one head's 128 query rows vs all 65536 keys (1/8192 of the cfg3 step), "
+                    "fp32 in / fp64 softmax, fwd+bwd via the oracle port"),
+           "cfg4": (setup_cfg4, cpu_sample_cfg4,
+                    "1 x 64 x 16 x 256 tiles (1/1024 of one GPU's 2048^2 stack step), fp32, "
+                    "4-layer fwd+bwd via the oracle port")}
 
 
 # ---------------------------------------------------------------------------
@@ -355,7 +521,8 @@ def run_reference(args):
     line = {"impl": "reference", "metric": "sharded fwd+bwd step latency & samples/s",
             "value": value, "unit": "samples/s", "n_gpus": args.gpus, "steps": len(times),
             "warmup": args.warmup, "ms_per_step": 1000.0 / value, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "scaling": "weak" if args.config == "cfg4" else "strong", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic",
             "config": {"workload": args.config, "sample": sample_desc},
             "cpu_baseline": {"value": value, "unit": "samples/s", "cores": cores,
                              "kind": "port", "sample": f"{cores} x {sample_desc}"},
@@ -411,14 +578,18 @@ def main():
     # its weight gradients back; the copy for step i+1 runs on a copy stream
     # while step i computes (double-buffered input, as a training loop's
     # prefetcher would), so the timed region = first H2D + K steps + last D2H.
-    x = W["x"]
-    host = torch.empty_strided(x.shape, x.stride(), dtype=x.dtype, pin_memory=True)
-    host.copy_(x)
-    bufs = [torch.empty_strided(x.shape, x.stride(), dtype=x.dtype, device=x.device)
-            for _ in range(2)]
+    ins = W["inputs"]
+    hosts = []
+    for t in ins:
+        h = torch.empty_strided(t.shape, t.stride(), dtype=t.dtype, pin_memory=True)
+        h.copy_(t)
+        hosts.append(h)
+    bufs = [[torch.empty_strided(t.shape, t.stride(), dtype=t.dtype, device=t.device)
+             for t in ins] for _ in range(2)]
     outs = step()
     host_out = [torch.empty(o.shape, dtype=o.dtype, pin_memory=True) for o in outs]
     d2h = sum(o.numel() * o.element_size() for o in outs)
+    h2d = sum(t.numel() * t.element_size() for t in ins)
     copy_stream = torch.cuda.Stream(device=ctx.device)
     compute = torch.cuda.current_stream()
     e2e_steps = max(1, args.steps)
@@ -427,10 +598,15 @@ def main():
     e_end = torch.cuda.Event(enable_timing=True)
     ready = [torch.cuda.Event() for _ in range(2)]
     free = [torch.cuda.Event() for _ in range(2)]
+
+    def upload(slot):
+        for dst, src in zip(bufs[slot], hosts):
+            dst.copy_(src, non_blocking=True)
+
     e_start.record(compute)
     with torch.cuda.stream(copy_stream):
         copy_stream.wait_event(e_start)
-        bufs[0].copy_(host, non_blocking=True)
+        upload(0)
         ready[0].record(copy_stream)
     for i in range(e2e_steps):
         cur = i % 2
@@ -439,7 +615,7 @@ def main():
             with torch.cuda.stream(copy_stream):
                 if i >= 1:
                     copy_stream.wait_event(free[nxt])
-                bufs[nxt].copy_(host, non_blocking=True)
+                upload(nxt)
                 ready[nxt].record(copy_stream)
         compute.wait_event(ready[cur])
         outs = step(bufs[cur])
@@ -471,7 +647,8 @@ def main():
             with open(tpath) as f:
                 tab = json.load(f).get(args.config, {})
             pat = {"conv_wgrad": "conv_wgrad_tc_kernel", "conv_fwd": "conv_tc_kernel",
-                   "conv_dgrad": "conv_tc_kernel"}.get(name, name)
+                   "conv_dgrad": "conv_tc_kernel", "attn_fwd_update": "attn_fwd_tc_kernel",
+                   "attn_bwd_update": "attn_bwd_tc_kernel"}.get(name, name)
             hits = [v for k, v in tab.items() if pat in k]
             if hits:
                 traffic = sum(hits) / len(hits)
@@ -485,7 +662,6 @@ def main():
         dt, frac = cpu_fn(1)
         cpu = {"value": frac / dt, "unit": W["unit"], "cores": 1, "kind": "port",
                "sample": sample_desc, "seconds": dt}
-    h2d = x.numel() * x.element_size()
     line = {
         "metric": "sharded fwd+bwd step latency & samples/s",
         "value": value, "unit": W["unit"], "n_gpus": ctx.mesh.world_size, "steps": args.steps,
@@ -495,8 +671,8 @@ def main():
         "roofline": roof, "cpu_baseline": cpu,
         "e2e": {"value": samples / (e2e_ms / 1000.0), "unit": W["unit"], "ms_per_step": e2e_ms,
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": e2e_steps,
-                "note": "pinned H2D of each step's input shard (prefetched one step ahead on "
-                        "a copy stream) + D2H of dW every step, through the public API"},
+                "note": "pinned H2D of each step's input shards (prefetched one step ahead on "
+                        "a copy stream) + D2H of the step's gradients, through the public API"},
         "gpu_launches": launches // args.steps * args.steps,
         "gpu_launches_per_step": launches / args.steps,
         "clocks": clk.summary(),

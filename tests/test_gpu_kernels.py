@@ -211,3 +211,61 @@ def test_conv_tc_fwd_dgrad_vs_oracle(case):
         assert rel_err(to_np(dw), gw) < 1e-3
     finally:
         k.set_algo(prev)
+
+
+ATTN_TC_CASES = [
+    # sq, sk, heads, key-block cuts (ring steps folded one after another)
+    (128, 128, 1, [128]),
+    (200, 300, 2, [0, 37, 300]),          # partial tiles, an uneven split
+    (1000, 513, 3, [100, 100, 513]),      # includes an empty block (no-op)
+    (64, 1030, 2, [1030]),
+    (384, 256, 4, [1, 256]),              # a one-key block
+]
+
+
+@pytest.mark.parametrize("case", ATTN_TC_CASES)
+@pytest.mark.parametrize("payload", [False, True])
+def test_attention_tc_fwd_bwd_vs_oracle(case, payload):
+    """tcgen05 path forced: forward fold + finalize and the backward block
+    over K/V blocks taken from the ring's [S, 2, H, d] K||V payload (strided
+    views) or from plain tensors; bf16, d = 64; vs fp64 oracle."""
+    k = kernels()
+    sq, sk, h, cuts = case
+    d = 64
+    rng = np.random.default_rng(sq * 7 + sk)
+    q, kk, v, do = (torch.tensor(rng.standard_normal((n, h, d))).to(torch.bfloat16)
+                    for n in (sq, sk, sk, sq))
+    qd = q.to(DEV)
+    if payload:
+        pay = torch.stack([kk, v], dim=1).to(DEV)  # [sk, 2, H, d]
+        kd, vd = pay[:, 0], pay[:, 1]
+    else:
+        kd, vd = kk.to(DEV), v.to(DEV)
+    dod = do.to(DEV)
+    scale = 1.0 / math.sqrt(d)
+    bounds = [0] + [c for c in cuts]
+    bounds = sorted(set(min(b, sk) for b in bounds) | {sk})
+    prev = k.set_algo("tc")
+    try:
+        m = torch.full((sq, h), -math.inf, device=DEV)
+        l = torch.zeros((sq, h), device=DEV)
+        acc = torch.zeros((sq, h, d), device=DEV)
+        for a, b in zip(bounds[:-1], bounds[1:]):
+            k.attn_fwd_update(qd, kd[a:b], vd[a:b], m, l, acc, scale)
+        out = torch.empty_like(qd)
+        lse = torch.empty_like(m)
+        k.attn_finalize(qd, m, l, acc, out, lse, 1.0)
+        delta = torch.empty((sq, h), device=DEV)
+        k.attn_bwd_preprocess(out, dod, delta)
+        dq = torch.zeros((sq, h, d), device=DEV)
+        dk = torch.zeros((sk, h, d), device=DEV)
+        dv = torch.zeros_like(dk)
+        for a, b in zip(bounds[:-1], bounds[1:]):
+            k.attn_bwd_update(qd, kd[a:b], vd[a:b], dod, lse, delta, dq, dk[a:b], dv[a:b], scale)
+        torch.cuda.synchronize()
+    finally:
+        k.set_algo(prev)
+    qr, kr, vr, dr = (to_np(t).astype(np.float64) for t in (q, kk, v, do))
+    assert rel_err(to_np(out), oatt.sdpa(qr, kr, vr)) < 1.5e-2
+    for got, want in zip((dq, dk, dv), oatt.sdpa_grads(qr, kr, vr, dr)):
+        assert rel_err(to_np(got), want, floor=1.0) < 1.5e-2
