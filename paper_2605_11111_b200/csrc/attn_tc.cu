@@ -32,24 +32,28 @@ constexpr int kBM = 128;      // query rows per tile
 constexpr int kBN = 128;      // keys per block
 constexpr int kD = 64;        // head dim
 constexpr int kStages = 3;    // K/V ring depth
-constexpr int kThreads = 192;
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kRescale = 8.0f;  // log2 units: rescale when the max grows by > 2^8
 
 constexpr int kTileBytes = kBM * kD * 2;           // 16 KB (Q, K or V tile)
 constexpr int kPBytes = kBM * kBN * 2;             // 32 KB (P tile)
+
+// Forward: two 128-row query tiles per CTA (two softmax warpgroups that
+// ping-pong against the single MMA warp).
+constexpr int kFwdTiles = 2;
+constexpr int kFwdThreads = 128 + 128 * kFwdTiles;  // WG0: TMA + MMA warps; WG1..: softmax
 constexpr int kSmemQ = 0;
-constexpr int kSmemKV = kSmemQ + kTileBytes;       // stages of [K | V]
+constexpr int kSmemKV = kSmemQ + kFwdTiles * kTileBytes;  // stages of [K | V]
 constexpr int kSmemP = kSmemKV + kStages * 2 * kTileBytes;
-constexpr int kSmemBar = kSmemP + 2 * kPBytes;
+constexpr int kSmemBar = kSmemP + kFwdTiles * kPBytes;
 constexpr int kSmemFwd = kSmemBar + 256;
 
-// TMEM columns: S0 [0,128), S1 [128,256), O [256,320)
+// TMEM columns: S_t [128 t, 128 t + 128), O_t [256 + 64 t, 256 + 64 t + 64)
 constexpr uint32_t kColS = 0, kColO = 256;
 
 struct FwdParams {
     int sq, sk, H;
-    int n_qt;
+    int n_qt;                 // CTAs per head (kFwdTiles query tiles each)
     float c;                  // scale * log2(e)
     float *m, *l, *acc;       // fp32 state: [sq,H], [sq,H], [sq,H,64]
 };
@@ -59,24 +63,42 @@ __device__ __forceinline__ float ex2(float x) {
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
 }
+// packed fp32x2 FMA / add (sm_100 FFMA2 / FADD2): two scores per instruction
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+    float2 d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;"
+        : "=l"(*reinterpret_cast<unsigned long long *>(&d))
+        : "l"(*reinterpret_cast<unsigned long long *>(&a)),
+          "l"(*reinterpret_cast<unsigned long long *>(&b)),
+          "l"(*reinterpret_cast<unsigned long long *>(&c)));
+    return d;
+}
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
+    float2 d;
+    asm("add.f32x2 %0, %1, %2;"
+        : "=l"(*reinterpret_cast<unsigned long long *>(&d))
+        : "l"(*reinterpret_cast<unsigned long long *>(&a)),
+          "l"(*reinterpret_cast<unsigned long long *>(&b)));
+    return d;
+}
 
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kFwdThreads, 1)
 attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap kmap,
                    const __grid_constant__ CUtensorMap vmap, const FwdParams p) {
     using namespace tc;
     extern __shared__ __align__(1024) uint8_t smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int qt = blockIdx.x % p.n_qt, h = blockIdx.x / p.n_qt;
-    const int q0 = qt * kBM;
+    const int q0 = qt * kBM * kFwdTiles;
     const int nblk = (p.sk + kBN - 1) / kBN;
 
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem + kSmemBar);
     uint64_t *q_full = bars;
     uint64_t *kv_full = bars + 1, *kv_empty = kv_full + kStages;
-    uint64_t *s_full = kv_empty + kStages;      // [2]
-    uint64_t *p_full = s_full + 2;              // [2] softmax -> MMA (count 128)
-    uint64_t *p_empty = p_full + 2;             // [2] PV done (commit)
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(p_empty + 2);
+    uint64_t *s_full = kv_empty + kStages;      // [tiles]  S_t(j) ready (and PV_t(j-1) done)
+    uint64_t *p_full = s_full + kFwdTiles;      // [tiles]  softmax -> MMA (count 128)
+    uint64_t *done = p_full + kFwdTiles;        // every MMA finished
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(done + 1);
 
     if (warp == 0) {
         if (lane == 0) {
@@ -85,11 +107,11 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
                 mbar_init(&kv_full[i], 1);
                 mbar_init(&kv_empty[i], 1);
             }
-            for (int i = 0; i < 2; ++i) {
+            for (int i = 0; i < kFwdTiles; ++i) {
                 mbar_init(&s_full[i], 1);
                 mbar_init(&p_full[i], 128);
-                mbar_init(&p_empty[i], 1);
             }
+            mbar_init(done, 1);
             mbar_fence_init();
             tma_prefetch(&qmap);
             tma_prefetch(&kmap);
@@ -103,10 +125,16 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
+    // Registers: the softmax warpgroups hold a 128-score row each; the
+    // producer warpgroup needs few.  setmaxnreg moves the budget (per SMSP:
+    // 80 + 208 + 208 regs x 32 lanes fits the 16K-register sub-partition).
+    if (warp < 4) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 80;");
     if (warp == 0) {
         // ===================== TMA producer =====================
-        mbar_expect_tx_e(q_full, kTileBytes);
-        tma_load_3d_e(smem + kSmemQ, &qmap, q_full, 0, h, q0);
+        mbar_expect_tx_e(q_full, kFwdTiles * kTileBytes);
+        for (int t = 0; t < kFwdTiles; ++t)
+            tma_load_3d_e(smem + kSmemQ + t * kTileBytes, &qmap, q_full, 0, h, q0 + t * kBM);
         for (int j = 0; j < nblk; ++j) {
             const int st = j % kStages;
             mbar_wait(&kv_empty[st], ((j / kStages) & 1) ^ 1);
@@ -119,14 +147,20 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
         // ===================== MMA issuer =====================
         const uint32_t id_s = idesc_bf16(kBM, kBN);            // K-major A, K-major B
         const uint32_t id_o = idesc_bf16(kBM, kD, 0, 1);       // P K-major, V MN-major
-        const uint64_t qd = sdesc_sw(smem_u32(smem + kSmemQ), 1024, 2);
         mbar_wait(q_full, 0);
-        auto issue_pv = [&](int jj) {
-            const int b = jj & 1;
-            mbar_wait(&p_full[b], (jj >> 1) & 1);
-            tc_fence_after();
-            const int st = jj % kStages;
-            const uint64_t pd = sdesc_sw(smem_u32(smem + kSmemP + b * kPBytes), 1024, 2);
+        auto issue_s = [&](int t, int j) {
+            const int st = j % kStages;
+            const uint64_t qd = sdesc_sw(smem_u32(smem + kSmemQ + t * kTileBytes), 1024, 2);
+            const uint64_t kd = sdesc_sw(smem_u32(smem + kSmemKV + st * 2 * kTileBytes), 1024, 2);
+            const uint32_t sc = tmem + kColS + t * kBN;
+#pragma unroll
+            for (int k = 0; k < kD / 16; ++k)
+                mma_bf16_e(sc, qd + ((k * 32) >> 4), kd + ((k * 32) >> 4), id_s, k ? 1u : 0u);
+            mma_commit_e(&s_full[t]);
+        };
+        auto issue_pv = [&](int t, int j) {
+            const int st = j % kStages;
+            const uint64_t pd = sdesc_sw(smem_u32(smem + kSmemP + t * kPBytes), 1024, 2);
             const uint64_t vd =
                 sdesc_mn(smem_u32(smem + kSmemKV + st * 2 * kTileBytes + kTileBytes), 8192, 1024, 2);
 #pragma unroll
@@ -134,31 +168,41 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
                 // P: key block k/4 (64 keys = one 128-B row), +32 B per 16 keys
                 const uint32_t pa = ((k >> 2) * (kBM * 128) + (k & 3) * 32) >> 4;
                 const uint32_t vb = (k * 16 * 128) >> 4;  // 16 key rows of V
-                mma_bf16_e(tmem + kColO, pd + pa, vd + vb, id_o, 1u);
+                mma_bf16_e(tmem + kColO + t * kD, pd + pa, vd + vb, id_o, 1u);
             }
-            mma_commit_e(&p_empty[b]);
-            mma_commit_e(&kv_empty[st]);
         };
-        for (int j = 0; j < nblk; ++j) {
-            const int st = j % kStages;
-            mbar_wait(&kv_full[st], (j / kStages) & 1);
+        if (nblk >= 1) {
+            mbar_wait(&kv_full[0], 0);
             tc_fence_after();
-            const uint64_t kd = sdesc_sw(smem_u32(smem + kSmemKV + st * 2 * kTileBytes), 1024, 2);
-            const uint32_t sc = tmem + kColS + (j & 1) * kBN;
-#pragma unroll
-            for (int k = 0; k < kD / 16; ++k)
-                mma_bf16_e(sc, qd + ((k * 32) >> 4), kd + ((k * 32) >> 4), id_s, k ? 1u : 0u);
-            mma_commit_e(&s_full[j & 1]);
-            if (j >= 1) issue_pv(j - 1);
+            for (int t = 0; t < kFwdTiles; ++t) issue_s(t, 0);
         }
-        if (nblk >= 1) issue_pv(nblk - 1);
+        for (int j = 0; j < nblk; ++j) {
+            const bool more = j + 1 < nblk;
+            if (more) mbar_wait(&kv_full[(j + 1) % kStages], ((j + 1) / kStages) & 1);
+            for (int t = 0; t < kFwdTiles; ++t) {
+                mbar_wait(&p_full[t], j & 1);
+                tc_fence_after();
+                issue_pv(t, j);
+                // S_t(j+1) overwrites S_t: softmax t is done with S_t(j).  Its
+                // commit also covers PV_t(j), so s_full tells softmax t that O_t
+                // and the P_t tile are free again.
+                if (more) issue_s(t, j + 1);
+                else mma_commit_e(&s_full[t]);
+            }
+            mma_commit_e(&kv_empty[j % kStages]);
+        }
+        mma_commit_e(done);
+    }
     } else {
-        // ===================== softmax / state =====================
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 208;");
+        // ===================== softmax / state (two warpgroups) =====================
+        const int t = (warp - 4) >> 2;               // query tile of this warpgroup
         const int quarter = warp & 3;
         const int rl = quarter * 32 + lane;          // row within the tile = TMEM lane
-        const int row = q0 + rl;
+        const int row = q0 + t * kBM + rl;
         const bool valid = row < p.sq;
         const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
+        const uint32_t colS = lane_base + kColS + t * kBN, colO = lane_base + kColO + t * kD;
         const size_t sidx = (size_t)row * p.H + h;
         float m_run = -INFINITY, l_run = 0.f;
         {
@@ -167,7 +211,7 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
 #pragma unroll
                 for (int i = 0; i < 16; ++i)
                     o[i] = valid ? __float_as_uint(p.acc[sidx * kD + c + i]) : 0u;
-                tmem_st16(lane_base + kColO + c, o);
+                tmem_st16(colO + c, o);
             }
             tmem_wait_st();
             if (valid) {
@@ -175,78 +219,78 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
                 l_run = p.l[sidx];
             }
         }
-        uint8_t *prow = smem + kSmemP + rl * 128;
+        uint8_t *prow = smem + kSmemP + t * kPBytes + rl * 128;
+        const float2 c2 = make_float2(p.c, p.c);
         for (int j = 0; j < nblk; ++j) {
-            mbar_wait(&s_full[j & 1], (j >> 1) & 1);
+            mbar_wait(&s_full[t], j & 1);
             tc_fence_after();
-            const uint32_t sc = lane_base + kColS + (j & 1) * kBN;
             float s[kBN];
 #pragma unroll
             for (int c = 0; c < kBN; c += 16) {
-                uint32_t t[16];
-                tmem_ld16(sc + c, t);
+                uint32_t u[16];
+                tmem_ld16(colS + c, u);
 #pragma unroll
-                for (int i = 0; i < 16; ++i) s[c + i] = __uint_as_float(t[i]);
+                for (int i = 0; i < 16; ++i) s[c + i] = __uint_as_float(u[i]);
             }
             tmem_wait_ld();
             const int kvalid = p.sk - j * kBN;  // keys of this block that exist
-            float t = -INFINITY;
+            if (kvalid < kBN) {
 #pragma unroll
-            for (int i = 0; i < kBN; ++i) {
-                s[i] = i < kvalid ? s[i] * p.c : -INFINITY;
-                t = fmaxf(t, s[i]);
+                for (int i = 0; i < kBN; ++i)
+                    if (i >= kvalid) s[i] = -INFINITY;
             }
+            float mx = fmaxf(s[0], s[1]);
+#pragma unroll
+            for (int i = 2; i < kBN; i += 2) mx = fmaxf(mx, fmaxf(s[i], s[i + 1]));
+            const float tnew = mx * p.c;
             // lazy rescale: only when this row's max grows by more than 2^kRescale
-            const bool grow = t > m_run + kRescale;
+            // (s_full already implies the previous P V finished, so O is quiescent)
+            const bool grow = tnew > m_run + kRescale;
             if (__any_sync(0xffffffffu, grow)) {
-                if (j >= 1) mbar_wait(&p_empty[(j - 1) & 1], ((j - 1) >> 1) & 1);
-                tc_fence_after();
-                const float f = grow ? ex2(m_run - t) : 1.f;
+                const float f = grow ? ex2(m_run - tnew) : 1.f;
                 for (int c = 0; c < kD; c += 16) {
                     uint32_t o[16];
-                    tmem_ld16(lane_base + kColO + c, o);
+                    tmem_ld16(colO + c, o);
                     tmem_wait_ld();
 #pragma unroll
                     for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * f);
-                    tmem_st16(lane_base + kColO + c, o);
+                    tmem_st16(colO + c, o);
                 }
                 tmem_wait_st();
                 if (grow) {
                     l_run *= f;
-                    m_run = t;
+                    m_run = tnew;
                 }
             }
-            // P = exp2(s - m) (bf16) into the swizzled P tile of buffer j & 1
-            if (j >= 2) mbar_wait(&p_empty[j & 1], ((j >> 1) & 1) ^ 1);
-            uint8_t *pb = prow + (j & 1) * kPBytes;
-            float sum = 0.f;
+            // P = exp2(s c - m) (bf16) into the swizzled P tile
+            const float2 nm = make_float2(-m_run, -m_run);
+            float2 sum2 = make_float2(0.f, 0.f);
 #pragma unroll
             for (int c = 0; c < kBN / 8; ++c) {
-                float e[8];
+                uint32_t pk[4];
 #pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                    e[i] = ex2(s[c * 8 + i] - m_run);
-                    sum += e[i];
+                for (int i = 0; i < 4; ++i) {
+                    float2 x = ffma2(make_float2(s[c * 8 + 2 * i], s[c * 8 + 2 * i + 1]), c2, nm);
+                    x.x = ex2(x.x);
+                    x.y = ex2(x.y);
+                    sum2 = fadd2(sum2, x);
+                    pk[i] = pack_bf16(x.x, x.y);
                 }
-                uint4 pk;
-                pk.x = pack_bf16(e[0], e[1]);
-                pk.y = pack_bf16(e[2], e[3]);
-                pk.z = pack_bf16(e[4], e[5]);
-                pk.w = pack_bf16(e[6], e[7]);
                 const int blk = c >> 3, ch = c & 7;
-                *reinterpret_cast<uint4 *>(pb + blk * (kBM * 128) + ((ch ^ (rl & 7)) << 4)) = pk;
+                *reinterpret_cast<uint4 *>(prow + blk * (kBM * 128) + ((ch ^ (rl & 7)) << 4)) =
+                    make_uint4(pk[0], pk[1], pk[2], pk[3]);
             }
-            l_run += sum;
+            l_run += sum2.x + sum2.y;
             fence_async_smem();
             tc_fence_before();
-            mbar_arrive(&p_full[j & 1]);
+            mbar_arrive(&p_full[t]);
         }
-        // final state back to HBM once the last P V has landed
-        if (nblk >= 1) mbar_wait(&p_empty[(nblk - 1) & 1], ((nblk - 1) >> 1) & 1);
+        // final state back to HBM once every MMA has landed
+        mbar_wait(done, 0);
         tc_fence_after();
         for (int c = 0; c < kD; c += 16) {
             uint32_t o[16];
-            tmem_ld16(lane_base + kColO + c, o);
+            tmem_ld16(colO + c, o);
             tmem_wait_ld();
             if (valid) {
                 float4 *dst = reinterpret_cast<float4 *>(p.acc + sidx * kD + c);
@@ -588,7 +632,7 @@ int attn_fwd_update_tc_launch(const dp_attn_geom *g, const void *q, const void *
     p.sq = (int)g->sq;
     p.sk = (int)g->sk;
     p.H = (int)g->heads;
-    p.n_qt = (int)((g->sq + kBM - 1) / kBM);
+    p.n_qt = (int)((g->sq + kBM * kFwdTiles - 1) / (kBM * kFwdTiles));
     p.c = (float)(g->scale * 1.4426950408889634);
     p.m = (float *)m;
     p.l = (float *)l;
@@ -596,8 +640,16 @@ int attn_fwd_update_tc_launch(const dp_attn_geom *g, const void *q, const void *
     DP_CUDA_CHECK(cudaFuncSetAttribute(attn_fwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        kSmemFwd));
     const int64_t grid = (int64_t)p.n_qt * p.H;
-    attn_fwd_tc_kernel<<<(unsigned)grid, kThreads, kSmemFwd, st>>>(qm, km, vm, p);
-    return launch_status("attn_fwd_tc_kernel");
+    attn_fwd_tc_kernel<<<(unsigned)grid, kFwdThreads, kSmemFwd, st>>>(qm, km, vm, p);
+    int rc2 = launch_status("attn_fwd_tc_kernel");
+    if (rc2) {
+        cudaFuncAttributes fa;
+        cudaFuncGetAttributes(&fa, attn_fwd_tc_kernel);
+        set_error("attn_fwd_tc_kernel launch failed: regs %d maxThreads %d static smem %zu "
+                  "max dyn smem %d local %zu", fa.numRegs, fa.maxThreadsPerBlock,
+                  fa.sharedSizeBytes, fa.maxDynamicSharedSizeBytes, fa.localSizeBytes);
+    }
+    return rc2;
 }
 
 int attn_bwd_tc_eligible(const dp_attn_geom *g, int dtype) {
