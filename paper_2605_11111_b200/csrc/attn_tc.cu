@@ -82,6 +82,30 @@ __device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
     return d;
 }
 
+// exp2 of two arguments on the FMA pipe (FA4-style MUFU offload): round to
+// nearest via the 1.5*2^23 magic constant, a cubic for 2^f on [-1/2, 1/2]
+// (max rel err 1.1e-4, far below the bf16 rounding of P), exponent bits
+// added with one integer multiply-add.  Arguments are <= 2^kRescale-bounded
+// from above; very negative ones flush to 0 through the clamp.
+__device__ __forceinline__ float2 ex2_poly2(float2 x) {
+    const float2 lo = make_float2(-127.f, -127.f);
+    x.x = fmaxf(x.x, lo.x);
+    x.y = fmaxf(x.y, lo.y);
+    const float2 M = make_float2(12582912.f, 12582912.f);
+    const float2 t = fadd2(x, M);
+    const float2 j = fadd2(t, make_float2(-12582912.f, -12582912.f));
+    const float2 f = fadd2(x, make_float2(-j.x, -j.y));
+    float2 pp = ffma2(make_float2(0.05459282f, 0.05459282f), f,
+                      make_float2(0.24221784f, 0.24221784f));
+    pp = ffma2(pp, f, make_float2(0.6933686f, 0.6933686f));
+    pp = ffma2(pp, f, make_float2(1.f, 1.f));
+    float2 r;
+    r.x = __int_as_float(__float_as_int(pp.x) + (__float_as_int(t.x) << 23));
+    r.y = __int_as_float(__float_as_int(pp.y) + (__float_as_int(t.y) << 23));
+    return r;
+}
+
+template <int POLY>  // pairs of every 4 computed on the FMA pipe instead of MUFU
 __global__ void __launch_bounds__(kFwdThreads, 1)
 attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap kmap,
                    const __grid_constant__ CUtensorMap vmap, const FwdParams p) {
@@ -271,8 +295,12 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
                     float2 x = ffma2(make_float2(s[c * 8 + 2 * i], s[c * 8 + 2 * i + 1]), c2, nm);
-                    x.x = ex2(x.x);
-                    x.y = ex2(x.y);
+                    if (i < POLY) {
+                        x = ex2_poly2(x);
+                    } else {
+                        x.x = ex2(x.x);
+                        x.y = ex2(x.y);
+                    }
                     sum2 = fadd2(sum2, x);
                     pk[i] = pack_bf16(x.x, x.y);
                 }
@@ -637,19 +665,18 @@ int attn_fwd_update_tc_launch(const dp_attn_geom *g, const void *q, const void *
     p.m = (float *)m;
     p.l = (float *)l;
     p.acc = (float *)acc;
-    DP_CUDA_CHECK(cudaFuncSetAttribute(attn_fwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       kSmemFwd));
-    const int64_t grid = (int64_t)p.n_qt * p.H;
-    attn_fwd_tc_kernel<<<(unsigned)grid, kFwdThreads, kSmemFwd, st>>>(qm, km, vm, p);
-    int rc2 = launch_status("attn_fwd_tc_kernel");
-    if (rc2) {
-        cudaFuncAttributes fa;
-        cudaFuncGetAttributes(&fa, attn_fwd_tc_kernel);
-        set_error("attn_fwd_tc_kernel launch failed: regs %d maxThreads %d static smem %zu "
-                  "max dyn smem %d local %zu", fa.numRegs, fa.maxThreadsPerBlock,
-                  fa.sharedSizeBytes, fa.maxDynamicSharedSizeBytes, fa.localSizeBytes);
+    static int poly = -1;  // DP_ATTN_POLY: exp2 pairs per 4 on the FMA pipe (tuning knob)
+    if (poly < 0) {
+        const char *e = getenv("DP_ATTN_POLY");
+        poly = e ? atoi(e) : 1;
+        if (poly < 0 || poly > 2) poly = 1;
     }
-    return rc2;
+    auto kern = poly == 0 ? attn_fwd_tc_kernel<0> : poly == 1 ? attn_fwd_tc_kernel<1>
+                                                               : attn_fwd_tc_kernel<2>;
+    DP_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemFwd));
+    const int64_t grid = (int64_t)p.n_qt * p.H;
+    kern<<<(unsigned)grid, kFwdThreads, kSmemFwd, st>>>(qm, km, vm, p);
+    return launch_status("attn_fwd_tc_kernel");
 }
 
 int attn_bwd_tc_eligible(const dp_attn_geom *g, int dtype) {
