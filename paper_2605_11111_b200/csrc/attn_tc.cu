@@ -82,6 +82,15 @@ __device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
     return d;
 }
 
+__device__ __forceinline__ float2 fmul2(float2 a, float2 b) {
+    float2 d;
+    asm("mul.f32x2 %0, %1, %2;"
+        : "=l"(*reinterpret_cast<unsigned long long *>(&d))
+        : "l"(*reinterpret_cast<unsigned long long *>(&a)),
+          "l"(*reinterpret_cast<unsigned long long *>(&b)));
+    return d;
+}
+
 // exp2 of two arguments on the FMA pipe (FA4-style MUFU offload): round to
 // nearest via the 1.5*2^23 magic constant, a cubic for 2^f on [-1/2, 1/2]
 // (max rel err 1.1e-4, far below the bf16 rounding of P), exponent bits
@@ -349,23 +358,29 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
 //
 // CTA = one 128-key tile of one head (K, V resident in smem; dK, dV
 // accumulate in TMEM over the whole query range), looping over 128-row
-// query blocks (Q, dO double-buffered by TMA).  320 threads:
+// query blocks (Q, dO double-buffered by TMA).  448 threads:
 //   warp 0     TMA producer
 //   warp 1     MMA issuer: S^T = K Q^T and dP^T = V dO^T into TMEM; once the
 //              softmax warps have written P^T / dS^T (bf16, swizzled smem):
 //              dV += P^T dO, dK += dS^T Q (A = the key-major tiles), and
 //              dQ = dS K into a double-buffered TMEM tile (A = the SAME dS^T
 //              bytes read as an MN-major operand)
-//   warps 2-5  thread = key row: P^T = exp2(S^T c - LSE2), dS^T =
-//              scale P^T (dP^T - D) -> smem; at the end dK, dV += TMEM
-//   warps 6-9  thread = query row: dQ tile TMEM -> float4 atomics into dq
+//   warps 2-9  two warps per TMEM lane quarter, each half of the 128 query
+//              columns; thread = (key row, column half): P^T = exp2(S^T c -
+//              LSE2), dS^T = scale P^T (dP^T - D) -> smem (packed fp32x2
+//              math); at the end dV (half 0) / dK (half 1) += TMEM
+//   warps 10-13 thread = query row: dQ tile TMEM -> swizzled fp32 smem ->
+//              TMA bulk reduce-add (cp.reduce.async.bulk.tensor .add) into dq
+//              (per-thread float4 atomics cost 34 of 84 ms at 64k)
 // The next block's S^T / dP^T MMAs are issued before this block's gradient
 // MMAs, so the softmax warps overlap the tensor pipe.
-constexpr int kBwdThreads = 320;
+constexpr int kBwdThreads = 448;   // TMA, MMA, 8 softmax warps, 4 dQ warps
 constexpr int kB_K = 0, kB_V = kTileBytes;
 constexpr int kB_QD = 2 * kTileBytes;                  // 2 stages of [Q | dO]
-constexpr int kB_PS = kB_QD + 2 * 2 * kTileBytes;      // 2 buffers of [P^T | dS^T]
-constexpr int kB_LD = kB_PS + 2 * 2 * kPBytes;         // lse2[2][128], delta[2][128]
+constexpr int kB_PS = kB_QD + 2 * 2 * kTileBytes;      // [P^T | dS^T] (single buffer)
+constexpr int kB_DQ = kB_PS + 2 * kPBytes;             // 2 dQ staging tiles (fp32, 2 x 16 KB)
+constexpr int kDQStage = kBM * kD * 4;                 // 32 KB
+constexpr int kB_LD = kB_DQ + 2 * kDQStage;            // -lse2[2][128], delta[2][128]
 constexpr int kB_BAR = kB_LD + 4 * 128 * 4;
 constexpr int kSmemBwd = kB_BAR + 256;
 // TMEM columns: S^T [0,128), dP^T [128,256), dV [256,320), dK [320,384), dQ x2 [384,512)
@@ -379,6 +394,7 @@ struct BwdParams {
     const float *lse, *delta;  // [sq, H]
     float *dq;                 // [sq, H, 64] (atomic +=)
     float *dk, *dv;            // [sk, H, 64] (+=)
+    int dbg;                   // DP_ATTN_DBG profiling ablation: 1 = skip the dQ atomics
 };
 
 __device__ __forceinline__ void named_bar(int id, int n) {
@@ -388,7 +404,7 @@ __device__ __forceinline__ void named_bar(int id, int n) {
 __global__ void __launch_bounds__(kBwdThreads, 1)
 attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap kmap,
                    const __grid_constant__ CUtensorMap vmap, const __grid_constant__ CUtensorMap dmap,
-                   const BwdParams p) {
+                   const __grid_constant__ CUtensorMap dqmap, const BwdParams p) {
     using namespace tc;
     extern __shared__ __align__(1024) uint8_t smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -400,8 +416,8 @@ attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
     uint64_t *kv_full = bars;
     uint64_t *qd_full = bars + 1, *qd_empty = qd_full + 2;
     uint64_t *s_full = qd_empty + 2, *s_free = s_full + 1;
-    uint64_t *p_full = s_free + 1, *p_empty = p_full + 2;
-    uint64_t *dq_full = p_empty + 2, *dq_empty = dq_full + 2;
+    uint64_t *p_full = s_free + 1, *p_empty = p_full + 2;   // p_empty: single P/dS buffer
+    uint64_t *dq_full = p_empty + 1, *dq_empty = dq_full + 2;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(dq_empty + 2);
     float *lse2_s = reinterpret_cast<float *>(smem + kB_LD);   // [2][128]
     float *delta_s = lse2_s + 256;                             // [2][128]
@@ -412,18 +428,19 @@ attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
             for (int i = 0; i < 2; ++i) {
                 mbar_init(&qd_full[i], 1);
                 mbar_init(&qd_empty[i], 1);
-                mbar_init(&p_full[i], 128);
-                mbar_init(&p_empty[i], 1);
+                mbar_init(&p_full[i], 256);
                 mbar_init(&dq_full[i], 1);
                 mbar_init(&dq_empty[i], 128);
             }
             mbar_init(s_full, 1);
-            mbar_init(s_free, 128);
+            mbar_init(s_free, 256);
+            mbar_init(p_empty, 1);
             mbar_fence_init();
             tma_prefetch(&qmap);
             tma_prefetch(&kmap);
             tma_prefetch(&vmap);
             tma_prefetch(&dmap);
+            tma_prefetch(&dqmap);
         }
         __syncwarp();
         tmem_alloc(tmem_slot, 512);
@@ -460,7 +477,7 @@ attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
             mbar_wait(&p_full[b], (j >> 1) & 1);
             tc_fence_after();
             uint8_t *qdst = smem + kB_QD + b * 2 * kTileBytes;
-            uint8_t *ps = smem + kB_PS + b * 2 * kPBytes;
+            uint8_t *ps = smem + kB_PS;
             const uint64_t pt = sdesc_sw(smem_u32(ps), 1024, 2);
             const uint64_t dst_k = sdesc_sw(smem_u32(ps + kPBytes), 1024, 2);
             const uint64_t ds_mn = sdesc_mn(smem_u32(ps + kPBytes), kBM * 128, 1024, 2);
@@ -481,7 +498,7 @@ attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
                 const uint32_t a = (k * 16 * 128) >> 4;     // 16 key rows of dS^T
                 mma_bf16_e(tmem + kColDQ + b * kD, ds_mn + a, kmn + a, id_q, k ? 1u : 0u);
             }
-            mma_commit_e(&p_empty[b]);
+            mma_commit_e(p_empty);
             mma_commit_e(&qd_empty[b]);
             mma_commit_e(&dq_full[b]);
         };
@@ -504,88 +521,93 @@ attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
             if (i >= 1) issue_grads(i - 1);
         }
         if (nq >= 1) issue_grads(nq - 1);
-    } else if (warp < 6) {
-        // ===================== P^T / dS^T (thread = key row) =====================
+    } else if (warp < 10) {
+        // ===================== P^T / dS^T (thread = key row, column half) ==========
         const int quarter = warp & 3;
+        const int half = (warp - 2) >> 2;                // query columns [64 half, 64 half + 64)
         const int rl = quarter * 32 + lane;
-        const int tid = threadIdx.x - 64;                 // 0..127
+        const int tid = threadIdx.x - 64;                // 0..255
         const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
+        const float2 c2 = make_float2(p.c, p.c);
+        const float2 sc2 = make_float2(p.scale, p.scale);
         for (int i = 0; i < nq; ++i) {
             const int b = i & 1;
-            {
+            if (tid < kBM) {
                 const int qrow = i * kBM + tid;
                 const bool qv = qrow < p.sq;
                 const size_t qi = (size_t)qrow * p.H + h;
-                lse2_s[b * 128 + tid] = qv ? p.lse[qi] * kLog2e : INFINITY;
+                lse2_s[b * 128 + tid] = qv ? -p.lse[qi] * kLog2e : -INFINITY;
                 delta_s[b * 128 + tid] = qv ? p.delta[qi] : 0.f;
             }
-            named_bar(1, 128);
-            if (i >= 2) mbar_wait(&p_empty[b], ((i >> 1) & 1) ^ 1);
+            named_bar(1, 256);
             mbar_wait(s_full, i & 1);
             tc_fence_after();
-            uint8_t *ps = smem + kB_PS + b * 2 * kPBytes + rl * 128;
-            const float *L2 = lse2_s + b * 128;
-            const float *Dl = delta_s + b * 128;
+            uint8_t *ps = smem + kB_PS + rl * 128 + half * (kBN * 128);
+            const float *NL2 = lse2_s + b * 128 + half * 64;
+            const float *Dl = delta_s + b * 128 + half * 64;
 #pragma unroll 1
-            for (int c0 = 0; c0 < kBM; c0 += 32) {
+            for (int cc = 0; cc < 2; ++cc) {          // 32 query columns at a time
                 uint32_t sv[32], dv[32];
-                tmem_ld16(lane_base + kColST + c0, *reinterpret_cast<uint32_t(*)[16]>(sv));
-                tmem_ld16(lane_base + kColST + c0 + 16, *reinterpret_cast<uint32_t(*)[16]>(sv + 16));
-                tmem_ld16(lane_base + kColDP + c0, *reinterpret_cast<uint32_t(*)[16]>(dv));
-                tmem_ld16(lane_base + kColDP + c0 + 16, *reinterpret_cast<uint32_t(*)[16]>(dv + 16));
+                const uint32_t col = half * 64 + cc * 32;
+                tmem_ld16(lane_base + kColST + col, *reinterpret_cast<uint32_t(*)[16]>(sv));
+                tmem_ld16(lane_base + kColST + col + 16, *reinterpret_cast<uint32_t(*)[16]>(sv + 16));
+                tmem_ld16(lane_base + kColDP + col, *reinterpret_cast<uint32_t(*)[16]>(dv));
+                tmem_ld16(lane_base + kColDP + col + 16, *reinterpret_cast<uint32_t(*)[16]>(dv + 16));
                 tmem_wait_ld();
-                if (c0 + 32 >= kBM) {
+                if (cc == 1) {
                     tc_fence_before();
                     mbar_arrive(s_free);   // S^T / dP^T TMEM may be overwritten
+                } else if (i >= 1) {
+                    mbar_wait(p_empty, (i - 1) & 1);   // grads(i-1) done with P^T / dS^T
                 }
 #pragma unroll
-                for (int g = 0; g < 4; ++g) {
-                    float pe[8], de[8];
+                for (int c = 0; c < 4; ++c) {         // 16-B chunks of 8 query columns
+                    uint32_t pk[4], dk4[4];
 #pragma unroll
-                    for (int e = 0; e < 8; ++e) {
-                        const int qc = c0 + g * 8 + e;
-                        const float pv = ex2(__uint_as_float(sv[g * 8 + e]) * p.c - L2[qc]);
-                        pe[e] = pv;
-                        de[e] = p.scale * pv * (__uint_as_float(dv[g * 8 + e]) - Dl[qc]);
+                    for (int e = 0; e < 4; ++e) {
+                        const int qc = c * 8 + 2 * e;
+                        const float2 nl = *reinterpret_cast<const float2 *>(NL2 + cc * 32 + qc);
+                        const float2 dd = *reinterpret_cast<const float2 *>(Dl + cc * 32 + qc);
+                        float2 x = ffma2(make_float2(__uint_as_float(sv[qc]), __uint_as_float(sv[qc + 1])),
+                                         c2, nl);
+                        x.x = ex2(x.x);
+                        x.y = ex2(x.y);
+                        float2 g = fadd2(make_float2(__uint_as_float(dv[qc]), __uint_as_float(dv[qc + 1])),
+                                         make_float2(-dd.x, -dd.y));
+                        g = fmul2(fmul2(x, g), sc2);
+                        pk[e] = pack_bf16(x.x, x.y);
+                        dk4[e] = pack_bf16(g.x, g.y);
                     }
-                    const int c = (c0 >> 3) + g;      // 16-B chunk index along q
-                    const int off = (c >> 3) * (kBN * 128) + (((c & 7) ^ (rl & 7)) << 4);
-                    uint4 pk, dk4;
-                    pk.x = pack_bf16(pe[0], pe[1]); pk.y = pack_bf16(pe[2], pe[3]);
-                    pk.z = pack_bf16(pe[4], pe[5]); pk.w = pack_bf16(pe[6], pe[7]);
-                    dk4.x = pack_bf16(de[0], de[1]); dk4.y = pack_bf16(de[2], de[3]);
-                    dk4.z = pack_bf16(de[4], de[5]); dk4.w = pack_bf16(de[6], de[7]);
-                    *reinterpret_cast<uint4 *>(ps + off) = pk;
-                    *reinterpret_cast<uint4 *>(ps + kPBytes + off) = dk4;
+                    const int off = (((cc * 4 + c) ^ (rl & 7)) << 4);
+                    *reinterpret_cast<uint4 *>(ps + off) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+                    *reinterpret_cast<uint4 *>(ps + kPBytes + off) =
+                        make_uint4(dk4[0], dk4[1], dk4[2], dk4[3]);
                 }
             }
             fence_async_smem();
             tc_fence_before();
             mbar_arrive(&p_full[b]);
         }
-        // dK, dV (+=) once the last gradient MMAs have landed
-        if (nq >= 1) mbar_wait(&p_empty[(nq - 1) & 1], ((nq - 1) >> 1) & 1);
+        // dV (half 0) / dK (half 1) += TMEM once the last gradient MMAs have landed
+        if (nq >= 1) mbar_wait(p_empty, (nq - 1) & 1);
         tc_fence_after();
         const int key = k0 + rl;
         const bool kv_ok = key < p.sk;
         const size_t ki = ((size_t)key * p.H + h) * kD;
+        float *gdst = half ? p.dk : p.dv;
+        const uint32_t gcol = half ? kColDK : kColDV;
         for (int c = 0; c < kD; c += 16) {
-            uint32_t a[16], bq[16];
-            tmem_ld16(lane_base + kColDV + c, a);
-            tmem_ld16(lane_base + kColDK + c, bq);
+            uint32_t a[16];
+            tmem_ld16(lane_base + gcol + c, a);
             tmem_wait_ld();
             if (kv_ok) {
-                float4 *pv = reinterpret_cast<float4 *>(p.dv + ki + c);
-                float4 *pk = reinterpret_cast<float4 *>(p.dk + ki + c);
+                float4 *pv = reinterpret_cast<float4 *>(gdst + ki + c);
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
-                    float4 x = pv[e], y = pk[e];
+                    float4 x = pv[e];
                     x.x += __uint_as_float(a[4 * e]); x.y += __uint_as_float(a[4 * e + 1]);
                     x.z += __uint_as_float(a[4 * e + 2]); x.w += __uint_as_float(a[4 * e + 3]);
-                    y.x += __uint_as_float(bq[4 * e]); y.y += __uint_as_float(bq[4 * e + 1]);
-                    y.z += __uint_as_float(bq[4 * e + 2]); y.w += __uint_as_float(bq[4 * e + 3]);
                     pv[e] = x;
-                    pk[e] = y;
                 }
             }
         }
@@ -594,29 +616,47 @@ attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
         const int quarter = warp & 3;
         const int rl = quarter * 32 + lane;
         const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
+        const bool leader = warp == 10;
         for (int i = 0; i < nq; ++i) {
             const int b = i & 1;
             mbar_wait(&dq_full[b], (i >> 1) & 1);
             tc_fence_after();
-            const int qrow = i * kBM + rl;
-            const bool qv = qrow < p.sq;
-            float *dst = p.dq + ((size_t)qrow * p.H + h) * kD;
+            // staging tile b was last reduced 2 blocks ago: its TMA reads must be done
+            if (leader && lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+            named_bar(2, 128);
+            uint8_t *stg = smem + kB_DQ + b * kDQStage;
             for (int c = 0; c < kD; c += 16) {
                 uint32_t a[16];
                 tmem_ld16(lane_base + kColDQ + b * kD + c, a);
                 tmem_wait_ld();
-                if (qv) {
 #pragma unroll
-                    for (int e = 0; e < 4; ++e)
-                        atomicAdd(reinterpret_cast<float4 *>(dst + c) + e,
-                                  make_float4(__uint_as_float(a[4 * e]), __uint_as_float(a[4 * e + 1]),
-                                              __uint_as_float(a[4 * e + 2]),
-                                              __uint_as_float(a[4 * e + 3])));
+                for (int e = 0; e < 4; ++e) {
+                    const int chunk = (c >> 2) + e;              // 16-B chunk of 4 floats, 0..15
+                    const int half = chunk >> 3, cc = chunk & 7;  // 32-column box, chunk in row
+                    *reinterpret_cast<uint4 *>(stg + half * (kDQStage / 2) + rl * 128 +
+                                               ((cc ^ (rl & 7)) << 4)) =
+                        make_uint4(a[4 * e], a[4 * e + 1], a[4 * e + 2], a[4 * e + 3]);
                 }
             }
             tc_fence_before();
-            mbar_arrive(&dq_empty[b]);
+            mbar_arrive(&dq_empty[b]);        // TMEM dQ buffer free
+            fence_async_smem();
+            named_bar(2, 128);
+            if (leader) {
+                if (lane == 0 && !(p.dbg & 1)) {
+                    for (int hf = 0; hf < 2; ++hf)
+                        asm volatile(
+                            "cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.tile.bulk_group "
+                            "[%0, {%1, %2, %3}], [%4];" ::"l"(reinterpret_cast<uint64_t>(&dqmap)),
+                            "r"(hf * 32), "r"(h), "r"(i * kBM),
+                            "r"(smem_u32(stg + hf * (kDQStage / 2)))
+                            : "memory");
+                    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                }
+                __syncwarp();
+            }
         }
+        if (leader && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     }
     tc_fence_before();
     __syncthreads();
@@ -695,6 +735,14 @@ int attn_bwd_update_tc_launch(const dp_attn_geom *g, const void *q, const void *
     if (!rc) rc = head_map(&km, k, g->sk, g->heads, g->k_rs, g->k_hs);
     if (!rc) rc = head_map(&vm, v, g->sk, g->heads, g->v_rs, g->v_hs);
     if (!rc) rc = head_map(&dm, dout, g->sq, g->heads, g->o_rs, g->o_hs);
+    CUtensorMap dqm;  // dq [sq, H, 64] fp32, box 32 x 1 x 128 (128-B swizzle): reduce-add target
+    if (!rc) {
+        uint64_t dims[3] = {(uint64_t)kD, (uint64_t)g->heads, (uint64_t)g->sq};
+        uint64_t strides[2] = {(uint64_t)kD * 4, (uint64_t)g->heads * kD * 4};
+        uint32_t box[3] = {32, 1, (uint32_t)kBM};
+        rc = encode_tensor_map(&dqm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, dq, dims, strides, box,
+                               CU_TENSOR_MAP_SWIZZLE_128B);
+    }
     if (rc) return rc;
     BwdParams p;
     p.sq = (int)g->sq;
@@ -708,10 +756,18 @@ int attn_bwd_update_tc_launch(const dp_attn_geom *g, const void *q, const void *
     p.dq = (float *)dq;
     p.dk = (float *)dk;
     p.dv = (float *)dv;
+    {
+        static int dbg = -1;
+        if (dbg < 0) {
+            const char *e = getenv("DP_ATTN_DBG");
+            dbg = e ? atoi(e) : 0;
+        }
+        p.dbg = dbg;
+    }
     DP_CUDA_CHECK(cudaFuncSetAttribute(attn_bwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        kSmemBwd));
     const int64_t grid = (int64_t)p.n_kt * p.H;
-    attn_bwd_tc_kernel<<<(unsigned)grid, kBwdThreads, kSmemBwd, st>>>(qm, km, vm, dm, p);
+    attn_bwd_tc_kernel<<<(unsigned)grid, kBwdThreads, kSmemBwd, st>>>(qm, km, vm, dm, dqm, p);
     return launch_status("attn_bwd_tc_kernel");
 }
 
