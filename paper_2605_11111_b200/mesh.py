@@ -154,6 +154,26 @@ class _ThreadRuntime:
         self.abort = threading.Event()
 
 
+class _Done:
+    def wait(self) -> None:
+        return None
+
+
+class _Pending:
+    """Outstanding point-to-point works of one exchange round (buffers kept
+    alive until waited)."""
+
+    def __init__(self, works, keep):
+        self.works = works
+        self.keep = keep
+
+    def wait(self) -> None:
+        for w in self.works:
+            w.wait()
+        self.works = []
+        self.keep = []
+
+
 class ThreadTransport:
     """Rank-to-rank FIFO mailboxes inside one process (one device)."""
 
@@ -200,6 +220,11 @@ class ThreadTransport:
                     f"{src}, got {tuple(got.shape)} {got.dtype}")
             if got.numel():
                 _copy_into(out, got)
+
+    def exchange_start(self, sends, recvs):
+        """Thread mailboxes complete eagerly; the handle is already done."""
+        self.exchange(sends, recvs)
+        return _Done()
 
     def exchange_any(self, sends, srcs) -> list:
         """Like exchange, but receive whatever tensor each source sent."""
@@ -280,22 +305,27 @@ class DistTransport:
                 self.groups[line] = g
                 self.meta_groups[line] = m
 
-    def exchange(self, sends, recvs) -> None:
+    def exchange_start(self, sends, recvs):
+        """Post every send/recv of one exchange round (one NCCL group) and
+        return a handle; `wait()` orders the caller's stream after them, so
+        device work launched in between overlaps the transfer."""
         dist = self.dist
         ops = []
+        keep = []
         for dst, t in sends:
-            ops.append(dist.P2POp(dist.isend, t.contiguous(), dst))
+            t = t.contiguous()
+            keep.append(t)
+            ops.append(dist.P2POp(dist.isend, t, dst))
         for src, out in recvs:
             ops.append(dist.P2POp(dist.irecv, out, src))
         if not ops:
-            return
+            return _Done()
         if self.kind == "nccl":
-            for w in dist.batch_isend_irecv(ops):
-                w.wait()
-        else:
-            works = [op.op(op.tensor, op.peer) for op in ops]
-            for w in works:
-                w.wait()
+            return _Pending(dist.batch_isend_irecv(ops), keep)
+        return _Pending([op.op(op.tensor, op.peer) for op in ops], keep)
+
+    def exchange(self, sends, recvs) -> None:
+        self.exchange_start(sends, recvs).wait()
 
     def gather_meta(self, members, me: int, obj) -> list:
         out = [None] * len(members)
@@ -513,12 +543,13 @@ def ring_shift(group: AxisGroup, payload: torch.Tensor) -> torch.Tensor:
 
 
 def halo_sendrecv(group: AxisGroup, local: torch.Tensor, dim: int, serve_left: int,
-                  serve_right: int, lw: int, rw: int):
+                  serve_right: int, lw: int, rw: int, *, wait: bool = True):
     """The data phase of a halo exchange with every width already known:
     send my first `serve_left` rows to the previous member and my last
     `serve_right` rows to the next, receive `lw` rows from the previous and
     `rw` rows from the next.  Returns (left_halo, right_halo) as contiguous
-    blocks (None when zero-width).  Uncounted."""
+    blocks (None when zero-width).  Uncounted.  With wait=False the transfer
+    is only posted and a third value, the handle to wait on, is returned."""
     i = group.index
     left = group.members[i - 1] if i > 0 else None
     right = group.members[i + 1] if i < group.size - 1 else None
@@ -539,6 +570,8 @@ def halo_sendrecv(group: AxisGroup, local: torch.Tensor, dim: int, serve_left: i
         shp[dim] = rw
         rh = torch.empty(shp, dtype=local.dtype, device=local.device)
         recvs.append((right, rh))
+    if not wait:
+        return lh, rh, group.ctx.transport.exchange_start(sends, recvs)
     group.ctx.transport.exchange(sends, recvs)
     return lh, rh
 

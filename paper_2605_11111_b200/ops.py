@@ -230,20 +230,46 @@ def halo_conv_forward(x: ShardTensor, weight, stride=1, padding=0):
     if any(m.lw for m in plan.members):  # cannot happen under anchor ownership
         raise UnsupportedConfigError("halo_conv: left halos are not produced by this ownership")
     serve_left = plan.members[me - 1].rw if me > 0 else 0
-    _, halo = halo_sendrecv(group, xb, sp + 2, serve_left, 0, 0, mine.rw)
+    _, halo, pending = halo_sendrecv(group, xb, sp + 2, serve_left, 0, 0, mine.rw, wait=False)
     out_global = tuple(list(x.global_shape[:first - 1]) + [weight.shape[0]] + out_spatial)
     out_sp = list(out_spatial)
     out_sp[sp] = mine.n_out
     base = [-p for p in pads]
     base[sp] = mine.base
     yb = _empty_like_layout(xb, [xb.shape[0], weight.shape[0]] + out_sp)
-    if yb.numel():
+    # Interior output rows read only local rows: they are convolved while the
+    # halo is in flight; the boundary rows follow once it has landed.
+    n_int = _interior_rows(mine.n_out, xb.shape[sp + 2], kernel[sp], strides[sp], mine.base) \
+        if mine.rw else mine.n_out
+    if yb.numel() and 0 < n_int < mine.n_out:
+        kernels.conv_fwd(xb, None, w, yb.narrow(sp + 2, 0, n_int), kernel=kernel,
+                         stride=strides, base=base, shard=sp, halo_rows=0)
+    pending.wait()
+    if yb.numel() and n_int < mine.n_out:
+        bb = list(base)
+        bb[sp] = mine.base + n_int * strides[sp]
+        kernels.conv_fwd(xb, halo, w, yb.narrow(sp + 2, n_int, mine.n_out - n_int),
+                         kernel=kernel, stride=strides, base=bb, shard=sp, halo_rows=mine.rw)
+    elif yb.numel() and n_int == mine.n_out:
         kernels.conv_fwd(xb, halo, w, yb, kernel=kernel, stride=strides, base=base, shard=sp,
                          halo_rows=mine.rw)
     y = yb if batched else yb[0]
     out = ShardTensor(y, out_global, x.ctx, x.placements, {axis: plan.out_extents})
     tape = ConvTape(x, w, halo, plan, axis, d, sp, strides, pads, batched, tuple(base), out)
     return out, tape
+
+
+def _interior_rows(n_out: int, extent: int, k: int, s: int, base: int) -> int:
+    """Output rows j whose window base + j*s + [0, k) stays inside the
+    local block [0, extent) on the sharded dim (a prefix, since base is the
+    window start of row 0 and never below the block start for j >= 1 under
+    anchor ownership)."""
+    if n_out <= 0:
+        return 0
+    last = extent - k - base  # largest j*s allowed
+    if last < 0:
+        return 0
+    return min(n_out, last // s + 1)
 
 
 def halo_conv(x: ShardTensor, weight, stride=1, padding=0) -> ShardTensor:
@@ -294,16 +320,16 @@ def halo_conv_backward(tape: ConvTape, dout):
         hshape = list(xb.shape)
         hshape[dim] = mine.rw
         halo_grad = torch.empty(hshape, dtype=xb.dtype, device=xb.device)
-    if mine.n_out and xb.shape[dim] + mine.rw:
+    work = mine.n_out and xb.shape[dim] + mine.rw
+    if work:
         kernels.conv_dgrad(dyb, w, dxb, halo_grad, kernel=kernel, stride=tape.strides,
-                           base=tape.base, shard=tape.sp, halo_rows=mine.rw)
-        kernels.conv_wgrad(xb, tape.halo, dyb, dw, kernel=kernel, stride=tape.strides,
                            base=tape.base, shard=tape.sp, halo_rows=mine.rw)
     else:
         if dxb.numel():
             dxb.zero_()
         dw.zero_()
-    # reverse halo: my halo rows' gradient goes to r+1, r-1's comes to me
+    # reverse halo: my halo rows' gradient goes to r+1, r-1's comes to me;
+    # posted before wgrad so the transfer overlaps it
     x.ctx.collective_count += 1
     from_left = tape.plan.members[me - 1].rw if me > 0 else 0
     nxt = group.members[me + 1] if me + 1 < group.size else None
@@ -317,7 +343,11 @@ def halo_conv_backward(tape: ConvTape, dout):
         ishape[dim] = from_left
         incoming = torch.empty(ishape, dtype=xb.dtype, device=xb.device)
         recvs.append((prv, incoming))
-    x.ctx.transport.exchange(sends, recvs)
+    pending = x.ctx.transport.exchange_start(sends, recvs)
+    if work:
+        kernels.conv_wgrad(xb, tape.halo, dyb, dw, kernel=kernel, stride=tape.strides,
+                           base=tape.base, shard=tape.sp, halo_rows=mine.rw)
+    pending.wait()
     if incoming is not None:
         kernels.accumulate(dxb.narrow(dim, 0, from_left), incoming)
     dw = all_reduce(group, dw, "sum")
@@ -439,19 +469,41 @@ def ring_attention_forward(q: ShardTensor, k: ShardTensor, v: ShardTensor):
     state = RingSoftmaxState(ql.shape[0], heads, d, ql.dtype, ql.device)
     pay = _kv_payload(k.local, v.local)
     for step in range(r):
+        # the next K||V hop is posted before this block's attention kernel, so
+        # the transfer over NVLink overlaps the compute (double-buffered)
+        nxt_pay = pending = None
+        if step < r - 1:
+            q.ctx.collective_count += 1
+            src = ring_source(me, step + 1, r)
+            nxt_pay, pending = _ring_post(group, pay, (kv_ext[src],) + tuple(pay.shape[1:]))
         if pay.shape[0]:
             kb, vb = pay[:, 0], pay[:, 1]
             if ql.dim() == 2:
                 kb, vb = kb[:, 0], vb[:, 0]
             state.update(ql, kb, vb, scale)
-        if step < r - 1:
-            q.ctx.collective_count += 1
-            src = ring_source(me, step + 1, r)
-            shape = (kv_ext[src],) + tuple(pay.shape[1:])
-            pay = ring_shift_known(group, pay, shape)
+        if pending is not None:
+            pending.wait()
+            pay = nxt_pay
     out, lse = state.output(ql, ql.dtype)
     res = ShardTensor(out, q.global_shape, q.ctx, q.placements, q.shard_shapes)
     return res, AttnTape(q, k, v, res, lse, qa, scale)
+
+
+def _ring_post(group: AxisGroup, payload: torch.Tensor, recv_shape):
+    """Post one ring hop (send to index+1, receive `recv_shape` from
+    index-1) and return (receive buffer, handle); R = 1 never posts."""
+    r = group.size
+    nxt = group.members[(group.index + 1) % r]
+    prv = group.members[(group.index - 1) % r]
+    out = torch.empty(tuple(recv_shape), dtype=payload.dtype, device=payload.device)
+    sends = [(nxt, payload.contiguous())] if payload.numel() else []
+    recvs = [(prv, out)] if out.numel() else []
+    if group.ctx.transport.kind == "thread":
+        # per-pair FIFO mailboxes: empty payloads still travel (pairing never
+        # depends on the data)
+        sends = [(nxt, payload.contiguous())]
+        recvs = [(prv, out)]
+    return out, group.ctx.transport.exchange_start(sends, recvs)
 
 
 def ring_attention(q: ShardTensor, k: ShardTensor, v: ShardTensor) -> ShardTensor:
@@ -497,19 +549,36 @@ def ring_attention_backward(tape: AttnTape, dout):
         r, me = group.size, group.index
         kv_ext = k.shard_shapes[tape.axis]
         pay = _kv_payload(k.local, v.local)
-        # dK and dV accumulators travel as one contiguous [2, S, H, d] payload
-        grads = torch.zeros((2, pay.shape[0], heads, d), dtype=sd, device=ql.device)
+        # dK and dV accumulators travel as one contiguous [2, S, H, d] payload.
+        # K||V hops are posted before each block's kernel (overlapped); the
+        # block's own contribution is computed into a fresh accumulator while
+        # the partial sums of the previous members are still in flight, and
+        # the two are added before the sum moves on.
+        incoming = pending_g = None
+        grads = None
         for step in range(r):
+            src_now = ring_source(me, step, r)
+            nxt_pay = pending = None
+            if step < r - 1:
+                q.ctx.collective_count += 1
+                src = ring_source(me, step + 1, r)
+                nxt_pay, pending = _ring_post(group, pay, (kv_ext[src],) + tuple(pay.shape[1:]))
+            grads = torch.zeros((2, kv_ext[src_now], heads, d), dtype=sd, device=ql.device)
             if pay.shape[0]:
                 kb, vb = pay[:, 0], pay[:, 1]
                 if ql.dim() == 2:
                     kb, vb = kb[:, 0], vb[:, 0]
                 run_block(kb, vb, grads[0], grads[1])
+            if pending_g is not None:
+                pending_g.wait()
+                if grads.numel():
+                    kernels.accumulate(grads, incoming)
             if step < r - 1:
-                q.ctx.collective_count += 1
-                src = ring_source(me, step + 1, r)
-                pay = ring_shift_known(group, pay, (kv_ext[src],) + tuple(pay.shape[1:]))
-                grads = ring_shift_known(group, grads, (2, kv_ext[src], heads, d))
+                incoming, pending_g = _ring_post(group, grads,
+                                                 (2, kv_ext[ring_source(me, step + 1, r)], heads, d))
+            if pending is not None:
+                pending.wait()
+                pay = nxt_pay
         if r > 1:
             # block held now is member (me - (r-1)) mod r = me + 1: one hop home
             q.ctx.collective_count += 1
