@@ -62,44 +62,95 @@ __device__ __forceinline__ void offsets(const Walk &w, int64_t row, int64_t &so,
     }
 }
 
-template <typename V>
-__global__ void __launch_bounds__(256) copy_kernel(Walk w, int64_t inner, int64_t total,
-                                                   const V *__restrict__ src, V *__restrict__ dst) {
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    // 4 vectors in flight per thread
-    for (; i < total; i += 4 * stride) {
-        V buf[4];
-        int64_t dofs[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            int64_t j = i + u * stride;
-            if (j < total) {
-                int64_t row = j / inner, col = j - row * inner, so, d_o;
-                offsets(w, row, so, d_o);
-                buf[u] = src[so + col];
-                dofs[u] = d_o + col;
-            }
+// Row-tiled walk: the index space is rows (outer dims) x `inner` vectors.
+// G lanes (a power of two <= 32, ~ the row length) share a row: the row's
+// source / destination offsets are computed once per row (64-bit div/mod
+// amortised over the run) and the lanes stride over its vectors, 4
+// independent loads in flight each.  Short rows (a 2-voxel halo face is 8
+// x 16 B) pack 32/G rows per warp so no lane idles.
+template <typename V, int G>
+__global__ void __launch_bounds__(256) copy_rows(Walk w, int64_t inner, int64_t rows,
+                                                 const V *__restrict__ src, V *__restrict__ dst) {
+    const int64_t groups = (int64_t)gridDim.x * (blockDim.x / G);
+    const int sub = threadIdx.x % G;
+    for (int64_t row = (int64_t)blockIdx.x * (blockDim.x / G) + threadIdx.x / G; row < rows;
+         row += groups) {
+        int64_t so, d_o;
+        offsets(w, row, so, d_o);
+        const V *s = src + so;
+        V *d = dst + d_o;
+        int64_t c = sub;
+        for (; c + 3 * G < inner; c += 4 * G) {
+            V a0 = s[c], a1 = s[c + G], a2 = s[c + 2 * G], a3 = s[c + 3 * G];
+            d[c] = a0;
+            d[c + G] = a1;
+            d[c + 2 * G] = a2;
+            d[c + 3 * G] = a3;
         }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            int64_t j = i + u * stride;
-            if (j < total) dst[dofs[u]] = buf[u];
-        }
+        for (; c < inner; c += G) d[c] = s[c];
     }
 }
 
 template <typename T>
-__global__ void __launch_bounds__(256) accum_kernel(Walk w, int64_t inner, int64_t total,
-                                                    int64_t s_inner, int64_t d_inner,
-                                                    const T *__restrict__ src, T *__restrict__ dst) {
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < total; j += stride) {
-        int64_t row = j / inner, col = j - row * inner, so, d_o;
-        offsets(w, row, so, d_o);
-        T *p = dst + d_o + col * d_inner;
-        *p = from_acc<T>(to_acc(*p) + to_acc(src[so + col * s_inner]));
+__device__ __forceinline__ void acc_vec(T *d, const T *s);
+template <>
+__device__ __forceinline__ void acc_vec<float>(float *d, const float *s) {
+    float4 a = *reinterpret_cast<const float4 *>(s);
+    float4 b = *reinterpret_cast<float4 *>(d);
+    b.x += a.x; b.y += a.y; b.z += a.z; b.w += a.w;
+    *reinterpret_cast<float4 *>(d) = b;
+}
+template <>
+__device__ __forceinline__ void acc_vec<double>(double *d, const double *s) {
+    double2 a = *reinterpret_cast<const double2 *>(s);
+    double2 b = *reinterpret_cast<double2 *>(d);
+    b.x += a.x; b.y += a.y;
+    *reinterpret_cast<double2 *>(d) = b;
+}
+template <>
+__device__ __forceinline__ void acc_vec<__nv_bfloat16>(__nv_bfloat16 *d, const __nv_bfloat16 *s) {
+    uint4 a = *reinterpret_cast<const uint4 *>(s);
+    uint4 b = *reinterpret_cast<uint4 *>(d);
+    __nv_bfloat162 *pa = reinterpret_cast<__nv_bfloat162 *>(&a);
+    __nv_bfloat162 *pb = reinterpret_cast<__nv_bfloat162 *>(&b);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        float2 x = __bfloat1622float2(pa[i]), y = __bfloat1622float2(pb[i]);
+        pb[i] = __floats2bfloat162_rn(x.x + y.x, x.y + y.y);
     }
+    *reinterpret_cast<uint4 *>(d) = b;
+}
+template <typename T> struct VecN { static constexpr int n = 16 / sizeof(T); };
+
+// dst += src, row-tiled like copy_rows; VEC: 16-B vectors along a unit-stride
+// inner run (fp32 adds in fp32, bf16 through fp32, fp64 in fp64).
+template <typename T, int G, bool VEC>
+__global__ void __launch_bounds__(256) accum_rows(Walk w, int64_t inner, int64_t rows,
+                                                  int64_t s_inner, int64_t d_inner,
+                                                  const T *__restrict__ src, T *__restrict__ dst) {
+    const int64_t groups = (int64_t)gridDim.x * (blockDim.x / G);
+    const int sub = threadIdx.x % G;
+    constexpr int NV = VecN<T>::n;
+    for (int64_t row = (int64_t)blockIdx.x * (blockDim.x / G) + threadIdx.x / G; row < rows;
+         row += groups) {
+        int64_t so, d_o;
+        offsets(w, row, so, d_o);
+        if (VEC) {
+            for (int64_t c = sub; c < inner / NV; c += G)
+                acc_vec<T>(dst + d_o + c * NV, src + so + c * NV);
+        } else {
+            for (int64_t c = sub; c < inner; c += G) {
+                T *p = dst + d_o + c * d_inner;
+                *p = from_acc<T>(to_acc(*p) + to_acc(src[so + c * s_inner]));
+            }
+        }
+    }
+}
+
+int lanes_for(int64_t inner) {
+    int g = 1;
+    while (g < 32 && g < inner) g <<= 1;
+    return g;
 }
 
 // Collapse (shape, src strides, dst strides) in place; returns new ndim.
@@ -142,6 +193,14 @@ int collapse(int nd, int64_t *shape, int64_t *ss, int64_t *ds) {
     return n;
 }
 
+template <typename V, int G>
+void launch_rows(const Walk &w, int64_t inner, int64_t rows, const void *src, void *dst,
+                 cudaStream_t st) {
+    const int64_t work = rows * ((inner + 4 * G - 1) / (4 * G)) * G;  // threads with work
+    const int grid = grid_for((work + 0) / 1, 256, 16);
+    copy_rows<V, G><<<grid, 256, 0, st>>>(w, inner, rows, (const V *)src, (V *)dst);
+}
+
 template <typename V>
 int launch_copy(int n, const int64_t *shape, const int64_t *ss, const int64_t *ds, int vec_elems,
                 const void *src, void *dst, cudaStream_t st) {
@@ -155,10 +214,56 @@ int launch_copy(int n, const int64_t *shape, const int64_t *ss, const int64_t *d
     int64_t inner = shape[n - 1] / vec_elems;
     int64_t rows = 1;
     for (int i = 0; i < n - 1; ++i) rows *= shape[i];
-    int64_t total = rows * inner;
-    int grid = grid_for((total + 3) / 4, 256, 16);
-    copy_kernel<V><<<grid, 256, 0, st>>>(w, inner, total, (const V *)src, (V *)dst);
+    // long runs are cut into kChunk-vector rows (a new innermost outer dim)
+    // so every SM gets rows; the tail of a run that does not divide goes in
+    // a second launch
+    constexpr int64_t kChunk = 2048;
+    if (inner > 2 * kChunk && w.nd < kMaxDims) {
+        const int64_t nch = inner / kChunk, rem = inner - nch * kChunk;
+        if (rem) {
+            Walk t = w;
+            int64_t rrows = rows;
+            const V *s2 = (const V *)src + nch * kChunk;
+            V *d2 = (V *)dst + nch * kChunk;
+            launch_rows<V, 32>(t, rem, rrows, s2, d2, st);
+        }
+        w.shape[w.nd] = nch;
+        w.ss[w.nd] = kChunk;
+        w.ds[w.nd] = kChunk;
+        ++w.nd;
+        rows *= nch;
+        inner = kChunk;
+    }
+    switch (lanes_for(inner)) {
+        case 1: launch_rows<V, 1>(w, inner, rows, src, dst, st); break;
+        case 2: launch_rows<V, 2>(w, inner, rows, src, dst, st); break;
+        case 4: launch_rows<V, 4>(w, inner, rows, src, dst, st); break;
+        case 8: launch_rows<V, 8>(w, inner, rows, src, dst, st); break;
+        case 16: launch_rows<V, 16>(w, inner, rows, src, dst, st); break;
+        default: launch_rows<V, 32>(w, inner, rows, src, dst, st); break;
+    }
     return launch_status("dp_copy_strided");
+}
+
+template <typename T, bool VEC>
+int launch_accum(const Walk &w, int64_t inner, int64_t rows, int64_t s_in, int64_t d_in,
+                 const void *src, void *dst, cudaStream_t st) {
+    const int64_t units = VEC ? inner / VecN<T>::n : inner;
+    const int g = lanes_for(units);
+    const int grid = grid_for(rows * g, 256, 16);
+#define DP_ACC(G)                                                                            \
+    accum_rows<T, G, VEC><<<grid, 256, 0, st>>>(w, inner, rows, s_in, d_in, (const T *)src, \
+                                                (T *)dst)
+    switch (g) {
+        case 1: DP_ACC(1); break;
+        case 2: DP_ACC(2); break;
+        case 4: DP_ACC(4); break;
+        case 8: DP_ACC(8); break;
+        case 16: DP_ACC(16); break;
+        default: DP_ACC(32); break;
+    }
+#undef DP_ACC
+    return launch_status("dp_accumulate_strided");
 }
 
 }  // namespace
@@ -259,25 +364,53 @@ extern "C" int dp_accumulate_strided(int ndim, const int64_t *shape, void *dst,
         w.ds[i] = ds[i];
     }
     int64_t inner = sh[n - 1];
-    int grid = grid_for(total, 256, 16);
+    int64_t rows = total / inner;
     cudaStream_t st = (cudaStream_t)stream;
+    const int eb = dtype == DP_F64 ? 8 : dtype == DP_F32 ? 4 : 2;
+    // long unit-stride runs: cut into 8192-element rows (tail in a 2nd launch)
+    if (inner > 16384 && ss[n - 1] == 1 && ds[n - 1] == 1 && w.nd < 8) {
+        constexpr int64_t kChunk = 8192;
+        const int64_t nch = inner / kChunk, rem = inner - nch * kChunk;
+        if (rem) {
+            int64_t tsh[8], tss[8], tds[8];
+            for (int i = 0; i < n; ++i) {
+                tsh[i] = sh[i];
+                tss[i] = ss[i];
+                tds[i] = ds[i];
+            }
+            tsh[n - 1] = rem;
+            const char *s2 = (const char *)src + nch * kChunk * eb;
+            char *d2 = (char *)dst + nch * kChunk * eb;
+            int rc = dp_accumulate_strided(n, tsh, d2, tds, s2, tss, dtype, stream);
+            if (rc) return rc;
+        }
+        w.shape[w.nd] = nch;
+        w.ss[w.nd] = kChunk;
+        w.ds[w.nd] = kChunk;
+        ++w.nd;
+        rows *= nch;
+        inner = kChunk;
+    }
+    // 16-B vectors when the inner run is unit-stride on both sides and every
+    // row start is 16-B aligned
+    bool vec = ss[n - 1] == 1 && ds[n - 1] == 1 && (inner * eb) % 16 == 0 &&
+               (uintptr_t)src % 16 == 0 && (uintptr_t)dst % 16 == 0;
+    for (int i = 0; i < n - 1 && vec; ++i)
+        vec = (ss[i] * eb) % 16 == 0 && (ds[i] * eb) % 16 == 0;
     switch (dtype) {
         case DP_F32:
-            accum_kernel<float><<<grid, 256, 0, st>>>(w, inner, total, ss[n - 1], ds[n - 1],
-                                                     (const float *)src, (float *)dst);
-            break;
+            return vec ? launch_accum<float, true>(w, inner, rows, ss[n - 1], ds[n - 1], src, dst, st)
+                       : launch_accum<float, false>(w, inner, rows, ss[n - 1], ds[n - 1], src, dst, st);
         case DP_F64:
-            accum_kernel<double><<<grid, 256, 0, st>>>(w, inner, total, ss[n - 1], ds[n - 1],
-                                                      (const double *)src, (double *)dst);
-            break;
+            return vec ? launch_accum<double, true>(w, inner, rows, ss[n - 1], ds[n - 1], src, dst, st)
+                       : launch_accum<double, false>(w, inner, rows, ss[n - 1], ds[n - 1], src, dst, st);
         case DP_BF16:
-            accum_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(
-                w, inner, total, ss[n - 1], ds[n - 1], (const __nv_bfloat16 *)src,
-                (__nv_bfloat16 *)dst);
-            break;
+            return vec ? launch_accum<__nv_bfloat16, true>(w, inner, rows, ss[n - 1], ds[n - 1], src,
+                                                           dst, st)
+                       : launch_accum<__nv_bfloat16, false>(w, inner, rows, ss[n - 1], ds[n - 1],
+                                                            src, dst, st);
         default:
             set_error("dp_accumulate_strided: dtype %d", dtype);
             return DP_ERR_INVALID;
     }
-    return launch_status("dp_accumulate_strided");
 }
