@@ -601,20 +601,24 @@ int run_conv_tc(const dp_conv_geom *g, bool dgrad, const void *in, const void *i
 //                            X_virtual[b, base_p+po+kp, base_q+qo+kq, base_w+wo+kw, ci]
 // Substituting w' = wo + kw: dW[..kw] = sum_w' X[base_w + w'] * dY[w' - kw].
 //
-// A unit is a column (b, po, w' tile) and a chunk of output rows [q0, q1);
-// like the forward kernel it streams INPUT rows along Q.  Step s loads
+// A unit is a column (b, po, w' tile) and a chunk of output rows [q0, q1); like
+// the forward kernel it streams INPUT rows along Q.  Step s loads
 //   * input row q = base_q + q0 + s: KP x (channel blocks) boxes of
-//     KT*16 w' voxels, swizzled, into the X ring, and
+//     16*kt w' voxels, swizzled, into the X ring, and
 //   * (s < nq) dY row q0 + s as KW copies, each TMA-loaded at w' - kw (zero
-//     outside [0, Wout)), into the dY ring,
-// then for every kq with j = s - kq in [0, nq):
-//   D[kq][M = (kp,ci)][N = (kw,co)] += X_step(s)[K = w'] . dY_row(j)[K = w']
-// with both operands MN-major straight out of the TMA boxes (K = w' runs
-// down the swizzled rows).  Each X row is loaded once per unit (not KQ
-// times), each dY row KW times.  All units of a CTA accumulate into the same
-// TMEM tiles; the per-CTA partials [cta][kq][m][n] are summed into dW by a
-// deterministic reduction.  M tiles cover (kp, ci) rows 128 at a time; rows
-// past KP*Cin read the next boxes (garbage rows, never stored into dW).
+//     outside [0, Wout)), into the dY ring.
+// Once input row j + KQ - 1 has landed, output row j's whole contribution is
+//   D[M = (kq, kp, ci)][N = (kw, co)] += X_{j..j+KQ-1}[K = w'] . dY_j[K = w']
+// with the KQ consecutive X rows read as ONE operand: the X ring slots are
+// contiguous and the first KQ-1 slots are mirrored after the last, so rows
+// j..j+KQ-1 are always adjacent boxes (uniform LBO).  Both operands are
+// MN-major straight out of the swizzled TMA boxes (K = w' runs down the
+// rows).  M tiles cover (kq, kp, ci) 128 rows at a time — 144 rows in 2
+// tiles for C_in = 16 (was 3 per-kq tiles of 48), 192 in 2 for the 2-D
+// 64-channel case — rows past KQ*KP*Cin read the next boxes (garbage rows,
+// never reduced into dW).  Each X row is loaded once per unit.  All units of
+// a CTA accumulate into the same TMEM tiles; the per-CTA partials
+// [cta][m][n] are summed into dW by a deterministic reduction.
 struct WgradTcParams {
     int B, Cin, N;                   // N = Cout (dY channels)
     int Pin, Qin, Win, Pout, Qout, Wout;
@@ -622,18 +626,18 @@ struct WgradTcParams {
     int base_p, base_q, base_w;
     int split, halo;
     int n_wt, n_qc, q_chunk, n_units, n_mt, kt;  // kt = 16-voxel K steps per w' tile
-    int nx, nd;                      // X ring / dY ring depth
-    int kq_lo, kq_hi;                // taps of this pass (TMEM holds (kq_hi-kq_lo) tiles)
-    float *partial;                  // [grid][KQ][n_mt*128][KW*N]
+    int nx, nd;                      // X ring slots (plus KQ-1 mirrors) / dY ring depth
+    float *partial;                  // [grid][n_mt*128][KW*N]
 };
 
 struct WLayout {
     int cbx, nbx, boxx;              // X channel block, blocks, box bytes
     int cbd, nbd, boxd;              // dY channel block, blocks, box bytes
-    int xslot, dslot, tail;          // ring slot bytes, garbage tail
+    int xslot, dslot, tail;          // ring slot bytes, garbage tail after the mirrors
 };
 
-__host__ __device__ inline WLayout wlayout(int cin, int cout, int KP, int KW, int kt, int n_mt) {
+__host__ __device__ inline WLayout wlayout(int cin, int cout, int KP, int KQ, int KW, int kt,
+                                           int n_mt) {
     WLayout L;
     L.cbx = chan_block(cin);
     L.nbx = cin / L.cbx;
@@ -643,7 +647,7 @@ __host__ __device__ inline WLayout wlayout(int cin, int cout, int KP, int KW, in
     L.boxd = (kt * 16 * L.cbd * 2 + 1023) / 1024 * 1024;
     L.xslot = KP * L.nbx * L.boxx;
     L.dslot = KW * L.nbd * L.boxd;
-    const int over = (n_mt * 128 / L.cbx - KP * L.nbx) * L.boxx;
+    const int over = (n_mt * 128 / L.cbx - KQ * KP * L.nbx) * L.boxx;
     L.tail = over > 0 ? over : 0;
     return L;
 }
@@ -661,18 +665,18 @@ conv_wgrad_tc_kernel(const __grid_constant__ CUtensorMap xmap,
     const int KQ = kStatic ? KQ_ : p.KQ;
     const int KW = kStatic ? KW_ : p.KW;
     const int CIN = kStatic ? CIN_ : p.Cin;
-    const int NMT = (KP * CIN + 127) / 128;
-    const WLayout L = wlayout(CIN, N, KP, KW, p.kt, NMT);
+    const int NMT = (KQ * KP * CIN + 127) / 128;
+    const WLayout L = wlayout(CIN, N, KP, KQ, KW, p.kt, NMT);
     const int NT = KW * N;  // MMA N
+    const int NXM = p.nx + KQ - 1;   // physical X slots incl. mirrors
     uint8_t *xring = smem;
-    uint8_t *dring = smem + (size_t)p.nx * L.xslot + L.tail;
+    uint8_t *dring = smem + (size_t)NXM * L.xslot + L.tail;
     uint64_t *bars = reinterpret_cast<uint64_t *>(dring + (size_t)p.nd * L.dslot);
     uint64_t *xfull = bars, *xempty = xfull + p.nx;
     uint64_t *dfull = xempty + p.nx, *dempty = dfull + p.nd, *done = dempty + p.nd;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(done + 1);
-    const int NKQ = p.kq_hi - p.kq_lo;
     uint32_t ncols = 32;
-    while (ncols < (uint32_t)(NKQ * NMT * NT)) ncols <<= 1;
+    while (ncols < (uint32_t)(NMT * NT)) ncols <<= 1;
     if (warp == 0) {
         if (lane == 0) {
             for (int i = 0; i < p.nx; ++i) {
@@ -701,7 +705,7 @@ conv_wgrad_tc_kernel(const __grid_constant__ CUtensorMap xmap,
     if (warp == 0) {
         // ===================== TMA producer (whole warp, elected issue) =====================
         uint32_t xi = 0, di = 0;
-        const uint32_t xbytes = (uint32_t)(KP * L.nbx * WK * L.cbx * 2);
+        const uint32_t xrow = (uint32_t)(KP * L.nbx * WK * L.cbx * 2);
         const uint32_t dbytes = (uint32_t)(KW * L.nbd * WK * L.cbd * 2);
         for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
             int r = u;
@@ -713,12 +717,12 @@ conv_wgrad_tc_kernel(const __grid_constant__ CUtensorMap xmap,
             const int nq = q1 - q0, nrows = nq + KQ - 1;
             const int w0 = wt * WK;
             for (int s = 0; s < nrows; ++s) {
-                {   // X: input row q = base_q + q0 + s, all kp
+                {   // X: input row q = base_q + q0 + s, all kp (and its mirror slot)
                     const uint32_t idx = xi % p.nx, ph = (xi / p.nx) & 1;
                     ++xi;
+                    const bool mirror = (int)idx < KQ - 1;
                     mbar_wait(&xempty[idx], ph ^ 1);
-                    mbar_expect_tx_e(&xfull[idx], xbytes);
-                    uint8_t *dst = xring + (size_t)idx * L.xslot;
+                    mbar_expect_tx_e(&xfull[idx], mirror ? 2 * xrow : xrow);
                     const int qv = p.base_q + q0 + s;
                     for (int kp = 0; kp < KP; ++kp) {
                         const int pv = p.base_p + po + kp;
@@ -731,9 +735,14 @@ conv_wgrad_tc_kernel(const __grid_constant__ CUtensorMap xmap,
                             map = &hmap;
                             qcrd = qv - p.Qin;
                         }
-                        for (int cb = 0; cb < L.nbx; ++cb)
-                            tma_load_5d_e(dst + (size_t)(kp * L.nbx + cb) * L.boxx, map,
-                                          &xfull[idx], cb * L.cbx, p.base_w + w0, qcrd, pc, b);
+                        for (int cb = 0; cb < L.nbx; ++cb) {
+                            const size_t off = (size_t)(kp * L.nbx + cb) * L.boxx;
+                            tma_load_5d_e(xring + (size_t)idx * L.xslot + off, map, &xfull[idx],
+                                          cb * L.cbx, p.base_w + w0, qcrd, pc, b);
+                            if (mirror)
+                                tma_load_5d_e(xring + (size_t)(p.nx + idx) * L.xslot + off, map,
+                                              &xfull[idx], cb * L.cbx, p.base_w + w0, qcrd, pc, b);
+                        }
                     }
                 }
                 if (s < nq) {  // dY row q0 + s, KW shifted copies
@@ -758,47 +767,41 @@ conv_wgrad_tc_kernel(const __grid_constant__ CUtensorMap xmap,
         const uint32_t bstep = (16 * L.cbd * 2) >> 4;
         const uint32_t mstep = (128 / L.cbx * L.boxx) >> 4;
         uint32_t xi = 0, di = 0;   // X / dY ring counters (consumption order)
-        uint32_t fresh = (1u << (NKQ * NMT)) - 1u;  // accumulators not yet written
+        uint32_t fresh = (1u << NMT) - 1u;  // accumulators not yet written
         for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
             int r = u / p.n_wt;
             const int qc = r % p.n_qc;
             const int q0 = qc * p.q_chunk, q1 = min(p.Qout, q0 + p.q_chunk);
             const int nq = q1 - q0, nrows = nq + KQ - 1;
-            const uint32_t dbase = di;  // ring index of this unit's dY row 0
+            const uint32_t xbase = xi;   // X ring index of this unit's row 0
             for (int s = 0; s < nrows; ++s) {
                 const uint32_t xidx = xi % p.nx, xph = (xi / p.nx) & 1;
                 ++xi;
-                if (s < nq) ++di;
                 mbar_wait(&xfull[xidx], xph);
-                if (s < nq) {
-                    const uint32_t j = dbase + s;
-                    mbar_wait(&dfull[j % p.nd], (j / p.nd) & 1);
-                }
+                const int j = s - (KQ - 1);   // output row complete with this input row
+                if (j < 0) continue;
+                const uint32_t didx = di % p.nd, dph = (di / p.nd) & 1;
+                ++di;
+                mbar_wait(&dfull[didx], dph);
                 tc_fence_after();
-                const uint64_t ax = a0 + ((xidx * L.xslot) >> 4);
+                const uint32_t xs = (xbase + j) % p.nx;   // slot of input row j (kq = 0)
+                const uint64_t ax = a0 + ((xs * L.xslot) >> 4);
+                const uint64_t bd = b0 + ((didx * L.dslot) >> 4);
 #pragma unroll
-                for (int kq = 0; kq < KQ; ++kq) {
-                    const int jr = s - kq;
-                    if (jr < 0 || jr >= nq || kq < p.kq_lo || kq >= p.kq_hi) continue;
-                    const uint32_t j = dbase + jr;
-                    const uint64_t bd = b0 + (((j % p.nd) * L.dslot) >> 4);
-                    const int t0 = (kq - p.kq_lo) * NMT;
-#pragma unroll
-                    for (int mt = 0; mt < NMT; ++mt) {
-                        const uint32_t d = tmem + (uint32_t)((t0 + mt) * NT);
-                        const uint32_t bit = 1u << (t0 + mt);
-                        uint32_t acc = (fresh & bit) ? 0u : 1u;
-                        fresh &= ~bit;
-                        for (int ks = 0; ks < p.kt; ++ks) {
-                            mma_bf16_e(d, ax + mt * mstep + ks * astep, bd + ks * bstep, idesc,
-                                       acc);
-                            acc = 1u;
-                        }
+                for (int mt = 0; mt < NMT; ++mt) {
+                    const uint32_t d = tmem + (uint32_t)(mt * NT);
+                    const uint32_t bit = 1u << mt;
+                    uint32_t acc = (fresh & bit) ? 0u : 1u;
+                    fresh &= ~bit;
+                    for (int ks = 0; ks < p.kt; ++ks) {
+                        mma_bf16_e(d, ax + mt * mstep + ks * astep, bd + ks * bstep, idesc, acc);
+                        acc = 1u;
                     }
-                    // dY row j is dead after this pass's last tap (always inside the unit)
-                    if (kq == p.kq_hi - 1) mma_commit_e(&dempty[j % p.nd]);
                 }
-                mma_commit_e(&xempty[xidx]);
+                mma_commit_e(&dempty[didx]);          // dY row j is done
+                mma_commit_e(&xempty[xs]);            // input row j: its last tap (kq = 0)
+                if (j == nq - 1)                      // unit end: rows j+1.. are never kq=0
+                    for (int t = 1; t < KQ; ++t) mma_commit_e(&xempty[(xbase + j + t) % p.nx]);
             }
         }
         mma_commit_e(done);
@@ -807,9 +810,8 @@ conv_wgrad_tc_kernel(const __grid_constant__ CUtensorMap xmap,
         const int m = quarter * 32 + lane;
         mbar_wait(done, 0);
         tc_fence_after();
-        for (int t = 0; t < NKQ * NMT; ++t) {
-            float *dst = p.partial +
-                         ((size_t)(blockIdx.x * KQ * NMT + p.kq_lo * NMT + t) * 128 + m) * NT;
+        for (int t = 0; t < NMT; ++t) {
+            float *dst = p.partial + ((size_t)(blockIdx.x * NMT + t) * 128 + m) * NT;
             for (int c = 0; c < NT; c += 16) {
                 uint32_t v[16];
                 tmem_ld16(tmem + ((uint32_t)(quarter * 32) << 16) + t * NT + c, v);
@@ -830,7 +832,7 @@ conv_wgrad_tc_kernel(const __grid_constant__ CUtensorMap xmap,
     }
 }
 
-// dw[co][ci][kp][kq][kw] = sum_cta partial[cta][kq][mt][m][kw*N + co], m = kp*Cin + ci
+// dw[co][ci][kp][kq][kw] = sum_cta partial[cta][row][kw*N + co], row = (kq*KP + kp)*Cin + ci
 __global__ void wgrad_tc_reduce(const float *__restrict__ part, float *__restrict__ dw, int ctas,
                                 int n_mt, int KP, int KQ, int KW, int Cin, int N) {
     const int taps = KP * KQ * KW;
@@ -843,9 +845,9 @@ __global__ void wgrad_tc_reduce(const float *__restrict__ part, float *__restric
         const int kp = r % KP; r /= KP;
         const int ci = r % Cin;
         const int co = r / Cin;
-        const int row = kp * Cin + ci;
-        const size_t per_cta = (size_t)KQ * n_mt * 128 * NT;
-        const size_t off = ((size_t)kq * n_mt * 128 + row) * NT + kw * N + co;
+        const int row = (kq * KP + kp) * Cin + ci;
+        const size_t per_cta = (size_t)n_mt * 128 * NT;
+        const size_t off = (size_t)row * NT + kw * N + co;
         float s = 0.f;
         for (int c = 0; c < ctas; ++c) s += part[c * per_cta + off];
         dw[e] = s;
@@ -854,7 +856,7 @@ __global__ void wgrad_tc_reduce(const float *__restrict__ part, float *__restric
 
 struct WPlan {
     Roles R;
-    int Cin, N, n_mt, kt, n_wt, nx, nd, smem, grid, q_chunk, n_qc, kq_group;
+    int Cin, N, n_mt, kt, n_wt, nx, nd, smem, grid, q_chunk, n_qc;
     WLayout L;
     int64_t n_units;
 };
@@ -872,31 +874,33 @@ bool make_wplan(const dp_conv_geom *g, WPlan &pl) {
         if (R.xs[i] % 8 || R.ys[i] % 8) return false;
         if (g->halo > 0 && R.hs[i] % 8) return false;
     }
-    pl.n_mt = (R.KP * pl.Cin + 127) / 128;
-    // TMEM holds kq_group taps' accumulators at a time; more taps -> more passes
-    pl.kq_group = 512 / (pl.n_mt * R.KW * pl.N);
-    if (pl.kq_group < 1) return false;
-    if (pl.kq_group > R.KQ) pl.kq_group = R.KQ;
+    pl.n_mt = (R.KQ * R.KP * pl.Cin + 127) / 128;
+    if (pl.n_mt * R.KW * pl.N > 512) return false;   // TMEM accumulators
     // w' tiles: K steps of 16 voxels, up to 16 steps (256-row boxes), balanced
     const int wr = R.Wout + R.KW - 1;
     const int steps = (wr + 15) / 16;
-    pl.n_wt = (steps + 15) / 16;
-    pl.kt = (steps + pl.n_wt - 1) / pl.n_wt;
-    // smem: X ring 2-3 slots, dY ring KQ+1.. slots
+    const int tiles0 = (steps + 15) / 16;
+    const int kt0 = (steps + tiles0 - 1) / tiles0;
+    // smem: X ring (KQ+1..KQ+2 slots, + KQ-1 mirrors + garbage tail), dY ring
     const int budget = 220 * 1024 - 512;
-    for (pl.kt = pl.kt; pl.kt >= 1; --pl.kt) {
-        pl.n_wt = (steps + pl.kt - 1) / pl.kt;
-        pl.L = wlayout(pl.Cin, pl.N, R.KP, R.KW, pl.kt, pl.n_mt);
-        pl.nx = 2;
-        pl.nd = R.KQ + 1;
-        const int need = pl.nx * pl.L.xslot + pl.L.tail + pl.nd * pl.L.dslot;
-        if (need <= budget) {
-            if (need + pl.L.xslot <= budget) ++pl.nx;
-            break;
+    pl.kt = 0;
+    for (int kt = kt0; kt >= 1 && !pl.kt; --kt) {
+        const WLayout L = wlayout(pl.Cin, pl.N, R.KP, R.KQ, R.KW, kt, pl.n_mt);
+        for (int nx = R.KQ + 2; nx >= R.KQ + 1; --nx) {
+            const int nd = 3;
+            const int need = (nx + R.KQ - 1) * L.xslot + L.tail + nd * L.dslot;
+            if (need <= budget) {
+                pl.kt = kt;
+                pl.L = L;
+                pl.nx = nx;
+                pl.nd = nd;
+                break;
+            }
         }
     }
     if (pl.kt < 1) return false;
-    pl.smem = pl.nx * pl.L.xslot + pl.L.tail + pl.nd * pl.L.dslot + 512;
+    pl.n_wt = (steps + pl.kt - 1) / pl.kt;
+    pl.smem = (pl.nx + R.KQ - 1) * pl.L.xslot + pl.L.tail + pl.nd * pl.L.dslot + 512;
     // q chunks: balance units over the SMs, amortise the KQ-1 extra rows
     const int sms = sm_count();
     const int64_t cols = (int64_t)g->batch * R.Pout * pl.n_wt;
@@ -948,7 +952,7 @@ int run_wgrad_tc(const dp_conv_geom *g, const void *x, const void *xh, const voi
     WPlan pl;
     DP_REQUIRE(make_wplan(g, pl), DP_ERR_UNSUPPORTED, "conv_wgrad_tc: outside the envelope");
     const Roles &R = pl.R;
-    const int64_t need = (int64_t)pl.grid * R.KQ * pl.n_mt * 128 * R.KW * pl.N * 4;
+    const int64_t need = (int64_t)pl.grid * pl.n_mt * 128 * R.KW * pl.N * 4;
     DP_REQUIRE(ws_bytes >= need, DP_ERR_INVALID, "conv_wgrad_tc: workspace too small");
     (void)need;
     const int taps = R.KP * R.KQ * R.KW;
@@ -1008,18 +1012,14 @@ int run_wgrad_tc(const dp_conv_geom *g, const void *x, const void *xh, const voi
     p.n_mt = pl.n_mt; p.kt = pl.kt;
     p.nx = pl.nx; p.nd = pl.nd;
     p.partial = (float *)ws;
-    for (int lo = 0; lo < R.KQ; lo += pl.kq_group) {
-        p.kq_lo = lo;
-        p.kq_hi = lo + pl.kq_group < R.KQ ? lo + pl.kq_group : R.KQ;
-        int rc;
-        switch (pl.N) {
-            case 16: rc = launch_wgrad_n<16>(xm, hm, dm, p, pl.grid, pl.smem, st); break;
-            case 32: rc = launch_wgrad_n<32>(xm, hm, dm, p, pl.grid, pl.smem, st); break;
-            case 48: rc = launch_wgrad_n<48>(xm, hm, dm, p, pl.grid, pl.smem, st); break;
-            default: rc = launch_wgrad_n<64>(xm, hm, dm, p, pl.grid, pl.smem, st); break;
-        }
-        if (rc) return rc;
+    int rc;
+    switch (pl.N) {
+        case 16: rc = launch_wgrad_n<16>(xm, hm, dm, p, pl.grid, pl.smem, st); break;
+        case 32: rc = launch_wgrad_n<32>(xm, hm, dm, p, pl.grid, pl.smem, st); break;
+        case 48: rc = launch_wgrad_n<48>(xm, hm, dm, p, pl.grid, pl.smem, st); break;
+        default: rc = launch_wgrad_n<64>(xm, hm, dm, p, pl.grid, pl.smem, st); break;
     }
+    if (rc) return rc;
     const int total = pl.N * pl.Cin * taps;
     wgrad_tc_reduce<<<grid_for(total, 256, 4), 256, 0, st>>>((const float *)ws, dw, pl.grid,
                                                              pl.n_mt, R.KP, R.KQ, R.KW, pl.Cin,
@@ -1063,7 +1063,7 @@ int64_t conv_tc_workspace(const dp_conv_geom *g, int which) {
     if (which == DP_CONV_WGRAD) {
         WPlan wp;
         if (!make_wplan(g, wp)) return -1;
-        return (int64_t)wp.grid * wp.R.KQ * wp.n_mt * 128 * wp.R.KW * wp.N * 4;
+        return (int64_t)wp.grid * wp.n_mt * 128 * wp.R.KW * wp.N * 4;
     }
     Plan pl;
     if (!make_plan(g, which == DP_CONV_DGRAD, pl)) return -1;
