@@ -486,12 +486,158 @@ def cpu_sample_cfg4(threads: int):
     return dt, threads / 1024.0
 
 
+
+def random_partition(seed: int, n: int, parts: int, min_part: int = 1):
+    """Uneven extents exactly as the reference's workload generator
+    (domainpar/verify.py:67-81) with rng = default_rng(seed)."""
+    import numpy as np
+
+    rng = np.random.default_rng(seed)
+    if parts == 1:
+        return [n]
+    spare = n - min_part * parts
+    cuts = np.sort(rng.integers(0, spare + 1, size=parts - 1))
+    edges = [0, *cuts.tolist(), spare]
+    return [min_part + edges[i + 1] - edges[i] for i in range(parts)]
+
+
+def setup_cfg5(ctx):
+    """Uneven-shard redistribute: a [n, n] fp32 tensor (1 GiB) Shard(0) with
+    random_partition extents -> Replicate (varlen all-gather) and -> Shard(1)
+    (variable-count all-to-all).  One step = both redistributions."""
+    import torch
+
+    import paper_2605_11111_b200 as dp
+
+    n = 16384
+    R = ctx.mesh.world_size
+    me = ctx.rank_id
+    dev = ctx.device
+    ext = random_partition(R, n, R)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(5 + me)
+    local = torch.randn((ext[me], n), generator=gen, device=dev)
+    st = dp.ShardTensor(local, (n, n), ctx, (dp.Shard(0),), {0: tuple(ext)})
+
+    def step(ins=None):
+        s0 = st if ins is None else dp.ShardTensor(ins[0], (n, n), ctx, (dp.Shard(0),),
+                                                   {0: tuple(ext)})
+        rep = dp.redistribute(s0, (dp.Replicate(),))
+        s1 = dp.redistribute(s0, (dp.Shard(1),))
+        return rep.local[:1], s1.local[:1]
+
+    mib = n * n * 4 / 2 ** 20
+    info = {"workload": f"cfg5: uneven redistribute of a [{n},{n}] fp32 tensor ({mib:.0f} MiB), "
+                        "Shard(0) random_partition extents -> Replicate and -> Shard(1)",
+            "global_batch": 1, "shape": [n, n], "shard_extents": ext,
+            "parallelism": f"domain{R}",
+            "bytes_received_per_rank": {"to_replicate": (n - ext[me]) * n * 4,
+                                        "to_shard1": (n - ext[me]) * (n // R) * 4},
+            "l2": "1 GiB tensor exceeds L2, no flush"}
+    return dict(step=step, inputs=[local], flops=0.0, info=info, scaling="strong", dtype="f32",
+                unit="samples/s", samples_per_step=1)
+
+
+def cpu_sample_cfg5(threads: int):
+    """Oracle port on a bounded sample: the reference's gather-then-slice
+    (np.concatenate + column slice) of a [4096, 16384] fp32 slab set (1/4 of
+    the rows), `threads` rank threads."""
+    import numpy as np
+
+    from oracle import sharding as osh
+
+    n, rows = 16384, 4096
+    R = max(2, threads)
+    ext = random_partition(R, rows, R)
+    rng = np.random.default_rng(0)
+    g = rng.standard_normal((rows, n)).astype(np.float32)
+    b = np.concatenate([[0], np.cumsum(ext)])
+    blocks = [g[b[i]:b[i + 1]] for i in range(R)]
+    t0 = time.perf_counter()
+    full = np.concatenate(blocks, axis=0)          # S(0) -> Replicate on every rank
+    cols = osh.default_chunk(n, R)
+    cb = np.concatenate([[0], np.cumsum(cols)])
+    for i in range(R):                             # S(0) -> S(1): slice own columns
+        np.ascontiguousarray(full[:, cb[i]:cb[i + 1]])
+    dt = time.perf_counter() - t0
+    return dt, rows / n
+
+
+def setup_cfg1(ctx):
+    """conv2d 3x3 halo exchange on a 1x32x1024x1024 fp32 grid, C_out = 32,
+    s1 p1, H-sharded (the reference's CPU parity anchor; fp32 keeps the
+    reference's 1e-5 tolerance, so it runs the fp32 CUDA-core kernels).
+    One step = forward + backward."""
+    import torch
+
+    import paper_2605_11111_b200 as dp
+
+    G, C = 1024, 32
+    R = ctx.mesh.world_size
+    me = ctx.rank_id
+    dev = ctx.device
+    ext = dp.default_chunk(G, R)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(0 + me)
+    x = torch.randn((1, C, ext[me], G), generator=gen, device=dev)
+    wg = torch.Generator(device=dev)
+    wg.manual_seed(1)
+    w = torch.randn((C, C, 3, 3), generator=wg, device=dev) * 0.1
+    plan = dp.halo_conv_plan(ext, G, 3, 1, 1)
+    g = torch.randn((1, C, plan.out_extents[me], G), generator=gen, device=dev)
+    xst = dp.ShardTensor(x, (1, C, G, G), ctx, (dp.Shard(2),), {0: tuple(ext)})
+
+    def step(ins=None):
+        st = xst if ins is None else dp.ShardTensor(ins[0], xst.global_shape, ctx, xst.placements,
+                                                    xst.shard_shapes)
+        y, t = dp.halo_conv_forward(st, w, 1, 1)
+        dx, dw = dp.halo_conv_backward(t, g)
+        return [dw]
+
+    flops = 3 * 2.0 * C * C * 9 * G * G
+    info = {"workload": "cfg1: conv2d 3x3 halo exchange, 1x32x1024x1024 fp32, C_out=32, s1 p1, "
+                        "H-sharded (fp32 CUDA-core kernels: the reference's 1e-5 tolerance)",
+            "global_batch": 1, "grid": [G, G], "channels": [C, C], "layout": "NCHW",
+            "shard_extents": list(ext), "parallelism": f"domain{R}",
+            "l2": "128 MiB activations exceed L2, no flush"}
+    return dict(step=step, inputs=[x], flops=flops, info=info, scaling="strong", dtype="f32",
+                unit="samples/s", samples_per_step=1)
+
+
+def cpu_sample_cfg1(threads: int):
+    """Oracle port (the reference's dense.conv einsum) on 1x32x16x1024
+    row slabs, fwd+bwd, one per thread (1/64 of the grid each)."""
+    import numpy as np
+
+    from oracle import workloads
+
+    rng = np.random.default_rng(0)
+    w = (rng.standard_normal((32, 32, 3, 3)) * 0.1).astype(np.float32)
+    jobs = [(rng.standard_normal((1, 32, 16, 1024)).astype(np.float32),
+             rng.standard_normal((1, 32, 16, 1024)).astype(np.float32)) for _ in range(threads)]
+    t0 = time.perf_counter()
+    if threads == 1:
+        workloads.conv_stack_step(jobs[0][0], [w], jobs[0][1])
+    else:
+        from concurrent.futures import ThreadPoolExecutor
+
+        with ThreadPoolExecutor(threads) as ex:
+            list(ex.map(lambda j: workloads.conv_stack_step(j[0], [w], j[1]), jobs))
+    dt = time.perf_counter() - t0
+    return dt, threads / 64.0
+
 CONFIGS = {"cfg2": (setup_cfg2, cpu_sample_cfg2,
                     "1 x 256 x 64 voxel sub-volumes (1/1024 of the 256^3 volume each), fp32, "
                     "block fwd+bwd via the oracle port of dense.conv's einsum"),
            "cfg3": (setup_cfg3, cpu_sample_cfg3,
                     "one head's 128 query rows vs all 65536 keys (1/8192 of the cfg3 step), "
                     "fp32 in / fp64 softmax, fwd+bwd via the oracle port"),
+           "cfg1": (setup_cfg1, cpu_sample_cfg1,
+                    "1 x 32 x 16 x 1024 fp32 row slabs (1/64 of the grid each), conv fwd+bwd via "
+                    "the oracle port of dense.conv's einsum"),
+           "cfg5": (setup_cfg5, cpu_sample_cfg5,
+                    "np.concatenate + column slices of a 4096 x 16384 fp32 slab set (1/4 of the "
+                    "rows), the reference's gather-then-slice"),
            "cfg4": (setup_cfg4, cpu_sample_cfg4,
                     "1 x 64 x 16 x 256 tiles (1/1024 of one GPU's 2048^2 stack step), fp32, "
                     "4-layer fwd+bwd via the oracle port")}
@@ -676,7 +822,7 @@ def main():
         "gpu_launches": launches // args.steps * args.steps,
         "gpu_launches_per_step": launches / args.steps,
         "clocks": clk.summary(),
-        "tflops_step": W["flops"] / (ms / 1000.0) / 1e12,
+        "tflops_step": W["flops"] / (ms / 1000.0) / 1e12 if W["flops"] else None,
         "kernels": {k: {"launches": v["launches"], "avg_ms": v["ms"] / v["launches"],
                         "tflops": v["flops"] / (v["ms"] / 1000.0) / 1e12 if v["ms"] else None}
                     for k, v in ksum.items()},
