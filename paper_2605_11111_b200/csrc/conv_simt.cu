@@ -263,11 +263,22 @@ int check_geom(const dp_conv_geom *g) {
 
 }  // namespace
 
+// tiled fp32/fp64 kernels (conv_tiled.cu) for stride-1 convolutions
+int conv_tiled_eligible(const dp_conv_geom *, int dtype);
+int conv_fwd_tiled_launch(const dp_conv_geom *, int, const void *, const void *, const void *,
+                          void *, cudaStream_t);
+int conv_dgrad_tiled_launch(const dp_conv_geom *, int, const void *, const void *, void *, void *,
+                            cudaStream_t);
+int64_t conv_wgrad_tiled_workspace(const dp_conv_geom *, int);
+int conv_wgrad_tiled_launch(const dp_conv_geom *, int, const void *, const void *, const void *,
+                            void *, void *, int64_t, cudaStream_t);
+
 // entry points used by capi (conv_tc.cu decides between TC and these)
 int conv_fwd_simt_launch(const dp_conv_geom *cg, int dtype, const void *x, const void *xh,
                          const void *w, void *y, cudaStream_t st) {
     int rc = check_geom(cg);
     if (rc) return rc;
+    if (conv_tiled_eligible(cg, dtype)) return conv_fwd_tiled_launch(cg, dtype, x, xh, w, y, st);
     Geo g = make_geo(cg);
     int64_t total = g.B * g.Co * g.out[0] * g.out[1] * g.out[2];
     if (total == 0) return DP_OK;
@@ -297,6 +308,7 @@ int conv_dgrad_simt_launch(const dp_conv_geom *cg, int dtype, const void *dy, co
                            void *dx, void *dxh, cudaStream_t st) {
     int rc = check_geom(cg);
     if (rc) return rc;
+    if (conv_tiled_eligible(cg, dtype)) return conv_dgrad_tiled_launch(cg, dtype, dy, w, dx, dxh, st);
     Geo g = make_geo(cg);
     int64_t vext = 1;
     for (int i = 0; i < 3; ++i) vext *= g.in[i] + (i == g.shard ? g.halo : 0);
@@ -325,6 +337,7 @@ int conv_dgrad_simt_launch(const dp_conv_geom *cg, int dtype, const void *dy, co
 }
 
 int64_t conv_wgrad_simt_workspace(const dp_conv_geom *cg, int dtype) {
+    if (conv_tiled_eligible(cg, dtype)) return conv_wgrad_tiled_workspace(cg, dtype);
     Geo g = make_geo(cg);
     int64_t taps = (int64_t)g.k[0] * g.k[1] * g.k[2];
     int64_t el = dtype == DP_F64 ? 8 : 4;
@@ -335,6 +348,8 @@ int conv_wgrad_simt_launch(const dp_conv_geom *cg, int dtype, const void *x, con
                            const void *dy, void *dw, void *ws, int64_t ws_bytes, cudaStream_t st) {
     int rc = check_geom(cg);
     if (rc) return rc;
+    if (conv_tiled_eligible(cg, dtype))
+        return conv_wgrad_tiled_launch(cg, dtype, x, xh, dy, dw, ws, ws_bytes, st);
     Geo g = make_geo(cg);
     const int taps = g.k[0] * g.k[1] * g.k[2];
     const int64_t n = g.Co * g.Ci * taps;
