@@ -42,14 +42,15 @@ constexpr int kPBytes = kBM * kBN * 2;             // 32 KB (P tile)
 // ping-pong against the single MMA warp).
 constexpr int kFwdTiles = 2;
 constexpr int kFwdThreads = 128 + 128 * kFwdTiles;  // WG0: TMA + MMA warps; WG1..: softmax
+constexpr int kFwdStages = 4;                              // K/V ring depth
 constexpr int kSmemQ = 0;
 constexpr int kSmemKV = kSmemQ + kFwdTiles * kTileBytes;  // stages of [K | V]
-constexpr int kSmemP = kSmemKV + kStages * 2 * kTileBytes;
-constexpr int kSmemBar = kSmemP + kFwdTiles * kPBytes;
+constexpr int kSmemBar = kSmemKV + kFwdStages * 2 * kTileBytes;
 constexpr int kSmemFwd = kSmemBar + 256;
 
-// TMEM columns: S_t [128 t, 128 t + 128), O_t [256 + 64 t, 256 + 64 t + 64)
-constexpr uint32_t kColS = 0, kColO = 256;
+// TMEM columns per tile t: S_t [128 t, +128) with P_t (bf16 pairs) aliased
+// over its first 64 columns, O_t [256 + 64 t, +64), Q_t [384 + 32 t, +32)
+constexpr uint32_t kColS = 0, kColO = 256, kColQ = 384;
 
 struct FwdParams {
     int sq, sk, H;
@@ -57,6 +58,21 @@ struct FwdParams {
     float c;                  // scale * log2(e)
     float *m, *l, *acc;       // fp32 state: [sq,H], [sq,H], [sq,H,64]
 };
+
+// tcgen05.mma with the A operand in TMEM ("TS"): lane m = row m, a K = 16
+// step = 8 consecutive 32-bit columns holding bf16 pairs (k = 2c, 2c + 1) —
+// verified exactly and timed at the N/2-cycle floor by scripts/umma_ts_probe.cu.
+__device__ __forceinline__ void mma_ts_e(uint32_t d_tmem, uint32_t a_tmem, uint64_t b,
+                                         uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p, e;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "elect.sync _|e, 0xffffffff;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n"
+        "}\n" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(b), "r"(idesc), "r"(accumulate));
+}
 
 __device__ __forceinline__ float ex2(float x) {
     float y;
@@ -127,16 +143,17 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
 
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem + kSmemBar);
     uint64_t *q_full = bars;
-    uint64_t *kv_full = bars + 1, *kv_empty = kv_full + kStages;
-    uint64_t *s_full = kv_empty + kStages;      // [tiles]  S_t(j) ready (and PV_t(j-1) done)
+    uint64_t *kv_full = bars + 1, *kv_empty = kv_full + kFwdStages;
+    uint64_t *s_full = kv_empty + kFwdStages;   // [tiles]  S_t(j) ready (and PV_t(j-1) done)
     uint64_t *p_full = s_full + kFwdTiles;      // [tiles]  softmax -> MMA (count 128)
     uint64_t *done = p_full + kFwdTiles;        // every MMA finished
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(done + 1);
+    uint64_t *q_tm = done + 1;                  // Q tiles staged in TMEM (count 128 * tiles)
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(q_tm + 1);
 
     if (warp == 0) {
         if (lane == 0) {
             mbar_init(q_full, 1);
-            for (int i = 0; i < kStages; ++i) {
+            for (int i = 0; i < kFwdStages; ++i) {
                 mbar_init(&kv_full[i], 1);
                 mbar_init(&kv_empty[i], 1);
             }
@@ -145,6 +162,7 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
                 mbar_init(&p_full[i], 128);
             }
             mbar_init(done, 1);
+            mbar_init(q_tm, 128 * kFwdTiles);
             mbar_fence_init();
             tma_prefetch(&qmap);
             tma_prefetch(&kmap);
@@ -169,8 +187,8 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
         for (int t = 0; t < kFwdTiles; ++t)
             tma_load_3d_e(smem + kSmemQ + t * kTileBytes, &qmap, q_full, 0, h, q0 + t * kBM);
         for (int j = 0; j < nblk; ++j) {
-            const int st = j % kStages;
-            mbar_wait(&kv_empty[st], ((j / kStages) & 1) ^ 1);
+            const int st = j % kFwdStages;
+            mbar_wait(&kv_empty[st], ((j / kFwdStages) & 1) ^ 1);
             mbar_expect_tx_e(&kv_full[st], 2 * kTileBytes);
             uint8_t *dst = smem + kSmemKV + st * 2 * kTileBytes;
             tma_load_3d_e(dst, &kmap, &kv_full[st], 0, h, j * kBN);
@@ -178,30 +196,28 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
         }
     } else if (warp == 1) {
         // ===================== MMA issuer =====================
+        // S_t = Q_t K^T with Q_t in TMEM (TS), O_t += P_t V with P_t in TMEM (TS)
         const uint32_t id_s = idesc_bf16(kBM, kBN);            // K-major A, K-major B
         const uint32_t id_o = idesc_bf16(kBM, kD, 0, 1);       // P K-major, V MN-major
-        mbar_wait(q_full, 0);
+        mbar_wait(q_tm, 0);
         auto issue_s = [&](int t, int j) {
-            const int st = j % kStages;
-            const uint64_t qd = sdesc_sw(smem_u32(smem + kSmemQ + t * kTileBytes), 1024, 2);
+            const int st = j % kFwdStages;
             const uint64_t kd = sdesc_sw(smem_u32(smem + kSmemKV + st * 2 * kTileBytes), 1024, 2);
             const uint32_t sc = tmem + kColS + t * kBN;
 #pragma unroll
             for (int k = 0; k < kD / 16; ++k)
-                mma_bf16_e(sc, qd + ((k * 32) >> 4), kd + ((k * 32) >> 4), id_s, k ? 1u : 0u);
+                mma_ts_e(sc, tmem + kColQ + t * (kD / 2) + k * 8, kd + ((k * 32) >> 4), id_s,
+                         k ? 1u : 0u);
             mma_commit_e(&s_full[t]);
         };
         auto issue_pv = [&](int t, int j) {
-            const int st = j % kStages;
-            const uint64_t pd = sdesc_sw(smem_u32(smem + kSmemP + t * kPBytes), 1024, 2);
+            const int st = j % kFwdStages;
             const uint64_t vd =
                 sdesc_mn(smem_u32(smem + kSmemKV + st * 2 * kTileBytes + kTileBytes), 8192, 1024, 2);
 #pragma unroll
             for (int k = 0; k < kBN / 16; ++k) {
-                // P: key block k/4 (64 keys = one 128-B row), +32 B per 16 keys
-                const uint32_t pa = ((k >> 2) * (kBM * 128) + (k & 3) * 32) >> 4;
                 const uint32_t vb = (k * 16 * 128) >> 4;  // 16 key rows of V
-                mma_bf16_e(tmem + kColO + t * kD, pd + pa, vd + vb, id_o, 1u);
+                mma_ts_e(tmem + kColO + t * kD, tmem + kColS + t * kBN + k * 8, vd + vb, id_o, 1u);
             }
         };
         if (nblk >= 1) {
@@ -211,7 +227,7 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
         }
         for (int j = 0; j < nblk; ++j) {
             const bool more = j + 1 < nblk;
-            if (more) mbar_wait(&kv_full[(j + 1) % kStages], ((j + 1) / kStages) & 1);
+            if (more) mbar_wait(&kv_full[(j + 1) % kFwdStages], ((j + 1) / kFwdStages) & 1);
             for (int t = 0; t < kFwdTiles; ++t) {
                 mbar_wait(&p_full[t], j & 1);
                 tc_fence_after();
@@ -222,7 +238,7 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
                 if (more) issue_s(t, j + 1);
                 else mma_commit_e(&s_full[t]);
             }
-            mma_commit_e(&kv_empty[j % kStages]);
+            mma_commit_e(&kv_empty[j % kFwdStages]);
         }
         mma_commit_e(done);
     }
@@ -252,7 +268,21 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
                 l_run = p.l[sidx];
             }
         }
-        uint8_t *prow = smem + kSmemP + t * kPBytes + rl * 128;
+        {   // Q_t row -> TMEM (A operand of S = Q K^T), once per CTA
+            mbar_wait(q_full, 0);
+            const uint8_t *qrow = smem + kSmemQ + t * kTileBytes + rl * 128;
+            uint32_t qv[32];
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+                const uint4 v = *reinterpret_cast<const uint4 *>(qrow + ((c ^ (rl & 7)) << 4));
+                qv[4 * c] = v.x; qv[4 * c + 1] = v.y; qv[4 * c + 2] = v.z; qv[4 * c + 3] = v.w;
+            }
+            tmem_st16(lane_base + kColQ + t * (kD / 2), *reinterpret_cast<uint32_t(*)[16]>(qv));
+            tmem_st16(lane_base + kColQ + t * (kD / 2) + 16, *reinterpret_cast<uint32_t(*)[16]>(qv + 16));
+            tmem_wait_st();
+            tc_fence_before();
+            mbar_arrive(q_tm);
+        }
         const float2 c2 = make_float2(p.c, p.c);
         for (int j = 0; j < nblk; ++j) {
             mbar_wait(&s_full[t], j & 1);
@@ -272,9 +302,16 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
                 for (int i = 0; i < kBN; ++i)
                     if (i >= kvalid) s[i] = -INFINITY;
             }
-            float mx = fmaxf(s[0], s[1]);
+            // row max: 8 independent chains (ILP), then a small tree
+            float mq[8];
 #pragma unroll
-            for (int i = 2; i < kBN; i += 2) mx = fmaxf(mx, fmaxf(s[i], s[i + 1]));
+            for (int a = 0; a < 8; ++a) mq[a] = fmaxf(s[a], s[a + 8]);
+#pragma unroll
+            for (int i = 16; i < kBN; i += 16)
+#pragma unroll
+                for (int a = 0; a < 8; ++a) mq[a] = fmaxf(mq[a], fmaxf(s[i + a], s[i + 8 + a]));
+            const float mx = fmaxf(fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3])),
+                                   fmaxf(fmaxf(mq[4], mq[5]), fmaxf(mq[6], mq[7])));
             const float tnew = mx * p.c;
             // lazy rescale: only when this row's max grows by more than 2^kRescale
             // (s_full already implies the previous P V finished, so O is quiescent)
@@ -295,30 +332,30 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
                     m_run = tnew;
                 }
             }
-            // P = exp2(s c - m) (bf16) into the swizzled P tile
+            // P = exp2(s c - m) as bf16 pairs into TMEM over S_t's first 64 columns
             const float2 nm = make_float2(-m_run, -m_run);
-            float2 sum2 = make_float2(0.f, 0.f);
+            float2 sumv[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                              make_float2(0.f, 0.f)};   // 4 independent sum chains
 #pragma unroll
-            for (int c = 0; c < kBN / 8; ++c) {
-                uint32_t pk[4];
+            for (int c = 0; c < kBN / 32; ++c) {
+                uint32_t pk[16];
 #pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    float2 x = ffma2(make_float2(s[c * 8 + 2 * i], s[c * 8 + 2 * i + 1]), c2, nm);
-                    if (i < POLY) {
+                for (int i = 0; i < 16; ++i) {
+                    float2 x = ffma2(make_float2(s[c * 32 + 2 * i], s[c * 32 + 2 * i + 1]), c2, nm);
+                    if ((i & 3) < POLY) {
                         x = ex2_poly2(x);
                     } else {
                         x.x = ex2(x.x);
                         x.y = ex2(x.y);
                     }
-                    sum2 = fadd2(sum2, x);
+                    sumv[i & 3] = fadd2(sumv[i & 3], x);
                     pk[i] = pack_bf16(x.x, x.y);
                 }
-                const int blk = c >> 3, ch = c & 7;
-                *reinterpret_cast<uint4 *>(prow + blk * (kBM * 128) + ((ch ^ (rl & 7)) << 4)) =
-                    make_uint4(pk[0], pk[1], pk[2], pk[3]);
+                tmem_st16(colS + c * 16, pk);
             }
+            tmem_wait_st();
+            const float2 sum2 = fadd2(fadd2(sumv[0], sumv[1]), fadd2(sumv[2], sumv[3]));
             l_run += sum2.x + sum2.y;
-            fence_async_smem();
             tc_fence_before();
             mbar_arrive(&p_full[t]);
         }
