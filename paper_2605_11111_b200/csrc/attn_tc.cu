@@ -59,21 +59,6 @@ struct FwdParams {
     float *m, *l, *acc;       // fp32 state: [sq,H], [sq,H], [sq,H,64]
 };
 
-// tcgen05.mma with the A operand in TMEM ("TS"): lane m = row m, a K = 16
-// step = 8 consecutive 32-bit columns holding bf16 pairs (k = 2c, 2c + 1) —
-// verified exactly and timed at the N/2-cycle floor by scripts/umma_ts_probe.cu.
-__device__ __forceinline__ void mma_ts_e(uint32_t d_tmem, uint32_t a_tmem, uint64_t b,
-                                         uint32_t idesc, uint32_t accumulate) {
-    asm volatile(
-        "{\n"
-        ".reg .pred p, e;\n"
-        "setp.ne.b32 p, %4, 0;\n"
-        "elect.sync _|e, 0xffffffff;\n"
-        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n"
-        "}\n" ::"r"(d_tmem),
-        "r"(a_tmem), "l"(b), "r"(idesc), "r"(accumulate));
-}
-
 __device__ __forceinline__ float ex2(float x) {
     float y;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));

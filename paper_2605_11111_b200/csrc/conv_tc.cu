@@ -1027,6 +1027,491 @@ int run_wgrad_tc(const dp_conv_geom *g, const void *x, const void *xh, const voi
     return launch_status("wgrad_tc_reduce");
 }
 
+
+// ---------------------------------------------------------------------------
+// Weight gradient, TS form (C_out = 32, KQ = KW = 3): dY in TMEM, X from smem.
+//
+//   D[m = (kw, co)][n = (kq, kp, ci)] += sum_w' dY[j][w' - kw][co] * X[j + kq][kp][w'][ci]
+//
+// The swapped roles put the 96 (kw, co) rows of one dY row into the A operand
+// and ALL of the (kq, kp, ci) columns (144 / 192 / 288) into N, so every X
+// row is read from shared memory exactly once per output row as a B operand
+// (no per-M-tile re-reads) and the MMA runs at its N/2-cycle compute floor
+// instead of the ~56-cycle shared-memory floor of the SS N = 96 form.  The A
+// operand is built in TMEM by the 3 "transposer" warps (warp kw owns TMEM
+// lanes 32 kw .. 32 kw + 31): per K = 16 step an ldmatrix.x4.trans of the
+// staged dY row (rows w' - kw, re-ordered {0,1,4,5,..} / {2,3,6,7,..} so the
+// transposed fragment IS the tcgen05 16x256b fragment) and one
+// tcgen05.st.16x256b.  Lanes 96..127 are junk rows (never reduced).
+// X rows come through the same mirrored TMA ring as the SS kernel (the KQ
+// rows j..j+2 of output row j are adjacent boxes, one uniform-LBO operand).
+// Only the w' range where X is real is visited (the zero padding columns
+// contribute nothing), so 256-wide rows are exactly two 128-voxel tiles.
+constexpr int kTsCo = 32, kTsKT = 8, kTsWK = kTsKT * 16;
+constexpr int kTsDRow = 16 * 2;                                  // staged dY half row: 16 co
+constexpr int kTsDHalf = ((kTsWK + 2) * kTsDRow + 1023) / 1024 * 1024;  // one co half, 130 rows
+constexpr int kTsDSlot = 2 * kTsDHalf;
+
+struct WgradTsParams {
+    int Pin, Qin, Win, Pout, Qout, Wout;
+    int base_p, base_q, base_w;
+    int split, halo;
+    int w_lo, n_wt, n_qc, q_chunk, n_units;
+    int nx, nd, na;
+    float *partial;   // [grid][96][NT]
+    int dbg;          // ablations (DP_CONV_DBG): 1 no transpose, 2 no MMA, 4 no TMA
+};
+
+__device__ __forceinline__ void ldsm_x4_trans(uint32_t addr, uint32_t (&r)[4]) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"(addr));
+}
+// 16 lanes x 16 repetitions of 128 bits: 64 consecutive columns (8 K = 16 steps);
+// register 2j + g -> lane (lane_id / 4 + 8 g), column 4 j + lane_id % 4.
+__device__ __forceinline__ void tmem_st_16x128b_x16(uint32_t addr, const uint32_t (&r)[8][4]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.16x128b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+        "%11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, "
+        "%28, %29, %30, %31, %32};" ::"r"(addr),
+        "r"(r[0][0]), "r"(r[0][1]), "r"(r[0][2]), "r"(r[0][3]), "r"(r[1][0]), "r"(r[1][1]),
+        "r"(r[1][2]), "r"(r[1][3]), "r"(r[2][0]), "r"(r[2][1]), "r"(r[2][2]), "r"(r[2][3]),
+        "r"(r[3][0]), "r"(r[3][1]), "r"(r[3][2]), "r"(r[3][3]), "r"(r[4][0]), "r"(r[4][1]),
+        "r"(r[4][2]), "r"(r[4][3]), "r"(r[5][0]), "r"(r[5][1]), "r"(r[5][2]), "r"(r[5][3]),
+        "r"(r[6][0]), "r"(r[6][1]), "r"(r[6][2]), "r"(r[6][3]), "r"(r[7][0]), "r"(r[7][1]),
+        "r"(r[7][2]), "r"(r[7][3])
+        : "memory");
+}
+
+template <int CIN, int KP>
+struct TsShape {
+    static constexpr int KQ = 3, KW = 3;
+    static constexpr int CBX = chan_block(CIN);
+    static constexpr int NBX = CIN / CBX;
+    static constexpr int NATOM = KQ * KP * NBX;
+    static constexpr int NT = NATOM * CBX;                 // MMA N total = KQ*KP*CIN
+    static constexpr int NCH = (NT + 255) / 256;           // MMAs per K step
+    static constexpr int APC = (NATOM + NCH - 1) / NCH;    // atoms per MMA (last may be short)
+    static constexpr int BOXX = kTsWK * CBX * 2;           // one (kp, cb) X box
+    static constexpr int XSLOT = KP * NBX * BOXX;
+    static constexpr int ACOL = (NT + 31) / 32 * 32;       // first A column in TMEM
+    static constexpr int ACOLS = kTsKT * 8;                // TMEM columns per A slot
+    static_assert(BOXX % 1024 == 0, "X boxes must keep the swizzle atom alignment");
+};
+
+template <int CIN, int KP>
+__global__ void __launch_bounds__(kThreads, 1)
+conv_wgrad_ts_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap hmap,
+                     const __grid_constant__ CUtensorMap dmap, const WgradTsParams p) {
+    using namespace tc;
+    using S = TsShape<CIN, KP>;
+    constexpr int KQ = S::KQ, KW = S::KW;
+    extern __shared__ __align__(1024) uint8_t smem[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int NXM = p.nx + KQ - 1;
+    uint8_t *xring = smem;
+    uint8_t *dring = smem + (size_t)NXM * S::XSLOT;
+    uint64_t *bars = reinterpret_cast<uint64_t *>(dring + (size_t)p.nd * kTsDSlot);
+    uint64_t *xfull = bars, *xempty = xfull + p.nx;
+    uint64_t *dfull = xempty + p.nx, *dempty = dfull + p.nd;
+    uint64_t *afull = dempty + p.nd, *aempty = afull + p.na, *done = aempty + p.na;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(done + 1);
+    if (warp == 0) {
+        if (lane == 0) {
+            for (int i = 0; i < p.nx; ++i) {
+                mbar_init(&xfull[i], 1);
+                mbar_init(&xempty[i], 1);
+            }
+            for (int i = 0; i < p.nd; ++i) {
+                mbar_init(&dfull[i], 1);
+                mbar_init(&dempty[i], KW);
+            }
+            for (int i = 0; i < p.na; ++i) {
+                mbar_init(&afull[i], KW);
+                mbar_init(&aempty[i], 1);
+            }
+            mbar_init(done, 1);
+            mbar_fence_init();
+            tma_prefetch(&xmap);
+            tma_prefetch(&hmap);
+            tma_prefetch(&dmap);
+        }
+        __syncwarp();
+        tmem_alloc(tmem_slot, 512);
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        // ===================== TMA producer =====================
+        uint32_t xi = 0, di = 0;
+        constexpr uint32_t xrow = (uint32_t)(KP * S::NBX * kTsWK * S::CBX * 2);
+        constexpr uint32_t dbytes = 2u * (kTsWK + KW - 1) * kTsDRow;
+        for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
+            int r = u;
+            const int wt = r % p.n_wt; r /= p.n_wt;
+            const int qc = r % p.n_qc; r /= p.n_qc;
+            const int po = r % p.Pout;
+            const int b = r / p.Pout;
+            const int q0 = qc * p.q_chunk, q1 = min(p.Qout, q0 + p.q_chunk);
+            const int nq = q1 - q0, nrows = nq + KQ - 1;
+            const int w0 = p.w_lo + wt * kTsWK;
+            for (int s = 0; s < nrows; ++s) {
+                {
+                    const uint32_t idx = xi % p.nx, ph = (xi / p.nx) & 1;
+                    ++xi;
+                    const bool mirror = (int)idx < KQ - 1;
+                    mbar_wait(&xempty[idx], ph ^ 1);
+                    if (p.dbg & 4) {
+                        if (lane == 0) mbar_arrive(&xfull[idx]);
+                        __syncwarp();
+                    } else {
+                    mbar_expect_tx_e(&xfull[idx], mirror ? 2 * xrow : xrow);
+                    const int qv = p.base_q + q0 + s;
+#pragma unroll
+                    for (int kp = 0; kp < KP; ++kp) {
+                        const int pv = p.base_p + po + kp;
+                        const CUtensorMap *map = &xmap;
+                        int pc = pv, qcrd = qv;
+                        if (p.split == 0 && pv >= p.Pin && pv < p.Pin + p.halo) {
+                            map = &hmap;
+                            pc = pv - p.Pin;
+                        } else if (p.split == 1 && qv >= p.Qin && qv < p.Qin + p.halo) {
+                            map = &hmap;
+                            qcrd = qv - p.Qin;
+                        }
+#pragma unroll
+                        for (int cb = 0; cb < S::NBX; ++cb) {
+                            const size_t off = (size_t)(kp * S::NBX + cb) * S::BOXX;
+                            tma_load_5d_e(xring + (size_t)idx * S::XSLOT + off, map, &xfull[idx],
+                                          cb * S::CBX, p.base_w + w0, qcrd, pc, b);
+                            if (mirror)
+                                tma_load_5d_e(xring + (size_t)(p.nx + idx) * S::XSLOT + off, map,
+                                              &xfull[idx], cb * S::CBX, p.base_w + w0, qcrd, pc, b);
+                        }
+                    }
+                    }
+                }
+                if (s < nq) {  // dY row q0 + s: two 16-channel halves, w' in [w0 - 2, w0 + 128)
+                    const uint32_t idx = di % p.nd, ph = (di / p.nd) & 1;
+                    ++di;
+                    mbar_wait(&dempty[idx], ph ^ 1);
+                    if (p.dbg & 4) {
+                        if (lane == 0) mbar_arrive(&dfull[idx]);
+                        __syncwarp();
+                        continue;
+                    }
+                    mbar_expect_tx_e(&dfull[idx], dbytes);
+                    uint8_t *dst = dring + (size_t)idx * kTsDSlot;
+                    tma_load_5d_e(dst, &dmap, &dfull[idx], 0, w0 - (KW - 1), q0 + s, po, b);
+                    tma_load_5d_e(dst + kTsDHalf, &dmap, &dfull[idx], 16, w0 - (KW - 1), q0 + s, po, b);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ===================== MMA issuer =====================
+        const uint64_t b0 = sdesc_mn(smem_u32(xring), S::BOXX, 8 * S::CBX * 2, swz_layout(S::CBX));
+        constexpr uint32_t bstep = (16 * S::CBX * 2) >> 4;   // one K step = 16 w' rows
+        uint32_t xi = 0, di = 0;
+        bool fresh = true;
+        for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
+            int r = u / p.n_wt;
+            const int qc = r % p.n_qc;
+            const int q0 = qc * p.q_chunk, q1 = min(p.Qout, q0 + p.q_chunk);
+            const int nq = q1 - q0, nrows = nq + KQ - 1;
+            const uint32_t xbase = xi;
+            for (int s = 0; s < nrows; ++s) {
+                const uint32_t xidx = xi % p.nx, xph = (xi / p.nx) & 1;
+                ++xi;
+                mbar_wait(&xfull[xidx], xph);
+                const int j = s - (KQ - 1);
+                if (j < 0) continue;
+                const uint32_t aidx = di % p.na, aph = (di / p.na) & 1;
+                ++di;
+                mbar_wait(&afull[aidx], aph);
+                tc_fence_after();
+                const uint32_t xs = (xbase + j) % p.nx;
+                const uint64_t bx = b0 + ((xs * S::XSLOT) >> 4);
+                const uint32_t acol = tmem + S::ACOL + aidx * S::ACOLS;
+#pragma unroll
+                for (int ks = 0; ks < kTsKT; ++ks) {
+                    if (p.dbg & 2) break;
+                    const uint32_t acc = (fresh && ks == 0) ? 0u : 1u;
+#pragma unroll
+                    for (int c = 0; c < S::NCH; ++c) {
+                        constexpr int last = S::NATOM - (S::NCH - 1) * S::APC;
+                        const int atoms = c < S::NCH - 1 ? S::APC : last;
+                        mma_ts_e(tmem + c * S::APC * S::CBX, acol + ks * 8,
+                                 bx + ((c * S::APC * S::BOXX) >> 4) + ks * bstep,
+                                 idesc_bf16(128, atoms * S::CBX, 0, 1), acc);
+                    }
+                }
+                fresh = false;
+                mma_commit_e(&aempty[aidx]);
+                mma_commit_e(&xempty[xs]);
+                if (j == nq - 1)
+                    for (int t = 1; t < KQ; ++t) mma_commit_e(&xempty[(xbase + j + t) % p.nx]);
+            }
+        }
+        mma_commit_e(done);
+    } else {
+        // ===================== transposers (dY -> TMEM A), then epilogue =====================
+        const int quarter = warp & 3;
+        if (quarter < KW) {
+            const int kw = quarter;
+            // ldmatrix.x4.trans per K = 16 step: matrix mi = lane / 8 covers channels
+            // 8 (mi & 1) .. +7 of the co half and w' rows 8 (mi >> 1) .. +7 (shifted by
+            // -kw); row ri = lane % 8.  The staged half rows are 32 B with the TMA
+            // 32-B swizzle (16-B chunk ^= row bit 2), so each matrix's 8 rows hit 8
+            // distinct bank groups.  Transposed, thread t gets (co = t/4 [+8],
+            // w' pair t%4 [+4]) = the 16x128b fragment, in x16 register order.
+            const int mi = lane >> 3, ri = lane & 7;
+            const int chunk = mi & 1;
+            const int rbase = 8 * (mi >> 1) + ri + KW - 1 - kw;
+            uint32_t di = 0;
+            for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
+                int r = u / p.n_wt;
+                const int qc = r % p.n_qc;
+                const int q0 = qc * p.q_chunk, q1 = min(p.Qout, q0 + p.q_chunk);
+                for (int s = 0; s < q1 - q0; ++s, ++di) {
+                    const uint32_t didx = di % p.nd, dph = (di / p.nd) & 1;
+                    const uint32_t aidx = di % p.na, aph = (di / p.na) & 1;
+                    mbar_wait(&dfull[didx], dph);
+                    mbar_wait(&aempty[aidx], aph ^ 1);
+                    tc_fence_after();
+                    const uint32_t src = smem_u32(dring + (size_t)didx * kTsDSlot);
+                    const uint32_t dst = tmem + ((uint32_t)(32 * kw) << 16) + S::ACOL + aidx * S::ACOLS;
+                    static_assert(kTsKT == 8, "one x16 store covers the 8 K steps of a tile");
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        if (p.dbg & 1) break;
+                        uint32_t v[kTsKT][4];
+#pragma unroll
+                        for (int ks = 0; ks < kTsKT; ++ks) {
+                            const int row = rbase + ks * 16;
+                            const uint32_t a = src + h * kTsDHalf + row * kTsDRow +
+                                               ((chunk ^ ((row >> 2) & 1)) << 4);
+                            ldsm_x4_trans(a, v[ks]);
+                        }
+                        tmem_st_16x128b_x16(dst + ((uint32_t)(16 * h) << 16), v);
+                    }
+                    tmem_wait_st();
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) {
+                        mbar_arrive(&dempty[didx]);
+                        mbar_arrive(&afull[aidx]);
+                    }
+                }
+            }
+            // epilogue: D rows (kw, co) of this warp's lane quarter -> per-CTA partial
+            mbar_wait(done, 0);
+            tc_fence_after();
+            float *dst = p.partial + ((size_t)blockIdx.x * 96 + kw * 32 + lane) * S::NT;
+#pragma unroll 1
+            for (int c = 0; c < S::NT; c += 16) {
+                uint32_t v[16];
+                tmem_ld16(tmem + ((uint32_t)(kw * 32) << 16) + c, v);
+                tmem_wait_ld();
+#pragma unroll
+                for (int i = 0; i < 16; i += 4)
+                    *reinterpret_cast<float4 *>(dst + c + i) =
+                        make_float4(__uint_as_float(v[i]), __uint_as_float(v[i + 1]),
+                                    __uint_as_float(v[i + 2]), __uint_as_float(v[i + 3]));
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        tc_fence_after();
+        tmem_dealloc(tmem, 512);
+    }
+}
+
+// dw[co][ci][kp][kq][kw] = sum_cta partial[cta][kw*32 + co][(kq*KP + kp)*Cin + ci]
+__global__ void wgrad_ts_reduce(const float *__restrict__ part, float *__restrict__ dw, int ctas,
+                                int KP, int Cin) {
+    const int KQ = 3, KW = 3;
+    const int NT = KQ * KP * Cin;
+    const int total = kTsCo * Cin * KP * KQ * KW;
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
+        int r = e;
+        const int kw = r % KW; r /= KW;
+        const int kq = r % KQ; r /= KQ;
+        const int kp = r % KP; r /= KP;
+        const int ci = r % Cin;
+        const int co = r / Cin;
+        const size_t off = (size_t)(kw * 32 + co) * NT + (kq * KP + kp) * Cin + ci;
+        const size_t per_cta = (size_t)96 * NT;
+        float s = 0.f;
+        for (int c = 0; c < ctas; ++c) s += part[c * per_cta + off];
+        dw[e] = s;
+    }
+}
+
+struct TsPlan {
+    Roles R;
+    int Cin, nt, xslot, nx, nd, na, smem, grid, q_chunk, n_qc, w_lo, n_wt;
+    int64_t n_units;
+};
+
+bool ts_disabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("DP_WGRAD_TS");
+        v = (e && e[0] == '0') ? 1 : 0;
+    }
+    return v == 1;
+}
+
+bool make_tsplan(const dp_conv_geom *g, TsPlan &pl) {
+    if (ts_disabled()) return false;
+    if (!map_roles(g, false, pl.R)) return false;
+    const Roles &R = pl.R;
+    pl.Cin = (int)g->c_in;
+    if (g->c_out != kTsCo || R.KQ != 3 || R.KW != 3) return false;
+    const bool ok = (R.KP == 3 && (pl.Cin == 16 || pl.Cin == 32)) ||
+                    (R.KP == 1 && (pl.Cin == 16 || pl.Cin == 32 || pl.Cin == 64));
+    if (!ok) return false;
+    if (g->xs[1] != 1 || g->ys[1] != 1) return false;
+    if (g->halo > 0 && g->hs[1] != 1) return false;
+    for (int i = 0; i < 4; ++i) {
+        if (R.xs[i] % 8 || R.ys[i] % 8) return false;
+        if (g->halo > 0 && R.hs[i] % 8) return false;
+    }
+    const int cbx = chan_block(pl.Cin);
+    pl.nt = 3 * R.KP * pl.Cin;
+    pl.xslot = R.KP * (pl.Cin / cbx) * kTsWK * cbx * 2;
+    const int acol = (pl.nt + 31) / 32 * 32;
+    pl.na = (512 - acol) / (kTsKT * 8);
+    static const int na_cap = getenv("DP_WGRAD_NA") ? atoi(getenv("DP_WGRAD_NA")) : 4;
+    if (pl.na > na_cap) pl.na = na_cap;
+    if (pl.na < 2) return false;
+    const int budget = 220 * 1024 - 512;
+    static const int nd = getenv("DP_WGRAD_ND") ? atoi(getenv("DP_WGRAD_ND")) : 4;
+    pl.nd = nd;
+    pl.nx = (budget - pl.nd * kTsDSlot) / pl.xslot - (3 - 1);
+    if (pl.nx > 8) pl.nx = 8;
+    if (pl.nx < 4) return false;
+    pl.smem = (pl.nx + 2) * pl.xslot + pl.nd * kTsDSlot + 512;
+    // useful w' columns: X real there (padding columns contribute zero)
+    const int wr = R.Wout + 3 - 1;
+    pl.w_lo = R.base_w < 0 ? -R.base_w : 0;
+    int w_hi = R.Win - R.base_w;
+    if (w_hi > wr) w_hi = wr;
+    pl.n_wt = w_hi > pl.w_lo ? (w_hi - pl.w_lo + kTsWK - 1) / kTsWK : 0;
+    const int sms = sm_count();
+    const int64_t cols = (int64_t)g->batch * R.Pout * pl.n_wt;
+    int best_chunk = R.Qout > 0 ? R.Qout : 1;
+    double best = -1;
+    for (int nq = 1; nq <= R.Qout && nq <= 64; ++nq) {
+        const int chunk = (R.Qout + nq - 1) / nq;
+        const int nqc = (R.Qout + chunk - 1) / chunk;
+        const int64_t units = cols * nqc;
+        const int64_t waves = (units + sms - 1) / sms;
+        const double balance = (double)units / (double)(waves * sms);
+        const double overhead = (double)(chunk + 2) / chunk;
+        const double score = balance / overhead;
+        if (score > best + 1e-9) {
+            best = score;
+            best_chunk = chunk;
+        }
+    }
+    pl.q_chunk = best_chunk;
+    pl.n_qc = R.Qout > 0 ? (R.Qout + best_chunk - 1) / best_chunk : 0;
+    pl.n_units = cols * pl.n_qc;
+    pl.grid = (int)(pl.n_units < sms ? pl.n_units : sms);
+    if (pl.grid < 1) pl.grid = 1;
+    return true;
+}
+
+int64_t ts_workspace(const TsPlan &pl) { return (int64_t)pl.grid * 96 * pl.nt * 4; }
+
+template <int CIN, int KP>
+int launch_ts_k(const CUtensorMap &xm, const CUtensorMap &hm, const CUtensorMap &dm,
+                const WgradTsParams &p, int grid, int smem, cudaStream_t st) {
+    auto kern = conv_wgrad_ts_kernel<CIN, KP>;
+    DP_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    kern<<<grid, kThreads, smem, st>>>(xm, hm, dm, p);
+    return launch_status("conv_wgrad_ts_kernel");
+}
+
+int run_wgrad_ts(const dp_conv_geom *g, const TsPlan &pl, const void *x, const void *xh,
+                 const void *dy, float *dw, void *ws, int64_t ws_bytes, cudaStream_t st) {
+    const Roles &R = pl.R;
+    DP_REQUIRE(ws_bytes >= ts_workspace(pl), DP_ERR_INVALID, "conv_wgrad_ts: workspace too small");
+    const int taps = R.KP * 9;
+    if (pl.n_units == 0) {
+        DP_CUDA_CHECK(cudaMemsetAsync(dw, 0, (size_t)kTsCo * pl.Cin * taps * 4, st));
+        return DP_OK;
+    }
+    const int cbx = chan_block(pl.Cin);
+    const CUtensorMapSwizzle sw = cbx == 16 ? CU_TENSOR_MAP_SWIZZLE_32B
+                                  : cbx == 32 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                              : CU_TENSOR_MAP_SWIZZLE_128B;
+    uint32_t xbox[5] = {(uint32_t)cbx, (uint32_t)kTsWK, 1, 1, 1};
+    CUtensorMap xm, hm, dm;
+    {
+        uint64_t dims[5] = {(uint64_t)pl.Cin, (uint64_t)R.Win, (uint64_t)R.Qin, (uint64_t)R.Pin,
+                            (uint64_t)g->batch};
+        uint64_t strides[4] = {(uint64_t)R.xs[3] * 2, (uint64_t)R.xs[2] * 2,
+                               (uint64_t)R.xs[1] * 2, (uint64_t)R.xs[0] * 2};
+        int rc = encode_tensor_map(&xm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void *>(x),
+                                   dims, strides, xbox, sw);
+        if (rc) return rc;
+    }
+    hm = xm;
+    if (g->halo > 0) {
+        uint64_t dims[5] = {(uint64_t)pl.Cin, (uint64_t)R.Win,
+                            (uint64_t)(R.split == 1 ? g->halo : R.Qin),
+                            (uint64_t)(R.split == 0 ? g->halo : R.Pin), (uint64_t)g->batch};
+        uint64_t strides[4] = {(uint64_t)R.hs[3] * 2, (uint64_t)R.hs[2] * 2,
+                               (uint64_t)R.hs[1] * 2, (uint64_t)R.hs[0] * 2};
+        int rc = encode_tensor_map(&hm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5,
+                                   const_cast<void *>(xh), dims, strides, xbox, sw);
+        if (rc) return rc;
+    }
+    {
+        uint64_t dims[5] = {(uint64_t)kTsCo, (uint64_t)R.Wout, (uint64_t)R.Qout, (uint64_t)R.Pout,
+                            (uint64_t)g->batch};
+        uint64_t strides[4] = {(uint64_t)R.ys[3] * 2, (uint64_t)R.ys[2] * 2,
+                               (uint64_t)R.ys[1] * 2, (uint64_t)R.ys[0] * 2};
+        uint32_t dbox[5] = {16, (uint32_t)(kTsWK + 2), 1, 1, 1};
+        int rc = encode_tensor_map(&dm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void *>(dy),
+                                   dims, strides, dbox, CU_TENSOR_MAP_SWIZZLE_32B);
+        if (rc) return rc;
+    }
+    WgradTsParams p;
+    memset(&p, 0, sizeof(p));
+    p.Pin = R.Pin; p.Qin = R.Qin; p.Win = R.Win;
+    p.Pout = R.Pout; p.Qout = R.Qout; p.Wout = R.Wout;
+    p.base_p = R.base_p; p.base_q = R.base_q; p.base_w = R.base_w;
+    p.split = g->halo > 0 ? R.split : -1;
+    p.halo = (int)g->halo;
+    p.w_lo = pl.w_lo; p.n_wt = pl.n_wt; p.n_qc = pl.n_qc; p.q_chunk = pl.q_chunk;
+    p.n_units = (int)pl.n_units;
+    p.nx = pl.nx; p.nd = pl.nd; p.na = pl.na;
+    p.partial = (float *)ws;
+    static const int dbg = getenv("DP_CONV_DBG") ? atoi(getenv("DP_CONV_DBG")) : 0;
+    p.dbg = dbg;
+    int rc;
+    if (R.KP == 3)
+        rc = pl.Cin == 16 ? launch_ts_k<16, 3>(xm, hm, dm, p, pl.grid, pl.smem, st)
+                          : launch_ts_k<32, 3>(xm, hm, dm, p, pl.grid, pl.smem, st);
+    else
+        rc = pl.Cin == 16   ? launch_ts_k<16, 1>(xm, hm, dm, p, pl.grid, pl.smem, st)
+             : pl.Cin == 32 ? launch_ts_k<32, 1>(xm, hm, dm, p, pl.grid, pl.smem, st)
+                            : launch_ts_k<64, 1>(xm, hm, dm, p, pl.grid, pl.smem, st);
+    if (rc) return rc;
+    const int total = kTsCo * pl.Cin * taps;
+    wgrad_ts_reduce<<<grid_for(total, 256, 4), 256, 0, st>>>((const float *)ws, dw, pl.grid, R.KP,
+                                                             pl.Cin);
+    return launch_status("wgrad_ts_reduce");
+}
+
 }  // namespace
 
 int encode_tensor_map(CUtensorMap *map, CUtensorMapDataType dtype, int rank, void *base,
@@ -1052,8 +1537,9 @@ int encode_tensor_map(CUtensorMap *map, CUtensorMapDataType dtype, int rank, voi
 int conv_tc_eligible(const dp_conv_geom *g, int dtype, int which) {
     if (dtype != DP_BF16 || !g) return 0;
     if (which == DP_CONV_WGRAD) {
+        TsPlan tp;
         WPlan wp;
-        return make_wplan(g, wp) ? 1 : 0;
+        return (make_tsplan(g, tp) || make_wplan(g, wp)) ? 1 : 0;
     }
     Plan pl;
     return make_plan(g, which == DP_CONV_DGRAD, pl) ? 1 : 0;
@@ -1061,6 +1547,8 @@ int conv_tc_eligible(const dp_conv_geom *g, int dtype, int which) {
 
 int64_t conv_tc_workspace(const dp_conv_geom *g, int which) {
     if (which == DP_CONV_WGRAD) {
+        TsPlan tp;
+        if (make_tsplan(g, tp)) return ts_workspace(tp);
         WPlan wp;
         if (!make_wplan(g, wp)) return -1;
         return (int64_t)wp.grid * wp.n_mt * 128 * wp.R.KW * wp.N * 4;
@@ -1082,6 +1570,8 @@ int conv_dgrad_tc_launch(const dp_conv_geom *g, const void *dy, const void *w, v
 
 int conv_wgrad_tc_launch(const dp_conv_geom *g, const void *x, const void *xh, const void *dy,
                          void *dw, void *ws, int64_t ws_bytes, cudaStream_t st) {
+    TsPlan tp;
+    if (make_tsplan(g, tp)) return run_wgrad_ts(g, tp, x, xh, dy, (float *)dw, ws, ws_bytes, st);
     return run_wgrad_tc(g, x, xh, dy, (float *)dw, ws, ws_bytes, st);
 }
 

@@ -242,6 +242,21 @@ __device__ __forceinline__ void tma_load_3d_e(void *dst, const CUtensorMap *map,
         : "memory");
 }
 
+// tcgen05.mma with the A operand in TMEM ("TS"): lane m = row m, a K = 16
+// step = 8 consecutive 32-bit columns holding bf16 pairs (k = 2c, 2c + 1) —
+// verified exactly and timed at the N/2-cycle floor by scripts/umma_ts_probe.cu.
+__device__ __forceinline__ void mma_ts_e(uint32_t d_tmem, uint32_t a_tmem, uint64_t b,
+                                         uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p, e;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "elect.sync _|e, 0xffffffff;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n"
+        "}\n" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(b), "r"(idesc), "r"(accumulate));
+}
+
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
     __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
     return *reinterpret_cast<uint32_t *>(&v);

@@ -155,6 +155,12 @@ TC_CASES = [
     (2, 1, 32, 48, (9, 129), 3, 1, 0),
     (2, 1, 16, 32, (12, 70), 5, 2, 4),
     (3, 1, 16, 48, (3, 4, 128), 3, 1, 0),
+    # C_out = 32, 3x3(x3): the TS-form wgrad (dY in TMEM) with 1, 2 and 3 w' tiles
+    (3, 2, 32, 32, (3, 6, 256), 3, 1, 1),
+    (2, 1, 32, 32, (10, 260), 3, 1, 1),
+    (2, 1, 64, 32, (7, 100), 3, 1, 0),
+    (2, 1, 16, 32, (5, 33), 3, 0, 0),
+    (3, 1, 16, 32, (4, 3, 300), 3, 1, 2),
 ]
 
 
