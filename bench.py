@@ -792,7 +792,7 @@ def main():
             # from the committed `ncu --set full` capture (scripts/ncu_summary.py)
             with open(tpath) as f:
                 tab = json.load(f).get(args.config, {})
-            pat = {"conv_wgrad": "conv_wgrad_tc_kernel", "conv_fwd": "conv_tc_kernel",
+            pat = {"conv_wgrad": "conv_wgrad_t", "conv_fwd": "conv_tc_kernel",
                    "conv_dgrad": "conv_tc_kernel", "attn_fwd_update": "attn_fwd_tc_kernel",
                    "attn_bwd_update": "attn_bwd_tc_kernel"}.get(name, name)
             hits = [v for k, v in tab.items() if pat in k]
