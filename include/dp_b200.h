@@ -27,6 +27,9 @@
  *                                                     RingSoftmaxState.update
  *   dp_attn_finalize       domainpar/ops.py:213-214,278   acc / l
  *   dp_attn_bwd_*          (no reference function)    ring attention bwd
+ *   dp_norm_stats/_apply   domainpar/ops.py:126-173     sharded_softmax /
+ *                                                     sharded_layer_norm
+ *   dp_elementwise         domainpar/ops.py:93-104      sharded_elementwise
  */
 #ifndef DP_B200_H
 #define DP_B200_H
@@ -168,6 +171,42 @@ int dp_attn_bwd_preprocess(const dp_attn_geom *g, int dtype, const void *o, cons
 int dp_attn_bwd_update(const dp_attn_geom *g, int dtype, int algo, const void *q, const void *k,
                        const void *v, const void *dout, const void *lse, const void *delta,
                        void *dq, void *dk, void *dv, void *stream);
+
+/* ---- sharded normalisations and pointwise ops -------- */
+
+/* The reduced dim is the middle of an [outer, n, inner] view with element
+ * strides xs = {outer, n, inner}.  Statistics are fp64 and laid out
+ * [nstat][outer * inner] (cell = o * inner + i):
+ *   kind 0  layer-norm moments: stats[0] = sum x, stats[1] = sum x^2
+ *           (domainpar/ops.py:165-168: both ride ONE all_reduce)
+ *   kind 1  softmax local max (-inf for n == 0)          (ops.py:141-145)
+ *   kind 2  softmax local sum exp(x - aux), aux = global max  (ops.py:146-148)
+ * Deterministic (fixed-order split + combine, no atomics). */
+#define DP_NORM_MOMENTS 0
+#define DP_NORM_MAX 1
+#define DP_NORM_EXPSUM 2
+int64_t dp_norm_workspace(int kind, int64_t outer, int64_t n, int64_t inner);
+int dp_norm_stats(int kind, int64_t outer, int64_t n, int64_t inner, const void *x,
+                  const int64_t *xs, int dtype, const void *aux, void *stats, void *workspace,
+                  int64_t workspace_bytes, void *stream);
+
+/* y = normalised x (y strides ys), from the GLOBAL statistics:
+ *   kind 0  layer norm: mean = s1/count, var = max(s2/count - mean^2, 0),
+ *           y = (x - mean) / sqrt(var + eps)           (domainpar/ops.py:169-172)
+ *   kind 1  softmax: y = exp(x - aux) / stats (aux = global max, stats =
+ *           global denominator)                         (ops.py:146-149) */
+int dp_norm_apply(int kind, int64_t outer, int64_t n, int64_t inner, const void *x,
+                  const int64_t *xs, void *y, const int64_t *ys, int dtype, const void *stats,
+                  const void *aux, double count, double eps, void *stream);
+
+/* out = a (op) b over n contiguous elements: op 0 add, 1 mul (b array, or
+ * the scalar when b is NULL), 2 scale (out = a * scalar) — domainpar/dense.py:65-98; fp32 math for
+ * DP_F32/DP_BF16, fp64 for DP_F64. */
+#define DP_EW_ADD 0
+#define DP_EW_MUL 1
+#define DP_EW_SCALE 2
+int dp_elementwise(int op, int64_t n, const void *a, const void *b, double scalar, void *out,
+                   int dtype, void *stream);
 
 #ifdef __cplusplus
 }

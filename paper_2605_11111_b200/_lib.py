@@ -20,6 +20,8 @@ DP_OK, DP_ERR_INVALID, DP_ERR_UNSUPPORTED, DP_ERR_CUDA = 0, 1, 2, 3
 DP_F32, DP_F64, DP_BF16 = 0, 1, 2
 ALGO_AUTO, ALGO_SIMT, ALGO_TC = 0, 1, 2
 CONV_FWD, CONV_DGRAD, CONV_WGRAD = 0, 1, 2
+NORM_MOMENTS, NORM_MAX, NORM_EXPSUM = 0, 1, 2
+EW_ADD, EW_MUL, EW_SCALE = 0, 1, 2
 
 _i64 = ctypes.c_int64
 _i32 = ctypes.c_int32
@@ -76,6 +78,16 @@ SIGNATURES = {
                                               _vp, _vp, _vp, _vp]),
     "dp_attn_bwd_update": (ctypes.c_int, [ctypes.POINTER(AttnGeom), ctypes.c_int, ctypes.c_int,
                                           _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "dp_norm_workspace": (ctypes.c_int64, [ctypes.c_int, ctypes.c_int64, ctypes.c_int64,
+                                           ctypes.c_int64]),
+    "dp_norm_stats": (ctypes.c_int, [ctypes.c_int, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
+                                     _vp, _i64p, ctypes.c_int, _vp, _vp, _vp, ctypes.c_int64,
+                                     _vp]),
+    "dp_norm_apply": (ctypes.c_int, [ctypes.c_int, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
+                                     _vp, _i64p, _vp, _i64p, ctypes.c_int, _vp, _vp,
+                                     ctypes.c_double, ctypes.c_double, _vp]),
+    "dp_elementwise": (ctypes.c_int, [ctypes.c_int, ctypes.c_int64, _vp, _vp, ctypes.c_double,
+                                      _vp, ctypes.c_int, _vp]),
 }
 
 _LIB = None

@@ -255,3 +255,67 @@ def attn_bwd_update(q, k, v, do, lse, delta, dq, dk, dv, scale) -> None:
 def default_scale(d: int) -> float:
     """1/sqrt(d) as a Python float (domainpar/ops.py:268)."""
     return 1.0 / math.sqrt(d)
+
+
+# ---------------------------------------------------------------------------
+# normalisations and pointwise ops (SURVEY §8(f) row 1)
+
+
+def contiguous(t: torch.Tensor) -> torch.Tensor:
+    """`t` itself when contiguous, else a contiguous copy made by dp_copy_strided."""
+    if t.is_contiguous():
+        return t
+    out = torch.empty(t.shape, dtype=t.dtype, device=t.device)
+    copy_strided(out, t)
+    return out
+
+
+def _view3(shape, dim):
+    outer = math.prod(shape[:dim])
+    inner = math.prod(shape[dim + 1:])
+    return outer, shape[dim], inner
+
+
+def norm_stats(kind: int, x: torch.Tensor, dim: int, aux=None) -> torch.Tensor:
+    """fp64 statistics of contiguous `x` reduced over `dim` (dp_norm_stats):
+    [2, cells] moments (kind 0), [1, cells] max (1) or exp-sum (2)."""
+    require_device("norm_stats", x, aux)
+    outer, n, inner = _view3(list(x.shape), dim)
+    nstat = 2 if kind == _lib.NORM_MOMENTS else 1
+    stats = torch.empty((nstat, outer * inner), dtype=torch.float64, device=x.device)
+    lib = _lib.load()
+    nb = int(lib.dp_norm_workspace(kind, outer, n, inner))
+    ws = torch.empty(max(nb, 16), dtype=torch.uint8, device=x.device)
+    rc = lib.dp_norm_stats(kind, outer, n, inner, _ptr(x), i64_array([n * inner, inner, 1]),
+                           dtype_code(x), _ptr(aux), _ptr(stats), _ptr(ws), ws.numel(),
+                           _stream(x))
+    _lib.check(rc, "dp_norm_stats")
+    return stats
+
+
+def norm_apply(kind: int, x: torch.Tensor, dim: int, stats: torch.Tensor, aux, count: float,
+               eps: float = 0.0) -> torch.Tensor:
+    """Normalised copy of contiguous `x` from GLOBAL statistics (dp_norm_apply)."""
+    require_device("norm_apply", x, stats, aux)
+    outer, n, inner = _view3(list(x.shape), dim)
+    y = torch.empty(x.shape, dtype=x.dtype, device=x.device)
+    st = i64_array([n * inner, inner, 1])
+    rc = _lib.load().dp_norm_apply(kind, outer, n, inner, _ptr(x), st, _ptr(y), st,
+                                   dtype_code(x), _ptr(stats), _ptr(aux), float(count),
+                                   float(eps), _stream(x))
+    _lib.check(rc, "dp_norm_apply")
+    return y
+
+
+def elementwise(op: int, a: torch.Tensor, b=None, scalar: float = 0.0) -> torch.Tensor:
+    """out = a (+|*) b, or a * scalar (dp_elementwise); contiguous result."""
+    require_device("elementwise", a, b if isinstance(b, torch.Tensor) else None)
+    a = contiguous(a)
+    if isinstance(b, torch.Tensor):
+        b = contiguous(b.to(a.dtype))
+    out = torch.empty(a.shape, dtype=a.dtype, device=a.device)
+    rc = _lib.load().dp_elementwise(op, a.numel(), _ptr(a),
+                                    _ptr(b) if isinstance(b, torch.Tensor) else None,
+                                    float(scalar), _ptr(out), dtype_code(a), _stream(a))
+    _lib.check(rc, "dp_elementwise")
+    return out

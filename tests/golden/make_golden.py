@@ -9,8 +9,10 @@ travel to the GPU box, so its outputs are committed here as small fixtures:
   conv_cases.npz    halo_conv inputs and the reference's gathered outputs
   ring_cases.npz    ring_attention inputs and the reference's outputs
   redist_cases.npz  redistribute inputs and the reference's per-rank blocks
+  layer_cases.npz   sharded_softmax / sharded_layer_norm (uneven shards),
+                    ddp_allreduce_grads and vit_block_pipeline outputs
 
-Run:  python tests/golden/make_golden.py   (needs /root/reference)
+Run:  python tests/golden/make_golden.py [core|layers]   (needs /root/reference)
 """
 
 from __future__ import annotations
@@ -224,12 +226,92 @@ def make_redist_cases():
     return out
 
 
+NORM_SPECS = [
+    # op, global shape, sharded dim, extents along it, reduce dim, dtype
+    ("softmax", (11, 6), 0, (5, 0, 4, 2), 0, np.float64),
+    ("softmax", (11, 6), 0, (5, 0, 4, 2), 1, np.float64),
+    ("softmax", (7, 9, 4), 1, (2, 4, 3), 1, np.float32),
+    ("softmax", (300, 3), 0, (100, 37, 163), 0, np.float32),
+    ("layer_norm", (11, 6), 0, (5, 0, 4, 2), 0, np.float64),
+    ("layer_norm", (11, 6), 0, (5, 0, 4, 2), 1, np.float64),
+    ("layer_norm", (7, 9, 4), 1, (2, 4, 3), 1, np.float32),
+    ("layer_norm", (5, 1000), 1, (400, 0, 600), 1, np.float32),
+    ("layer_norm", (12, 8), 0, (6, 6), -2, np.float32),
+]
+
+VIT_SPECS = [
+    # image (c, h, w), extents along h, config kwargs, dtype
+    ((3, 20, 15), (10, 10), dict(embed_dim=16, n_layers=2, n_heads=2, mlp_ratio=2), np.float64),
+    ((3, 25, 10), (10, 5, 10), dict(embed_dim=16, n_layers=2, n_heads=4, mlp_ratio=2),
+     np.float64),
+    ((2, 30, 20), (15, 15), dict(image_channels=2, embed_dim=32, n_layers=1, n_heads=2,
+                                 mlp_ratio=4), np.float32),
+]
+
+
+def make_layer_cases():
+    """sharded_softmax / sharded_layer_norm over uneven shards, ddp averaging
+    and the ViT block pipeline, from the reference (domainpar/ops.py)."""
+    rng = np.random.default_rng(11)
+    out = {}
+    for i, (op, shape, sdim, ext, rdim, dt) in enumerate(NORM_SPECS):
+        g = (rng.standard_normal(shape) * 3).astype(dt)
+        fn = rops.sharded_softmax if op == "softmax" else rops.sharded_layer_norm
+
+        def prog(ctx, g=g, sdim=sdim, ext=ext, rdim=rdim, fn=fn):
+            pl = tuple(Shard(sdim) if a == 0 else Replicate() for a in range(1))
+            st = scatter_global(ctx, g if ctx.rank_id == 0 else None, pl, {0: ext})
+            before = ctx.collective_count
+            y = fn(st, rdim)
+            n_coll = ctx.collective_count - before
+            return y.full_tensor(), n_coll
+
+        res = spawn_mesh((len(ext),), ("domain",), prog)
+        out[f"n{i}_x"], out[f"n{i}_y"] = g, res[0][0]
+        out[f"n{i}_coll"] = np.array(res[0][1])
+    out["n_count"] = np.array(len(NORM_SPECS))
+    # ddp_allreduce_grads over 3 ranks: per-rank grads, the group mean
+    grads = [rng.standard_normal((4, 5)) for _ in range(3)]
+
+    def dprog(ctx):
+        g = {"w": grads[ctx.rank_id], "b": grads[ctx.rank_id][0]}
+        return rops.ddp_allreduce_grads(ctx.axis_group("data"), g)
+
+    dres = spawn_mesh((3,), ("data",), dprog)
+    out["ddp_grads"] = np.stack(grads)
+    out["ddp_w"], out["ddp_b"] = dres[0]["w"], dres[0]["b"]
+    for i, (img, ext, kw, dt) in enumerate(VIT_SPECS):
+        cfg = rops.VitConfig(image_channels=img[0], **{k: v for k, v in kw.items()
+                                                       if k != "image_channels"})
+        weights = rops.make_vit_weights(cfg, seed=i, dtype=dt)
+        x = rng.standard_normal(img).astype(dt)
+
+        def vprog(ctx, x=x, ext=ext, cfg=cfg, weights=weights):
+            st = scatter_global(ctx, x if ctx.rank_id == 0 else None, (Shard(1),), {0: ext})
+            from domainpar.memory import ActivationLedger
+            led = ActivationLedger()
+            seq = rops.vit_block_pipeline(st, cfg, weights, ledger=led)
+            return seq.full_tensor(), led.peak_bytes, list(seq.shard_shapes[0])
+
+        res = spawn_mesh((len(ext),), ("domain",), vprog)
+        dense = rops.vit_block_pipeline_dense(x, cfg, weights)
+        out[f"v{i}_x"], out[f"v{i}_y"], out[f"v{i}_dense"] = x, res[0][0], dense
+        out[f"v{i}_ledger"] = np.array([r[1] for r in res])
+        out[f"v{i}_shapes"] = np.array(res[0][2])
+    out["v_count"] = np.array(len(VIT_SPECS))
+    return out
+
+
 def main():
-    with open(os.path.join(HERE, "plans.json"), "w") as f:
-        json.dump(make_plans(), f, indent=0)
-    np.savez_compressed(os.path.join(HERE, "conv_cases.npz"), **make_conv_cases())
-    np.savez_compressed(os.path.join(HERE, "ring_cases.npz"), **make_ring_cases())
-    np.savez_compressed(os.path.join(HERE, "redist_cases.npz"), **make_redist_cases())
+    only = sys.argv[1] if len(sys.argv) > 1 else None
+    if only in (None, "core"):
+        with open(os.path.join(HERE, "plans.json"), "w") as f:
+            json.dump(make_plans(), f, indent=0)
+        np.savez_compressed(os.path.join(HERE, "conv_cases.npz"), **make_conv_cases())
+        np.savez_compressed(os.path.join(HERE, "ring_cases.npz"), **make_ring_cases())
+        np.savez_compressed(os.path.join(HERE, "redist_cases.npz"), **make_redist_cases())
+    if only in (None, "layers"):
+        np.savez_compressed(os.path.join(HERE, "layer_cases.npz"), **make_layer_cases())
     print("golden fixtures written to", HERE)
 
 

@@ -188,3 +188,57 @@ def test_redistribute_restatement_vs_reference_blocks():
         for rank in range(r):
             assert np.array_equal(blocks[rank], d[f"d{i}_local{rank}"])
     assert math.isfinite(1.0)
+
+
+# ---- §8(f): normalisations and the ViT pipeline (tests/golden/layer_cases.npz)
+
+def _layer_specs():
+    import importlib.util
+    import os
+    from conftest import GOLDEN
+
+    spec = importlib.util.spec_from_file_location("_mk", os.path.join(GOLDEN, "make_golden.py"))
+    src = open(os.path.join(GOLDEN, "make_golden.py")).read()
+    # the spec tables only (the module itself imports the reference)
+    ns = {"np": np}
+    start = src.index("NORM_SPECS = [")
+    end = src.index("def make_layer_cases")
+    exec(src[start:end], ns)
+    return ns["NORM_SPECS"], ns["VIT_SPECS"]
+
+
+def test_norm_restatement_vs_reference_outputs():
+    from oracle import layers as olay
+
+    d = load_npz("layer_cases.npz")
+    norm_specs, _ = _layer_specs()
+    for i, (op, shape, sdim, ext, rdim, dt) in enumerate(norm_specs):
+        x, want = d[f"n{i}_x"], d[f"n{i}_y"]
+        got = olay.softmax(x, rdim) if op == "softmax" else olay.layer_norm(x, rdim)
+        tol = 1e-12 if dt == np.float64 else 1e-6
+        assert rel_err(got, want) < tol, (i, op)
+        # collectives: 2 for a sharded softmax, 1 for a sharded layer norm, 0 local
+        sharded = (rdim % len(shape)) == sdim
+        assert int(d[f"n{i}_coll"]) == ((2 if op == "softmax" else 1) if sharded else 0)
+
+
+def test_vit_restatement_vs_reference_outputs():
+    from oracle import layers as olay
+
+    d = load_npz("layer_cases.npz")
+    _, vit_specs = _layer_specs()
+    for i, (img, ext, kw, dt) in enumerate(vit_specs):
+        cfg = dict(dict(embed_dim=64, n_layers=16, n_heads=4, mlp_ratio=4), **kw)
+        w = olay.vit_weights(cfg["embed_dim"], img[0], 5, cfg["n_layers"],
+                             cfg["embed_dim"] * cfg["mlp_ratio"], seed=i, dtype=dt)
+        got = olay.vit_dense(d[f"v{i}_x"], w, 5, cfg["n_layers"], cfg["n_heads"])
+        tol = 1e-10 if dt == np.float64 else 1e-4
+        assert rel_err(got, d[f"v{i}_dense"]) < tol
+        assert rel_err(got, d[f"v{i}_y"]) < tol   # the sharded reference run agrees
+
+
+def test_ddp_mean_golden():
+    d = load_npz("layer_cases.npz")
+    g = d["ddp_grads"]
+    assert rel_err(d["ddp_w"], g.sum(0) / 3) < 1e-15
+    assert rel_err(d["ddp_b"], g[:, 0].sum(0) / 3) < 1e-15
