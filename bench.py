@@ -43,6 +43,15 @@ sys.path.insert(0, ROOT)
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
 
 
+# workload names shared by both arms (ours and --impl reference)
+WORKLOAD_TEXT = {
+    "cfg2": "cfg2: conv3d 3x3x3 UNet-style encoder block conv(16->32)->conv(32->32), s1 p1, "
+            "no bias/activation, 1x16x256^3 bf16, D-sharded",
+    "cfg3": "cfg3: ring-attention SDPA, ViT-style 64k-token sequence, 16 heads, d=64, bf16, "
+            "non-causal, scale 1/8, sequence-sharded",
+}
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -295,8 +304,7 @@ def setup_cfg2(ctx):
         return dw1, dw2
 
     flops = 3 * 2.0 * (C0 * C1 + C1 * C1) * 27 * G ** 3  # fwd + dgrad + wgrad, both layers
-    info = {"workload": "cfg2: conv3d 3x3x3 UNet-style encoder block conv(16->32)->conv(32->32), "
-                        "s1 p1, no bias/activation, 1x16x256^3 bf16, D-sharded",
+    info = {"workload": WORKLOAD_TEXT["cfg2"],
             "global_batch": 1, "volume": [G, G, G], "channels": [C0, C1, C1],
             "layout": "NDHWC (channels_last_3d)", "shard_extents": list(ext),
             "parallelism": f"domain{R}",
@@ -369,8 +377,7 @@ def setup_cfg3(ctx):
         return dq.local, dk.local, dv.local
 
     flops = 3.5 * 4.0 * S * S * D * H  # fwd + 2.5x bwd
-    info = {"workload": "cfg3: ring-attention SDPA, ViT-style 64k-token sequence, 16 heads, "
-                        "d=64, bf16, non-causal, scale 1/8, sequence-sharded",
+    info = {"workload": WORKLOAD_TEXT["cfg3"],
             "global_batch": 1, "seq_len": S, "heads": H, "head_dim": D,
             "shard_extents": list(ext), "parallelism": f"ring{R}",
             "l2": "inputs (q,k,v,dO 8 MiB/head-tile stream, 512 MiB total) exceed L2, no flush"}
@@ -669,7 +676,8 @@ def run_reference(args):
             "warmup": args.warmup, "ms_per_step": 1000.0 / value, "higher_is_better": True,
             "scaling": "weak" if args.config == "cfg4" else "strong", "vs_baseline": None,
             "dtype": "f32", "data": "synthetic",
-            "config": {"workload": args.config, "sample": sample_desc},
+            "config": {"workload": WORKLOAD_TEXT.get(args.config, args.config),
+                       "sample": sample_desc},
             "cpu_baseline": {"value": value, "unit": "samples/s", "cores": cores,
                              "kind": "port", "sample": f"{cores} x {sample_desc}"},
             "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0,
@@ -830,5 +838,18 @@ def main():
     print(json.dumps(line), flush=True)
 
 
+def _shutdown():
+    try:
+        import torch.distributed as dist
+
+        if dist.is_available() and dist.is_initialized():
+            dist.destroy_process_group()
+    except Exception:  # noqa: BLE001 - best effort at exit
+        pass
+
+
 if __name__ == "__main__":
-    main()
+    try:
+        main()
+    finally:
+        _shutdown()
