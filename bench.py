@@ -43,6 +43,8 @@ sys.path.insert(0, ROOT)
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
 
 
+SIZE_MIB = 1024   # cfg5 tensor size (--size-mib)
+
 # workload names shared by both arms (ours and --impl reference)
 WORKLOAD_TEXT = {
     "cfg2": "cfg2: conv3d 3x3x3 UNet-style encoder block conv(16->32)->conv(32->32), s1 p1, "
@@ -70,6 +72,8 @@ def parse():
     ap.add_argument("--config", default="cfg2", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--algo", default="auto", choices=["auto", "simt", "tc"])
+    ap.add_argument("--size-mib", type=int, default=1024,
+                    help="cfg5: global tensor size (the sweep runs 64 .. 8192)")
     return ap.parse_args()
 
 
@@ -516,7 +520,7 @@ def setup_cfg5(ctx):
 
     import paper_2605_11111_b200 as dp
 
-    n = 16384
+    n = int(round((SIZE_MIB * 2 ** 20 / 4) ** 0.5)) // 8 * 8   # [n, n] fp32
     R = ctx.mesh.world_size
     me = ctx.rank_id
     dev = ctx.device
@@ -687,6 +691,8 @@ def run_reference(args):
 
 def main():
     args = parse()
+    global SIZE_MIB
+    SIZE_MIB = args.size_mib
     if args.impl == "reference":
         run_reference(args)
         return

@@ -225,7 +225,8 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
                         for (int kw = 0; kw < KW; ++kw)
 #pragma unroll
                             for (int kc = 0; kc < KC; ++kc) {
-                                const uint32_t aoff = (kp * NBLK + kc / KPB) * BOXB + kw * ROWB +
+                                const uint32_t aoff = (kp * NBLK + kc / KPB) * BOXB +
+                                                      ((p.dbg & 16) ? kw * 8 * ROWB : kw * ROWB) +
                                                       (kc % KPB) * 32;
                                 const uint32_t boff = ((kp * KW + kw) * KC + kc) * blk;
                                 mma_bf16_e(d, adesc + (aoff >> 4), bdesc0 + (boff >> 4),
