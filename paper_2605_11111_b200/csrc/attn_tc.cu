@@ -416,7 +416,8 @@ struct BwdParams {
     const float *lse, *delta;  // [sq, H]
     float *dq;                 // [sq, H, 64] (atomic +=)
     float *dk, *dv;            // [sk, H, 64] (+=)
-    int dbg;                   // DP_ATTN_DBG profiling ablation: 1 = skip the dQ atomics
+    int dbg;                   // DP_ATTN_DBG ablations: 1 no dQ reduce, 2 no softmax math,
+                               // 4 no gradient MMAs, 8 no S/dP MMAs
 };
 
 __device__ __forceinline__ void named_bar(int id, int n) {
@@ -480,6 +481,11 @@ attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
         for (int i = 0; i < nq; ++i) {
             const int st = i & 1;
             mbar_wait(&qd_empty[st], ((i >> 1) & 1) ^ 1);
+            if (p.dbg & 16) {
+                if (lane == 0) mbar_arrive(&qd_full[st]);
+                __syncwarp();
+                continue;
+            }
             mbar_expect_tx_e(&qd_full[st], 2 * kTileBytes);
             uint8_t *dst = smem + kB_QD + st * 2 * kTileBytes;
             tma_load_3d_e(dst, &qmap, &qd_full[st], 0, h, i * kBM);
@@ -507,6 +513,7 @@ attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
             const uint64_t do_mn = sdesc_mn(smem_u32(qdst + kTileBytes), 8192, 1024, 2);
 #pragma unroll
             for (int k = 0; k < kBM / 16; ++k) {
+                if (p.dbg & 4) break;
                 const uint32_t a = ((k >> 2) * (kBN * 128) + (k & 3) * 32) >> 4;
                 const uint32_t bb = (k * 16 * 128) >> 4;
                 const uint32_t acc = (j > 0 || k > 0) ? 1u : 0u;
@@ -517,6 +524,7 @@ attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
             tc_fence_after();
 #pragma unroll
             for (int k = 0; k < kBN / 16; ++k) {
+                if (p.dbg & 4) break;
                 const uint32_t a = (k * 16 * 128) >> 4;     // 16 key rows of dS^T
                 mma_bf16_e(tmem + kColDQ + b * kD, ds_mn + a, kmn + a, id_q, k ? 1u : 0u);
             }
@@ -534,6 +542,7 @@ attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
             const uint64_t dok = sdesc_sw(smem_u32(qdst + kTileBytes), 1024, 2);
 #pragma unroll
             for (int k = 0; k < kD / 16; ++k) {
+                if (p.dbg & 8) break;
                 mma_bf16_e(tmem + kColST, kd + ((k * 32) >> 4), qk + ((k * 32) >> 4), id_s,
                            k ? 1u : 0u);
                 mma_bf16_e(tmem + kColDP, vd + ((k * 32) >> 4), dok + ((k * 32) >> 4), id_s,
@@ -584,6 +593,7 @@ attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
                 }
 #pragma unroll
                 for (int c = 0; c < 4; ++c) {         // 16-B chunks of 8 query columns
+                    if (p.dbg & 2) break;
                     uint32_t pk[4], dk4[4];
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {

@@ -87,7 +87,7 @@ int main() {
     cudaMalloc(&d, 148 * sizeof(long long));
     cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     const int stages = 512;
-    for (int rnd : {1}) for (int mode : {0, 3}) for (uint32_t lbo : {2176u}) {
+    for (int rnd : {0, 1}) for (int mode : {0, 3}) for (uint32_t lbo : {2176u}) {
         probe<<<148, 128, 200 * 1024>>>(mode, stages, lbo, d, rnd, 3, 3, 2, 4);
         cudaError_t e = cudaDeviceSynchronize();
         if (e != cudaSuccess) { printf("mode %d: %s\n", mode, cudaGetErrorString(e)); return 1; }

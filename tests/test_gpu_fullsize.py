@@ -1,0 +1,165 @@
+"""Parity at BASELINE.json's full sizes through size-independent properties
+(the fp64 oracle cannot run these sizes in test time):
+
+* sharding invariance — halo_conv over R thread-ranks reproduces the dense
+  convolution (bit for bit except rare last-bit differences in the rows
+  that read the halo), and its backward matches the dense backward;
+* ring attention over R ranks matches R = 1, and V == 1 gives O == 1;
+* redistribute round trips are bit-exact at 1 GiB with uneven extents.
+"""
+
+import math
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda"
+
+
+@pytest.fixture(autouse=True)
+def _need_gpu():
+    from conftest import gpu_ready
+
+    if not gpu_ready():
+        pytest.fail("gpu tests need CUDA and libdpb200.so (no CPU path exists)")
+
+
+def dp():
+    import paper_2605_11111_b200 as m
+
+    return m
+
+
+def rel(a, b):
+    a, b = a.double(), b.double()
+    return float((a - b).abs().max() / b.abs().max().clamp_min(1e-30))
+
+
+def _sharded_conv(m, x, w, R, fmt, dim):
+    ext = m.default_chunk(x.shape[dim], R)
+
+    def prog(ctx):
+        lo = sum(ext[:ctx.rank_id])
+        xl = x.narrow(dim, lo, ext[ctx.rank_id]).contiguous(memory_format=fmt)
+        st = m.ShardTensor(xl, tuple(x.shape), ctx, (m.Shard(dim),), {0: tuple(ext)})
+        out, tape = m.halo_conv_forward(st, w, 1, 1)
+        return out.full_tensor(), tape, out.shard_shapes[0]
+
+    return m.spawn_mesh((R,), ("domain",), prog)
+
+
+@pytest.mark.parametrize("cfg", ["cfg2", "cfg4"])
+def test_conv_sharding_invariance_full_size(cfg):
+    """cfg2: 1x16x256^3 bf16 conv(16->32) D-sharded over 8 ranks; cfg4: two
+    ranks of the weak-scaling 64-channel 2048^2 grid (global 4096 x 2048)."""
+    m = dp()
+    torch.manual_seed(0)
+    if cfg == "cfg2":
+        shape, cout, R, fmt, dim = (1, 16, 256, 256, 256), 32, 8, torch.channels_last_3d, 2
+        w = (torch.randn(cout, 16, 3, 3, 3, device=DEV) * 0.05).to(torch.bfloat16)
+    else:
+        shape, cout, R, fmt, dim = (1, 64, 4096, 2048), 64, 2, torch.channels_last, 2
+        w = (torch.randn(cout, 64, 3, 3, device=DEV) * 0.05).to(torch.bfloat16)
+    x = torch.randn(shape, device=DEV).to(torch.bfloat16).contiguous(memory_format=fmt)
+    dense = m.dense_conv(x, w, stride=1, padding=1)
+    res = _sharded_conv(m, x, w, R, fmt, dim)
+    for full, _, shapes in res:
+        # identical everywhere except rare last-bit differences in the two
+        # output rows per shard that read the received halo (their launch
+        # runs a different q-chunk / TMEM-ring schedule): measured 1.4e-5 of
+        # the cfg2 output, at most 1 bf16 ulp
+        diff = (full.float() - dense.float()).abs()
+        assert float((diff > 0).float().mean()) < 1e-4
+        assert rel(full, dense) < 1e-2
+        assert sum(shapes) == dense.shape[dim]
+    # backward: sharded (dgrad + reverse halo + wgrad all-reduce) vs R = 1
+    dy = torch.randn(dense.shape, device=DEV).to(torch.bfloat16).contiguous(memory_format=fmt)
+    out_ext = list(res[0][2])
+
+    def prog(ctx):
+        lo = sum(m.default_chunk(x.shape[dim], R)[:ctx.rank_id])
+        ext = m.default_chunk(x.shape[dim], R)
+        xl = x.narrow(dim, lo, ext[ctx.rank_id]).contiguous(memory_format=fmt)
+        st = m.ShardTensor(xl, tuple(x.shape), ctx, (m.Shard(dim),), {0: tuple(ext)})
+        out, tape = m.halo_conv_forward(st, w, 1, 1)
+        olo = sum(out_ext[:ctx.rank_id])
+        dyl = dy.narrow(dim, olo, out_ext[ctx.rank_id]).contiguous(memory_format=fmt)
+        dx, dw = m.halo_conv_backward(tape, dyl)
+        return dx.full_tensor(), dw
+
+    sharded = m.spawn_mesh((R,), ("domain",), prog)
+
+    def prog1(ctx):
+        st = m.ShardTensor(x, tuple(x.shape), ctx, (m.Shard(dim),), {0: (x.shape[dim],)})
+        out, tape = m.halo_conv_forward(st, w, 1, 1)
+        dx, dw = m.halo_conv_backward(tape, dy)
+        return dx.full_tensor(), dw
+
+    dx1, dw1 = m.spawn_mesh((1,), ("domain",), prog1)[0]
+    for dx, dw in sharded:
+        assert rel(dx, dx1) < 1e-2
+        assert rel(dw, dw1) < 1e-3   # fp32 sums of 16.7M products, different partition
+
+
+def test_ring_attention_full_size_cfg3():
+    """64k tokens x 16 heads x 64, bf16: R = 4 ring vs R = 1 (forward), and
+    the V == 1 invariant (softmax rows sum to one) at full length."""
+    m = dp()
+    S, H, D = 65536, 16, 64
+    torch.manual_seed(0)
+    q, k = (torch.randn(S, H, D, device=DEV).to(torch.bfloat16) for _ in range(2))
+    v = torch.randn(S, H, D, device=DEV).to(torch.bfloat16)
+    ones = torch.ones(S, H, D, device=DEV, dtype=torch.bfloat16)
+
+    def run(R, vv):
+        ext = m.default_chunk(S, R)
+
+        def prog(ctx):
+            lo = sum(ext[:ctx.rank_id])
+            mk = lambda t: m.ShardTensor(t.narrow(0, lo, ext[ctx.rank_id]), (S, H, D), ctx,  # noqa
+                                         (m.Shard(0),), {0: tuple(ext)})
+            out = m.ring_attention(mk(q), mk(k), mk(vv))
+            return out.local
+
+        return torch.cat(m.spawn_mesh((R,), ("domain",), prog), dim=0)
+
+    o1 = run(1, v)
+    o4 = run(4, v)
+    assert rel(o4, o1) < 1e-2
+    one = run(4, ones)
+    assert float((one.double() - 1.0).abs().max()) < 8e-3
+    assert math.isfinite(float(o4.double().abs().max()))
+
+
+def test_redistribute_round_trips_1gib():
+    """cfg5 size: [16384, 16384] fp32 with the reference's uneven
+    random_partition extents over 4 ranks: S(0) -> R, S(0) -> S(1) -> S(0)
+    are bit-exact."""
+    m = dp()
+    import bench
+
+    n, R = 16384, 4
+    ext = bench.random_partition(R, n, R)
+    g = torch.randn(n, n, device=DEV)
+
+    def prog(ctx):
+        lo = sum(ext[:ctx.rank_id])
+        st = m.ShardTensor(g.narrow(0, lo, ext[ctx.rank_id]).clone(), (n, n), ctx,
+                           (m.Shard(0),), {0: tuple(ext)})
+        rep = m.redistribute(st, (m.Replicate(),))
+        ok_rep = torch.equal(rep.local, g)
+        del rep
+        s1 = m.redistribute(st, (m.Shard(1),))
+        c = m.default_chunk(n, R)
+        clo = sum(c[:ctx.rank_id])
+        ok_s1 = torch.equal(s1.local, g[:, clo:clo + c[ctx.rank_id]])
+        back = m.redistribute(s1, (m.Shard(0),))
+        r0 = m.default_chunk(n, R)
+        rlo = sum(r0[:ctx.rank_id])
+        ok_back = torch.equal(back.local, g[rlo:rlo + r0[ctx.rank_id]])
+        return ok_rep, ok_s1, ok_back, s1.shard_shapes[0]
+
+    for ok_rep, ok_s1, ok_back, shapes in m.spawn_mesh((R,), ("domain",), prog):
+        assert ok_rep and ok_s1 and ok_back
+        assert shapes == tuple(m.default_chunk(n, R))
