@@ -161,6 +161,12 @@ TC_CASES = [
     (2, 1, 64, 32, (7, 100), 3, 1, 0),
     (2, 1, 16, 32, (5, 33), 3, 0, 0),
     (3, 1, 16, 32, (4, 3, 300), 3, 1, 2),
+    # rows of 161..256 voxels with padding 1: the CTA-pair (cta_group::2) fwd/dgrad
+    (3, 1, 16, 32, (4, 5, 256), 3, 1, 2),
+    (3, 1, 32, 16, (3, 4, 200), 3, 1, 1),
+    (2, 1, 32, 32, (6, 256), 3, 1, 0),
+    (3, 2, 16, 16, (3, 3, 181), 3, 1, 1),
+    (2, 2, 16, 32, (5, 170), 3, 1, 3),
 ]
 
 
@@ -275,3 +281,18 @@ def test_attention_tc_fwd_bwd_vs_oracle(case, payload):
     assert rel_err(to_np(out), oatt.sdpa(qr, kr, vr)) < 1.5e-2
     for got, want in zip((dq, dk, dv), oatt.sdpa_grads(qr, kr, vr, dr)):
         assert rel_err(to_np(got), want, floor=1.0) < 1.5e-2
+
+
+def test_conv_pair_kernel_opt_in():
+    """The CTA-pair (cta_group::2) conv kernel is opt-in (DP_CONV_PAIR=1, read
+    once per process): run the tcgen05 conv parity cases with it enabled."""
+    import os
+    import subprocess
+    import sys
+
+    env = dict(os.environ, DP_CONV_PAIR="1")
+    here = os.path.dirname(os.path.abspath(__file__))
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", os.path.join(here, "test_gpu_kernels.py"),
+                        "-k", "test_conv_tc_fwd_dgrad_vs_oracle"], env=env, capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
