@@ -644,16 +644,21 @@ struct PairShape {
     static constexpr int STAGE = KP * NBLK * BOX;
     static constexpr int BHALF = SW / 2 * 32;                // B rows of one CTA per MMA block
     static constexpr int WIMG = KP * KC * KQ * BHALF;        // per-CTA weight image bytes
-    static constexpr int EDGE = NSLOT * 6 * 2 * N0 * 4;      // quarter-edge ring bytes
-    static constexpr int DR = 16, LAG = 4;                   // pair-boundary ring / lag (rows)
+    static constexpr int HC = N0 / 2;                        // channels per epilogue half
+    static constexpr int EDGE = NSLOT * 2 * 6 * 2 * HC * 4;  // quarter-edge ring bytes
+    static constexpr int DR = 32, LAG = 4;                   // pair-boundary ring / lag (rows)
     static constexpr int BOUND = 2 * DR * N0 * 4 + DR * 8;   // own partials, peer slices, dst
-    static_assert(LAG <= DR - NSLOT - 1, "boundary ring reuse must trail the TMEM slot ring");
+    static_assert(LAG % 2 == 0 && LAG <= DR - NSLOT - 3,
+                  "boundary ring reuse must trail the TMEM slot ring");
+    static_assert(NSLOT >= KQ + 2, "3 rows accumulate while 2 drain");
     static_assert(BOX % 1024 == 0, "swizzle atoms");
     static_assert((SW / 2) % 8 == 0, "B halves are whole core-matrix groups");
 };
 
+constexpr int kPairThreads = 18 * 32;   // TMA, MMA, 16 epilogue warps
+
 template <int N0, int CIN, int KP>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
 conv_tc2_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap hmap,
                 const ConvTcParams p) {
     using namespace tc;
@@ -674,13 +679,13 @@ conv_tc2_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant_
                                                   S::BOUND);
     uint64_t *full = bars, *empty = bars + p.nstage;
     uint64_t *tfull = empty + p.nstage, *tempty = tfull + NSLOT, *ebar = tempty + NSLOT;
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(ebar + S::DR);
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(ebar + 2 * S::DR);
 
     // this CTA's half of the weight image, zeroed edge ring
     const uint8_t *wsrc = reinterpret_cast<const uint8_t *>(p.wimg) + (size_t)rank * S::WIMG;
-    for (int i = threadIdx.x * 16; i < S::WIMG; i += kThreads * 16)
+    for (int i = threadIdx.x * 16; i < S::WIMG; i += kPairThreads * 16)
         *reinterpret_cast<int4 *>(wsm + i) = *reinterpret_cast<const int4 *>(wsrc + i);
-    for (int i = threadIdx.x; i < S::EDGE / 4; i += kThreads) edges[i] = 0.f;
+    for (int i = threadIdx.x; i < S::EDGE / 4; i += kPairThreads) edges[i] = 0.f;
     fence_async_smem();
     if (warp == 0) {
         if (lane == 0) {
@@ -690,9 +695,9 @@ conv_tc2_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant_
             }
             for (int i = 0; i < NSLOT; ++i) {
                 mbar_init(&tfull[i], 1);
-                mbar_init(&tempty[i], 8);     // 4 epilogue warps x 2 CTAs (even CTA's copy)
+                mbar_init(&tempty[i], 16);    // 8 draining warps x 2 CTAs (even CTA's copy)
             }
-            for (int i = 0; i < S::DR; ++i) mbar_init(&ebar[i], 1);
+            for (int i = 0; i < 2 * S::DR; ++i) mbar_init(&ebar[i], 1);
             mbar_fence_init();
             tma_prefetch(&xmap);
             tma_prefetch(&hmap);
@@ -705,14 +710,6 @@ conv_tc2_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant_
     cluster_sync();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
-    if (warp >= 2) {
-        const uint32_t lane_base = tmem + ((uint32_t)((warp & 3) * 32) << 16);
-        uint32_t z[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) z[i] = 0u;
-        for (int c = 0; c < NSLOT * SW; c += 16) tmem_st16(lane_base + c, z);
-        tmem_wait_st();
-    }
     tc_fence_before();
     __syncthreads();
     cluster_sync();
@@ -809,17 +806,22 @@ conv_tc2_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant_
             }
         }
     } else {
-        // ===================== epilogue (both CTAs) =====================
+        // ===================== epilogue (both CTAs, 16 warps) =====================
         // Thread = input voxel v = 128 rank + 32 quarter + lane = output voxel w.
         // out[w] = D[w-1][kw 0] + D[w][kw 1] + D[w+1][kw 2]: neighbours within the
         // warp by shuffles; across quarters through edge entries e = quarter + 1
         // of a per-slot smem ring ([e][0] = lane 0's kw 2 slice, [e][1] = lane
-        // 31's kw 0 slice; entries 0 and 5 stay zero = the row padding).  The
-        // pair boundary (voxels 127 | 128) is NOT synchronised per row: the two
-        // boundary threads keep their partial sums in a ring, st.async their
-        // slice into the peer's ring (complete_tx on the peer's mbarrier), and
-        // finish row r LAG rows later, when the peer's slice has long landed.
+        // 31's kw 0 slice; entries 0 and 5 stay zero = the row padding).  Warp
+        // group g = (warp - 2) / 4 (one warp per TMEM lane quarter) handles rows
+        // of parity g & 1 and channel half g >> 1, so two rows drain at once and
+        // each warp reads 3 x N0/2 columns.  The pair boundary (voxels 127 | 128)
+        // is not synchronised per row: the boundary threads keep partial sums in
+        // a ring, st.async their slice into the peer's ring (complete_tx on the
+        // peer's mbarrier) and finish row r LAG rows later.
         const int quarter = warp & 3;
+        const int grp = (warp - 2) >> 2;
+        const int parity = grp & 1, chalf = grp >> 1;
+        const int cofs = chalf * S::HC;                        // first channel of this warp
         const int w = (int)rank * 128 + quarter * 32 + lane;
         const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
         const uint32_t lead_tempty = mapa_shared(smem_u32(tempty), 0);
@@ -827,31 +829,30 @@ conv_tc2_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant_
                              (rank == 1 && quarter == 0 && lane == 0);
         const uint32_t peer_bpeer = mapa_shared(smem_u32(bpeer), rank ^ 1u);
         const uint32_t peer_ebar = mapa_shared(smem_u32(ebar), rank ^ 1u);
-        uint32_t z[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) z[i] = 0u;
         auto edge = [&](uint32_t slot, int e, int side) {
-            return edges + ((size_t)(slot * 6 + e) * 2 + side) * N0;
+            return edges + ((((size_t)slot * 2 + chalf) * 6 + e) * 2 + side) * S::HC;
         };
         auto finish_boundary = [&](uint32_t r) {      // boundary thread: row r is complete
             const uint32_t e = r % S::DR;
-            mbar_expect_tx(&ebar[e], N0 * 4);
-            mbar_wait(&ebar[e], (r / S::DR) & 1);
+            uint64_t *bar = &ebar[e * 2 + chalf];
+            mbar_expect_tx(bar, S::HC * 4);
+            mbar_wait(bar, (r / S::DR) & 1);
             __nv_bfloat16 *dst = bdst[e];
             if (dst) {
-                const float *pa = bpart + e * N0, *pb = bpeer + e * N0;
+                const float *pa = bpart + e * N0 + cofs, *pb = bpeer + e * N0 + cofs;
 #pragma unroll
-                for (int c = 0; c < N0; c += 8) {
+                for (int c = 0; c < S::HC; c += 8) {
                     uint4 pk;
                     pk.x = pack_bf16(pa[c + 0] + pb[c + 0], pa[c + 1] + pb[c + 1]);
                     pk.y = pack_bf16(pa[c + 2] + pb[c + 2], pa[c + 3] + pb[c + 3]);
                     pk.z = pack_bf16(pa[c + 4] + pb[c + 4], pa[c + 5] + pb[c + 5]);
                     pk.w = pack_bf16(pa[c + 6] + pb[c + 6], pa[c + 7] + pb[c + 7]);
-                    *reinterpret_cast<uint4 *>(dst + c) = pk;
+                    *reinterpret_cast<uint4 *>(dst + cofs + c) = pk;
                 }
             }
         };
-        uint32_t row_base = 0;
+        uint32_t row_base = 0, last_mine = 0;
+        bool any_mine = false;
         for (int u = cluster; u < p.n_units; u += nclusters) {
             int r = u;
             const int qc = r % p.n_qc; r /= p.n_qc;
@@ -859,57 +860,66 @@ conv_tc2_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant_
             const int b = r / p.Pout;
             const int q0 = qc * p.q_chunk, q1 = min(p.Qout, q0 + p.q_chunk);
             for (int j = 0; j < q1 - q0; ++j) {
-                const uint32_t row = row_base + j, slot = row % NSLOT, par = (row / NSLOT) & 1;
+                const uint32_t row = row_base + j;
+                if ((int)(row & 1) != parity) continue;
+                const uint32_t slot = row % NSLOT, par = (row / NSLOT) & 1;
                 mbar_wait(&tfull[slot], par);
                 tc_fence_after();
-                const uint32_t col = lane_base + slot * SW;
-                uint32_t v[SW];
+                const uint32_t col = lane_base + slot * SW + cofs;
+                uint32_t v[3 * S::HC];      // [kw][c] for this warp's channel half
 #pragma unroll
-                for (int c = 0; c < SW; c += 16) {
-                    uint32_t t[16];
-                    tmem_ld16(col + c, t);
+                for (int kw = 0; kw < 3; ++kw)
 #pragma unroll
-                    for (int i = 0; i < 16; ++i) v[c + i] = t[i];
-                }
+                    for (int c = 0; c < S::HC; c += 8) {
+                        uint32_t t[8];
+                        asm volatile(
+                            "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                            : "=r"(t[0]), "=r"(t[1]), "=r"(t[2]), "=r"(t[3]), "=r"(t[4]), "=r"(t[5]),
+                              "=r"(t[6]), "=r"(t[7])
+                            : "r"(col + kw * N0 + c));
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) v[kw * S::HC + c + i] = t[i];
+                    }
                 tmem_wait_ld();
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) {   // TMEM slot drained: one arrival per warp
+                if (lane == 0) {   // this warp's columns of the slot are drained
                     if (rank == 0) mbar_arrive(&tempty[slot]);
                     else mbar_arrive_remote(lead_tempty + slot * 8);
                 }
-                // quarter edges
                 if (lane == 0) {
                     uint4 *e0 = reinterpret_cast<uint4 *>(edge(slot, quarter + 1, 0));
 #pragma unroll
-                    for (int c = 0; c < N0; c += 4)
-                        e0[c / 4] = make_uint4(v[2 * N0 + c], v[2 * N0 + c + 1], v[2 * N0 + c + 2],
-                                               v[2 * N0 + c + 3]);
+                    for (int c = 0; c < S::HC; c += 4)
+                        e0[c / 4] = make_uint4(v[2 * S::HC + c], v[2 * S::HC + c + 1],
+                                               v[2 * S::HC + c + 2], v[2 * S::HC + c + 3]);
                 }
                 if (lane == 31) {
                     uint4 *e1 = reinterpret_cast<uint4 *>(edge(slot, quarter + 1, 1));
 #pragma unroll
-                    for (int c = 0; c < N0; c += 4)
+                    for (int c = 0; c < S::HC; c += 4)
                         e1[c / 4] = make_uint4(v[c], v[c + 1], v[c + 2], v[c + 3]);
                 }
-                if (bthread) {   // the slice the peer's boundary voxel needs
-                    const int base = rank == 0 ? 0 : 2 * N0;
+                if (bthread) {   // the slice the peer's boundary voxel needs (kw 0 / kw 2)
+                    const bool k0 = rank == 0;
                     const uint32_t e = row % S::DR;
 #pragma unroll
-                    for (int c = 0; c < N0; c += 4)
-                        st_async_v4(peer_bpeer + (e * N0 + c) * 4,
-                                    make_uint4(v[base + c], v[base + c + 1], v[base + c + 2],
-                                               v[base + c + 3]),
-                                    peer_ebar + e * 8);
+                    for (int c = 0; c < S::HC; c += 4)
+                        st_async_v4(peer_bpeer + (e * N0 + cofs + c) * 4,
+                                    make_uint4(k0 ? v[c] : v[2 * S::HC + c],
+                                               k0 ? v[c + 1] : v[2 * S::HC + c + 1],
+                                               k0 ? v[c + 2] : v[2 * S::HC + c + 2],
+                                               k0 ? v[c + 3] : v[2 * S::HC + c + 3]),
+                                    peer_ebar + (e * 2 + chalf) * 8);
                 }
-                named_bar_sync(1, 128);
+                named_bar_sync(1 + grp, 128);
                 // branch-free combine (entries 5 of the even CTA / 0 of the odd CTA
                 // are zero: the boundary threads get their partial sums)
                 const float4 *lo_prev = reinterpret_cast<const float4 *>(edge(slot, quarter, 1));
                 const float4 *hi_next = reinterpret_cast<const float4 *>(edge(slot, quarter + 2, 0));
-                float o[N0];
+                float o[S::HC];
 #pragma unroll
-                for (int c4 = 0; c4 < N0 / 4; ++c4) {
+                for (int c4 = 0; c4 < S::HC / 4; ++c4) {
                     const float4 lp = lo_prev[c4], hn = hi_next[c4];
                     const float lpa[4] = {lp.x, lp.y, lp.z, lp.w};
                     const float hna[4] = {hn.x, hn.y, hn.z, hn.w};
@@ -918,10 +928,10 @@ conv_tc2_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant_
                         const int c = c4 * 4 + e;
                         const float a0 = __shfl_up_sync(0xffffffffu, __uint_as_float(v[c]), 1);
                         const float a2 =
-                            __shfl_down_sync(0xffffffffu, __uint_as_float(v[2 * N0 + c]), 1);
+                            __shfl_down_sync(0xffffffffu, __uint_as_float(v[2 * S::HC + c]), 1);
                         const float left = lane == 0 ? lpa[e] : a0;
                         const float right = lane == 31 ? hna[e] : a2;
-                        o[c] = (left + __uint_as_float(v[N0 + c])) + right;
+                        o[c] = (left + __uint_as_float(v[S::HC + c])) + right;
                     }
                 }
                 __nv_bfloat16 *dst = nullptr;
@@ -939,28 +949,32 @@ conv_tc2_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant_
                 }
                 if (bthread) {
                     const uint32_t e = row % S::DR;
-                    float4 *pa = reinterpret_cast<float4 *>(bpart + e * N0);
+                    float4 *pa = reinterpret_cast<float4 *>(bpart + e * N0 + cofs);
 #pragma unroll
-                    for (int c = 0; c < N0; c += 4) pa[c / 4] = make_float4(o[c], o[c + 1], o[c + 2], o[c + 3]);
-                    bdst[e] = dst;
-                    if (row >= (uint32_t)S::LAG) finish_boundary(row - S::LAG);
+                    for (int c = 0; c < S::HC; c += 4)
+                        pa[c / 4] = make_float4(o[c], o[c + 1], o[c + 2], o[c + 3]);
+                    bdst[e] = dst;      // both channel halves write the same pointer
+                    if (any_mine && row >= (uint32_t)S::LAG) finish_boundary(row - S::LAG);
                 } else if (dst) {
 #pragma unroll
-                    for (int c = 0; c < N0; c += 8) {
+                    for (int c = 0; c < S::HC; c += 8) {
                         uint4 pk;
                         pk.x = pack_bf16(o[c + 0], o[c + 1]);
                         pk.y = pack_bf16(o[c + 2], o[c + 3]);
                         pk.z = pack_bf16(o[c + 4], o[c + 5]);
                         pk.w = pack_bf16(o[c + 6], o[c + 7]);
-                        *reinterpret_cast<uint4 *>(dst + c) = pk;
+                        *reinterpret_cast<uint4 *>(dst + cofs + c) = pk;
                     }
                 }
+                any_mine = true;
+                last_mine = row;
             }
             row_base += q1 - q0;
         }
-        if (bthread) {
-            const uint32_t first = row_base > (uint32_t)S::LAG ? row_base - S::LAG : 0;
-            for (uint32_t rr = first; rr < row_base; ++rr) finish_boundary(rr);
+        if (bthread && any_mine) {
+            // rows of this parity not yet finished: last_mine - LAG + 2 .. last_mine
+            const uint32_t lo = last_mine >= (uint32_t)S::LAG - 2 ? last_mine - (S::LAG - 2) : parity;
+            for (uint32_t rr = lo; rr <= last_mine; rr += 2) finish_boundary(rr);
         }
     }
     tc_fence_before();
@@ -1020,7 +1034,7 @@ template <int N0, int CIN, int KP>
 int pair_smem(int nstage) {
     using S = PairShape<N0, CIN, KP>;
     return ((S::WIMG + 1023) & ~1023) + nstage * S::STAGE + S::EDGE + S::BOUND +
-           (2 * nstage + 2 * S::NSLOT + S::DR) * 8 + 16;
+           (2 * nstage + 2 * S::NSLOT + 2 * S::DR) * 8 + 16;
 }
 
 bool make_pair_plan(const dp_conv_geom *g, bool dgrad, PairPlan &pl) {
@@ -1068,7 +1082,7 @@ int launch_pair_k(const CUtensorMap &xm, const CUtensorMap &hm, const ConvTcPara
                   int smem, cudaStream_t st) {
     auto kern = conv_tc2_kernel<N0, CIN, KP>;
     DP_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    kern<<<grid, kThreads, smem, st>>>(xm, hm, p);
+    kern<<<grid, kPairThreads, smem, st>>>(xm, hm, p);
     return launch_status("conv_tc2_kernel");
 }
 
