@@ -16,10 +16,23 @@
 // wgrad: a CTA owns 32 output x 32 input channels and sweeps a share of the
 // (row, 64-position) units; thread = (4 output channels, 1 input channel)
 // x all taps in registers; per-CTA partials are reduced deterministically.
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace dp {
 namespace {
+
+// packed fp32x2 FMA (sm_100 FFMA2): two output channels per instruction
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+    float2 d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;"
+        : "=l"(*reinterpret_cast<unsigned long long *>(&d))
+        : "l"(*reinterpret_cast<unsigned long long *>(&a)),
+          "l"(*reinterpret_cast<unsigned long long *>(&b)),
+          "l"(*reinterpret_cast<unsigned long long *>(&c)));
+    return d;
+}
 
 constexpr int kTW = 128;      // fwd positions per CTA
 constexpr int kCoT = 32;      // fwd output channels per CTA
@@ -45,6 +58,17 @@ struct TG {
 // dst with zero fill; lanes of a warp stride over the columns, the row's
 // validity / base pointer are computed once.
 template <typename T>
+__device__ __forceinline__ void async_copy(T *dst, const T *src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(
+                     static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+                 "l"(src), "n"(sizeof(T))
+                 : "memory");
+}
+__device__ __forceinline__ void async_wait_all() {
+    asm volatile("cp.async.wait_all;" ::: "memory");
+}
+
+template <typename T>
 __device__ __forceinline__ void stage_row(const TG &g, const T *__restrict__ x,
                                           const T *__restrict__ xh, int64_t b, int64_t c,
                                           int64_t v0, int64_t v1, int64_t v2a, int n, T *dst,
@@ -68,13 +92,16 @@ __device__ __forceinline__ void stage_row(const TG &g, const T *__restrict__ x,
     const int64_t st2 = hal ? g.hs[4] : g.xs[4];
     for (int i = lane; i < n; i += 32) {
         int64_t v2 = v2a + i;
-        T val = T(0);
+        const T *src = nullptr;
         if (v2 >= 0) {
-            if (v2 < g.in[2]) val = row[v2 * st2];
+            if (v2 < g.in[2]) src = row + v2 * st2;
             else if (g.shard == 2 && !hal && v2 - g.in[2] < g.halo)
-                val = rowh[(v2 - g.in[2]) * g.hs[4]];
+                src = rowh + (v2 - g.in[2]) * g.hs[4];
         }
-        dst[i] = val;
+        // async global -> smem copy: every row of the slab is in flight at once
+        // (a load -> store round trip per row serialised the staging on latency)
+        if (src) async_copy(dst + i, src);
+        else dst[i] = T(0);
     }
 }
 
@@ -121,6 +148,7 @@ conv_tiled_fwd(TG g, const T *__restrict__ x, const T *__restrict__ xh, const T 
             const int cc = e / (taps * kCoT), t = (e / kCoT) % taps, c = e % kCoT;
             ws_[e] = fetch_w<T>(g, w, co0 + c, ci0 + cc, t, taps);
         }
+        async_wait_all();
         __syncthreads();
 #pragma unroll 2
         for (int cc = 0; cc < kCiT; ++cc) {
@@ -173,22 +201,36 @@ conv_tiled_fwd(TG g, const T *__restrict__ x, const T *__restrict__ xh, const T 
 template <typename T, int TMAX, int CPT, int K2_>  // K2_ = 0: runtime
 __global__ void __launch_bounds__(32 * 32 / CPT)
 conv_tiled_wgrad(TG g, const T *__restrict__ x, const T *__restrict__ xh, const T *__restrict__ dy,
-                 T *__restrict__ part, int64_t units) {
+                 T *__restrict__ part, int64_t units, int nbuf) {
     constexpr int kWThreads = 32 * 32 / CPT;
     extern __shared__ __align__(16) unsigned char smraw[];
     const int R = g.k[0] * g.k[1], K2 = K2_ ? K2_ : g.k[2], taps = R * K2;
     const int XW = (kWTW + K2 - 1) | 1;     // odd row length: conflict-free across ci
     T *xs_ = reinterpret_cast<T *>(smraw);  // [32 ci][R][XW]
-    T *ds_ = xs_ + 32 * R * XW;             // [32 co][kWTW]
+    // dY tile: [32 co][kWTW], or [kWTW][32 co] (co innermost: 16-B loads of 4
+    // output channels) on the fp32 sliding-window path
+    constexpr bool kF2 = std::is_same<T, float>::value && K2_ == 3 && TMAX % 3 == 0 && CPT % 4 == 0;
     const int tid = threadIdx.x, cil = tid & 31, cob = tid >> 5;
     const int64_t co0 = (int64_t)blockIdx.y * 32, ci0 = (int64_t)blockIdx.z * 32;
-    T acc[CPT][TMAX];
+    T acc[kF2 ? 1 : CPT][kF2 ? 1 : TMAX];
+    float2 acc2[kF2 ? CPT / 2 : 1][kF2 ? TMAX : 1];
+    if constexpr (kF2) {
 #pragma unroll
-    for (int j = 0; j < CPT; ++j)
+        for (int j = 0; j < CPT / 2; ++j)
 #pragma unroll
-        for (int t = 0; t < TMAX; ++t) acc[j][t] = T(0);
+            for (int t = 0; t < TMAX; ++t) acc2[j][t] = make_float2(0.f, 0.f);
+    } else {
+#pragma unroll
+        for (int j = 0; j < CPT; ++j)
+#pragma unroll
+            for (int t = 0; t < TMAX; ++t) acc[j][t] = T(0);
+    }
     const int64_t n_wt = (g.out[2] + kWTW - 1) / kWTW;
-    for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+    // two staging buffers: unit k+1 is copied (cp.async) while unit k computes
+    const int buf_elems = ((32 * R * XW + 3) & ~3) + 32 * kWTW;
+    auto stage = [&](int64_t u, int buf) {
+        T *xb = xs_ + (size_t)buf * buf_elems;
+        T *db = xb + ((32 * R * XW + 3) & ~3);
         int64_t r = u;
         const int64_t wt = r % n_wt; r /= n_wt;
         const int64_t o1 = r % g.out[1]; r /= g.out[1];
@@ -198,33 +240,117 @@ conv_tiled_wgrad(TG g, const T *__restrict__ x, const T *__restrict__ xh, const 
         for (int rowi = tid >> 5; rowi < 32 * R; rowi += kWThreads / 32) {
             const int cc = rowi / R, rr = rowi % R;
             stage_row<T>(g, x, xh, b, ci0 + cc, g.base[0] + o0 + rr / g.k[1],
-                         g.base[1] + o1 + rr % g.k[1], g.base[2] + ow0, XW, xs_ + rowi * XW,
+                         g.base[1] + o1 + rr % g.k[1], g.base[2] + ow0, XW, xb + rowi * XW,
                          tid & 31);
         }
         for (int e = tid; e < 32 * kWTW; e += kWThreads) {
             const int cc = e / kWTW, c = e % kWTW;
             const int64_t co = co0 + cc, ow = ow0 + c;
-            ds_[e] = (co < g.CO && ow < g.out[2])
-                         ? dy[b * g.ys[0] + co * g.ys[1] + o0 * g.ys[2] + o1 * g.ys[3] +
-                              ow * g.ys[4]]
-                         : T(0);
+            T *dd = db + (kF2 ? c * 32 + cc : e);
+            if (co < g.CO && ow < g.out[2])
+                async_copy(dd, dy + b * g.ys[0] + co * g.ys[1] + o0 * g.ys[2] + o1 * g.ys[3] +
+                                   ow * g.ys[4]);
+            else
+                *dd = T(0);
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    if ((int64_t)blockIdx.x < units) stage(blockIdx.x, 0);
+    int buf = 0;
+    for (int64_t u = blockIdx.x; u < units; u += gridDim.x, buf ^= (nbuf - 1)) {
+        if (nbuf == 2 && u + gridDim.x < units) {
+            stage(u + gridDim.x, buf ^ 1);
+            asm volatile("cp.async.wait_group 1;" ::: "memory");
+        } else {
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
         }
         __syncthreads();
-        const T *xr = xs_ + cil * R * XW;
-        for (int p = 0; p < kWTW; ++p) {
-            T d[CPT];
+        const T *xr = xs_ + (size_t)buf * buf_elems + cil * R * XW;
+        T *ds_ = xs_ + (size_t)buf * buf_elems + ((32 * R * XW + 3) & ~3);
+        if constexpr (kF2) {
+            // fp32: sliding window along the row (each staged input value loaded
+            // once per (row r, position), reused by the 3 kw taps), 16-B dY loads,
+            // packed fma.rn.f32x2 over output-channel pairs
+            constexpr int RM = TMAX / 3;
+            float win[RM][3];
 #pragma unroll
-            for (int j = 0; j < CPT; ++j) d[j] = ds_[(cob * CPT + j) * kWTW + p];
+            for (int rr = 0; rr < RM; ++rr)
+                if (rr < R) {
+                    win[rr][1] = xr[rr * XW + 0];
+                    win[rr][2] = xr[rr * XW + 1];
+                }
+#pragma unroll 2
+            for (int p = 0; p < kWTW; ++p) {
+                float2 d2[CPT / 2];
 #pragma unroll
-            for (int t = 0; t < TMAX; ++t) {
-                if (t < taps) {
-                    const T xv = xr[(t / K2) * XW + p + t % K2];
+                for (int j = 0; j < CPT / 4; ++j) {
+                    const float4 v = *reinterpret_cast<const float4 *>(
+                        reinterpret_cast<const float *>(ds_) + p * 32 + cob * CPT + 4 * j);
+                    d2[2 * j] = make_float2(v.x, v.y);
+                    d2[2 * j + 1] = make_float2(v.z, v.w);
+                }
 #pragma unroll
-                    for (int j = 0; j < CPT; ++j) acc[j][t] += d[j] * xv;
+                for (int rr = 0; rr < RM; ++rr) {
+                    if (rr < R) {
+                        win[rr][0] = win[rr][1];
+                        win[rr][1] = win[rr][2];
+                        win[rr][2] = xr[rr * XW + p + 2];
+#pragma unroll
+                        for (int kw = 0; kw < 3; ++kw) {
+                            const float2 xv = make_float2(win[rr][kw], win[rr][kw]);
+#pragma unroll
+                            for (int j = 0; j < CPT / 2; ++j)
+                                acc2[j][rr * 3 + kw] = ffma2(d2[j], xv, acc2[j][rr * 3 + kw]);
+                        }
+                    }
+                }
+            }
+        } else if (K2_ == 3 && TMAX % 3 == 0) {
+            // sliding window along the row: each staged input value is loaded once
+            // per (row r, position) and reused by the 3 kw taps from registers
+            constexpr int RM = TMAX / 3;
+            T win[RM][3];
+#pragma unroll
+            for (int rr = 0; rr < RM; ++rr)
+                if (rr < R) {
+                    win[rr][1] = xr[rr * XW + 0];
+                    win[rr][2] = xr[rr * XW + 1];
+                }
+#pragma unroll 4
+            for (int p = 0; p < kWTW; ++p) {
+                T d[CPT];
+#pragma unroll
+                for (int j = 0; j < CPT; ++j) d[j] = ds_[(cob * CPT + j) * kWTW + p];
+#pragma unroll
+                for (int rr = 0; rr < RM; ++rr) {
+                    if (rr < R) {
+                        win[rr][0] = win[rr][1];
+                        win[rr][1] = win[rr][2];
+                        win[rr][2] = xr[rr * XW + p + 2];
+#pragma unroll
+                        for (int kw = 0; kw < 3; ++kw)
+#pragma unroll
+                            for (int j = 0; j < CPT; ++j) acc[j][rr * 3 + kw] += d[j] * win[rr][kw];
+                    }
+                }
+            }
+        } else {
+            for (int p = 0; p < kWTW; ++p) {
+                T d[CPT];
+#pragma unroll
+                for (int j = 0; j < CPT; ++j) d[j] = ds_[(cob * CPT + j) * kWTW + p];
+#pragma unroll
+                for (int t = 0; t < TMAX; ++t) {
+                    if (t < taps) {
+                        const T xv = xr[(t / K2) * XW + p + t % K2];
+#pragma unroll
+                        for (int j = 0; j < CPT; ++j) acc[j][t] += d[j] * xv;
+                    }
                 }
             }
         }
         __syncthreads();
+        if (nbuf == 1 && u + gridDim.x < units) stage(u + gridDim.x, 0);
     }
     // partial [blockIdx.x][co][ci][taps]
     const int64_t ci = ci0 + cil;
@@ -236,7 +362,12 @@ conv_tiled_wgrad(TG g, const T *__restrict__ x, const T *__restrict__ xh, const 
         T *dst = part + (((int64_t)blockIdx.x * g.CO + co) * g.CI + ci) * taps;
 #pragma unroll
         for (int t = 0; t < TMAX; ++t)
-            if (t < taps) dst[t] = acc[j][t];
+            if (t < taps) {
+                if constexpr (kF2)
+                    dst[t] = (j & 1) ? acc2[j / 2][t].y : acc2[j / 2][t].x;
+                else
+                    dst[t] = acc[j][t];
+            }
     }
 }
 
@@ -284,7 +415,8 @@ size_t fwd_smem(const TG &g, int es) {
 size_t wgrad_smem(const TG &g, int es) {
     const int R = g.k[0] * g.k[1];
     const int XW = (kWTW + g.k[2] - 1) | 1;
-    return ((size_t)32 * R * XW + 32 * kWTW) * es;
+    const size_t one = ((((size_t)32 * R * XW + 3) & ~(size_t)3) + 32 * kWTW) * es;
+    return 2 * one <= 200 * 1024 ? 2 * one : one;   // double-buffered when it fits
 }
 
 template <typename T>
@@ -385,7 +517,7 @@ static TG wgrad_geom(const dp_conv_geom *cg) {
 
 static int wgrad_chunks_tiled(const TG &g, int64_t units) {
     const int64_t tiles = ((g.CO + 31) / 32) * ((g.CI + 31) / 32);
-    int64_t want = (2 * sm_count() + tiles - 1) / tiles;
+    int64_t want = (6 * sm_count() + tiles - 1) / tiles;   // several CTAs per SM hide staging
     if (want > units) want = units;
     return (int)(want < 1 ? 1 : want);
 }
@@ -412,6 +544,10 @@ int conv_wgrad_tiled_launch(const dp_conv_geom *cg, int dtype, const void *x, co
     DP_REQUIRE(ws_bytes >= (int64_t)chunks * n * es, DP_ERR_INVALID,
                "conv_wgrad_tiled: workspace too small");
     const size_t smem = wgrad_smem(g, es);
+    const int R = g.k[0] * g.k[1];
+    const size_t one = ((((size_t)32 * R * ((kWTW + g.k[2] - 1) | 1) + 3) & ~(size_t)3) +
+                        32 * kWTW) * es;
+    const int nbuf = smem >= 2 * one ? 2 : 1;
     dim3 grid((unsigned)chunks, (unsigned)((g.CO + 31) / 32), (unsigned)((g.CI + 31) / 32));
     const int rgrid = grid_for(n, 256, 4);
     const bool small = taps <= 9;
@@ -421,7 +557,7 @@ int conv_wgrad_tiled_launch(const dp_conv_geom *cg, int dtype, const void *x, co
         DP_CUDA_CHECK(cudaFuncSetAttribute(kern,                                                  \
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
         kern<<<grid, 32 * 32 / CP, smem, st>>>(                                                   \
-            g, (const T *)x, (const T *)xh, (const T *)dy, (T *)ws, units);                       \
+            g, (const T *)x, (const T *)xh, (const T *)dy, (T *)ws, units, nbuf);                 \
         tiled_wgrad_reduce<T><<<rgrid, 256, 0, st>>>((const T *)ws, (T *)dw, n, chunks);          \
     } while (0)
     if (dtype == DP_F64) {
