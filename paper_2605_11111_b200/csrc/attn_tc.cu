@@ -399,14 +399,16 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
 constexpr int kBwdThreads = 448;   // TMA, MMA, 8 softmax warps, 4 dQ warps
 constexpr int kB_K = 0, kB_V = kTileBytes;
 constexpr int kB_QD = 2 * kTileBytes;                  // 2 stages of [Q | dO]
-constexpr int kB_PS = kB_QD + 2 * 2 * kTileBytes;      // [P^T | dS^T] (single buffer)
+constexpr int kB_PS = kB_QD + 2 * 2 * kTileBytes;      // dS^T x 2 (double buffer)
 constexpr int kB_DQ = kB_PS + 2 * kPBytes;             // 2 dQ staging tiles (fp32, 2 x 16 KB)
 constexpr int kDQStage = kBM * kD * 4;                 // 32 KB
 constexpr int kB_LD = kB_DQ + 2 * kDQStage;            // -lse2[2][128], delta[2][128]
 constexpr int kB_BAR = kB_LD + 4 * 128 * 4;
 constexpr int kSmemBwd = kB_BAR + 256;
-// TMEM columns: S^T [0,128), dP^T [128,256), dV [256,320), dK [320,384), dQ x2 [384,512)
-constexpr uint32_t kColST = 0, kColDP = 128, kColDV = 256, kColDK = 320, kColDQ = 384;
+// TMEM columns: S^T [0,128), dP^T [128,256), dV [256,320), dK [320,384), dQ [384,448),
+// P^T (bf16 pairs, the TS A operand of dV += P^T dO) [448,512)
+constexpr uint32_t kColST = 0, kColDP = 128, kColDV = 256, kColDK = 320, kColDQ = 384,
+                   kColPT = 448;
 
 struct BwdParams {
     int sq, sk, H;
@@ -439,9 +441,11 @@ attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
     uint64_t *kv_full = bars;
     uint64_t *qd_full = bars + 1, *qd_empty = qd_full + 2;
     uint64_t *s_full = qd_empty + 2, *s_free = s_full + 1;
-    uint64_t *p_full = s_free + 1, *p_empty = p_full + 2;   // p_empty: single P/dS buffer
-    uint64_t *dq_full = p_empty + 1, *dq_empty = dq_full + 2;
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(dq_empty + 2);
+    uint64_t *p_full = s_free + 1;                          // P^T + dS^T(b) written
+    uint64_t *pv_empty = p_full + 2;                        // dV done with P^T (TMEM)
+    uint64_t *ds_empty = pv_empty + 1;                      // dK + dQ done with dS^T(b)
+    uint64_t *dq_full = ds_empty + 2, *dq_empty = dq_full + 1;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(dq_empty + 1);
     float *lse2_s = reinterpret_cast<float *>(smem + kB_LD);   // [2][128]
     float *delta_s = lse2_s + 256;                             // [2][128]
 
@@ -452,12 +456,13 @@ attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
                 mbar_init(&qd_full[i], 1);
                 mbar_init(&qd_empty[i], 1);
                 mbar_init(&p_full[i], 256);
-                mbar_init(&dq_full[i], 1);
-                mbar_init(&dq_empty[i], 128);
+                mbar_init(&ds_empty[i], 1);
             }
+            mbar_init(dq_full, 1);
+            mbar_init(dq_empty, 128);
             mbar_init(s_full, 1);
             mbar_init(s_free, 256);
-            mbar_init(p_empty, 1);
+            mbar_init(pv_empty, 1);
             mbar_fence_init();
             tma_prefetch(&qmap);
             tma_prefetch(&kmap);
@@ -495,6 +500,7 @@ attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
         // ===================== MMA issuer =====================
         const uint32_t id_s = idesc_bf16(kBN, kBM);           // M = keys, N = queries
         const uint32_t id_g = idesc_bf16(kBN, kD, 0, 1);      // dV / dK: A K-major, B MN-major
+                                                              // (dV: A = P^T from TMEM, TS)
         const uint32_t id_q = idesc_bf16(kBM, kD, 1, 1);      // dQ: A (dS) MN-major, B MN-major
         const uint64_t kd = sdesc_sw(smem_u32(smem + kB_K), 1024, 2);
         const uint64_t vd = sdesc_sw(smem_u32(smem + kB_V), 1024, 2);
@@ -505,32 +511,37 @@ attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
             mbar_wait(&p_full[b], (j >> 1) & 1);
             tc_fence_after();
             uint8_t *qdst = smem + kB_QD + b * 2 * kTileBytes;
-            uint8_t *ps = smem + kB_PS;
-            const uint64_t pt = sdesc_sw(smem_u32(ps), 1024, 2);
-            const uint64_t dst_k = sdesc_sw(smem_u32(ps + kPBytes), 1024, 2);
-            const uint64_t ds_mn = sdesc_mn(smem_u32(ps + kPBytes), kBM * 128, 1024, 2);
+            uint8_t *ps = smem + kB_PS + b * kPBytes;            // dS^T(b)
+            const uint64_t dst_k = sdesc_sw(smem_u32(ps), 1024, 2);
+            const uint64_t ds_mn = sdesc_mn(smem_u32(ps), kBM * 128, 1024, 2);
             const uint64_t q_mn = sdesc_mn(smem_u32(qdst), 8192, 1024, 2);
             const uint64_t do_mn = sdesc_mn(smem_u32(qdst + kTileBytes), 8192, 1024, 2);
 #pragma unroll
-            for (int k = 0; k < kBM / 16; ++k) {
+            for (int k = 0; k < kBM / 16; ++k) {   // dV += P^T dO (P^T in TMEM)
+                if (p.dbg & 4) break;
+                const uint32_t bb = (k * 16 * 128) >> 4;
+                mma_ts_e(tmem + kColDV, tmem + kColPT + k * 8, do_mn + bb, id_g,
+                         (j > 0 || k > 0) ? 1u : 0u);
+            }
+            mma_commit_e(pv_empty);                 // the softmax may overwrite P^T
+#pragma unroll
+            for (int k = 0; k < kBM / 16; ++k) {   // dK += dS^T Q
                 if (p.dbg & 4) break;
                 const uint32_t a = ((k >> 2) * (kBN * 128) + (k & 3) * 32) >> 4;
                 const uint32_t bb = (k * 16 * 128) >> 4;
-                const uint32_t acc = (j > 0 || k > 0) ? 1u : 0u;
-                mma_bf16_e(tmem + kColDV, pt + a, do_mn + bb, id_g, acc);
-                mma_bf16_e(tmem + kColDK, dst_k + a, q_mn + bb, id_g, acc);
+                mma_bf16_e(tmem + kColDK, dst_k + a, q_mn + bb, id_g, (j > 0 || k > 0) ? 1u : 0u);
             }
-            if (j >= 2) mbar_wait(&dq_empty[b], ((j >> 1) & 1) ^ 1);
+            if (j >= 1) mbar_wait(dq_empty, (j - 1) & 1);   // dQ(j-1) drained from TMEM
             tc_fence_after();
 #pragma unroll
-            for (int k = 0; k < kBN / 16; ++k) {
+            for (int k = 0; k < kBN / 16; ++k) {   // dQ = dS K
                 if (p.dbg & 4) break;
                 const uint32_t a = (k * 16 * 128) >> 4;     // 16 key rows of dS^T
-                mma_bf16_e(tmem + kColDQ + b * kD, ds_mn + a, kmn + a, id_q, k ? 1u : 0u);
+                mma_bf16_e(tmem + kColDQ, ds_mn + a, kmn + a, id_q, k ? 1u : 0u);
             }
-            mma_commit_e(p_empty);
+            mma_commit_e(&ds_empty[b]);
             mma_commit_e(&qd_empty[b]);
-            mma_commit_e(&dq_full[b]);
+            mma_commit_e(dq_full);
         };
         for (int i = 0; i < nq; ++i) {
             const int st = i & 1;
@@ -573,7 +584,7 @@ attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
             named_bar(1, 256);
             mbar_wait(s_full, i & 1);
             tc_fence_after();
-            uint8_t *ps = smem + kB_PS + rl * 128 + half * (kBN * 128);
+            uint8_t *ps = smem + kB_PS + b * kPBytes + rl * 128 + half * (kBN * 128);   // dS^T(b)
             const float *NL2 = lse2_s + b * 128 + half * 64;
             const float *Dl = delta_s + b * 128 + half * 64;
 #pragma unroll 1
@@ -588,9 +599,12 @@ attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
                 if (cc == 1) {
                     tc_fence_before();
                     mbar_arrive(s_free);   // S^T / dP^T TMEM may be overwritten
-                } else if (i >= 1) {
-                    mbar_wait(p_empty, (i - 1) & 1);   // grads(i-1) done with P^T / dS^T
+                } else {
+                    if (i >= 1) mbar_wait(pv_empty, (i - 1) & 1);         // dV(i-1) read P^T
+                    if (i >= 2) mbar_wait(&ds_empty[b], ((i - 2) >> 1) & 1);   // dS^T(b) free
+                    tc_fence_after();
                 }
+                uint32_t pall[16];
 #pragma unroll
                 for (int c = 0; c < 4; ++c) {         // 16-B chunks of 8 query columns
                     if (p.dbg & 2) break;
@@ -611,17 +625,20 @@ attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
                         dk4[e] = pack_bf16(g.x, g.y);
                     }
                     const int off = (((cc * 4 + c) ^ (rl & 7)) << 4);
-                    *reinterpret_cast<uint4 *>(ps + off) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-                    *reinterpret_cast<uint4 *>(ps + kPBytes + off) =
-                        make_uint4(dk4[0], dk4[1], dk4[2], dk4[3]);
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) pall[c * 4 + e] = pk[e];
+                    *reinterpret_cast<uint4 *>(ps + off) = make_uint4(dk4[0], dk4[1], dk4[2], dk4[3]);
                 }
+                // P^T pairs (q, q+1) -> TMEM column kColPT + q / 2 (the TS A layout)
+                if (!(p.dbg & 2)) tmem_st16(lane_base + kColPT + half * 32 + cc * 16, pall);
             }
+            tmem_wait_st();
             fence_async_smem();
             tc_fence_before();
             mbar_arrive(&p_full[b]);
         }
         // dV (half 0) / dK (half 1) += TMEM once the last gradient MMAs have landed
-        if (nq >= 1) mbar_wait(p_empty, (nq - 1) & 1);
+        if (nq >= 1) mbar_wait(&ds_empty[(nq - 1) & 1], ((nq - 1) >> 1) & 1);
         tc_fence_after();
         const int key = k0 + rl;
         const bool kv_ok = key < p.sk;
@@ -651,7 +668,7 @@ attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
         const bool leader = warp == 10;
         for (int i = 0; i < nq; ++i) {
             const int b = i & 1;
-            mbar_wait(&dq_full[b], (i >> 1) & 1);
+            mbar_wait(dq_full, i & 1);
             tc_fence_after();
             // staging tile b was last reduced 2 blocks ago: its TMA reads must be done
             if (leader && lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
@@ -659,7 +676,7 @@ attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
             uint8_t *stg = smem + kB_DQ + b * kDQStage;
             for (int c = 0; c < kD; c += 16) {
                 uint32_t a[16];
-                tmem_ld16(lane_base + kColDQ + b * kD + c, a);
+                tmem_ld16(lane_base + kColDQ + c, a);
                 tmem_wait_ld();
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
@@ -671,7 +688,7 @@ attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
                 }
             }
             tc_fence_before();
-            mbar_arrive(&dq_empty[b]);        // TMEM dQ buffer free
+            mbar_arrive(dq_empty);            // TMEM dQ free
             fence_async_smem();
             named_bar(2, 128);
             if (leader) {
