@@ -33,7 +33,21 @@ int attn_bwd_update_tc_launch(const dp_attn_geom *, const void *, const void *, 
                               cudaStream_t);
 }  // namespace dp
 
+namespace dp {
+int conv_x3_eligible(const dp_conv_geom *, int which);
+int64_t conv_x3_workspace(const dp_conv_geom *, int which);
+int conv_x3_launch(const dp_conv_geom *, int which, const void *, const void *, const void *, void *,
+                   void *, void *, int64_t, cudaStream_t);
+}  // namespace dp
+
 using namespace dp;
+
+// fp32 convs go to the bf16x3 tensor-core path (conv_x3.cu) when it covers
+// the shape (auto / tc), else to the CUDA-core kernels
+static int eligible_tc(const dp_conv_geom *g, int dtype, int which) {
+    if (dtype == DP_F32) return conv_x3_eligible(g, which);
+    return conv_tc_eligible(g, dtype, which);
+}
 
 static int pick(int algo, int eligible, const char *what) {
     if (algo == DP_ALGO_SIMT) return DP_ALGO_SIMT;
@@ -48,18 +62,21 @@ static int pick(int algo, int eligible, const char *what) {
 }
 
 extern "C" int64_t dp_conv_workspace(const dp_conv_geom *g, int dtype, int algo, int which) {
-    int a = pick(algo, conv_tc_eligible(g, dtype, which), "dp_conv_workspace");
+    int a = pick(algo, eligible_tc(g, dtype, which), "dp_conv_workspace");
     if (a < 0) return -1;
-    if (a == DP_ALGO_TC) return conv_tc_workspace(g, which);
+    if (a == DP_ALGO_TC)
+        return dtype == DP_F32 ? conv_x3_workspace(g, which) : conv_tc_workspace(g, which);
     return which == DP_CONV_WGRAD ? conv_wgrad_simt_workspace(g, dtype) : 0;
 }
 
 extern "C" int dp_conv_fwd(const dp_conv_geom *g, int dtype, int algo, const void *x,
                            const void *xh, const void *w, void *y, void *ws, int64_t ws_bytes,
                            void *stream) {
-    int a = pick(algo, conv_tc_eligible(g, dtype, DP_CONV_FWD), "dp_conv_fwd");
+    int a = pick(algo, eligible_tc(g, dtype, DP_CONV_FWD), "dp_conv_fwd");
     if (a < 0) return DP_ERR_UNSUPPORTED;
     cudaStream_t st = (cudaStream_t)stream;
+    if (a == DP_ALGO_TC && dtype == DP_F32)
+        return conv_x3_launch(g, DP_CONV_FWD, x, xh, w, y, nullptr, ws, ws_bytes, st);
     if (a == DP_ALGO_TC) return conv_fwd_tc_launch(g, x, xh, w, y, ws, ws_bytes, st);
     return conv_fwd_simt_launch(g, dtype, x, xh, w, y, st);
 }
@@ -67,9 +84,11 @@ extern "C" int dp_conv_fwd(const dp_conv_geom *g, int dtype, int algo, const voi
 extern "C" int dp_conv_dgrad(const dp_conv_geom *g, int dtype, int algo, const void *dy,
                              const void *w, void *dx, void *dxh, void *ws, int64_t ws_bytes,
                              void *stream) {
-    int a = pick(algo, conv_tc_eligible(g, dtype, DP_CONV_DGRAD), "dp_conv_dgrad");
+    int a = pick(algo, eligible_tc(g, dtype, DP_CONV_DGRAD), "dp_conv_dgrad");
     if (a < 0) return DP_ERR_UNSUPPORTED;
     cudaStream_t st = (cudaStream_t)stream;
+    if (a == DP_ALGO_TC && dtype == DP_F32)
+        return conv_x3_launch(g, DP_CONV_DGRAD, dy, nullptr, w, dx, dxh, ws, ws_bytes, st);
     if (a == DP_ALGO_TC) return conv_dgrad_tc_launch(g, dy, w, dx, dxh, ws, ws_bytes, st);
     return conv_dgrad_simt_launch(g, dtype, dy, w, dx, dxh, st);
 }
@@ -77,9 +96,11 @@ extern "C" int dp_conv_dgrad(const dp_conv_geom *g, int dtype, int algo, const v
 extern "C" int dp_conv_wgrad(const dp_conv_geom *g, int dtype, int algo, const void *x,
                              const void *xh, const void *dy, void *dw, void *ws, int64_t ws_bytes,
                              void *stream) {
-    int a = pick(algo, conv_tc_eligible(g, dtype, DP_CONV_WGRAD), "dp_conv_wgrad");
+    int a = pick(algo, eligible_tc(g, dtype, DP_CONV_WGRAD), "dp_conv_wgrad");
     if (a < 0) return DP_ERR_UNSUPPORTED;
     cudaStream_t st = (cudaStream_t)stream;
+    if (a == DP_ALGO_TC && dtype == DP_F32)
+        return conv_x3_launch(g, DP_CONV_WGRAD, x, xh, dy, dw, nullptr, ws, ws_bytes, st);
     if (a == DP_ALGO_TC) return conv_wgrad_tc_launch(g, x, xh, dy, dw, ws, ws_bytes, st);
     return conv_wgrad_simt_launch(g, dtype, x, xh, dy, dw, ws, ws_bytes, st);
 }

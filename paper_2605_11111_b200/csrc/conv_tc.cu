@@ -76,6 +76,8 @@ struct ConvTcParams {
     int wimg_bytes;
     const __nv_bfloat16 *wimg;
     int dbg;                  // profiling ablations (DP_CONV_DBG): 1 no stores, 2 no MMA, 4 no TMA
+    float *yf, *yf2;          // fp32 outputs (the bf16x3 fp32 path) instead of y / y2
+    int64_t ycs, y2cs;        // their channel strides (elements)
 };
 
 // Template arguments KP_/KQ_/KW_/CIN_ = 0 select the runtime-shaped kernel;
@@ -301,7 +303,27 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
                 }
                 tc_fence_before();
                 mbar_arrive(&tempty[slot]);
-                if (w < p.Wout && !(p.dbg & 1)) {
+                if (w < p.Wout && !(p.dbg & 1) && p.yf) {
+                    // fp32 output (bf16x3 path): any channel stride, one value per channel
+                    const int qo = q0 + j;
+                    float *dst;
+                    int64_t cs;
+                    if (p.ysplit_dim == 0 && po >= p.ysplit) {
+                        dst = p.yf2 + b * p.y2s[0] + (int64_t)(po - p.ysplit) * p.y2s[1] +
+                              (int64_t)qo * p.y2s[2] + (int64_t)w * p.y2s[3];
+                        cs = p.y2cs;
+                    } else if (p.ysplit_dim == 1 && qo >= p.ysplit) {
+                        dst = p.yf2 + b * p.y2s[0] + (int64_t)po * p.y2s[1] +
+                              (int64_t)(qo - p.ysplit) * p.y2s[2] + (int64_t)w * p.y2s[3];
+                        cs = p.y2cs;
+                    } else {
+                        dst = p.yf + b * p.ys[0] + (int64_t)po * p.ys[1] + (int64_t)qo * p.ys[2] +
+                              (int64_t)w * p.ys[3];
+                        cs = p.ycs;
+                    }
+#pragma unroll
+                    for (int c = 0; c < N; ++c) dst[c * cs] = __uint_as_float(v[c]);
+                } else if (w < p.Wout && !(p.dbg & 1)) {
                     const int qo = q0 + j;
                     __nv_bfloat16 *dst;
                     if (p.ysplit_dim == 0 && po >= p.ysplit)
@@ -429,11 +451,12 @@ struct Plan {
     int cblk, stage_bytes, wimg_bytes, nstage, smem;
 };
 
-bool make_plan(const dp_conv_geom *g, bool dgrad, Plan &pl) {
+bool make_plan(const dp_conv_geom *g, bool dgrad, Plan &pl, bool f32out = false) {
     if (!map_roles(g, dgrad, pl.R)) return false;
     pl.Cin = (int)(dgrad ? g->c_out : g->c_in);
     pl.N = pick_n((int)(dgrad ? g->c_in : g->c_out));
-    if (!pl.N || pl.Cin % 16 || pl.Cin > 128) return false;
+    if (!pl.N || pl.Cin % 16 || pl.Cin > 192) return false;
+    if (pl.Cin > 128 && !(pl.R.KP == 1 && pl.R.KQ == 3 && pl.R.KW == 3)) return false;
     const Roles &R = pl.R;
     if (R.KW > 15 || R.KQ > 7 || R.KP > 7) return false;
     if (R.KQ * pl.N > 256) return false;                 // merged-tap MMA: N <= 256
@@ -441,11 +464,13 @@ bool make_plan(const dp_conv_geom *g, bool dgrad, Plan &pl) {
     // channel stride 1 on input and output, 16-B aligned row strides
     const int64_t *is = dgrad ? g->ys : g->xs;
     const int64_t *os = dgrad ? g->xs : g->ys;
-    if (is[1] != 1 || os[1] != 1) return false;
-    if (g->halo > 0 && g->hs[1] != 1) return false;
+    if (is[1] != 1 || (!f32out && os[1] != 1)) return false;
+    // the halo block is an input in the forward (TMA: 16-B strides) and a bf16 /
+    // fp32 output in dgrad
+    if (g->halo > 0 && !(dgrad && f32out) && g->hs[1] != 1) return false;
     for (int i = 0; i < 4; ++i) {
-        if (R.xs[i] % 8 || R.ys[i] % 8) return false;
-        if (g->halo > 0 && R.hs[i] % 8) return false;
+        if (R.xs[i] % 8 || (!f32out && R.ys[i] % 8)) return false;
+        if (g->halo > 0 && !(dgrad && f32out) && R.hs[i] % 8) return false;
     }
     pl.cblk = chan_block(pl.Cin);
     pl.stage_bytes = R.KP * (pl.Cin / pl.cblk) * box_bytes(pl.cblk, R.KW);
@@ -480,6 +505,10 @@ int launch_n(const CUtensorMap &xm, const CUtensorMap &hm, const ConvTcParams &p
     if (k333 && p.Cin == 32) return launch_k<N, 3, 3, 3, 32>(xm, hm, p, grid, smem, st);
     if (k133 && p.Cin == 32) return launch_k<N, 1, 3, 3, 32>(xm, hm, p, grid, smem, st);
     if (k133 && p.Cin == 64) return launch_k<N, 1, 3, 3, 64>(xm, hm, p, grid, smem, st);
+    if constexpr (N == 16 || N == 32) {     // the bf16x3 fp32 path: 6 x 16 / 6 x 32 channels
+        if (k133 && p.Cin == 96) return launch_k<N, 1, 3, 3, 96>(xm, hm, p, grid, smem, st);
+        if (k133 && p.Cin == 192) return launch_k<N, 1, 3, 3, 192>(xm, hm, p, grid, smem, st);
+    }
     return launch_k<N, 0, 0, 0, 0>(xm, hm, p, grid, smem, st);
 }
 
@@ -495,10 +524,11 @@ int run_conv_pair(const dp_conv_geom *g, bool dgrad, const PairPlan &pl, const v
 
 int run_conv_tc(const dp_conv_geom *g, bool dgrad, const void *in, const void *in_halo,
                 const void *w, void *out, void *out2, void *ws, int64_t ws_bytes,
-                cudaStream_t st) {
+                cudaStream_t st, bool f32out = false) {
     Plan pl;
-    DP_REQUIRE(make_plan(g, dgrad, pl), DP_ERR_UNSUPPORTED, "conv_tc: outside the envelope");
-    {
+    DP_REQUIRE(make_plan(g, dgrad, pl, f32out), DP_ERR_UNSUPPORTED,
+               "conv_tc: outside the envelope");
+    if (!f32out) {
         PairPlan pp;
         if (make_pair_plan(g, dgrad, pp))
             return run_conv_pair(g, dgrad, pp, in, in_halo, w, out, out2, ws, ws_bytes, st);
@@ -557,6 +587,12 @@ int run_conv_tc(const dp_conv_geom *g, bool dgrad, const void *in, const void *i
     p.halo = dgrad ? 0 : (int)g->halo;
     p.y = (__nv_bfloat16 *)out;
     p.y2 = (__nv_bfloat16 *)(out2 ? out2 : out);
+    if (f32out) {
+        p.yf = (float *)out;
+        p.yf2 = (float *)(out2 ? out2 : out);
+        p.ycs = dgrad ? g->xs[1] : g->ys[1];
+        p.y2cs = g->hs[1];
+    }
     for (int i = 0; i < 4; ++i) {
         p.ys[i] = R.ys[i];
         p.y2s[i] = R.hs[i];
@@ -2148,6 +2184,17 @@ int64_t conv_tc_workspace(const dp_conv_geom *g, int which) {
     Plan pl;
     if (!make_plan(g, which == DP_CONV_DGRAD, pl)) return -1;
     return pl.wimg_bytes;
+}
+
+// bf16 tcgen05 conv with fp32 outputs (the bf16x3 fp32 path, conv_x3.cu)
+int64_t conv_tc_f32out_workspace(const dp_conv_geom *g, bool dgrad) {
+    Plan pl;
+    return make_plan(g, dgrad, pl, true) ? pl.wimg_bytes : -1;
+}
+int conv_tc_f32out_launch(const dp_conv_geom *g, bool dgrad, const void *in, const void *in_halo,
+                          const void *w, void *out, void *out2, void *ws, int64_t ws_bytes,
+                          cudaStream_t st) {
+    return run_conv_tc(g, dgrad, in, in_halo, w, out, out2, ws, ws_bytes, st, true);
 }
 
 int conv_fwd_tc_launch(const dp_conv_geom *g, const void *x, const void *xh, const void *w, void *y,

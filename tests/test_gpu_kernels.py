@@ -296,3 +296,54 @@ def test_conv_pair_kernel_opt_in():
                         "-k", "test_conv_tc_fwd_dgrad_vs_oracle"], env=env, capture_output=True,
                        text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+
+
+X3_CASES = [
+    # batch, cin, cout, (H, W), pad, halo rows: fp32 convs on the bf16x3 tensor-core path
+    (1, 32, 32, (40, 300), 1, 0),
+    (2, 16, 32, (21, 77), 1, 2),
+    (1, 32, 16, (9, 130), 0, 2),
+    (1, 16, 16, (12, 33), 1, 1),
+]
+
+
+@pytest.mark.parametrize("case", X3_CASES)
+def test_conv_fp32_bf16x3_vs_oracle(case):
+    """fp32 fwd / dgrad / wgrad on the tensor cores through three-way bf16
+    splits (conv_x3.cu) hold the reference's fp32 tolerance (1e-5) against the
+    fp64 oracle, over the virtual [main | halo] block."""
+    k = kernels()
+    batch, cin, cout, sp, pad, hrows = case
+    rng = np.random.default_rng(cin * 7 + sp[1])
+    full = (sp[0] + hrows, sp[1])
+    xfull = torch.tensor(rng.standard_normal((batch, cin) + full)).float()
+    w = torch.tensor(rng.standard_normal((cout, cin, 3, 3)) * 0.1).float()
+    x = xfull[:, :, :sp[0]].to(DEV).contiguous()
+    xh = xfull[:, :, sp[0]:].to(DEV).contiguous() if hrows else None
+    n0 = sp[0] + hrows - 3 + 1 + pad
+    out_sp = (n0, sp[1] + 2 * pad - 2)
+    y = torch.empty((batch, cout) + out_sp, device=DEV)
+    base = [-pad, -pad]
+    prev = k.set_algo("tc")
+    try:
+        k.conv_fwd(x, xh, w.to(DEV), y, kernel=(3, 3), stride=(1, 1), base=base, shard=0,
+                   halo_rows=hrows)
+        xr, wr = to_np(xfull).astype(np.float64), to_np(w).astype(np.float64)
+        big = np.pad(xr, [(0, 0), (0, 0), (pad, 0), (pad, pad)])
+        want = oconv.conv(big, wr, 1, 0)[:, :, :n0]
+        assert rel_err(to_np(y), want) < 1e-5
+        dy = torch.tensor(rng.standard_normal(tuple(y.shape))).float()
+        dx = torch.empty(x.shape, device=DEV)
+        dxh = torch.empty(xh.shape, device=DEV) if hrows else None
+        k.conv_dgrad(dy.to(DEV), w.to(DEV), dx, dxh, kernel=(3, 3), stride=(1, 1), base=base,
+                     shard=0, halo_rows=hrows)
+        gx, gw = oconv.conv_grads(big[:, :, :n0 + 2], wr, to_np(dy).astype(np.float64), 1, 0)
+        gx = gx[:, :, pad:, pad:pad + sp[1]]
+        got = to_np(dx) if not hrows else np.concatenate([to_np(dx), to_np(dxh)], axis=2)
+        assert rel_err(got, gx[:, :, :got.shape[2]]) < 1e-5
+        dw = torch.empty(w.shape, device=DEV)
+        k.conv_wgrad(x, xh, dy.to(DEV), dw, kernel=(3, 3), stride=(1, 1), base=base, shard=0,
+                     halo_rows=hrows)
+        assert rel_err(to_np(dw), gw) < 1e-5
+    finally:
+        k.set_algo(prev)
