@@ -1688,7 +1688,13 @@ struct WgradTsParams {
     int nx, nd, na;
     float *partial;   // [grid][96][NT]
     int dbg;          // ablations (DP_CONV_DBG): 1 no transpose, 2 no MMA, 4 no TMA
+    int pairB;        // > 0: batch b = k * pairB + bb pairs X part kTsPairX[k] with dY part
+                      // kTsPairD[k] (the bf16x3 fp32 wgrad: 6 pairings of 3 + 3 parts)
 };
+// part (hi 0, mid 1, lo 2) pairings of the bf16x3 wgrad, 2 bits per pairing k:
+// X {0,1,0,2,1,0}, dY {0,0,1,0,1,2}
+constexpr uint32_t kTsPairX = 0u | (1u << 2) | (0u << 4) | (2u << 6) | (1u << 8) | (0u << 10);
+constexpr uint32_t kTsPairD = 0u | (0u << 2) | (1u << 4) | (0u << 6) | (1u << 8) | (2u << 10);
 
 __device__ __forceinline__ void ldsm_x4_trans(uint32_t addr, uint32_t (&r)[4]) {
     asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0, %1, %2, %3}, [%4];"
@@ -1783,6 +1789,12 @@ conv_wgrad_ts_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_cons
             const int qc = r % p.n_qc; r /= p.n_qc;
             const int po = r % p.Pout;
             const int b = r / p.Pout;
+            int bx = b, bd = b;
+            if (p.pairB > 0) {
+                const int kk = b / p.pairB, bb = b % p.pairB;
+                bx = (int)((kTsPairX >> (2 * kk)) & 3u) * p.pairB + bb;
+                bd = (int)((kTsPairD >> (2 * kk)) & 3u) * p.pairB + bb;
+            }
             const int q0 = qc * p.q_chunk, q1 = min(p.Qout, q0 + p.q_chunk);
             const int nq = q1 - q0, nrows = nq + KQ - 1;
             const int w0 = p.w_lo + wt * kTsWK;
@@ -1814,10 +1826,10 @@ conv_wgrad_ts_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_cons
                         for (int cb = 0; cb < S::NBX; ++cb) {
                             const size_t off = (size_t)(kp * S::NBX + cb) * S::BOXX;
                             tma_load_5d_e(xring + (size_t)idx * S::XSLOT + off, map, &xfull[idx],
-                                          cb * S::CBX, p.base_w + w0, qcrd, pc, b);
+                                          cb * S::CBX, p.base_w + w0, qcrd, pc, bx);
                             if (mirror)
                                 tma_load_5d_e(xring + (size_t)(p.nx + idx) * S::XSLOT + off, map,
-                                              &xfull[idx], cb * S::CBX, p.base_w + w0, qcrd, pc, b);
+                                              &xfull[idx], cb * S::CBX, p.base_w + w0, qcrd, pc, bx);
                         }
                     }
                     }
@@ -1833,8 +1845,8 @@ conv_wgrad_ts_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_cons
                     }
                     mbar_expect_tx_e(&dfull[idx], dbytes);
                     uint8_t *dst = dring + (size_t)idx * kTsDSlot;
-                    tma_load_5d_e(dst, &dmap, &dfull[idx], 0, w0 - (KW - 1), q0 + s, po, b);
-                    tma_load_5d_e(dst + kTsDHalf, &dmap, &dfull[idx], 16, w0 - (KW - 1), q0 + s, po, b);
+                    tma_load_5d_e(dst, &dmap, &dfull[idx], 0, w0 - (KW - 1), q0 + s, po, bd);
+                    tma_load_5d_e(dst + kTsDHalf, &dmap, &dfull[idx], 16, w0 - (KW - 1), q0 + s, po, bd);
                 }
             }
         }
@@ -2068,7 +2080,9 @@ int launch_ts_k(const CUtensorMap &xm, const CUtensorMap &hm, const CUtensorMap 
 }
 
 int run_wgrad_ts(const dp_conv_geom *g, const TsPlan &pl, const void *x, const void *xh,
-                 const void *dy, float *dw, void *ws, int64_t ws_bytes, cudaStream_t st) {
+                 const void *dy, float *dw, void *ws, int64_t ws_bytes, cudaStream_t st,
+                 int pairB = 0) {
+    const uint64_t nb = pairB > 0 ? (uint64_t)3 * pairB : (uint64_t)g->batch;   // tensor batch
     const Roles &R = pl.R;
     DP_REQUIRE(ws_bytes >= ts_workspace(pl), DP_ERR_INVALID, "conv_wgrad_ts: workspace too small");
     const int taps = R.KP * 9;
@@ -2084,7 +2098,7 @@ int run_wgrad_ts(const dp_conv_geom *g, const TsPlan &pl, const void *x, const v
     CUtensorMap xm, hm, dm;
     {
         uint64_t dims[5] = {(uint64_t)pl.Cin, (uint64_t)R.Win, (uint64_t)R.Qin, (uint64_t)R.Pin,
-                            (uint64_t)g->batch};
+                            nb};
         uint64_t strides[4] = {(uint64_t)R.xs[3] * 2, (uint64_t)R.xs[2] * 2,
                                (uint64_t)R.xs[1] * 2, (uint64_t)R.xs[0] * 2};
         int rc = encode_tensor_map(&xm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void *>(x),
@@ -2095,7 +2109,7 @@ int run_wgrad_ts(const dp_conv_geom *g, const TsPlan &pl, const void *x, const v
     if (g->halo > 0) {
         uint64_t dims[5] = {(uint64_t)pl.Cin, (uint64_t)R.Win,
                             (uint64_t)(R.split == 1 ? g->halo : R.Qin),
-                            (uint64_t)(R.split == 0 ? g->halo : R.Pin), (uint64_t)g->batch};
+                            (uint64_t)(R.split == 0 ? g->halo : R.Pin), nb};
         uint64_t strides[4] = {(uint64_t)R.hs[3] * 2, (uint64_t)R.hs[2] * 2,
                                (uint64_t)R.hs[1] * 2, (uint64_t)R.hs[0] * 2};
         int rc = encode_tensor_map(&hm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5,
@@ -2104,7 +2118,7 @@ int run_wgrad_ts(const dp_conv_geom *g, const TsPlan &pl, const void *x, const v
     }
     {
         uint64_t dims[5] = {(uint64_t)kTsCo, (uint64_t)R.Wout, (uint64_t)R.Qout, (uint64_t)R.Pout,
-                            (uint64_t)g->batch};
+                            nb};
         uint64_t strides[4] = {(uint64_t)R.ys[3] * 2, (uint64_t)R.ys[2] * 2,
                                (uint64_t)R.ys[1] * 2, (uint64_t)R.ys[0] * 2};
         uint32_t dbox[5] = {16, (uint32_t)(kTsWK + 2), 1, 1, 1};
@@ -2123,6 +2137,7 @@ int run_wgrad_ts(const dp_conv_geom *g, const TsPlan &pl, const void *x, const v
     p.n_units = (int)pl.n_units;
     p.nx = pl.nx; p.nd = pl.nd; p.na = pl.na;
     p.partial = (float *)ws;
+    p.pairB = pairB;
     static const int dbg = getenv("DP_CONV_DBG") ? atoi(getenv("DP_CONV_DBG")) : 0;
     p.dbg = dbg;
     int rc;
@@ -2184,6 +2199,19 @@ int64_t conv_tc_workspace(const dp_conv_geom *g, int which) {
     Plan pl;
     if (!make_plan(g, which == DP_CONV_DGRAD, pl)) return -1;
     return pl.wimg_bytes;
+}
+
+// bf16x3 fp32 wgrad (conv_x3.cu): x / dy hold 3 parts each as batch blocks
+// [3B]; the 6 pairings run as batch entries of g (g->batch = 6B)
+int conv_wgrad_x3_launch(const dp_conv_geom *g, const void *x, const void *xh, const void *dy,
+                         void *dw, void *ws, int64_t ws_bytes, cudaStream_t st, int B) {
+    TsPlan tp;
+    DP_REQUIRE(make_tsplan(g, tp), DP_ERR_UNSUPPORTED, "conv_wgrad_x3: outside the envelope");
+    return run_wgrad_ts(g, tp, x, xh, dy, (float *)dw, ws, ws_bytes, st, B);
+}
+int64_t conv_wgrad_x3_workspace(const dp_conv_geom *g) {
+    TsPlan tp;
+    return make_tsplan(g, tp) ? ts_workspace(tp) : -1;
 }
 
 // bf16 tcgen05 conv with fp32 outputs (the bf16x3 fp32 path, conv_x3.cu)

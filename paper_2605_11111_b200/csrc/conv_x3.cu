@@ -10,10 +10,11 @@
 // by concatenating along the contraction:
 //   fwd    channels: X' = [xh xh xh xm xm xl] (6 C_in), W' = [wh wm wl wh wm wh]
 //   dgrad  channels: dY' = [dh dh dh dm dm dl] (6 C_out), W' split on c_out
-//   wgrad  batch:    X'' = [xh xm xh xl xm xh], dY'' = [dh dh dm dh dm dl]
-//          (pairs: xh dh, xm dh, xh dm, xl dh, xm dm, xh dl)
+//   wgrad  batch:    pairs (xh dh, xm dh, xh dm, xl dh, xm dm, xh dl)
 // (wgrad contracts over positions, so the six pairings are six batch entries
-// of a bf16 wgrad whose batch sum is the answer).  Split kernels write the
+// of a bf16 wgrad whose batch sum is the answer; X and dY hold their 3 parts
+// once as batch blocks and the TS wgrad kernel maps batch entry k to its
+// (X part, dY part) pair, conv_tc.cu kTsPairX / kTsPairD).  Split kernels write the
 // channels-last bf16 operands (a tiled transpose from the caller's fp32
 // strides); the tcgen05 kernels of conv_tc.cu run unchanged except for an
 // fp32-output epilogue.  Measured error vs fp64: ~1e-7 (tests/).
@@ -25,6 +26,9 @@ int64_t conv_tc_f32out_workspace(const dp_conv_geom *g, bool dgrad);
 int conv_tc_f32out_launch(const dp_conv_geom *g, bool dgrad, const void *in, const void *in_halo,
                           const void *w, void *out, void *out2, void *ws, int64_t ws_bytes,
                           cudaStream_t st);
+int conv_wgrad_x3_launch(const dp_conv_geom *g, const void *x, const void *xh, const void *dy,
+                         void *dw, void *ws, int64_t ws_bytes, cudaStream_t st, int B);
+int64_t conv_wgrad_x3_workspace(const dp_conv_geom *g);
 int conv_tc_eligible(const dp_conv_geom *g, int dtype, int which);
 int64_t conv_tc_workspace(const dp_conv_geom *g, int which);
 int conv_wgrad_tc_launch(const dp_conv_geom *g, const void *x, const void *xh, const void *dy,
@@ -35,9 +39,11 @@ namespace {
 constexpr int kParts = 6;
 // part index (0 = hi, 1 = mid, 2 = lo) of each concatenated block
 __constant__ int c_xpat[kParts] = {0, 0, 0, 1, 1, 2};   // activations (fwd / dgrad input)
-__constant__ int c_wpat[kParts] = {0, 1, 2, 0, 1, 0};   // weights / wgrad's X''
-__constant__ int c_dpat[kParts] = {0, 0, 1, 0, 1, 2};   // wgrad's dY''
-__constant__ int c_ppat[kParts] = {0, 1, 0, 2, 1, 0};   // wgrad's X'' (pairs with c_dpat)
+__constant__ int c_wpat[kParts] = {0, 1, 2, 0, 1, 0};   // weights
+__constant__ int c_ppat[kParts] = {0, 1, 0, 2, 1, 0};   // wgrad X'' (6 blocks, SS fallback)
+__constant__ int c_dpat[kParts] = {0, 0, 1, 0, 1, 2};   // wgrad dY'' (6 blocks, SS fallback)
+__constant__ int c_ipat[kParts] = {0, 1, 2, 0, 0, 0};   // the 3 parts once (wgrad, paired
+                                                        // in the kernel: conv_tc.cu kTsPair*)
 
 __device__ __forceinline__ void split3(float x, __nv_bfloat16 (&pt)[3]) {
     pt[0] = __float2bfloat16_rn(x);
@@ -46,45 +52,64 @@ __device__ __forceinline__ void split3(float x, __nv_bfloat16 (&pt)[3]) {
     pt[2] = __float2bfloat16_rn(r1 - __bfloat162float(pt[1]));
 }
 
-// fp32 activation [B][C][S0][S1] (any strides, spatial dims right-aligned to
-// (S0, S1); 2-D only) -> bf16 channels-last.  mode 0: channel blocks
-// out[b][s0][s1][blk*C + c] = part_{pat[blk]}; mode 1: batch blocks
-// out[blk*B + b][s0][s1][c] = part_{pat[blk]}.  Tile: 32 channels x 32
-// positions along S1 through smem (coalesced fp32 reads along S1,
-// coalesced bf16 writes along C).
-__global__ void x3_split_act(const float *__restrict__ x, int64_t B, int64_t C, int64_t S0,
-                             int64_t S1, int64_t sb, int64_t sc, int64_t s0, int64_t s1,
-                             __nv_bfloat16 *__restrict__ out, int mode, int which_pat) {
-    __shared__ float tile[32][33];
-    const int *pat = which_pat == 0 ? c_xpat : which_pat == 1 ? c_ppat : c_dpat;
-    const int64_t n1 = (S1 + 31) / 32, nc = (C + 31) / 32;
+// fp32 activation [B][C][S0][S1] (any strides, 2-D) -> bf16 channels-last.
+// mode 0: channel blocks out[b][s0][s1][blk*C + c] = part_{pat[blk]};
+// mode 1: batch blocks out[blk*B + b][s0][s1][c] = part_{pat[blk]}.
+// Tile: 32 channels x 64 positions along S1 through smem — coalesced fp32
+// reads along S1; then a thread splits 8 consecutive channels of one
+// position and writes each part as one 16-B vector (C % 8 == 0).
+__global__ void __launch_bounds__(256)
+x3_split_act(const float *__restrict__ x, int64_t B, int64_t C, int64_t S0, int64_t S1,
+             int64_t sb, int64_t sc, int64_t s0, int64_t s1, __nv_bfloat16 *__restrict__ out,
+             int mode, int which_pat) {
+    __shared__ float tile[32][65];
+    const int *pat = which_pat == 0 ? c_xpat : which_pat == 1 ? c_ipat
+                     : which_pat == 2 ? c_ppat : c_dpat;
+    const int nblk = which_pat == 1 ? 3 : kParts;
+    const int64_t n1 = (S1 + 63) / 64, nc = (C + 31) / 32;
     int64_t t = blockIdx.x;
     const int64_t t1 = t % n1; t /= n1;
     const int64_t tc = t % nc; t /= nc;
     const int64_t i0 = t % S0;
     const int64_t b = t / S0;
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;   // 32 x 8
+    const float *src = x + b * sb + i0 * s0;
+#pragma unroll
     for (int k = ty; k < 32; k += 8) {
-        const int64_t c = tc * 32 + k, i1 = t1 * 32 + tx;
-        tile[k][tx] = (c < C && i1 < S1) ? x[b * sb + c * sc + i0 * s0 + i1 * s1] : 0.f;
+        const int64_t c = tc * 32 + k;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int64_t i1 = t1 * 64 + h * 32 + tx;
+            tile[k][h * 32 + tx] = (c < C && i1 < S1) ? src[c * sc + i1 * s1] : 0.f;
+        }
     }
     __syncthreads();
-    const int64_t c = tc * 32 + tx;
-    if (c >= C) return;
-    for (int k = ty; k < 32; k += 8) {
-        const int64_t i1 = t1 * 32 + k;
-        if (i1 >= S1) continue;
-        __nv_bfloat16 pt[3];
-        split3(tile[tx][k], pt);
-        if (mode == 0) {
-            __nv_bfloat16 *o = out + ((b * S0 + i0) * S1 + i1) * (kParts * C) + c;
+    const int pos = threadIdx.x >> 2, cg = threadIdx.x & 3;   // 64 positions x 4 groups of 8
+    const int64_t i1 = t1 * 64 + pos, c0 = tc * 32 + cg * 8;
+    if (i1 >= S1 || c0 >= C) return;
+    uint32_t pk[3][4];
 #pragma unroll
-            for (int blk = 0; blk < kParts; ++blk) o[blk * C] = pt[pat[blk]];
-        } else {
+    for (int e = 0; e < 4; ++e) {
+        __nv_bfloat16 a[3], bb[3];
+        split3(tile[cg * 8 + 2 * e][pos], a);
+        split3(tile[cg * 8 + 2 * e + 1][pos], bb);
 #pragma unroll
-            for (int blk = 0; blk < kParts; ++blk)
-                out[((((int64_t)blk * B + b) * S0 + i0) * S1 + i1) * C + c] = pt[pat[blk]];
+        for (int q = 0; q < 3; ++q) {
+            __nv_bfloat162 v;
+            v.x = a[q];
+            v.y = bb[q];
+            pk[q][e] = *reinterpret_cast<uint32_t *>(&v);
         }
+    }
+#pragma unroll
+    for (int blk = 0; blk < kParts; ++blk) {
+        if (blk >= nblk) break;
+        const int q = pat[blk];
+        const uint4 v = make_uint4(pk[q][0], pk[q][1], pk[q][2], pk[q][3]);
+        __nv_bfloat16 *dst =
+            mode == 0 ? out + ((b * S0 + i0) * S1 + i1) * (kParts * C) + blk * C + c0
+                      : out + ((((int64_t)blk * B + b) * S0 + i0) * S1 + i1) * C + c0;
+        *reinterpret_cast<uint4 *>(dst) = v;
     }
 }
 
@@ -151,6 +176,13 @@ dp_conv_geom x3_geom(const dp_conv_geom *g, int which) {
     return h;
 }
 
+// the TS wgrad kernel pairs the parts itself (3 + 3 parts); other shapes run
+// the SS wgrad kernel over the 6 materialised pairings
+bool x3_wgrad_paired(const dp_conv_geom *g) {
+    const dp_conv_geom h = x3_geom(g, DP_CONV_WGRAD);
+    return conv_wgrad_x3_workspace(&h) >= 0;
+}
+
 X3Layout x3_layout(const dp_conv_geom *g, int which) {
     X3Layout L{};
     const int64_t Hin = g->in_ext[0], Win = g->in_ext[1];
@@ -165,14 +197,17 @@ X3Layout x3_layout(const dp_conv_geom *g, int which) {
         L.dy = off; off += align256(g->batch * Hout * Wout * kParts * g->c_out * 2);
         L.wimg = off; off += align256(kParts * g->c_out * g->c_in * taps * 2);
     } else {
-        L.act = off; off += align256(kParts * g->batch * Hin * Win * g->c_in * 2);
-        L.act_h = off; off += align256(kParts * g->batch * g->halo * Win * g->c_in * 2);
-        L.dy = off; off += align256(kParts * g->batch * Hout * Wout * g->c_out * 2);
+        const int64_t np = x3_wgrad_paired(g) ? 3 : kParts;   // parts once, or 6 pairings
+        L.act = off; off += align256(np * g->batch * Hin * Win * g->c_in * 2);
+        L.act_h = off; off += align256(np * g->batch * g->halo * Win * g->c_in * 2);
+        L.dy = off; off += align256(np * g->batch * Hout * Wout * g->c_out * 2);
     }
     L.inner = off;
     const dp_conv_geom h = x3_geom(g, which);
-    const int64_t in_ws = which == DP_CONV_WGRAD ? conv_tc_workspace(&h, DP_CONV_WGRAD)
-                                                 : conv_tc_f32out_workspace(&h, which == DP_CONV_DGRAD);
+    const int64_t in_ws = which != DP_CONV_WGRAD
+                              ? conv_tc_f32out_workspace(&h, which == DP_CONV_DGRAD)
+                              : (x3_wgrad_paired(g) ? conv_wgrad_x3_workspace(&h)
+                                                    : conv_tc_workspace(&h, DP_CONV_WGRAD));
     L.total = in_ws < 0 ? -1 : off + align256(in_ws);
     return L;
 }
@@ -180,7 +215,7 @@ X3Layout x3_layout(const dp_conv_geom *g, int which) {
 int launch_split(const float *x, int64_t B, int64_t C, int64_t S0, int64_t S1, const int64_t *st,
                  __nv_bfloat16 *out, int mode, int pat, cudaStream_t s) {
     if (B * C * S0 * S1 == 0) return DP_OK;
-    const int64_t blocks = B * S0 * ((C + 31) / 32) * ((S1 + 31) / 32);
+    const int64_t blocks = B * S0 * ((C + 31) / 32) * ((S1 + 63) / 64);
     DP_REQUIRE(blocks < (1ll << 31), DP_ERR_UNSUPPORTED, "x3 split: grid too large");
     x3_split_act<<<(unsigned)blocks, 256, 0, s>>>(x, B, C, S0, S1, st[0], st[1], st[2], st[3], out,
                                                   mode, pat);
@@ -193,7 +228,8 @@ int conv_x3_eligible(const dp_conv_geom *g, int which) {
     if (!g || !x3_shape_ok(g)) return 0;
     if (which == DP_CONV_WGRAD) {
         const dp_conv_geom h = x3_geom(g, which);
-        return conv_tc_eligible(&h, DP_BF16, DP_CONV_WGRAD);
+        return (conv_wgrad_x3_workspace(&h) >= 0 || conv_tc_eligible(&h, DP_BF16, DP_CONV_WGRAD))
+                   ? 1 : 0;
     }
     const dp_conv_geom h = x3_geom(g, which);
     return conv_tc_f32out_workspace(&h, which == DP_CONV_DGRAD) >= 0 ? 1 : 0;
@@ -248,19 +284,25 @@ int conv_x3_launch(const dp_conv_geom *g, int which, const void *a, const void *
     // wgrad: a = x, ah = x halo, b = dy, out = dw (fp32)
     __nv_bfloat16 *xa = (__nv_bfloat16 *)(w8 + L.act), *xha = (__nv_bfloat16 *)(w8 + L.act_h);
     __nv_bfloat16 *da = (__nv_bfloat16 *)(w8 + L.dy);
+    const bool paired = x3_wgrad_paired(g);
+    const int px = paired ? 1 : 2, pd = paired ? 1 : 3;
     int64_t sx[4] = {g->xs[0], g->xs[1], g->xs[2], g->xs[3]};
-    if ((rc = launch_split((const float *)a, g->batch, g->c_in, Hin, Win, sx, xa, 1, 1, st)))
+    if ((rc = launch_split((const float *)a, g->batch, g->c_in, Hin, Win, sx, xa, 1, px, st)))
         return rc;
     if (g->halo > 0) {
         int64_t sh[4] = {g->hs[0], g->hs[1], g->hs[2], g->hs[3]};
-        if ((rc = launch_split((const float *)ah, g->batch, g->c_in, g->halo, Win, sh, xha, 1, 1, st)))
+        if ((rc = launch_split((const float *)ah, g->batch, g->c_in, g->halo, Win, sh, xha, 1, px,
+                               st)))
             return rc;
     }
     int64_t sd[4] = {g->ys[0], g->ys[1], g->ys[2], g->ys[3]};
-    if ((rc = launch_split((const float *)b, g->batch, g->c_out, Hout, Wout, sd, da, 1, 2, st)))
+    if ((rc = launch_split((const float *)b, g->batch, g->c_out, Hout, Wout, sd, da, 1, pd, st)))
         return rc;
-    return conv_wgrad_tc_launch(&h, xa, g->halo > 0 ? xha : nullptr, da, out, w8 + L.inner,
-                                ws_bytes - L.inner, st);
+    if (!paired)
+        return conv_wgrad_tc_launch(&h, xa, g->halo > 0 ? xha : nullptr, da, out, w8 + L.inner,
+                                    ws_bytes - L.inner, st);
+    return conv_wgrad_x3_launch(&h, xa, g->halo > 0 ? xha : nullptr, da, out, w8 + L.inner,
+                                ws_bytes - L.inner, st, (int)g->batch);
 }
 
 }  // namespace dp
