@@ -84,13 +84,21 @@ struct ConvTcParams {
 // non-zero values give the fully unrolled MMA issue the hot shapes use (a
 // runtime-bounded loop costs ~180 issue cycles per MMA vs ~56 of operand
 // time for N=96 — measured, scripts/umma_probe2.cu).
-template <int N, int KP_, int KQ_, int KW_, int CIN_>
+// PAIR: the CTA pair of a (2,1,1) cluster runs M = 256 tcgen05.mma.cta_group::2
+// over two adjacent 128-voxel W tiles (CTA r holds tile 2 wp + r: its A rows,
+// its half of the B columns, its D rows); only the even CTA issues MMAs.  Per
+// CTA an N = 96 MMA then reads 4 KB of A + 1.5 KB of B (compute-bound, 48
+// cycles) instead of 4 KB + 3 KB (shared-memory-bound, 56 cycles).
+template <int N, int KP_, int KQ_, int KW_, int CIN_, bool PAIR = false>
 __global__ void __launch_bounds__(kThreads, 1)
 conv_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap hmap,
                const ConvTcParams p) {
     using namespace tc;
     extern __shared__ __align__(1024) uint8_t smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = PAIR ? cluster_ctarank() : 0u;
+    const int u0 = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;          // first unit
+    const int ustep = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
     constexpr bool kStatic = KP_ > 0;
     const int KP = kStatic ? KP_ : p.KP;
     const int KQ = kStatic ? KQ_ : p.KQ;
@@ -114,9 +122,10 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + NSLOT);
 
     // weights: global image -> smem once per CTA (generic proxy), then fence
+    // (PAIR: this CTA's half of the B columns, image [rank][...])
+    const uint8_t *wsrc = reinterpret_cast<const uint8_t *>(p.wimg) + (size_t)rank * p.wimg_bytes;
     for (int i = threadIdx.x * 16; i < p.wimg_bytes; i += kThreads * 16)
-        *reinterpret_cast<int4 *>(wsm + i) =
-            *reinterpret_cast<const int4 *>(reinterpret_cast<const uint8_t *>(p.wimg) + i);
+        *reinterpret_cast<int4 *>(wsm + i) = *reinterpret_cast<const int4 *>(wsrc + i);
     fence_async_smem();
     if (warp == 0) {
         if (lane == 0) {
@@ -126,17 +135,19 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
             }
             for (int i = 0; i < NSLOT; ++i) {
                 mbar_init(&tfull[i], 1);
-                mbar_init(&tempty[i], 128);
+                mbar_init(&tempty[i], PAIR ? 8 : 128);   // PAIR: one arrival per warp x 2 CTAs
             }
             mbar_fence_init();
             tma_prefetch(&xmap);
             tma_prefetch(&hmap);
         }
         __syncwarp();
-        tmem_alloc(tmem_slot, 512);
+        if constexpr (PAIR) tmem_alloc2(tmem_slot, 512);
+        else tmem_alloc(tmem_slot, 512);
     }
     tc_fence_before();
     __syncthreads();
+    if constexpr (PAIR) cluster_sync();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
     if (warp >= 2) {
@@ -150,14 +161,16 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
     }
     tc_fence_before();
     __syncthreads();
+    if constexpr (PAIR) cluster_sync();
     tc_fence_after();
 
     if (warp == 0) {
         // ===================== TMA producer (whole warp, elected issue) =====================
+        const uint32_t lead_full = PAIR ? mapa_shared(smem_u32(full), 0) : 0u;
         uint32_t it = 0;
-        for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
+        for (int u = u0; u < p.n_units; u += ustep) {
             int r = u;
-            const int wt = r % p.n_wt; r /= p.n_wt;
+            const int wt = PAIR ? (r % p.n_wt) * 2 + (int)rank : r % p.n_wt; r /= p.n_wt;
             const int qc = r % p.n_qc; r /= p.n_qc;
             const int po = r % p.Pout;
             const int b = r / p.Pout;
@@ -172,7 +185,8 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
                     __syncwarp();
                     continue;
                 }
-                mbar_expect_tx_e(&full[idx], (uint32_t)(KP * NBLK * BW * ROWB));
+                if (!PAIR || rank == 0)
+                    mbar_expect_tx_e(&full[idx], (uint32_t)((PAIR ? 2 : 1) * KP * NBLK * BW * ROWB));
                 uint8_t *dst = stages + (size_t)idx * stage_bytes;
                 const int qv = p.base_q + q0 + s;
                 for (int kp = 0; kp < KP; ++kp) {
@@ -186,21 +200,38 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
                         map = &hmap;
                         qcrd = qv - p.Qin;
                     }
-                    for (int cb = 0; cb < NBLK; ++cb)
-                        tma_load_5d_e(dst + (size_t)(kp * NBLK + cb) * BOXB, map, &full[idx],
-                                      cb * CBLK, wc, qcrd, pc, b);
+                    for (int cb = 0; cb < NBLK; ++cb) {
+                        if constexpr (PAIR)
+                            tma_load_5d_2sm_e(dst + (size_t)(kp * NBLK + cb) * BOXB, map,
+                                              lead_full + idx * 8, cb * CBLK, wc, qcrd, pc, b);
+                        else
+                            tma_load_5d_e(dst + (size_t)(kp * NBLK + cb) * BOXB, map, &full[idx],
+                                          cb * CBLK, wc, qcrd, pc, b);
+                    }
                 }
             }
         }
-    } else if (warp == 1) {
+    } else if (warp == 1 && (!PAIR || rank == 0)) {
         // ===================== MMA issuer (whole warp, elected issue) =====================
-        const uint32_t idesc_one = idesc_bf16(128, N);
-        const uint32_t idesc_all = idesc_bf16(128, N * KQ);
-        const uint32_t blk = (uint32_t)KQ * N * 32;   // bytes per (kp,kw,kc) B block
+        const uint32_t idesc_one = idesc_bf16(PAIR ? 256 : 128, N);
+        const uint32_t idesc_all = idesc_bf16(PAIR ? 256 : 128, N * KQ);
+        // B blocks: single CTA: (kp,kw,kc) blocks of KQ*N rows (the per-kq MMAs use row
+        // slices); PAIR: this CTA's halves — merged blocks of KQ*N/2 rows, then per-kq
+        // blocks of N/2 rows (the two MMA shapes split their columns differently)
+        const uint32_t blk = PAIR ? (uint32_t)KQ * N * 16 : (uint32_t)KQ * N * 32;
+        const uint32_t kqblk0 = (uint32_t)(KP * KW * KC) * blk, kqblk = (uint32_t)N * 16;
         const uint64_t bdesc0 = sdesc(smem_u32(wsm), 128, 256);
         const uint64_t adesc0 = sdesc_sw(smem_u32(stages), 8 * ROWB, swz_layout(CBLK));
+        auto mma = [&](uint32_t d, uint64_t a, uint64_t b, uint32_t id) {
+            if constexpr (PAIR) mma2_bf16_e(d, a, b, id, 1u);
+            else mma_bf16_e(d, a, b, id, 1u);
+        };
+        auto commit = [&](uint64_t *bar) {
+            if constexpr (PAIR) mma2_commit_mc_e(bar);
+            else mma_commit_e(bar);
+        };
         uint32_t it = 0, row_base = 0;
-        for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
+        for (int u = u0; u < p.n_units; u += ustep) {
             int r = u / p.n_wt;
             const int qc = r % p.n_qc;
             const int q0 = qc * p.q_chunk, q1 = min(p.Qout, q0 + p.q_chunk);
@@ -231,8 +262,7 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
                                                       ((p.dbg & 16) ? kw * 8 * ROWB : kw * ROWB) +
                                                       (kc % KPB) * 32;
                                 const uint32_t boff = ((kp * KW + kw) * KC + kc) * blk;
-                                mma_bf16_e(d, adesc + (aoff >> 4), bdesc0 + (boff >> 4),
-                                           idesc_all, 1u);
+                                mma(d, adesc + (aoff >> 4), bdesc0 + (boff >> 4), idesc_all);
                             }
                 } else {
 #pragma unroll
@@ -250,30 +280,32 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
                                     const uint32_t aoff = (kp * NBLK + kc / KPB) * BOXB +
                                                           kw * ROWB + (kc % KPB) * 32;
                                     const uint32_t boff =
-                                        ((kp * KW + kw) * KC + kc) * blk + kq * (N / 8) * 256;
-                                    mma_bf16_e(d, adesc + (aoff >> 4), bdesc0 + (boff >> 4),
-                                               idesc_one, 1u);
+                                        PAIR ? kqblk0 + (((kp * KW + kw) * KC + kc) * KQ + kq) * kqblk
+                                             : ((kp * KW + kw) * KC + kc) * blk +
+                                                   kq * (N / 8) * 256;
+                                    mma(d, adesc + (aoff >> 4), bdesc0 + (boff >> 4), idesc_one);
                                 }
                     }
                 }
-                mma_commit_e(&empty[idx]);
+                commit(&empty[idx]);
                 const int jd = s - (KQ - 1);
-                if (jd >= 0 && jd < nq) mma_commit_e(&tfull[(row_base + jd) % NSLOT]);
+                if (jd >= 0 && jd < nq) commit(&tfull[(row_base + jd) % NSLOT]);
             }
             row_base += nq;
         }
-    } else {
+    } else if (warp >= 2) {
         // ===================== epilogue =====================
         const int quarter = warp & 3;
         const int m = quarter * 32 + lane;  // TMEM lane = voxel within the tile
         const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
+        const uint32_t lead_tempty = PAIR ? mapa_shared(smem_u32(tempty), 0) : 0u;
         uint32_t z[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) z[i] = 0u;
         uint32_t row_base = 0;
-        for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
+        for (int u = u0; u < p.n_units; u += ustep) {
             int r = u;
-            const int wt = r % p.n_wt; r /= p.n_wt;
+            const int wt = PAIR ? (r % p.n_wt) * 2 + (int)rank : r % p.n_wt; r /= p.n_wt;
             const int qc = r % p.n_qc; r /= p.n_qc;
             const int po = r % p.Pout;
             const int b = r / p.Pout;
@@ -302,7 +334,15 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
                     for (int i = 0; i < N; ++i) v[i] = 0u;
                 }
                 tc_fence_before();
-                mbar_arrive(&tempty[slot]);
+                if constexpr (PAIR) {
+                    __syncwarp();
+                    if (lane == 0) {
+                        if (rank == 0) mbar_arrive(&tempty[slot]);
+                        else mbar_arrive_remote(lead_tempty + slot * 8);
+                    }
+                } else {
+                    mbar_arrive(&tempty[slot]);
+                }
                 if (w < p.Wout && !(p.dbg & 1) && p.yf) {
                     // fp32 output (bf16x3 path): any channel stride, one value per channel
                     const int qo = q0 + j;
@@ -351,9 +391,11 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
     }
     tc_fence_before();
     __syncthreads();
+    if constexpr (PAIR) cluster_sync();
     if (warp == 0) {
         tc_fence_after();
-        tmem_dealloc(tmem, 512);
+        if constexpr (PAIR) tmem_dealloc2(tmem, 512);
+        else tmem_dealloc(tmem, 512);
     }
 }
 
@@ -387,6 +429,56 @@ __global__ void conv_tc_weight_image(const __nv_bfloat16 *__restrict__ w,
         else
             v = w[((int64_t)k * n_rows + n) * taps + (taps - 1 - t)];    // W[co=k][ci=n][T-1-t]
         img[e] = v;
+    }
+}
+
+// CTA-pair weight image: [rank][merged halves][per-kq halves].  Merged block
+// (kp, kw, kc): rows n = r*KQ*N/2 + nn of the KQ*N merged rows (n = kq*N + c);
+// per-kq block (kp, kw, kc, kq): rows c = r*N/2 + nn.  Canonical K-major as
+// conv_tc_weight_image; flip = the dgrad image.
+__global__ void conv_tc_weight_image_pair(const __nv_bfloat16 *__restrict__ w,
+                                          __nv_bfloat16 *__restrict__ img, int n_rows, int k_cols,
+                                          int KP, int KQ, int KW, int flip) {
+    const int KC = k_cols / 16;
+    const int taps = KP * KQ * KW;
+    const int MH = KQ * n_rows / 2, QH = n_rows / 2;          // rows per half block
+    const int nblk = KP * KW * KC;
+    const int per_cta = nblk * (MH + KQ * QH) * 16;           // elements
+    const int total = 2 * per_cta;
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
+        const int r = e / per_cta;
+        int x = e % per_cta;
+        int kq, c, bi, nn;
+        int rows;
+        if (x < nblk * MH * 16) {
+            rows = MH;
+            bi = x / (MH * 16);
+            x %= MH * 16;
+        } else {
+            x -= nblk * MH * 16;
+            rows = QH;
+            const int bj = x / (QH * 16);
+            x %= QH * 16;
+            bi = bj / KQ;
+            kq = bj % KQ;
+        }
+        const int kk = x % 8;
+        const int nn8 = (x / 8) % 8;
+        const int h = (x / 64) % 2;
+        const int g = x / 128;
+        nn = g * 8 + nn8;
+        if (rows == MH) {
+            const int n = r * MH + nn;
+            kq = n / n_rows;
+            c = n % n_rows;
+        } else {
+            c = r * QH + nn;
+        }
+        const int kc = bi % KC, kw = (bi / KC) % KW, kp = bi / (KC * KW);
+        const int k = kc * 16 + h * 8 + kk;
+        const int t = (kp * KQ + kq) * KW + kw;
+        img[e] = !flip ? w[((int64_t)c * k_cols + k) * taps + t]
+                       : w[((int64_t)k * n_rows + c) * taps + (taps - 1 - t)];
     }
 }
 
@@ -494,6 +586,48 @@ int launch_k(const CUtensorMap &xm, const CUtensorMap &hm, const ConvTcParams &p
     return launch_status("conv_tc_kernel");
 }
 
+// CTA-pair instantiation: (2, 1, 1) clusters, grid = 2 x clusters
+template <int N, int KP, int KQ, int KW, int CIN>
+int launch_k_pair(const CUtensorMap &xm, const CUtensorMap &hm, const ConvTcParams &p, int grid,
+                  int smem, cudaStream_t st) {
+    auto kern = conv_tc_kernel<N, KP, KQ, KW, CIN, true>;
+    DP_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = (size_t)smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    DP_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, xm, hm, p));
+    return launch_status("conv_tc_kernel<pair>");
+}
+
+// shapes with a CTA-pair instantiation (the hot, statically unrolled ones)
+bool pair_shape(int N, int KP, int KQ, int KW, int Cin) {
+    if (!(N == 16 || N == 32)) return false;
+    const bool k333 = KP == 3 && KQ == 3 && KW == 3, k133 = KP == 1 && KQ == 3 && KW == 3;
+    return (k333 && (Cin == 16 || Cin == 32)) ||
+           (k133 && (Cin == 32 || Cin == 64 || Cin == 96 || Cin == 192));
+}
+
+template <int N>
+int launch_n_pair(const CUtensorMap &xm, const CUtensorMap &hm, const ConvTcParams &p, int grid,
+                  int smem, cudaStream_t st) {
+    const bool k333 = p.KP == 3 && p.KQ == 3 && p.KW == 3;
+    if (k333 && p.Cin == 16) return launch_k_pair<N, 3, 3, 3, 16>(xm, hm, p, grid, smem, st);
+    if (k333 && p.Cin == 32) return launch_k_pair<N, 3, 3, 3, 32>(xm, hm, p, grid, smem, st);
+    if (p.Cin == 32) return launch_k_pair<N, 1, 3, 3, 32>(xm, hm, p, grid, smem, st);
+    if (p.Cin == 64) return launch_k_pair<N, 1, 3, 3, 64>(xm, hm, p, grid, smem, st);
+    if (p.Cin == 96) return launch_k_pair<N, 1, 3, 3, 96>(xm, hm, p, grid, smem, st);
+    return launch_k_pair<N, 1, 3, 3, 192>(xm, hm, p, grid, smem, st);
+}
+
 // Hot shapes get a fully unrolled instantiation; everything else in the
 // envelope runs the runtime-shaped kernel.
 template <int N>
@@ -538,12 +672,24 @@ int run_conv_tc(const dp_conv_geom *g, bool dgrad, const void *in, const void *i
     DP_REQUIRE(ws_bytes >= pl.wimg_bytes, DP_ERR_INVALID, "conv_tc: workspace too small");
     int64_t outs = (int64_t)g->batch * R.Pout * R.Qout * R.Wout;
     if (outs == 0) return DP_OK;
+    // CTA pairs (cta_group::2) over two adjacent W tiles when the shape has an
+    // instantiation, there are >= 2 tiles and the workspace holds both images
+    const int n_wt_all = (R.Wout + kTileW - 1) / kTileW;
+    static const bool pair_off = getenv("DP_CONV_2CTA") && getenv("DP_CONV_2CTA")[0] == '0';
+    const bool use_pair = !pair_off && n_wt_all >= 2 && sm_count() >= 2 &&
+                          pair_shape(pl.N, R.KP, R.KQ, R.KW, pl.Cin) &&
+                          ws_bytes >= 2 * (int64_t)pl.wimg_bytes;
     // weight image
     {
         int total = taps * pl.Cin * pl.N;
-        conv_tc_weight_image<<<grid_for(total, 256, 2), 256, 0, st>>>(
-            (const __nv_bfloat16 *)w, (__nv_bfloat16 *)ws, pl.N, pl.Cin, R.KP, R.KQ, R.KW,
-            dgrad ? 1 : 0);
+        if (use_pair)
+            conv_tc_weight_image_pair<<<grid_for(2 * total, 256, 2), 256, 0, st>>>(
+                (const __nv_bfloat16 *)w, (__nv_bfloat16 *)ws, pl.N, pl.Cin, R.KP, R.KQ, R.KW,
+                dgrad ? 1 : 0);
+        else
+            conv_tc_weight_image<<<grid_for(total, 256, 2), 256, 0, st>>>(
+                (const __nv_bfloat16 *)w, (__nv_bfloat16 *)ws, pl.N, pl.Cin, R.KP, R.KQ, R.KW,
+                dgrad ? 1 : 0);
         int rc = launch_status("conv_tc_weight_image");
         if (rc) return rc;
     }
@@ -603,9 +749,9 @@ int run_conv_tc(const dp_conv_geom *g, bool dgrad, const void *in, const void *i
         p.ysplit_dim = R.split;                       // rows >= main extent -> dx_halo
         p.ysplit = R.split == 0 ? (int)g->in_ext[0] : (int)g->in_ext[0];
     }
-    p.n_wt = (R.Wout + kTileW - 1) / kTileW;
-    // choose the Q chunk so the unit count balances well over the SMs
-    const int sms = sm_count();
+    p.n_wt = use_pair ? (n_wt_all + 1) / 2 : n_wt_all;   // PAIR: tile pairs
+    // choose the Q chunk so the unit count balances well over the SMs (pairs)
+    const int sms = use_pair ? sm_count() / 2 : sm_count();
     const int64_t cols = (int64_t)p.B * R.Pout * p.n_wt;
     int best_chunk = R.Qout;
     double best = -1;
@@ -637,6 +783,9 @@ int run_conv_tc(const dp_conv_geom *g, bool dgrad, const void *in, const void *i
         p.dbg = dbg;
     }
     int grid = p.n_units < sms ? p.n_units : sms;
+    if (use_pair)
+        return pl.N == 16 ? launch_n_pair<16>(xm, hm, p, 2 * grid, pl.smem, st)
+                          : launch_n_pair<32>(xm, hm, p, 2 * grid, pl.smem, st);
     switch (pl.N) {
         case 16: return launch_n<16>(xm, hm, p, grid, pl.smem, st);
         case 32: return launch_n<32>(xm, hm, p, grid, pl.smem, st);
@@ -2198,7 +2347,7 @@ int64_t conv_tc_workspace(const dp_conv_geom *g, int which) {
     }
     Plan pl;
     if (!make_plan(g, which == DP_CONV_DGRAD, pl)) return -1;
-    return pl.wimg_bytes;
+    return 2 * (int64_t)pl.wimg_bytes;   // room for the CTA-pair image ([2][...])
 }
 
 // bf16x3 fp32 wgrad (conv_x3.cu): x / dy hold 3 parts each as batch blocks
@@ -2217,7 +2366,7 @@ int64_t conv_wgrad_x3_workspace(const dp_conv_geom *g) {
 // bf16 tcgen05 conv with fp32 outputs (the bf16x3 fp32 path, conv_x3.cu)
 int64_t conv_tc_f32out_workspace(const dp_conv_geom *g, bool dgrad) {
     Plan pl;
-    return make_plan(g, dgrad, pl, true) ? pl.wimg_bytes : -1;
+    return make_plan(g, dgrad, pl, true) ? 2 * (int64_t)pl.wimg_bytes : -1;
 }
 int conv_tc_f32out_launch(const dp_conv_geom *g, bool dgrad, const void *in, const void *in_halo,
                           const void *w, void *out, void *out2, void *ws, int64_t ws_bytes,

@@ -1,4 +1,5 @@
-for d in ${DBGS:-0 1 2 4 8 14 15}; do
-  DP_CONV_DBG=$d timeout 60 python scripts/conv_time.py fwd 32 32 >> gpurun_out/pair_time.log 2>&1
+timeout 600 python -m pytest tests/test_gpu_kernels.py -q -x -k "conv" 2>&1 | tail -2
+for w in "fwd 16 32" "fwd 32 32" "dgrad 16 32" "dgrad 32 32"; do
+  for e in 0 1; do DP_CONV_2CTA=$e timeout 60 python scripts/conv_time.py $w; done
 done
-cat gpurun_out/pair_time.log
+python scripts/conv_time_f32.py
