@@ -572,15 +572,28 @@ attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
         const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
         const float2 c2 = make_float2(p.c, p.c);
         const float2 sc2 = make_float2(p.scale, p.scale);
+        // -LSE*log2(e) and D of each query block: loaded one block ahead into
+        // registers (strided, latency-bound global loads off the critical path)
+        float nl_pf = -INFINITY, d_pf = 0.f;
+        auto fetch_rows = [&](int blkq) {
+            const int qrow = blkq * kBM + tid;
+            if (tid < kBM && blkq < nq && qrow < p.sq) {
+                const size_t qi = (size_t)qrow * p.H + h;
+                nl_pf = -p.lse[qi] * kLog2e;
+                d_pf = p.delta[qi];
+            } else {
+                nl_pf = -INFINITY;
+                d_pf = 0.f;
+            }
+        };
+        fetch_rows(0);
         for (int i = 0; i < nq; ++i) {
             const int b = i & 1;
             if (tid < kBM) {
-                const int qrow = i * kBM + tid;
-                const bool qv = qrow < p.sq;
-                const size_t qi = (size_t)qrow * p.H + h;
-                lse2_s[b * 128 + tid] = qv ? -p.lse[qi] * kLog2e : -INFINITY;
-                delta_s[b * 128 + tid] = qv ? p.delta[qi] : 0.f;
+                lse2_s[b * 128 + tid] = nl_pf;
+                delta_s[b * 128 + tid] = d_pf;
             }
+            fetch_rows(i + 1);
             named_bar(1, 256);
             mbar_wait(s_full, i & 1);
             tc_fence_after();
