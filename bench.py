@@ -186,7 +186,8 @@ def max_over_ranks(ctx, value: float) -> float:
 
     if ctx.mesh.world_size == 1:
         return value
-    t = torch.tensor([value], dtype=torch.float64, device=ctx.device)
+    dev = ctx.device if dist.get_backend() == "nccl" else "cpu"   # gloo dry runs: host
+    t = torch.tensor([value], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 

@@ -161,17 +161,21 @@ class _Done:
 
 class _Pending:
     """Outstanding point-to-point works of one exchange round (buffers kept
-    alive until waited)."""
+    alive until waited; `after` = host->device copies of staged receives)."""
 
-    def __init__(self, works, keep):
+    def __init__(self, works, keep, after=()):
         self.works = works
         self.keep = keep
+        self.after = list(after)
 
     def wait(self) -> None:
         for w in self.works:
             w.wait()
+        for dst, host in self.after:
+            dst.copy_(host)
         self.works = []
         self.keep = []
+        self.after = []
 
 
 class ThreadTransport:
@@ -312,17 +316,28 @@ class DistTransport:
         dist = self.dist
         ops = []
         keep = []
+        after = []
+        # gloo carries host tensors: device payloads (the "gloo-cuda" test mesh:
+        # several processes on one GPU, where NCCL refuses duplicate devices)
+        # are staged through host memory
+        stage = self.kind != "nccl"
         for dst, t in sends:
             t = t.contiguous()
+            if stage and t.is_cuda:
+                t = t.cpu()
             keep.append(t)
             ops.append(dist.P2POp(dist.isend, t, dst))
         for src, out in recvs:
+            if stage and out.is_cuda:
+                host = torch.empty(out.shape, dtype=out.dtype)
+                after.append((out, host))
+                out = host
             ops.append(dist.P2POp(dist.irecv, out, src))
         if not ops:
             return _Done()
         if self.kind == "nccl":
             return _Pending(dist.batch_isend_irecv(ops), keep)
-        return _Pending([op.op(op.tensor, op.peer) for op in ops], keep)
+        return _Pending([op.op(op.tensor, op.peer) for op in ops], keep, after)
 
     def exchange(self, sends, recvs) -> None:
         self.exchange_start(sends, recvs).wait()
@@ -342,10 +357,11 @@ class DistTransport:
 
     def all_reduce(self, members, me: int, t: torch.Tensor, op: str) -> torch.Tensor:
         dist = self.dist
-        out = t.clone()
+        staged = self.kind != "nccl" and t.is_cuda
+        out = t.cpu() if staged else t.clone()
         rop = dist.ReduceOp.SUM if op == "sum" else dist.ReduceOp.MAX
         dist.all_reduce(out, op=rop, group=self.groups[tuple(members)])
-        return out
+        return out.to(t.device) if staged else out
 
     def barrier(self, members, me: int) -> None:
         self.dist.barrier(group=self.meta_groups[tuple(members)])
@@ -711,14 +727,15 @@ def _proc_main(rank, world, port, mesh_shape, names, fn, seed, timeout, backend,
     try:
         os.environ["MASTER_ADDR"] = "127.0.0.1"
         os.environ["MASTER_PORT"] = str(port)
-        if backend == "nccl":
+        on_gpu = backend in ("nccl", "gloo-cuda")
+        pg_backend = "gloo" if backend == "gloo-cuda" else backend
+        if on_gpu:
             torch.cuda.set_device(rank % torch.cuda.device_count())
-        dist.init_process_group(backend, rank=rank, world_size=world,
+        dist.init_process_group(pg_backend, rank=rank, world_size=world,
                                 timeout=datetime.timedelta(seconds=max(timeout, 1.0)))
         mesh = DeviceMesh(mesh_shape, names)
-        dev = torch.device("cuda", torch.cuda.current_device()) if backend == "nccl" \
-            else torch.device("cpu")
-        ctx = RankContext(mesh, rank, DistTransport(mesh, rank, backend), seed=seed, device=dev)
+        dev = torch.device("cuda", torch.cuda.current_device()) if on_gpu else torch.device("cpu")
+        ctx = RankContext(mesh, rank, DistTransport(mesh, rank, pg_backend), seed=seed, device=dev)
         res = _to_host(fn(ctx))
         out_q.put((rank, "ok", pickle.dumps(res)))
     except BaseException as exc:  # noqa: BLE001
@@ -786,8 +803,11 @@ def spawn_mesh(shape, axis_names, fn, *, seed: int = 0, timeout: float | None = 
 
     backend "thread" (default, the reference's model — domainpar/mesh.py:420)
     runs every rank as a thread of this process on `device` (default: the
-    current CUDA device, else CPU).  "nccl" launches one process per GPU and
-    "gloo" one CPU process per rank; their fn must be picklable and results
+    current CUDA device, else CPU).  "nccl" launches one process per GPU,
+    "gloo" one CPU process per rank, and "gloo-cuda" one process per rank that
+    all share the GPU (device payloads staged through host memory: the
+    multi-process path with real kernels on a one-GPU box); their fn must be
+    picklable and results
     come back on the host.  Any rank failing surfaces as one MeshError naming
     the primary failure(s).
     """
@@ -795,7 +815,7 @@ def spawn_mesh(shape, axis_names, fn, *, seed: int = 0, timeout: float | None = 
     tmo = _resolve_timeout(timeout)
     if backend == "thread":
         return _spawn_threads(mesh, fn, seed, tmo, device)
-    if backend in ("nccl", "gloo"):
+    if backend in ("nccl", "gloo", "gloo-cuda"):
         return _spawn_procs(mesh, fn, seed, tmo, backend)
     raise DimensionError(f"unknown mesh backend {backend!r}")
 
@@ -813,18 +833,25 @@ def init_mesh(shape=None, axis_names=("domain",), *, seed: int = 0,
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", str(rank)))
     if backend is None:
-        backend = "nccl" if torch.cuda.is_available() else "gloo"
+        # DP_MESH_BACKEND=gloo-cuda: ranks share the visible GPU(s) over gloo
+        # (a multi-process dry run of the N-GPU path on a one-GPU box)
+        backend = os.environ.get("DP_MESH_BACKEND") or (
+            "nccl" if torch.cuda.is_available() else "gloo")
     if shape is None:
         shape = (world,)
     mesh = DeviceMesh(tuple(shape), tuple(axis_names))
     if mesh.world_size != world:
         raise DimensionError(f"mesh {mesh.shape} needs {mesh.world_size} ranks, world is {world}")
-    if backend == "nccl":
+    gpu_gloo = backend == "gloo-cuda"
+    if gpu_gloo:
+        backend = "gloo"
+        local = local % torch.cuda.device_count()
+    if backend == "nccl" or gpu_gloo:
         torch.cuda.set_device(local)
     if not dist.is_initialized():
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ.setdefault("MASTER_PORT", "29533")
         dist.init_process_group(backend, rank=rank, world_size=world,
                                 timeout=datetime.timedelta(seconds=_resolve_timeout(None) * 20))
-    dev = torch.device("cuda", local) if backend == "nccl" else torch.device("cpu")
+    dev = torch.device("cuda", local) if (backend == "nccl" or gpu_gloo) else torch.device("cpu")
     return RankContext(mesh, rank, DistTransport(mesh, rank, backend), seed=seed, device=dev)
