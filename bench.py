@@ -546,7 +546,13 @@ def setup_cfg5(ctx):
             "bytes_received_per_rank": {"to_replicate": (n - ext[me]) * n * 4,
                                         "to_shard1": (n - ext[me]) * (n // R) * 4},
             "l2": "1 GiB tensor exceeds L2, no flush"}
+    # algorithmic HBM bytes of this rank's step: read its input block once and
+    # write each output once (S(0) -> R: the whole [n, n]; S(0) -> S(1): [n, n/R])
+    cshare = dp.default_chunk(n, R)[me]
+    hbm = (ext[me] * n + n * n) * 4 + (ext[me] * n + n * cshare) * 4
+    info["hbm_bytes_per_step"] = hbm
     return dict(step=step, inputs=[local], flops=0.0, info=info, scaling="strong", dtype="f32",
+                hbm_bytes_per_step=hbm,
                 unit="samples/s", samples_per_step=1)
 
 
@@ -795,6 +801,16 @@ def main():
     # dominant kernel
     dom = max(ksum.items(), key=lambda kv: kv[1]["ms"]) if ksum else None
     roof = None
+    if not dom and W.get("hbm_bytes_per_step"):
+        # data-movement workload (cfg5): the pack / unpack / copy kernels are the
+        # step; algorithmic HBM bytes (read + write of every element moved) per
+        # device-timed step against the measured copy bandwidth
+        gbs = W["hbm_bytes_per_step"] / (ms / 1000.0) / 1e9
+        hbm = pk.get("hbm_gbs", PEAKS_FALLBACK["hbm_gbs"])
+        roof = {"bound": "hbm", "kernel": "copy_rows (redistribute pack / unpack)",
+                "achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": gbs / hbm,
+                "traffic": None, "peak_kind": f"{pk_kind} HBM copy bandwidth",
+                "bytes_per_step": W["hbm_bytes_per_step"]}
     if dom:
         name, d = dom
         avg_ms = d["ms"] / d["launches"]
