@@ -220,3 +220,47 @@ def test_redistribute_bitexact_vs_reference(i):
         want = REDIST[f"d{i}_local{rank}"]
         assert tuple(loc.shape) == want.shape
         assert np.array_equal(to_np(loc), want)  # bit-exact
+
+
+def test_two_d_mesh_data_x_domain():
+    """(data, domain) = (2, 2) mesh: halo conv and ring attention use the
+    domain-axis group only (domainpar/ops.py:328-338); dW is
+    then averaged over the data axis (ddp_allreduce_grads, ops.py:429-444)."""
+    m = dp()
+    rng = np.random.default_rng(9)
+    x = rng.standard_normal((1, 16, 12, 6, 40))
+    w = rng.standard_normal((32, 16, 3, 3, 3)) * 0.1
+    q, k, v = (rng.standard_normal((300, 2, 64)) for _ in range(3))
+    xt = torch.tensor(x).to(torch.bfloat16)
+    wt = torch.tensor(w).to(torch.bfloat16)
+    qt, kt, vt = (torch.tensor(a).to(torch.bfloat16) for a in (q, k, v))
+
+    def prog(ctx):
+        root = ctx.rank_id == 0
+        pl = (m.Replicate(), m.Shard(2))
+        st = m.scatter_global(ctx, xt if root else None, pl, {1: (7, 5)})
+        st = m.ShardTensor(st.local.contiguous(memory_format=torch.channels_last_3d),
+                           st.global_shape, ctx, st.placements, st.shard_shapes)
+        before = ctx.collective_count
+        y, tape = m.halo_conv_forward(st, wt.to(DEV), 1, 1)
+        assert ctx.collective_count - before == 1
+        o_ext = y.shard_shapes[1]
+        lo = sum(o_ext[:ctx.coords[1]])
+        dyl = torch.ones((1, 32, o_ext[ctx.coords[1]], 6, 40), dtype=torch.bfloat16,
+                         device=DEV).contiguous(memory_format=torch.channels_last_3d)
+        _, dw = m.halo_conv_backward(tape, dyl)
+        dw_mean = m.ddp_allreduce_grads(ctx.axis_group("data"), [dw])[0]
+        apl = (m.Replicate(), m.Shard(0))
+        qs, ks, vs = (m.scatter_global(ctx, t if root else None, apl, {1: (120, 180)})
+                      for t in (qt, kt, vt))
+        o = m.ring_attention(qs, ks, vs)
+        return y.full_tensor(), o.full_tensor(), dw, dw_mean, lo
+
+    res = m.spawn_mesh((2, 2), ("data", "domain"), prog)
+    xr, wr = to_np(xt).astype(np.float64), to_np(wt).astype(np.float64)
+    want_y = oconv.conv(xr, wr, 1, 1)
+    want_o = oatt.sdpa(*(to_np(t).astype(np.float64) for t in (qt, kt, vt)))
+    for y, o, dw, dw_mean, _ in res:
+        assert rel_err(to_np(y), want_y) < 1e-2
+        assert rel_err(to_np(o), want_o) < 1.5e-2
+        assert rel_err(to_np(dw_mean), to_np(dw)) < 1e-6   # data replicas agree
