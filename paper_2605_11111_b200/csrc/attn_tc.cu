@@ -580,7 +580,7 @@ attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
             if (tid < kBM && blkq < nq && qrow < p.sq) {
                 const size_t qi = (size_t)qrow * p.H + h;
                 nl_pf = -p.lse[qi] * kLog2e;
-                d_pf = p.delta[qi];
+                d_pf = p.delta[qi] * p.scale;   // dS = P (scale dP - scale D)
             } else {
                 nl_pf = -INFINITY;
                 d_pf = 0.f;
@@ -631,9 +631,9 @@ attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
                                          c2, nl);
                         x.x = ex2(x.x);
                         x.y = ex2(x.y);
-                        float2 g = fadd2(make_float2(__uint_as_float(dv[qc]), __uint_as_float(dv[qc + 1])),
-                                         make_float2(-dd.x, -dd.y));
-                        g = fmul2(fmul2(x, g), sc2);
+                        const float2 g = fmul2(
+                            x, ffma2(make_float2(__uint_as_float(dv[qc]), __uint_as_float(dv[qc + 1])),
+                                     sc2, make_float2(-dd.x, -dd.y)));
                         pk[e] = pack_bf16(x.x, x.y);
                         dk4[e] = pack_bf16(g.x, g.y);
                     }
