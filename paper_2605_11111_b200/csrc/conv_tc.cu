@@ -1612,22 +1612,17 @@ conv_wgrad_tc_kernel(const __grid_constant__ CUtensorMap xmap,
 // dw[co][ci][kp][kq][kw] = sum_cta partial[cta][row][kw*N + co], row = (kq*KP + kp)*Cin + ci
 __global__ void wgrad_tc_reduce(const float *__restrict__ part, float *__restrict__ dw, int ctas,
                                 int n_mt, int KP, int KQ, int KW, int Cin, int N) {
-    const int taps = KP * KQ * KW;
-    const int total = N * Cin * taps;
     const int NT = KW * N;
-    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
-        int r = e;
-        const int kw = r % KW; r /= KW;
-        const int kq = r % KQ; r /= KQ;
-        const int kp = r % KP; r /= KP;
-        const int ci = r % Cin;
-        const int co = r / Cin;
-        const int row = (kq * KP + kp) * Cin + ci;
-        const size_t per_cta = (size_t)n_mt * 128 * NT;
-        const size_t off = (size_t)row * NT + kw * N + co;
+    const int total = KQ * KP * Cin * NT;          // real rows, partial layout order (coalesced)
+    const size_t per_cta = (size_t)n_mt * 128 * NT;
+    for (int o = blockIdx.x * blockDim.x + threadIdx.x; o < total; o += gridDim.x * blockDim.x) {
+        const int row = o / NT, col = o % NT;
+        const int kw = col / N, co = col % N;
+        const int ci = row % Cin, kqkp = row / Cin;
+        const int kp = kqkp % KP, kq = kqkp / KP;
         float s = 0.f;
-        for (int c = 0; c < ctas; ++c) s += part[c * per_cta + off];
-        dw[e] = s;
+        for (int c = 0; c < ctas; ++c) s += part[c * per_cta + o];
+        dw[(((co * Cin + ci) * KP + kp) * KQ + kq) * KW + kw] = s;
     }
 }
 
@@ -2125,19 +2120,16 @@ __global__ void wgrad_ts_reduce(const float *__restrict__ part, float *__restric
                                 int KP, int Cin) {
     const int KQ = 3, KW = 3;
     const int NT = KQ * KP * Cin;
-    const int total = kTsCo * Cin * KP * KQ * KW;
-    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
-        int r = e;
-        const int kw = r % KW; r /= KW;
-        const int kq = r % KQ; r /= KQ;
-        const int kp = r % KP; r /= KP;
-        const int ci = r % Cin;
-        const int co = r / Cin;
-        const size_t off = (size_t)(kw * 32 + co) * NT + (kq * KP + kp) * Cin + ci;
-        const size_t per_cta = (size_t)96 * NT;
+    const int total = 96 * NT;            // partial layout order: coalesced reads
+    const size_t per_cta = (size_t)total;
+    for (int o = blockIdx.x * blockDim.x + threadIdx.x; o < total; o += gridDim.x * blockDim.x) {
+        const int kwco = o / NT, col = o % NT;
+        const int kw = kwco / 32, co = kwco % 32;
+        const int ci = col % Cin, kqkp = col / Cin;
+        const int kp = kqkp % KP, kq = kqkp / KP;
         float s = 0.f;
-        for (int c = 0; c < ctas; ++c) s += part[c * per_cta + off];
-        dw[e] = s;
+        for (int c = 0; c < ctas; ++c) s += part[c * per_cta + o];
+        dw[(((co * Cin + ci) * KP + kp) * KQ + kq) * KW + kw] = s;
     }
 }
 
@@ -2298,7 +2290,7 @@ int run_wgrad_ts(const dp_conv_geom *g, const TsPlan &pl, const void *x, const v
              : pl.Cin == 32 ? launch_ts_k<32, 1>(xm, hm, dm, p, pl.grid, pl.smem, st)
                             : launch_ts_k<64, 1>(xm, hm, dm, p, pl.grid, pl.smem, st);
     if (rc) return rc;
-    const int total = kTsCo * pl.Cin * taps;
+    const int total = 96 * 3 * R.KP * pl.Cin;
     wgrad_ts_reduce<<<grid_for(total, 256, 4), 256, 0, st>>>((const float *)ws, dw, pl.grid, R.KP,
                                                              pl.Cin);
     return launch_status("wgrad_ts_reduce");
