@@ -572,35 +572,38 @@ attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
         const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
         const float2 c2 = make_float2(p.c, p.c);
         const float2 sc2 = make_float2(p.scale, p.scale);
-        // -LSE*log2(e) and D of each query block: loaded one block ahead into
-        // registers (strided, latency-bound global loads off the critical path)
-        float nl_pf = -INFINITY, d_pf = 0.f;
+        // LSE and D of each query block: loaded one block ahead into registers
+        // (strided, latency-bound global loads off the critical path; the
+        // transforms are applied at the smem store one iteration later, so no
+        // instruction consumes the loads before then)
+        float l_pf = INFINITY, d_pf = 0.f;
         auto fetch_rows = [&](int blkq) {
             const int qrow = blkq * kBM + tid;
+            if ((p.dbg & 32) && blkq > 0) return;
+            l_pf = INFINITY;
+            d_pf = 0.f;
             if (tid < kBM && blkq < nq && qrow < p.sq) {
                 const size_t qi = (size_t)qrow * p.H + h;
-                nl_pf = -p.lse[qi] * kLog2e;
-                d_pf = p.delta[qi] * p.scale;   // dS = P (scale dP - scale D)
-            } else {
-                nl_pf = -INFINITY;
-                d_pf = 0.f;
+                l_pf = __ldg(p.lse + qi);
+                d_pf = __ldg(p.delta + qi);
             }
         };
         fetch_rows(0);
         for (int i = 0; i < nq; ++i) {
             const int b = i & 1;
             if (tid < kBM) {
-                lse2_s[b * 128 + tid] = nl_pf;
-                delta_s[b * 128 + tid] = d_pf;
+                lse2_s[b * 128 + tid] = -l_pf * kLog2e;
+                delta_s[b * 128 + tid] = d_pf * p.scale;   // dS = P (scale dP - scale D)
             }
             fetch_rows(i + 1);
-            named_bar(1, 256);
+            if (!(p.dbg & 128)) named_bar(1, 256);
             mbar_wait(s_full, i & 1);
             tc_fence_after();
             uint8_t *ps = smem + kB_PS + b * kPBytes + rl * 128 + half * (kBN * 128);   // dS^T(b)
             const float *NL2 = lse2_s + b * 128 + half * 64;
             const float *Dl = delta_s + b * 128 + half * 64;
-#pragma unroll 1
+            uint32_t pall[32];
+#pragma unroll
             for (int cc = 0; cc < 2; ++cc) {          // 32 query columns at a time
                 uint32_t sv[32], dv[32];
                 const uint32_t col = half * 64 + cc * 32;
@@ -613,11 +616,8 @@ attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
                     tc_fence_before();
                     mbar_arrive(s_free);   // S^T / dP^T TMEM may be overwritten
                 } else {
-                    if (i >= 1) mbar_wait(pv_empty, (i - 1) & 1);         // dV(i-1) read P^T
                     if (i >= 2) mbar_wait(&ds_empty[b], ((i - 2) >> 1) & 1);   // dS^T(b) free
-                    tc_fence_after();
                 }
-                uint32_t pall[16];
 #pragma unroll
                 for (int c = 0; c < 4; ++c) {         // 16-B chunks of 8 query columns
                     if (p.dbg & 2) break;
@@ -639,11 +639,18 @@ attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
                     }
                     const int off = (((cc * 4 + c) ^ (rl & 7)) << 4);
 #pragma unroll
-                    for (int e = 0; e < 4; ++e) pall[c * 4 + e] = pk[e];
+                    for (int e = 0; e < 4; ++e) pall[cc * 16 + c * 4 + e] = pk[e];
                     *reinterpret_cast<uint4 *>(ps + off) = make_uint4(dk4[0], dk4[1], dk4[2], dk4[3]);
                 }
-                // P^T pairs (q, q+1) -> TMEM column kColPT + q / 2 (the TS A layout)
-                if (!(p.dbg & 2)) tmem_st16(lane_base + kColPT + half * 32 + cc * 16, pall);
+            }
+            // P^T pairs (q, q+1) -> TMEM column kColPT + q / 2 (the TS A layout).
+            // Written last: dV(i-1), issued when block i-1's softmax finished,
+            // has had this whole block's softmax math to read the previous P^T.
+            if (i >= 1 && !(p.dbg & 64)) mbar_wait(pv_empty, (i - 1) & 1);
+            tc_fence_after();
+            if (!(p.dbg & 2)) {
+                tmem_st16(lane_base + kColPT + half * 32, *reinterpret_cast<uint32_t(*)[16]>(pall));
+                tmem_st16(lane_base + kColPT + half * 32 + 16, *reinterpret_cast<uint32_t(*)[16]>(pall + 16));
             }
             tmem_wait_st();
             fence_async_smem();
