@@ -24,6 +24,7 @@
 // 128-B swizzle (K-major A/B of S = Q K^T); V lands the same way and is
 // read as the MN-major B operand of P V; P is written K-major SW128.
 #include "tc_common.cuh"
+#include <cstdio>
 
 namespace dp {
 namespace {
@@ -393,18 +394,28 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
 //              math); at the end dV (half 0) / dK (half 1) += TMEM
 //   warps 10-13 thread = query row: dQ tile TMEM -> swizzled fp32 smem ->
 //              TMA bulk reduce-add (cp.reduce.async.bulk.tensor .add) into dq
-//              (per-thread float4 atomics cost 34 of 84 ms at 64k)
+//              (per-thread float4 atomics cost 34 of 84 ms at 64k); they also
+//              stage each query block's -LSE*log2(e) / scale*D rows into a
+//              smem ring two blocks ahead (mbarrier hand-off, so the softmax
+//              warps never wait on global loads or a CTA-wide barrier)
 // The next block's S^T / dP^T MMAs are issued before this block's gradient
-// MMAs, so the softmax warps overlap the tensor pipe.
+// MMAs, so the softmax warps overlap the tensor pipe; a Q / dO stage is
+// released once dK has read it (dQ only needs dS and K).
+// Debug: DP_ATTN_TRACE=1 prints CTA 0's per-block event clocks (the timeline
+// behind these choices), DP_ATTN_DBG=<bits> the ablations listed in BwdParams.
 constexpr int kBwdThreads = 448;   // TMA, MMA, 8 softmax warps, 4 dQ warps
 constexpr int kB_K = 0, kB_V = kTileBytes;
-constexpr int kB_QD = 2 * kTileBytes;                  // 2 stages of [Q | dO]
-constexpr int kB_PS = kB_QD + 2 * 2 * kTileBytes;      // dS^T x 2 (double buffer)
-constexpr int kB_DQ = kB_PS + 2 * kPBytes;             // 2 dQ staging tiles (fp32, 2 x 16 KB)
+constexpr int kQDStages = 2;                           // [Q | dO] ring (a stage frees when
+                                                       // the block's dK MMAs complete)
+constexpr int kB_QD = 2 * kTileBytes;
+constexpr int kB_PS = kB_QD + kQDStages * 2 * kTileBytes;  // dS^T x 2 (double buffer)
+constexpr int kB_DQ = kB_PS + 2 * kPBytes;             // 2 dQ staging tiles (fp32, 2 x 16 KB halves)
 constexpr int kDQStage = kBM * kD * 4;                 // 32 KB
-constexpr int kB_LD = kB_DQ + 2 * kDQStage;            // -lse2[2][128], delta[2][128]
-constexpr int kB_BAR = kB_LD + 4 * 128 * 4;
+constexpr int kLDBufs = 2;                             // -lse2 / scale*D ring (dQ warps -> softmax)
+constexpr int kB_LD = kB_DQ + 2 * kDQStage;                // -lse2[2][128], delta[2][128]
+constexpr int kB_BAR = kB_LD + 2 * kLDBufs * 128 * 4;
 constexpr int kSmemBwd = kB_BAR + 256;
+static_assert(kSmemBwd <= 232448, "attention bwd smem");
 // TMEM columns: S^T [0,128), dP^T [128,256), dV [256,320), dK [320,384), dQ [384,448),
 // P^T (bf16 pairs, the TS A operand of dV += P^T dO) [448,512)
 constexpr uint32_t kColST = 0, kColDP = 128, kColDV = 256, kColDK = 320, kColDQ = 384,
@@ -420,7 +431,14 @@ struct BwdParams {
     float *dk, *dv;            // [sk, H, 64] (+=)
     int dbg;                   // DP_ATTN_DBG ablations: 1 no dQ reduce, 2 no softmax math,
                                // 4 no gradient MMAs, 8 no S/dP MMAs
+    unsigned long long *trace; // DP_ATTN_TRACE: per-block event clocks of CTA 0 (debug)
 };
+
+#define BWD_TRACE(blk, ev)                                                              \
+    do {                                                                                \
+        if (p.trace && blockIdx.x == 0 && lane == 0 && (blk) >= 0 && (blk) < 64)         \
+            p.trace[(blk) * 16 + (ev)] = clock64();                                     \
+    } while (0)
 
 __device__ __forceinline__ void named_bar(int id, int n) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
@@ -439,27 +457,34 @@ attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
 
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem + kB_BAR);
     uint64_t *kv_full = bars;
-    uint64_t *qd_full = bars + 1, *qd_empty = qd_full + 2;
-    uint64_t *s_full = qd_empty + 2, *s_free = s_full + 1;
+    uint64_t *qd_full = bars + 1, *qd_empty = qd_full + kQDStages;
+    uint64_t *s_full = qd_empty + kQDStages, *s_free = s_full + 1;
     uint64_t *p_full = s_free + 1;                          // P^T + dS^T(b) written
     uint64_t *pv_empty = p_full + 2;                        // dV done with P^T (TMEM)
     uint64_t *ds_empty = pv_empty + 1;                      // dK + dQ done with dS^T(b)
     uint64_t *dq_full = ds_empty + 2, *dq_empty = dq_full + 1;
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(dq_empty + 1);
-    float *lse2_s = reinterpret_cast<float *>(smem + kB_LD);   // [2][128]
-    float *delta_s = lse2_s + 256;                             // [2][128]
+    uint64_t *ld_full = dq_empty + 1, *ld_empty = ld_full + kLDBufs;   // [kLDBufs] each
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(ld_empty + kLDBufs);
+    float *lse2_s = reinterpret_cast<float *>(smem + kB_LD);   // [kLDBufs][128]
+    float *delta_s = lse2_s + kLDBufs * 128;                   // [kLDBufs][128]
 
     if (warp == 0) {
         if (lane == 0) {
             mbar_init(kv_full, 1);
-            for (int i = 0; i < 2; ++i) {
+            for (int i = 0; i < kQDStages; ++i) {
                 mbar_init(&qd_full[i], 1);
                 mbar_init(&qd_empty[i], 1);
+            }
+            for (int i = 0; i < 2; ++i) {
                 mbar_init(&p_full[i], 256);
                 mbar_init(&ds_empty[i], 1);
             }
             mbar_init(dq_full, 1);
             mbar_init(dq_empty, 128);
+            for (int i = 0; i < kLDBufs; ++i) {
+                mbar_init(&ld_full[i], 128);   // the dQ warps' threads (one query row each)
+                mbar_init(&ld_empty[i], 8);    // one arrival per softmax warp
+            }
             mbar_init(s_full, 1);
             mbar_init(s_free, 256);
             mbar_init(pv_empty, 1);
@@ -484,8 +509,9 @@ attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
         tma_load_3d_e(smem + kB_K, &kmap, kv_full, 0, h, k0);
         tma_load_3d_e(smem + kB_V, &vmap, kv_full, 0, h, k0);
         for (int i = 0; i < nq; ++i) {
-            const int st = i & 1;
-            mbar_wait(&qd_empty[st], ((i >> 1) & 1) ^ 1);
+            const int st = i % kQDStages;
+            mbar_wait(&qd_empty[st], ((i / kQDStages) & 1) ^ 1);
+            BWD_TRACE(i, 14);
             if (p.dbg & 16) {
                 if (lane == 0) mbar_arrive(&qd_full[st]);
                 __syncwarp();
@@ -509,8 +535,10 @@ attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
         auto issue_grads = [&](int j) {
             const int b = j & 1;
             mbar_wait(&p_full[b], (j >> 1) & 1);
+            BWD_TRACE(j, 1);
             tc_fence_after();
-            uint8_t *qdst = smem + kB_QD + b * 2 * kTileBytes;
+            const int qs = j % kQDStages;
+            uint8_t *qdst = smem + kB_QD + qs * 2 * kTileBytes;
             uint8_t *ps = smem + kB_PS + b * kPBytes;            // dS^T(b)
             const uint64_t dst_k = sdesc_sw(smem_u32(ps), 1024, 2);
             const uint64_t ds_mn = sdesc_mn(smem_u32(ps), kBM * 128, 1024, 2);
@@ -524,6 +552,7 @@ attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
                          (j > 0 || k > 0) ? 1u : 0u);
             }
             mma_commit_e(pv_empty);                 // the softmax may overwrite P^T
+            BWD_TRACE(j, 3);
 #pragma unroll
             for (int k = 0; k < kBM / 16; ++k) {   // dK += dS^T Q
                 if (p.dbg & 4) break;
@@ -531,7 +560,10 @@ attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
                 const uint32_t bb = (k * 16 * 128) >> 4;
                 mma_bf16_e(tmem + kColDK, dst_k + a, q_mn + bb, id_g, (j > 0 || k > 0) ? 1u : 0u);
             }
+            mma_commit_e(&qd_empty[qs]);            // Q / dO(j) no longer read (dQ uses dS, K)
+            BWD_TRACE(j, 8);
             if (j >= 1) mbar_wait(dq_empty, (j - 1) & 1);   // dQ(j-1) drained from TMEM
+            BWD_TRACE(j, 2);
             tc_fence_after();
 #pragma unroll
             for (int k = 0; k < kBN / 16; ++k) {   // dQ = dS K
@@ -540,13 +572,15 @@ attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
                 mma_bf16_e(tmem + kColDQ, ds_mn + a, kmn + a, id_q, k ? 1u : 0u);
             }
             mma_commit_e(&ds_empty[b]);
-            mma_commit_e(&qd_empty[b]);
             mma_commit_e(dq_full);
+            BWD_TRACE(j, 11);
         };
         for (int i = 0; i < nq; ++i) {
-            const int st = i & 1;
-            mbar_wait(&qd_full[st], (i >> 1) & 1);
+            const int st = i % kQDStages;
+            mbar_wait(&qd_full[st], (i / kQDStages) & 1);
+            BWD_TRACE(i, 5);
             if (i >= 1) mbar_wait(s_free, (i - 1) & 1);
+            BWD_TRACE(i, 0);
             tc_fence_after();
             uint8_t *qdst = smem + kB_QD + st * 2 * kTileBytes;
             const uint64_t qk = sdesc_sw(smem_u32(qdst), 1024, 2);
@@ -560,6 +594,7 @@ attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
                            k ? 1u : 0u);
             }
             mma_commit_e(s_full);
+            BWD_TRACE(i, 15);
             if (i >= 1) issue_grads(i - 1);
         }
         if (nq >= 1) issue_grads(nq - 1);
@@ -572,36 +607,16 @@ attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
         const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
         const float2 c2 = make_float2(p.c, p.c);
         const float2 sc2 = make_float2(p.scale, p.scale);
-        // LSE and D of each query block: loaded one block ahead into registers
-        // (strided, latency-bound global loads off the critical path; the
-        // transforms are applied at the smem store one iteration later, so no
-        // instruction consumes the loads before then)
-        float l_pf = INFINITY, d_pf = 0.f;
-        auto fetch_rows = [&](int blkq) {
-            const int qrow = blkq * kBM + tid;
-            if ((p.dbg & 32) && blkq > 0) return;
-            l_pf = INFINITY;
-            d_pf = 0.f;
-            if (tid < kBM && blkq < nq && qrow < p.sq) {
-                const size_t qi = (size_t)qrow * p.H + h;
-                l_pf = __ldg(p.lse + qi);
-                d_pf = __ldg(p.delta + qi);
-            }
-        };
-        fetch_rows(0);
         for (int i = 0; i < nq; ++i) {
             const int b = i & 1;
-            if (tid < kBM) {
-                lse2_s[b * 128 + tid] = -l_pf * kLog2e;
-                delta_s[b * 128 + tid] = d_pf * p.scale;   // dS = P (scale dP - scale D)
-            }
-            fetch_rows(i + 1);
-            if (!(p.dbg & 128)) named_bar(1, 256);
+            const int lb = i % kLDBufs;
+            mbar_wait(&ld_full[lb], (i / kLDBufs) & 1);   // this block's -LSE2 / D rows staged
             mbar_wait(s_full, i & 1);
+            if (warp == 2) BWD_TRACE(i, 4);
             tc_fence_after();
             uint8_t *ps = smem + kB_PS + b * kPBytes + rl * 128 + half * (kBN * 128);   // dS^T(b)
-            const float *NL2 = lse2_s + b * 128 + half * 64;
-            const float *Dl = delta_s + b * 128 + half * 64;
+            const float *NL2 = lse2_s + lb * 128 + half * 64;
+            const float *Dl = delta_s + lb * 128 + half * 64;
             uint32_t pall[32];
 #pragma unroll
             for (int cc = 0; cc < 2; ++cc) {          // 32 query columns at a time
@@ -615,6 +630,7 @@ attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
                 if (cc == 1) {
                     tc_fence_before();
                     mbar_arrive(s_free);   // S^T / dP^T TMEM may be overwritten
+                    if (warp == 2) BWD_TRACE(i, 6);
                 } else {
                     if (i >= 2) mbar_wait(&ds_empty[b], ((i - 2) >> 1) & 1);   // dS^T(b) free
                 }
@@ -643,10 +659,14 @@ attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
                     *reinterpret_cast<uint4 *>(ps + off) = make_uint4(dk4[0], dk4[1], dk4[2], dk4[3]);
                 }
             }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&ld_empty[lb]);     // done reading the staged rows
             // P^T pairs (q, q+1) -> TMEM column kColPT + q / 2 (the TS A layout).
             // Written last: dV(i-1), issued when block i-1's softmax finished,
             // has had this whole block's softmax math to read the previous P^T.
+            if (warp == 2) BWD_TRACE(i, 7);
             if (i >= 1 && !(p.dbg & 64)) mbar_wait(pv_empty, (i - 1) & 1);
+            if (warp == 2) BWD_TRACE(i, 9);
             tc_fence_after();
             if (!(p.dbg & 2)) {
                 tmem_st16(lane_base + kColPT + half * 32, *reinterpret_cast<uint32_t(*)[16]>(pall));
@@ -656,6 +676,7 @@ attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
             fence_async_smem();
             tc_fence_before();
             mbar_arrive(&p_full[b]);
+            if (warp == 2) BWD_TRACE(i, 10);
         }
         // dV (half 0) / dK (half 1) += TMEM once the last gradient MMAs have landed
         if (nq >= 1) mbar_wait(&ds_empty[(nq - 1) & 1], ((nq - 1) >> 1) & 1);
@@ -686,10 +707,31 @@ attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
         const int rl = quarter * 32 + lane;
         const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
         const bool leader = warp == 10;
+        // -LSE*log2(e) and scale*D of query block q -> ring slot q % kLDBufs
+        // (strided global loads, off the softmax's critical path)
+        auto stage_rows = [&](int q) {
+            if (q >= nq) return;
+            const int sl = q % kLDBufs;
+            if (q >= kLDBufs) mbar_wait(&ld_empty[sl], ((q / kLDBufs) - 1) & 1);
+            const int qrow = q * kBM + rl;
+            float nl = -INFINITY, dd = 0.f;
+            if (qrow < p.sq) {
+                const size_t qi = (size_t)qrow * p.H + h;
+                nl = -__ldg(p.lse + qi) * kLog2e;
+                dd = __ldg(p.delta + qi) * p.scale;   // dS = P (scale dP - scale D)
+            }
+            lse2_s[sl * 128 + rl] = nl;
+            delta_s[sl * 128 + rl] = dd;
+            mbar_arrive(&ld_full[sl]);
+        };
+        stage_rows(0);
+        stage_rows(1);
         for (int i = 0; i < nq; ++i) {
-            const int b = i & 1;
+            stage_rows(i + 2);
             mbar_wait(dq_full, i & 1);
+            if (warp == 10) BWD_TRACE(i, 12);
             tc_fence_after();
+            const int b = i & 1;
             // staging tile b was last reduced 2 blocks ago: its TMA reads must be done
             if (leader && lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
             named_bar(2, 128);
@@ -701,14 +743,15 @@ attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
                     const int chunk = (c >> 2) + e;              // 16-B chunk of 4 floats, 0..15
-                    const int half = chunk >> 3, cc = chunk & 7;  // 32-column box, chunk in row
-                    *reinterpret_cast<uint4 *>(stg + half * (kDQStage / 2) + rl * 128 +
+                    const int hf = chunk >> 3, cc = chunk & 7;   // 32-column box, chunk in row
+                    *reinterpret_cast<uint4 *>(stg + hf * (kDQStage / 2) + rl * 128 +
                                                ((cc ^ (rl & 7)) << 4)) =
                         make_uint4(a[4 * e], a[4 * e + 1], a[4 * e + 2], a[4 * e + 3]);
                 }
             }
             tc_fence_before();
             mbar_arrive(dq_empty);            // TMEM dQ free
+            if (warp == 10) BWD_TRACE(i, 13);
             fence_async_smem();
             named_bar(2, 128);
             if (leader) {
@@ -833,10 +876,29 @@ int attn_bwd_update_tc_launch(const dp_attn_geom *g, const void *q, const void *
         }
         p.dbg = dbg;
     }
+    static unsigned long long *trace = nullptr;
+    static int want_trace = -1;
+    if (want_trace < 0) want_trace = getenv("DP_ATTN_TRACE") ? 1 : 0;
+    if (want_trace && !trace) DP_CUDA_CHECK(cudaMalloc(&trace, 64 * 16 * 8));
+    if (trace) DP_CUDA_CHECK(cudaMemsetAsync(trace, 0, 64 * 16 * 8, st));
+    p.trace = trace;
     DP_CUDA_CHECK(cudaFuncSetAttribute(attn_bwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        kSmemBwd));
     const int64_t grid = (int64_t)p.n_kt * p.H;
     attn_bwd_tc_kernel<<<(unsigned)grid, kBwdThreads, kSmemBwd, st>>>(qm, km, vm, dm, dqm, p);
+    if (trace) {  // debug: CTA 0's per-block event clocks relative to block 20's s_full
+        unsigned long long hbuf[64 * 16];
+        DP_CUDA_CHECK(cudaStreamSynchronize(st));
+        DP_CUDA_CHECK(cudaMemcpy(hbuf, trace, sizeof hbuf, cudaMemcpyDeviceToHost));
+        const long long t0 = (long long)hbuf[20 * 16 + 4];
+        fprintf(stderr, "blk  Msfree  Mpful  Mdqem   MdV  Ssful  Mqdfl  Ssfre  Smath  MdVdK  Spvem  Spful  Mgrds  Qdqfl  Qdrn  Pqdem  Mscmt\n");
+        for (int bb = 18; bb < 26; ++bb) {
+            fprintf(stderr, "%3d", bb);
+            for (int e = 0; e < 16; ++e)
+                fprintf(stderr, " %6lld", hbuf[bb * 16 + e] ? (long long)hbuf[bb * 16 + e] - t0 : -1);
+            fprintf(stderr, "\n");
+        }
+    }
     return launch_status("attn_bwd_tc_kernel");
 }
 
