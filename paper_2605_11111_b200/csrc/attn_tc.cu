@@ -381,18 +381,23 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
 //
 // CTA = one 128-key tile of one head (K, V resident in smem; dK, dV
 // accumulate in TMEM over the whole query range), looping over 128-row
-// query blocks (Q, dO double-buffered by TMA).  448 threads:
+// query blocks (Q, dO in a 3-stage TMA ring).  768 threads, six warpgroups
+// (setmaxnreg: 64 / 4 x 88 / 64 registers):
 //   warp 0     TMA producer
 //   warp 1     MMA issuer: S^T = K Q^T and dP^T = V dO^T into TMEM; once the
 //              softmax warps have written P^T / dS^T (bf16, swizzled smem):
 //              dV += P^T dO, dK += dS^T Q (A = the key-major tiles), and
 //              dQ = dS K into a double-buffered TMEM tile (A = the SAME dS^T
 //              bytes read as an MN-major operand)
-//   warps 2-9  two warps per TMEM lane quarter, each half of the 128 query
-//              columns; thread = (key row, column half): P^T = exp2(S^T c -
-//              LSE2), dS^T = scale P^T (dP^T - D) -> smem (packed fp32x2
-//              math); at the end dV (half 0) / dK (half 1) += TMEM
-//   warps 10-13 thread = query row: dQ tile TMEM -> swizzled fp32 smem ->
+//   warps 2-3  idle
+//   warps 4-19 four warps per TMEM lane quarter, each a 32-column quarter of
+//              the 128 query columns; thread = (key row, column quarter):
+//              P^T = exp2(S^T c - LSE2), dS^T = scale P^T (dP^T - D) -> smem
+//              (packed fp32x2 math); at the end dV / dK += TMEM (32-column
+//              halves).  Four softmax warps per SM sub-partition (was two)
+//              hide the MUFU / TMEM-load latency: 16k block 3.09 -> 2.90 ms
+//              together with the 3-stage Q / dO ring
+//   warps 20-23 thread = query row: dQ tile TMEM -> swizzled fp32 smem ->
 //              TMA bulk reduce-add (cp.reduce.async.bulk.tensor .add) into dq
 //              (per-thread float4 atomics cost 34 of 84 ms at 64k); they also
 //              stage each query block's -LSE*log2(e) / scale*D rows into a
@@ -403,16 +408,16 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
 // released once dK has read it (dQ only needs dS and K).
 // Debug: DP_ATTN_TRACE=1 prints CTA 0's per-block event clocks (the timeline
 // behind these choices), DP_ATTN_DBG=<bits> the ablations listed in BwdParams.
-constexpr int kBwdThreads = 448;   // TMA, MMA, 8 softmax warps, 4 dQ warps
+constexpr int kBwdThreads = 768;   // TMA, MMA, 2 idle, 16 softmax warps, 4 dQ warps
 constexpr int kB_K = 0, kB_V = kTileBytes;
-constexpr int kQDStages = 2;                           // [Q | dO] ring (a stage frees when
+constexpr int kQDStages = 3;                           // [Q | dO] ring (a stage frees when
                                                        // the block's dK MMAs complete)
 constexpr int kB_QD = 2 * kTileBytes;
 constexpr int kB_PS = kB_QD + kQDStages * 2 * kTileBytes;  // dS^T x 2 (double buffer)
-constexpr int kB_DQ = kB_PS + 2 * kPBytes;             // 2 dQ staging tiles (fp32, 2 x 16 KB halves)
+constexpr int kB_DQ = kB_PS + 2 * kPBytes;             // dQ staging tile (fp32, 2 x 16 KB halves)
 constexpr int kDQStage = kBM * kD * 4;                 // 32 KB
 constexpr int kLDBufs = 2;                             // -lse2 / scale*D ring (dQ warps -> softmax)
-constexpr int kB_LD = kB_DQ + 2 * kDQStage;                // -lse2[2][128], delta[2][128]
+constexpr int kB_LD = kB_DQ + kDQStage;                // -lse2[2][128], delta[2][128]
 constexpr int kB_BAR = kB_LD + 2 * kLDBufs * 128 * 4;
 constexpr int kSmemBwd = kB_BAR + 256;
 static_assert(kSmemBwd <= 232448, "attention bwd smem");
@@ -476,17 +481,17 @@ attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
                 mbar_init(&qd_empty[i], 1);
             }
             for (int i = 0; i < 2; ++i) {
-                mbar_init(&p_full[i], 256);
+                mbar_init(&p_full[i], 512);
                 mbar_init(&ds_empty[i], 1);
             }
             mbar_init(dq_full, 1);
             mbar_init(dq_empty, 128);
             for (int i = 0; i < kLDBufs; ++i) {
                 mbar_init(&ld_full[i], 128);   // the dQ warps' threads (one query row each)
-                mbar_init(&ld_empty[i], 8);    // one arrival per softmax warp
+                mbar_init(&ld_empty[i], 16);   // one arrival per softmax warp
             }
             mbar_init(s_full, 1);
-            mbar_init(s_free, 256);
+            mbar_init(s_free, 512);
             mbar_init(pv_empty, 1);
             mbar_fence_init();
             tma_prefetch(&qmap);
@@ -503,6 +508,10 @@ attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
+    // registers: 64 for the TMA / MMA warpgroup, 88 for the four softmax
+    // warpgroups, 64 for the dQ one (launch: 80 x 768 threads)
+    if (warp < 4) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 64;");
     if (warp == 0) {
         // ===================== TMA producer =====================
         mbar_expect_tx_e(kv_full, 2 * kTileBytes);
@@ -598,12 +607,13 @@ attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
             if (i >= 1) issue_grads(i - 1);
         }
         if (nq >= 1) issue_grads(nq - 1);
-    } else if (warp < 10) {
-        // ===================== P^T / dS^T (thread = key row, column half) ==========
+    }
+    } else if (warp < 20) {
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 88;");
+        // ============ P^T / dS^T (thread = key row, 32-column quarter) ============
         const int quarter = warp & 3;
-        const int half = (warp - 2) >> 2;                // query columns [64 half, 64 half + 64)
+        const int cq = (warp - 4) >> 2;                  // query columns [32 cq, 32 cq + 32)
         const int rl = quarter * 32 + lane;
-        const int tid = threadIdx.x - 64;                // 0..255
         const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
         const float2 c2 = make_float2(p.c, p.c);
         const float2 sc2 = make_float2(p.scale, p.scale);
@@ -612,37 +622,35 @@ attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
             const int lb = i % kLDBufs;
             mbar_wait(&ld_full[lb], (i / kLDBufs) & 1);   // this block's -LSE2 / D rows staged
             mbar_wait(s_full, i & 1);
-            if (warp == 2) BWD_TRACE(i, 4);
+            if (warp == 4) BWD_TRACE(i, 4);
             tc_fence_after();
-            uint8_t *ps = smem + kB_PS + b * kPBytes + rl * 128 + half * (kBN * 128);   // dS^T(b)
-            const float *NL2 = lse2_s + lb * 128 + half * 64;
-            const float *Dl = delta_s + lb * 128 + half * 64;
-            uint32_t pall[32];
+            uint8_t *ps = smem + kB_PS + b * kPBytes + rl * 128 + (cq >> 1) * (kBN * 128);   // dS^T(b)
+            const float *NL2 = lse2_s + lb * 128 + cq * 32;
+            const float *Dl = delta_s + lb * 128 + cq * 32;
+            uint32_t pall[16];
 #pragma unroll
-            for (int cc = 0; cc < 2; ++cc) {          // 32 query columns at a time
-                uint32_t sv[32], dv[32];
-                const uint32_t col = half * 64 + cc * 32;
-                tmem_ld16(lane_base + kColST + col, *reinterpret_cast<uint32_t(*)[16]>(sv));
-                tmem_ld16(lane_base + kColST + col + 16, *reinterpret_cast<uint32_t(*)[16]>(sv + 16));
-                tmem_ld16(lane_base + kColDP + col, *reinterpret_cast<uint32_t(*)[16]>(dv));
-                tmem_ld16(lane_base + kColDP + col + 16, *reinterpret_cast<uint32_t(*)[16]>(dv + 16));
+            for (int cc = 0; cc < 2; ++cc) {          // 16 query columns at a time
+                uint32_t sv[16], dv[16];
+                const uint32_t col = cq * 32 + cc * 16;
+                tmem_ld16(lane_base + kColST + col, sv);
+                tmem_ld16(lane_base + kColDP + col, dv);
                 tmem_wait_ld();
                 if (cc == 1) {
                     tc_fence_before();
                     mbar_arrive(s_free);   // S^T / dP^T TMEM may be overwritten
-                    if (warp == 2) BWD_TRACE(i, 6);
+                    if (warp == 4) BWD_TRACE(i, 6);
                 } else {
                     if (i >= 2) mbar_wait(&ds_empty[b], ((i - 2) >> 1) & 1);   // dS^T(b) free
                 }
 #pragma unroll
-                for (int c = 0; c < 4; ++c) {         // 16-B chunks of 8 query columns
+                for (int c = 0; c < 2; ++c) {         // 16-B chunks of 8 query columns
                     if (p.dbg & 2) break;
-                    uint32_t pk[4], dk4[4];
+                    uint32_t dk4[4];
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
                         const int qc = c * 8 + 2 * e;
-                        const float2 nl = *reinterpret_cast<const float2 *>(NL2 + cc * 32 + qc);
-                        const float2 dd = *reinterpret_cast<const float2 *>(Dl + cc * 32 + qc);
+                        const float2 nl = *reinterpret_cast<const float2 *>(NL2 + cc * 16 + qc);
+                        const float2 dd = *reinterpret_cast<const float2 *>(Dl + cc * 16 + qc);
                         float2 x = ffma2(make_float2(__uint_as_float(sv[qc]), __uint_as_float(sv[qc + 1])),
                                          c2, nl);
                         x.x = ex2(x.x);
@@ -650,13 +658,12 @@ attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
                         const float2 g = fmul2(
                             x, ffma2(make_float2(__uint_as_float(dv[qc]), __uint_as_float(dv[qc + 1])),
                                      sc2, make_float2(-dd.x, -dd.y)));
-                        pk[e] = pack_bf16(x.x, x.y);
+                        pall[cc * 8 + c * 4 + e] = pack_bf16(x.x, x.y);
                         dk4[e] = pack_bf16(g.x, g.y);
                     }
-                    const int off = (((cc * 4 + c) ^ (rl & 7)) << 4);
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) pall[cc * 16 + c * 4 + e] = pk[e];
-                    *reinterpret_cast<uint4 *>(ps + off) = make_uint4(dk4[0], dk4[1], dk4[2], dk4[3]);
+                    const int chunk = (cq & 1) * 4 + cc * 2 + c;   // 16-B chunk in the 128-B half-tile row
+                    *reinterpret_cast<uint4 *>(ps + ((chunk ^ (rl & 7)) << 4)) =
+                        make_uint4(dk4[0], dk4[1], dk4[2], dk4[3]);
                 }
             }
             __syncwarp();
@@ -664,34 +671,33 @@ attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
             // P^T pairs (q, q+1) -> TMEM column kColPT + q / 2 (the TS A layout).
             // Written last: dV(i-1), issued when block i-1's softmax finished,
             // has had this whole block's softmax math to read the previous P^T.
-            if (warp == 2) BWD_TRACE(i, 7);
+            if (warp == 4) BWD_TRACE(i, 7);
             if (i >= 1 && !(p.dbg & 64)) mbar_wait(pv_empty, (i - 1) & 1);
-            if (warp == 2) BWD_TRACE(i, 9);
+            if (warp == 4) BWD_TRACE(i, 9);
             tc_fence_after();
-            if (!(p.dbg & 2)) {
-                tmem_st16(lane_base + kColPT + half * 32, *reinterpret_cast<uint32_t(*)[16]>(pall));
-                tmem_st16(lane_base + kColPT + half * 32 + 16, *reinterpret_cast<uint32_t(*)[16]>(pall + 16));
-            }
+            if (!(p.dbg & 2)) tmem_st16(lane_base + kColPT + cq * 16, pall);
             tmem_wait_st();
             fence_async_smem();
             tc_fence_before();
             mbar_arrive(&p_full[b]);
-            if (warp == 2) BWD_TRACE(i, 10);
+            if (warp == 4) BWD_TRACE(i, 10);
         }
-        // dV (half 0) / dK (half 1) += TMEM once the last gradient MMAs have landed
+        // dV (cq 0, 1) / dK (cq 2, 3) 32-column halves += TMEM once the last
+        // gradient MMAs have landed
         if (nq >= 1) mbar_wait(&ds_empty[(nq - 1) & 1], ((nq - 1) >> 1) & 1);
         tc_fence_after();
         const int key = k0 + rl;
         const bool kv_ok = key < p.sk;
         const size_t ki = ((size_t)key * p.H + h) * kD;
-        float *gdst = half ? p.dk : p.dv;
-        const uint32_t gcol = half ? kColDK : kColDV;
-        for (int c = 0; c < kD; c += 16) {
+        float *gdst = cq >= 2 ? p.dk : p.dv;
+        const int c0 = (cq & 1) * 32;
+        const uint32_t gcol = (cq >= 2 ? kColDK : kColDV) + c0;
+        for (int c = 0; c < 32; c += 16) {
             uint32_t a[16];
             tmem_ld16(lane_base + gcol + c, a);
             tmem_wait_ld();
             if (kv_ok) {
-                float4 *pv = reinterpret_cast<float4 *>(gdst + ki + c);
+                float4 *pv = reinterpret_cast<float4 *>(gdst + ki + c0 + c);
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
                     float4 x = pv[e];
@@ -702,13 +708,17 @@ attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
             }
         }
     } else {
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 64;");
         // ===================== dQ epilogue (thread = query row) =====================
         const int quarter = warp & 3;
         const int rl = quarter * 32 + lane;
         const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
-        const bool leader = warp == 10;
+        const bool leader = warp == 20;
         // -LSE*log2(e) and scale*D of query block q -> ring slot q % kLDBufs
-        // (strided global loads, off the softmax's critical path)
+        // (strided global loads, off the softmax's critical path).  Staging
+        // block i + 2 before waiting for dQ(i) measured faster than deferring
+        // it past the drain (2.90 vs 3.10 ms at 16k): the later dq_empty holds
+        // the MMA warp back just enough to keep S^T / dP^T ahead of dQ.
         auto stage_rows = [&](int q) {
             if (q >= nq) return;
             const int sl = q % kLDBufs;
@@ -729,13 +739,12 @@ attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
         for (int i = 0; i < nq; ++i) {
             stage_rows(i + 2);
             mbar_wait(dq_full, i & 1);
-            if (warp == 10) BWD_TRACE(i, 12);
+            if (warp == 20) BWD_TRACE(i, 12);
             tc_fence_after();
-            const int b = i & 1;
-            // staging tile b was last reduced 2 blocks ago: its TMA reads must be done
-            if (leader && lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+            // the staging tile was last reduced one block ago: its TMA reads must be done
+            if (leader && lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
             named_bar(2, 128);
-            uint8_t *stg = smem + kB_DQ + b * kDQStage;
+            uint8_t *stg = smem + kB_DQ;
             for (int c = 0; c < kD; c += 16) {
                 uint32_t a[16];
                 tmem_ld16(lane_base + kColDQ + c, a);
@@ -751,7 +760,7 @@ attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
             }
             tc_fence_before();
             mbar_arrive(dq_empty);            // TMEM dQ free
-            if (warp == 10) BWD_TRACE(i, 13);
+            if (warp == 20) BWD_TRACE(i, 13);
             fence_async_smem();
             named_bar(2, 128);
             if (leader) {
