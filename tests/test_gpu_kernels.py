@@ -232,6 +232,8 @@ ATTN_TC_CASES = [
     (1000, 513, 3, [100, 100, 513]),      # includes an empty block (no-op)
     (64, 1030, 2, [1030]),
     (384, 256, 4, [1, 256]),              # a one-key block
+    (700, 640, 2, [640]),                 # 6 query blocks: Q/dO ring + LSE/D ring wrap
+    (2048, 384, 1, [200, 384]),           # 16 query blocks, ragged key tiles
 ]
 
 
