@@ -715,29 +715,36 @@ attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
         const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
         const bool leader = warp == 20;
         // -LSE*log2(e) and scale*D of query block q -> ring slot q % kLDBufs
-        // (strided global loads, off the softmax's critical path).  Staging
-        // block i + 2 before waiting for dQ(i) measured faster than deferring
-        // it past the drain (2.90 vs 3.10 ms at 16k): the later dq_empty holds
-        // the MMA warp back just enough to keep S^T / dP^T ahead of dQ.
-        auto stage_rows = [&](int q) {
+        // (strided global loads, off the softmax's critical path).  The loads
+        // for block i + 3 are issued right after block i + 2's rows are
+        // stored, so their latency overlaps this warp's dQ wait and drain.
+        float l_pf = INFINITY, d_pf = 0.f;
+        auto fetch_rows = [&](int q) {
+            l_pf = INFINITY;
+            d_pf = 0.f;
+            const int qrow = q * kBM + rl;
+            if (q < nq && qrow < p.sq) {
+                const size_t qi = (size_t)qrow * p.H + h;
+                l_pf = __ldg(p.lse + qi);
+                d_pf = __ldg(p.delta + qi);
+            }
+        };
+        auto store_rows = [&](int q) {
             if (q >= nq) return;
             const int sl = q % kLDBufs;
             if (q >= kLDBufs) mbar_wait(&ld_empty[sl], ((q / kLDBufs) - 1) & 1);
-            const int qrow = q * kBM + rl;
-            float nl = -INFINITY, dd = 0.f;
-            if (qrow < p.sq) {
-                const size_t qi = (size_t)qrow * p.H + h;
-                nl = -__ldg(p.lse + qi) * kLog2e;
-                dd = __ldg(p.delta + qi) * p.scale;   // dS = P (scale dP - scale D)
-            }
-            lse2_s[sl * 128 + rl] = nl;
-            delta_s[sl * 128 + rl] = dd;
+            lse2_s[sl * 128 + rl] = -l_pf * kLog2e;
+            delta_s[sl * 128 + rl] = d_pf * p.scale;   // dS = P (scale dP - scale D)
             mbar_arrive(&ld_full[sl]);
         };
-        stage_rows(0);
-        stage_rows(1);
+        fetch_rows(0);
+        store_rows(0);
+        fetch_rows(1);
+        store_rows(1);
+        fetch_rows(2);
         for (int i = 0; i < nq; ++i) {
-            stage_rows(i + 2);
+            store_rows(i + 2);
+            fetch_rows(i + 3);
             mbar_wait(dq_full, i & 1);
             if (warp == 20) BWD_TRACE(i, 12);
             tc_fence_after();
