@@ -49,9 +49,11 @@ constexpr int kSmemKV = kSmemQ + kFwdTiles * kTileBytes;  // stages of [K | V]
 constexpr int kSmemBar = kSmemKV + kFwdStages * 2 * kTileBytes;
 constexpr int kSmemFwd = kSmemBar + 256;
 
-// TMEM columns per tile t: S_t [128 t, +128) with P_t (bf16 pairs) aliased
-// over its first 64 columns, O_t [256 + 64 t, +64), Q_t [384 + 32 t, +32)
-constexpr uint32_t kColS = 0, kColO = 256, kColQ = 384;
+// TMEM columns per tile t: S_t [128 t, +128), P_t (bf16 pairs) [256 + 64 t,
+// +64), O_t [384 + 64 t, +64).  P has its own columns so S_t(j+1) can be
+// computed while the softmax still works on block j (Q stays in smem: the S
+// MMA is SS, 64 cycles per K step either way).
+constexpr uint32_t kColS = 0, kColP = 256, kColO = 384;
 
 struct FwdParams {
     int sq, sk, H;
@@ -130,11 +132,12 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem + kSmemBar);
     uint64_t *q_full = bars;
     uint64_t *kv_full = bars + 1, *kv_empty = kv_full + kFwdStages;
-    uint64_t *s_full = kv_empty + kFwdStages;   // [tiles]  S_t(j) ready (and PV_t(j-1) done)
-    uint64_t *p_full = s_full + kFwdTiles;      // [tiles]  softmax -> MMA (count 128)
-    uint64_t *done = p_full + kFwdTiles;        // every MMA finished
-    uint64_t *q_tm = done + 1;                  // Q tiles staged in TMEM (count 128 * tiles)
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(q_tm + 1);
+    uint64_t *s_full = kv_empty + kFwdStages;   // [tiles]  S_t(j) ready
+    uint64_t *s_free = s_full + kFwdTiles;      // [tiles]  softmax loaded S_t(j) (count 128)
+    uint64_t *p_full = s_free + kFwdTiles;      // [tiles]  P_t(j) written (count 128)
+    uint64_t *pv_done = p_full + kFwdTiles;     // [tiles]  PV_t(j) finished (O, P_t quiescent)
+    uint64_t *done = pv_done + kFwdTiles;       // every MMA finished
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(done + 1);
 
     if (warp == 0) {
         if (lane == 0) {
@@ -145,10 +148,11 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
             }
             for (int i = 0; i < kFwdTiles; ++i) {
                 mbar_init(&s_full[i], 1);
+                mbar_init(&s_free[i], 128);
                 mbar_init(&p_full[i], 128);
+                mbar_init(&pv_done[i], 1);
             }
             mbar_init(done, 1);
-            mbar_init(q_tm, 128 * kFwdTiles);
             mbar_fence_init();
             tma_prefetch(&qmap);
             tma_prefetch(&kmap);
@@ -182,18 +186,20 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
         }
     } else if (warp == 1) {
         // ===================== MMA issuer =====================
-        // S_t = Q_t K^T with Q_t in TMEM (TS), O_t += P_t V with P_t in TMEM (TS)
+        // S_t = Q_t K^T (SS, Q from smem), O_t += P_t V with P_t in TMEM (TS).
+        // S_t(j+1) is issued as soon as softmax t has LOADED S_t(j) (s_free),
+        // so it runs under that softmax; PV_t(j) follows P_t(j) (p_full).
         const uint32_t id_s = idesc_bf16(kBM, kBN);            // K-major A, K-major B
         const uint32_t id_o = idesc_bf16(kBM, kD, 0, 1);       // P K-major, V MN-major
-        mbar_wait(q_tm, 0);
+        mbar_wait(q_full, 0);
         auto issue_s = [&](int t, int j) {
             const int st = j % kFwdStages;
             const uint64_t kd = sdesc_sw(smem_u32(smem + kSmemKV + st * 2 * kTileBytes), 1024, 2);
+            const uint64_t qd = sdesc_sw(smem_u32(smem + kSmemQ + t * kTileBytes), 1024, 2);
             const uint32_t sc = tmem + kColS + t * kBN;
 #pragma unroll
             for (int k = 0; k < kD / 16; ++k)
-                mma_ts_e(sc, tmem + kColQ + t * (kD / 2) + k * 8, kd + ((k * 32) >> 4), id_s,
-                         k ? 1u : 0u);
+                mma_bf16_e(sc, qd + ((k * 32) >> 4), kd + ((k * 32) >> 4), id_s, k ? 1u : 0u);
             mma_commit_e(&s_full[t]);
         };
         auto issue_pv = [&](int t, int j) {
@@ -203,8 +209,9 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
 #pragma unroll
             for (int k = 0; k < kBN / 16; ++k) {
                 const uint32_t vb = (k * 16 * 128) >> 4;  // 16 key rows of V
-                mma_ts_e(tmem + kColO + t * kD, tmem + kColS + t * kBN + k * 8, vd + vb, id_o, 1u);
+                mma_ts_e(tmem + kColO + t * kD, tmem + kColP + t * (kBN / 2) + k * 8, vd + vb, id_o, 1u);
             }
+            mma_commit_e(&pv_done[t]);
         };
         if (nblk >= 1) {
             mbar_wait(&kv_full[0], 0);
@@ -215,14 +222,14 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
             const bool more = j + 1 < nblk;
             if (more) mbar_wait(&kv_full[(j + 1) % kFwdStages], ((j + 1) / kFwdStages) & 1);
             for (int t = 0; t < kFwdTiles; ++t) {
+                if (more) {
+                    mbar_wait(&s_free[t], j & 1);      // softmax t holds S_t(j) in registers
+                    tc_fence_after();
+                    issue_s(t, j + 1);
+                }
                 mbar_wait(&p_full[t], j & 1);
                 tc_fence_after();
                 issue_pv(t, j);
-                // S_t(j+1) overwrites S_t: softmax t is done with S_t(j).  Its
-                // commit also covers PV_t(j), so s_full tells softmax t that O_t
-                // and the P_t tile are free again.
-                if (more) issue_s(t, j + 1);
-                else mma_commit_e(&s_full[t]);
             }
             mma_commit_e(&kv_empty[j % kFwdStages]);
         }
@@ -238,6 +245,7 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
         const bool valid = row < p.sq;
         const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
         const uint32_t colS = lane_base + kColS + t * kBN, colO = lane_base + kColO + t * kD;
+        const uint32_t colP = lane_base + kColP + t * (kBN / 2);
         const size_t sidx = (size_t)row * p.H + h;
         float m_run = -INFINITY, l_run = 0.f;
         {
@@ -254,21 +262,6 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
                 l_run = p.l[sidx];
             }
         }
-        {   // Q_t row -> TMEM (A operand of S = Q K^T), once per CTA
-            mbar_wait(q_full, 0);
-            const uint8_t *qrow = smem + kSmemQ + t * kTileBytes + rl * 128;
-            uint32_t qv[32];
-#pragma unroll
-            for (int c = 0; c < 8; ++c) {
-                const uint4 v = *reinterpret_cast<const uint4 *>(qrow + ((c ^ (rl & 7)) << 4));
-                qv[4 * c] = v.x; qv[4 * c + 1] = v.y; qv[4 * c + 2] = v.z; qv[4 * c + 3] = v.w;
-            }
-            tmem_st16(lane_base + kColQ + t * (kD / 2), *reinterpret_cast<uint32_t(*)[16]>(qv));
-            tmem_st16(lane_base + kColQ + t * (kD / 2) + 16, *reinterpret_cast<uint32_t(*)[16]>(qv + 16));
-            tmem_wait_st();
-            tc_fence_before();
-            mbar_arrive(q_tm);
-        }
         const float2 c2 = make_float2(p.c, p.c);
         for (int j = 0; j < nblk; ++j) {
             mbar_wait(&s_full[t], j & 1);
@@ -282,6 +275,8 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
                 for (int i = 0; i < 16; ++i) s[c + i] = __uint_as_float(u[i]);
             }
             tmem_wait_ld();
+            tc_fence_before();
+            mbar_arrive(&s_free[t]);            // S_t may be overwritten by S_t(j+1)
             const int kvalid = p.sk - j * kBN;  // keys of this block that exist
             if (kvalid < kBN) {
 #pragma unroll
@@ -300,9 +295,11 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
                                    fmaxf(fmaxf(mq[4], mq[5]), fmaxf(mq[6], mq[7])));
             const float tnew = mx * p.c;
             // lazy rescale: only when this row's max grows by more than 2^kRescale
-            // (s_full already implies the previous P V finished, so O is quiescent)
+            // (O must be quiescent: PV_t(j-1) finished)
             const bool grow = tnew > m_run + kRescale;
             if (__any_sync(0xffffffffu, grow)) {
+                if (j >= 1) mbar_wait(&pv_done[t], (j - 1) & 1);
+                tc_fence_after();
                 const float f = grow ? ex2(m_run - tnew) : 1.f;
                 for (int c = 0; c < kD; c += 16) {
                     uint32_t o[16];
@@ -318,13 +315,15 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
                     m_run = tnew;
                 }
             }
-            // P = exp2(s c - m) as bf16 pairs into TMEM over S_t's first 64 columns
+            // P = exp2(s c - m) as bf16 pairs into P_t's TMEM columns (written once
+            // PV_t(j-1) has read the previous P_t; it had this whole block's
+            // exp math to do so)
             const float2 nm = make_float2(-m_run, -m_run);
+            uint32_t pk[kBN / 2];
             float2 sumv[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
                               make_float2(0.f, 0.f)};   // 4 independent sum chains
 #pragma unroll
             for (int c = 0; c < kBN / 32; ++c) {
-                uint32_t pk[16];
 #pragma unroll
                 for (int i = 0; i < 16; ++i) {
                     float2 x = ffma2(make_float2(s[c * 32 + 2 * i], s[c * 32 + 2 * i + 1]), c2, nm);
@@ -335,10 +334,14 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
                         x.y = ex2(x.y);
                     }
                     sumv[i & 3] = fadd2(sumv[i & 3], x);
-                    pk[i] = pack_bf16(x.x, x.y);
+                    pk[c * 16 + i] = pack_bf16(x.x, x.y);
                 }
-                tmem_st16(colS + c * 16, pk);
             }
+            if (j >= 1) mbar_wait(&pv_done[t], (j - 1) & 1);
+            tc_fence_after();
+#pragma unroll
+            for (int c = 0; c < kBN / 32; ++c)
+                tmem_st16(colP + c * 16, *reinterpret_cast<uint32_t(*)[16]>(pk + c * 16));
             tmem_wait_st();
             const float2 sum2 = fadd2(fadd2(sumv[0], sumv[1]), fadd2(sumv[2], sumv[3]));
             l_run += sum2.x + sum2.y;
