@@ -350,6 +350,47 @@ __device__ __forceinline__ void mma2_bf16_e(uint32_t d_tmem, uint64_t a, uint64_
         "}\n" ::"r"(d_tmem),
         "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
 }
+// Three cta_group::2 MMAs into the same accumulator under ONE elect, the
+// second and third at fixed descriptor offsets (DA, DB in 16-B units): the kw
+// taps of a merged conv step.  Cuts the per-MMA issue work (elect, votes,
+// uniform-register moves) the single-MMA helper pays three times.
+template <uint32_t DA, uint32_t DB>
+__device__ __forceinline__ void mma2_bf16_x3(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p, e;\n"
+        ".reg .b64 a1, a2, b1, b2;\n"
+        "setp.eq.u32 p, 1, 1;\n"
+        "add.s64 a1, %1, %4;\n"
+        "add.s64 a2, %1, %5;\n"
+        "add.s64 b1, %2, %6;\n"
+        "add.s64 b2, %2, %7;\n"
+        "elect.sync _|e, 0xffffffff;\n"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a1, b1, %3, p;\n"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a2, b2, %3, p;\n"
+        "}\n" ::"r"(d_tmem),
+        "l"(a), "l"(b), "r"(idesc), "n"(DA), "n"(2 * DA), "n"(DB), "n"(2 * DB));
+}
+// cta_group::1 form of mma2_bf16_x3.
+template <uint32_t DA, uint32_t DB>
+__device__ __forceinline__ void mma_bf16_x3(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p, e;\n"
+        ".reg .b64 a1, a2, b1, b2;\n"
+        "setp.eq.u32 p, 1, 1;\n"
+        "add.s64 a1, %1, %4;\n"
+        "add.s64 a2, %1, %5;\n"
+        "add.s64 b1, %2, %6;\n"
+        "add.s64 b2, %2, %7;\n"
+        "elect.sync _|e, 0xffffffff;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a1, b1, %3, p;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a2, b2, %3, p;\n"
+        "}\n" ::"r"(d_tmem),
+        "l"(a), "l"(b), "r"(idesc), "n"(DA), "n"(2 * DA), "n"(DB), "n"(2 * DB));
+}
 // commit: arrive on `bar` (same offset) in both CTAs of the pair
 __device__ __forceinline__ void mma2_commit_mc_e(uint64_t *bar) {
     asm volatile(
