@@ -36,7 +36,6 @@
 //   warp 1     tcgen05.mma issuer (one lane)    TMEM ring: tfull/tempty mbarriers
 //   warps 2-5  epilogue: tcgen05.ld -> bf16 -> 16-B global stores
 #include "tc_common.cuh"
-#include <cstdio>
 #include <type_traits>
 
 namespace dp {
@@ -77,19 +76,10 @@ struct ConvTcParams {
     int nstage;               // pipeline depth
     int wimg_bytes;
     const __nv_bfloat16 *wimg;
-    int dbg;                  // profiling ablations (DP_CONV_DBG): 1 no stores, 2 no MMA, 4 no TMA,
-                              // 8 no TMEM epilogue, 32 per-MMA issue, 64 / 128 MMA warp skips
-                              // its TMEM-empty / stage-full waits (timing only)
+    int dbg;                  // profiling ablations (DP_CONV_DBG): 1 no stores, 2 no MMA, 4 no TMA
     float *yf, *yf2;          // fp32 outputs (the bf16x3 fp32 path) instead of y / y2
     int64_t ycs, y2cs;        // their channel strides (elements)
-    unsigned long long *trace;  // DP_CONV_TRACE: per-stage / per-row event clocks of CTA 0 (debug)
 };
-
-// debug timeline (DP_CONV_TRACE): slot [i][ev] for stage / row i < 96 of CTA 0
-#define CONV_TRACE(i, ev)                                                                   \
-    do {                                                                                    \
-        if (p.trace && blockIdx.x == 0 && lane == 0 && (i) < 96) p.trace[(i) * 8 + (ev)] = clock64(); \
-    } while (0)
 
 // Template arguments KP_/KQ_/KW_/CIN_ = 0 select the runtime-shaped kernel;
 // non-zero values give the fully unrolled MMA issue the hot shapes use (a
@@ -178,7 +168,7 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
     if (warp == 0) {
         // ===================== TMA producer (whole warp, elected issue) =====================
         const uint32_t lead_full = PAIR ? mapa_shared(smem_u32(full), 0) : 0u;
-        uint32_t it = 0, idx = 0, ph = 0;
+        uint32_t it = 0;
         for (int u = u0; u < p.n_units; u += ustep) {
             int r = u;
             const int wt = PAIR ? (r % p.n_wt) * 2 + (int)rank : r % p.n_wt; r /= p.n_wt;
@@ -188,8 +178,8 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
             const int q0 = qc * p.q_chunk, q1 = min(p.Qout, q0 + p.q_chunk);
             const int nrows = (q1 - q0) + KQ - 1;
             const int wc = p.base_w + wt * kTileW;
-            for (int s = 0; s < nrows;
-                 ++s, ++it, (++idx == (uint32_t)p.nstage ? (idx = 0u, ph ^= 1u) : 0u)) {
+            for (int s = 0; s < nrows; ++s, ++it) {
+                const uint32_t idx = it % p.nstage, ph = (it / p.nstage) & 1;
                 mbar_wait(&empty[idx], ph ^ 1);
                 if (p.dbg & 4) {
                     if (lane == 0) mbar_arrive(&full[idx]);
@@ -241,26 +231,21 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
             if constexpr (PAIR) mma2_commit_mc_e(bar);
             else mma_commit_e(bar);
         };
-        // stage slot / phase carried across units (no integer division per stage:
-        // it kept the stage index out of the uniform datapath)
-        uint32_t it = 0, row_base = 0, idx = 0, ph = 0;
+        uint32_t it = 0, row_base = 0;
         for (int u = u0; u < p.n_units; u += ustep) {
             int r = u / p.n_wt;
             const int qc = r % p.n_qc;
             const int q0 = qc * p.q_chunk, q1 = min(p.Qout, q0 + p.q_chunk);
             const int nq = q1 - q0;
             const int nrows = nq + KQ - 1;
-            for (int s = 0; s < nrows;
-                 ++s, ++it, (++idx == (uint32_t)p.nstage ? (idx = 0u, ph ^= 1u) : 0u)) {
-                CONV_TRACE(it, 0);
-                if (s < nq && !(p.dbg & 64)) {
+            for (int s = 0; s < nrows; ++s, ++it) {
+                const uint32_t idx = it % p.nstage, ph = (it / p.nstage) & 1;
+                if (s < nq) {
                     // row s starts here: its slot must have been drained + zeroed
                     const uint32_t row = row_base + s;
                     mbar_wait(&tempty[row % NSLOT], ((row / NSLOT) & 1) ^ 1);
                 }
-                CONV_TRACE(it, 1);
-                if (!(p.dbg & 128)) mbar_wait(&full[idx], ph);
-                CONV_TRACE(it, 2);
+                mbar_wait(&full[idx], ph);
                 tc_fence_after();
                 const uint64_t adesc = adesc0 + ((idx * stage_bytes) >> 4);
                 const uint32_t top = row_base + s;  // row fed through kq = 0
@@ -348,11 +333,9 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
                                 }
                     }
                 }
-                CONV_TRACE(it, 3);
                 commit(&empty[idx]);
                 const int jd = s - (KQ - 1);
                 if (jd >= 0 && jd < nq) commit(&tfull[(row_base + jd) % NSLOT]);
-                CONV_TRACE(it, 4);
             }
             row_base += nq;
         }
@@ -377,7 +360,6 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
             for (int j = 0; j < q1 - q0; ++j) {
                 const uint32_t row = row_base + j, slot = row % NSLOT;
                 mbar_wait(&tfull[slot], (row / NSLOT) & 1);
-                if (warp == 2) CONV_TRACE(row, 5);
                 tc_fence_after();
                 const uint32_t col = lane_base + (NSLOT - 1 - slot) * N;
                 uint32_t v[N];
@@ -398,7 +380,6 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
                     for (int i = 0; i < N; ++i) v[i] = 0u;
                 }
                 tc_fence_before();
-                if (warp == 2) CONV_TRACE(row, 6);
                 if constexpr (PAIR) {
                     __syncwarp();
                     if (lane == 0) {
@@ -785,7 +766,7 @@ int run_conv_tc(const dp_conv_geom *g, bool dgrad, const void *in, const void *i
                                    const_cast<void *>(in_halo), dims, strides, box, swz);
         if (rc) return rc;
     }
-    ConvTcParams p{};
+    ConvTcParams p;
     memset(&p, 0, sizeof(p));
     p.B = (int)g->batch;
     p.Cin = pl.Cin;
@@ -846,32 +827,6 @@ int run_conv_tc(const dp_conv_geom *g, bool dgrad, const void *in, const void *i
             dbg = e ? atoi(e) : 0;
         }
         p.dbg = dbg;
-    }
-    static unsigned long long *trace = nullptr;
-    static int trace_calls = 0;
-    const bool do_trace = getenv("DP_CONV_TRACE") && ++trace_calls == 4;   // after warm-up
-    if (do_trace && !trace) DP_CUDA_CHECK(cudaMalloc(&trace, 96 * 8 * 8));
-    if (do_trace) DP_CUDA_CHECK(cudaMemsetAsync(trace, 0, 96 * 8 * 8, st));
-    p.trace = do_trace ? trace : nullptr;
-    if (do_trace) {
-        int rc = 0;
-        int grid = p.n_units < sms ? p.n_units : sms;
-        if (use_pair)
-            rc = pl.N == 16 ? launch_n_pair<16>(xm, hm, p, 2 * grid, pl.smem, st)
-                            : launch_n_pair<32>(xm, hm, p, 2 * grid, pl.smem, st);
-        else
-            rc = pl.N == 32 ? launch_n<32>(xm, hm, p, grid, pl.smem, st) : launch_n<64>(xm, hm, p, grid, pl.smem, st);
-        unsigned long long hb[96 * 8];
-        DP_CUDA_CHECK(cudaStreamSynchronize(st));
-        DP_CUDA_CHECK(cudaMemcpy(hb, trace, sizeof hb, cudaMemcpyDeviceToHost));
-        const long long t0 = (long long)hb[20 * 8 + 0];
-        fprintf(stderr, "conv trace (CTA 0): i  M:top  M:tempty  M:full  M:issued  M:commits  E:tfull(row i)  E:drained\n");
-        for (int i = 16; i < 40; ++i) {
-            fprintf(stderr, "%3d", i);
-            for (int e = 0; e < 7; ++e) fprintf(stderr, " %7lld", hb[i * 8 + e] ? (long long)hb[i * 8 + e] - t0 : -1);
-            fprintf(stderr, "\n");
-        }
-        return rc;
     }
     int grid = p.n_units < sms ? p.n_units : sms;
     if (use_pair)
@@ -1400,7 +1355,7 @@ int run_conv_pair(const dp_conv_geom *g, bool dgrad, const PairPlan &pl, const v
                                    const_cast<void *>(in_halo), dims, strides, box, swz);
         if (rc) return rc;
     }
-    ConvTcParams p{};
+    ConvTcParams p;
     memset(&p, 0, sizeof(p));
     p.B = (int)g->batch;
     p.Cin = pl.Cin;
