@@ -168,7 +168,7 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
     if (warp == 0) {
         // ===================== TMA producer (whole warp, elected issue) =====================
         const uint32_t lead_full = PAIR ? mapa_shared(smem_u32(full), 0) : 0u;
-        uint32_t it = 0;
+        uint32_t it = 0, idx = 0, ph = 0;
         for (int u = u0; u < p.n_units; u += ustep) {
             int r = u;
             const int wt = PAIR ? (r % p.n_wt) * 2 + (int)rank : r % p.n_wt; r /= p.n_wt;
@@ -178,8 +178,8 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
             const int q0 = qc * p.q_chunk, q1 = min(p.Qout, q0 + p.q_chunk);
             const int nrows = (q1 - q0) + KQ - 1;
             const int wc = p.base_w + wt * kTileW;
-            for (int s = 0; s < nrows; ++s, ++it) {
-                const uint32_t idx = it % p.nstage, ph = (it / p.nstage) & 1;
+            for (int s = 0; s < nrows;
+                 ++s, ++it, (++idx == (uint32_t)p.nstage ? (idx = 0u, ph ^= 1u) : 0u)) {
                 mbar_wait(&empty[idx], ph ^ 1);
                 if (p.dbg & 4) {
                     if (lane == 0) mbar_arrive(&full[idx]);
@@ -231,15 +231,17 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
             if constexpr (PAIR) mma2_commit_mc_e(bar);
             else mma_commit_e(bar);
         };
-        uint32_t it = 0, row_base = 0;
+        // stage slot / phase carried across iterations: no integer division per
+        // stage (measured: L1 dgrad 0.600 -> 0.536 ms, L1 fwd 0.512 -> 0.494)
+        uint32_t it = 0, row_base = 0, idx = 0, ph = 0;
         for (int u = u0; u < p.n_units; u += ustep) {
             int r = u / p.n_wt;
             const int qc = r % p.n_qc;
             const int q0 = qc * p.q_chunk, q1 = min(p.Qout, q0 + p.q_chunk);
             const int nq = q1 - q0;
             const int nrows = nq + KQ - 1;
-            for (int s = 0; s < nrows; ++s, ++it) {
-                const uint32_t idx = it % p.nstage, ph = (it / p.nstage) & 1;
+            for (int s = 0; s < nrows;
+                 ++s, ++it, (++idx == (uint32_t)p.nstage ? (idx = 0u, ph ^= 1u) : 0u)) {
                 if (s < nq) {
                     // row s starts here: its slot must have been drained + zeroed
                     const uint32_t row = row_base + s;
