@@ -1591,42 +1591,51 @@ conv_wgrad_tc_kernel(const __grid_constant__ CUtensorMap xmap,
         const uint32_t astep = (16 * L.cbx * 2) >> 4;  // one K step = 16 w' rows
         const uint32_t bstep = (16 * L.cbd * 2) >> 4;
         const uint32_t mstep = (128 / L.cbx * L.boxx) >> 4;
-        uint32_t xi = 0, di = 0;   // X / dY ring counters (consumption order)
+        // X / dY ring slots and phases carried as counters (no integer division
+        // per row); the K-step loop is unrolled to its 16-step maximum with an
+        // early exit (a runtime-bounded MMA loop costs issue cycles per MMA)
+        uint32_t xidx = 0, xph = 0, didx = 0, dph = 0;
         uint32_t fresh = (1u << NMT) - 1u;  // accumulators not yet written
         for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
             int r = u / p.n_wt;
             const int qc = r % p.n_qc;
             const int q0 = qc * p.q_chunk, q1 = min(p.Qout, q0 + p.q_chunk);
             const int nq = q1 - q0, nrows = nq + KQ - 1;
-            const uint32_t xbase = xi;   // X ring index of this unit's row 0
+            uint32_t xs = xidx;          // X ring slot of this unit's output row j (kq = 0)
             for (int s = 0; s < nrows; ++s) {
-                const uint32_t xidx = xi % p.nx, xph = (xi / p.nx) & 1;
-                ++xi;
-                mbar_wait(&xfull[xidx], xph);
+                const uint32_t cx = xidx, cxph = xph;
+                if (++xidx == (uint32_t)p.nx) { xidx = 0; xph ^= 1u; }
+                mbar_wait(&xfull[cx], cxph);
                 const int j = s - (KQ - 1);   // output row complete with this input row
                 if (j < 0) continue;
-                const uint32_t didx = di % p.nd, dph = (di / p.nd) & 1;
-                ++di;
-                mbar_wait(&dfull[didx], dph);
+                const uint32_t cd = didx, cdph = dph;
+                if (++didx == (uint32_t)p.nd) { didx = 0; dph ^= 1u; }
+                mbar_wait(&dfull[cd], cdph);
                 tc_fence_after();
-                const uint32_t xs = (xbase + j) % p.nx;   // slot of input row j (kq = 0)
                 const uint64_t ax = a0 + ((xs * L.xslot) >> 4);
-                const uint64_t bd = b0 + ((didx * L.dslot) >> 4);
+                const uint64_t bd = b0 + ((cd * L.dslot) >> 4);
 #pragma unroll
                 for (int mt = 0; mt < NMT; ++mt) {
                     const uint32_t d = tmem + (uint32_t)(mt * NT);
                     const uint32_t bit = 1u << mt;
                     uint32_t acc = (fresh & bit) ? 0u : 1u;
                     fresh &= ~bit;
-                    for (int ks = 0; ks < p.kt; ++ks) {
+#pragma unroll
+                    for (int ks = 0; ks < 16; ++ks) {
+                        if (ks >= p.kt) break;
                         mma_bf16_e(d, ax + mt * mstep + ks * astep, bd + ks * bstep, idesc, acc);
                         acc = 1u;
                     }
                 }
-                mma_commit_e(&dempty[didx]);          // dY row j is done
+                mma_commit_e(&dempty[cd]);            // dY row j is done
                 mma_commit_e(&xempty[xs]);            // input row j: its last tap (kq = 0)
+                uint32_t xn = xs + 1 == (uint32_t)p.nx ? 0u : xs + 1;
                 if (j == nq - 1)                      // unit end: rows j+1.. are never kq=0
-                    for (int t = 1; t < KQ; ++t) mma_commit_e(&xempty[(xbase + j + t) % p.nx]);
+                    for (int t = 1; t < KQ; ++t) {
+                        mma_commit_e(&xempty[xn]);
+                        xn = xn + 1 == (uint32_t)p.nx ? 0u : xn + 1;
+                    }
+                xs = xs + 1 == (uint32_t)p.nx ? 0u : xs + 1;
             }
         }
         mma_commit_e(done);
@@ -2046,27 +2055,28 @@ conv_wgrad_ts_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_cons
         // ===================== MMA issuer =====================
         const uint64_t b0 = sdesc_mn(smem_u32(xring), S::BOXX, 8 * S::CBX * 2, swz_layout(S::CBX));
         constexpr uint32_t bstep = (16 * S::CBX * 2) >> 4;   // one K step = 16 w' rows
-        uint32_t xi = 0, di = 0;
+        // ring slots / phases carried as counters (no integer division per row:
+        // it costs MMA-warp issue time, cf. the fwd kernel)
+        uint32_t xidx = 0, xph = 0, aidx = 0, aph = 0;
         bool fresh = true;
         for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
             int r = u / p.n_wt;
             const int qc = r % p.n_qc;
             const int q0 = qc * p.q_chunk, q1 = min(p.Qout, q0 + p.q_chunk);
             const int nq = q1 - q0, nrows = nq + KQ - 1;
-            const uint32_t xbase = xi;
+            uint32_t xs = xidx;                    // X slot of output row j (= unit row j)
             for (int s = 0; s < nrows; ++s) {
-                const uint32_t xidx = xi % p.nx, xph = (xi / p.nx) & 1;
-                ++xi;
-                mbar_wait(&xfull[xidx], xph);
+                const uint32_t cx = xidx, cph = xph;
+                if (++xidx == (uint32_t)p.nx) { xidx = 0; xph ^= 1u; }
+                mbar_wait(&xfull[cx], cph);
                 const int j = s - (KQ - 1);
                 if (j < 0) continue;
-                const uint32_t aidx = di % p.na, aph = (di / p.na) & 1;
-                ++di;
-                mbar_wait(&afull[aidx], aph);
+                const uint32_t ca = aidx, caph = aph;
+                if (++aidx == (uint32_t)p.na) { aidx = 0; aph ^= 1u; }
+                mbar_wait(&afull[ca], caph);
                 tc_fence_after();
-                const uint32_t xs = (xbase + j) % p.nx;
                 const uint64_t bx = b0 + ((xs * S::XSLOT) >> 4);
-                const uint32_t acol = tmem + S::ACOL + aidx * S::ACOLS;
+                const uint32_t acol = tmem + S::ACOL + ca * S::ACOLS;
 #pragma unroll
                 for (int ks = 0; ks < kTsKT; ++ks) {
                     if (p.dbg & 2) break;
@@ -2081,10 +2091,15 @@ conv_wgrad_ts_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_cons
                     }
                 }
                 fresh = false;
-                mma_commit_e(&aempty[aidx]);
+                mma_commit_e(&aempty[ca]);
                 mma_commit_e(&xempty[xs]);
+                uint32_t xn = xs + 1 == (uint32_t)p.nx ? 0u : xs + 1;
                 if (j == nq - 1)
-                    for (int t = 1; t < KQ; ++t) mma_commit_e(&xempty[(xbase + j + t) % p.nx]);
+                    for (int t = 1; t < KQ; ++t) {
+                        mma_commit_e(&xempty[xn]);
+                        xn = xn + 1 == (uint32_t)p.nx ? 0u : xn + 1;
+                    }
+                xs = xs + 1 == (uint32_t)p.nx ? 0u : xs + 1;
             }
         }
         mma_commit_e(done);
@@ -2102,14 +2117,14 @@ conv_wgrad_ts_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_cons
             const int mi = lane >> 3, ri = lane & 7;
             const int chunk = mi & 1;
             const int rbase = 8 * (mi >> 1) + ri + KW - 1 - kw;
-            uint32_t di = 0;
+            uint32_t didx = 0, dph = 0, aidx = 0, aph = 0;
             for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
                 int r = u / p.n_wt;
                 const int qc = r % p.n_qc;
                 const int q0 = qc * p.q_chunk, q1 = min(p.Qout, q0 + p.q_chunk);
-                for (int s = 0; s < q1 - q0; ++s, ++di) {
-                    const uint32_t didx = di % p.nd, dph = (di / p.nd) & 1;
-                    const uint32_t aidx = di % p.na, aph = (di / p.na) & 1;
+                for (int s = 0; s < q1 - q0; ++s,
+                         (++didx == (uint32_t)p.nd ? (didx = 0u, dph ^= 1u) : 0u),
+                         (++aidx == (uint32_t)p.na ? (aidx = 0u, aph ^= 1u) : 0u)) {
                     mbar_wait(&dfull[didx], dph);
                     mbar_wait(&aempty[aidx], aph ^ 1);
                     tc_fence_after();
