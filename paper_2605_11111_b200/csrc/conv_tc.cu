@@ -1529,7 +1529,7 @@ conv_wgrad_tc_kernel(const __grid_constant__ CUtensorMap xmap,
 
     if (warp == 0) {
         // ===================== TMA producer (whole warp, elected issue) =====================
-        uint32_t xi = 0, di = 0;
+        uint32_t pxi = 0, pxph = 0, pdi = 0, pdph = 0;   // X / dY ring slots and phases
         const uint32_t xrow = (uint32_t)(KP * L.nbx * WK * L.cbx * 2);
         const uint32_t dbytes = (uint32_t)(KW * L.nbd * WK * L.cbd * 2);
         for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
@@ -1543,8 +1543,8 @@ conv_wgrad_tc_kernel(const __grid_constant__ CUtensorMap xmap,
             const int w0 = wt * WK;
             for (int s = 0; s < nrows; ++s) {
                 {   // X: input row q = base_q + q0 + s, all kp (and its mirror slot)
-                    const uint32_t idx = xi % p.nx, ph = (xi / p.nx) & 1;
-                    ++xi;
+                    const uint32_t idx = pxi, ph = pxph;
+                    if (++pxi == (uint32_t)p.nx) { pxi = 0; pxph ^= 1u; }
                     const bool mirror = (int)idx < KQ - 1;
                     mbar_wait(&xempty[idx], ph ^ 1);
                     mbar_expect_tx_e(&xfull[idx], mirror ? 2 * xrow : xrow);
@@ -1571,8 +1571,8 @@ conv_wgrad_tc_kernel(const __grid_constant__ CUtensorMap xmap,
                     }
                 }
                 if (s < nq) {  // dY row q0 + s, KW shifted copies
-                    const uint32_t idx = di % p.nd, ph = (di / p.nd) & 1;
-                    ++di;
+                    const uint32_t idx = pdi, ph = pdph;
+                    if (++pdi == (uint32_t)p.nd) { pdi = 0; pdph ^= 1u; }
                     mbar_wait(&dempty[idx], ph ^ 1);
                     mbar_expect_tx_e(&dfull[idx], dbytes);
                     uint8_t *dst = dring + (size_t)idx * L.dslot;
@@ -1981,7 +1981,7 @@ conv_wgrad_ts_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_cons
 
     if (warp == 0) {
         // ===================== TMA producer =====================
-        uint32_t xi = 0, di = 0;
+        uint32_t pxi = 0, pxph = 0, pdi = 0, pdph = 0;   // X / dY ring slots and phases
         constexpr uint32_t xrow = (uint32_t)(KP * S::NBX * kTsWK * S::CBX * 2);
         constexpr uint32_t dbytes = 2u * (kTsWK + KW - 1) * kTsDRow;
         for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
@@ -2001,8 +2001,8 @@ conv_wgrad_ts_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_cons
             const int w0 = p.w_lo + wt * kTsWK;
             for (int s = 0; s < nrows; ++s) {
                 {
-                    const uint32_t idx = xi % p.nx, ph = (xi / p.nx) & 1;
-                    ++xi;
+                    const uint32_t idx = pxi, ph = pxph;
+                    if (++pxi == (uint32_t)p.nx) { pxi = 0; pxph ^= 1u; }
                     const bool mirror = (int)idx < KQ - 1;
                     mbar_wait(&xempty[idx], ph ^ 1);
                     if (p.dbg & 4) {
@@ -2036,8 +2036,8 @@ conv_wgrad_ts_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_cons
                     }
                 }
                 if (s < nq) {  // dY row q0 + s: two 16-channel halves, w' in [w0 - 2, w0 + 128)
-                    const uint32_t idx = di % p.nd, ph = (di / p.nd) & 1;
-                    ++di;
+                    const uint32_t idx = pdi, ph = pdph;
+                    if (++pdi == (uint32_t)p.nd) { pdi = 0; pdph ^= 1u; }
                     mbar_wait(&dempty[idx], ph ^ 1);
                     if (p.dbg & 4) {
                         if (lane == 0) mbar_arrive(&dfull[idx]);
