@@ -285,6 +285,24 @@ def test_attention_tc_fwd_bwd_vs_oracle(case, payload):
         assert rel_err(to_np(got), want, floor=1.0) < 1.5e-2
 
 
+def test_conv_single_cta_and_per_mma_issue_paths():
+    """The non-default conv issue paths stay correct: single-CTA MMAs
+    (DP_CONV_2CTA=0) and one elect per MMA instead of the grouped kw taps
+    (DP_CONV_DBG=32), each over the tcgen05 conv parity cases."""
+    import os
+    import subprocess
+    import sys
+
+    here = os.path.dirname(os.path.abspath(__file__))
+    for env_extra in ({"DP_CONV_2CTA": "0"}, {"DP_CONV_DBG": "32"}):
+        env = dict(os.environ, **env_extra)
+        r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x",
+                            os.path.join(here, "test_gpu_kernels.py"),
+                            "-k", "test_conv_tc_fwd_dgrad_vs_oracle"], env=env, capture_output=True,
+                           text=True, timeout=600)
+        assert r.returncode == 0, str(env_extra) + r.stdout[-2000:] + r.stderr[-2000:]
+
+
 def test_conv_pair_kernel_opt_in():
     """The CTA-pair (cta_group::2) conv kernel is opt-in (DP_CONV_PAIR=1, read
     once per process): run the tcgen05 conv parity cases with it enabled."""
