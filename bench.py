@@ -844,9 +844,16 @@ def main():
                 "flops_per_launch": d["flops"] / d["launches"]}
     cpu = None
     if not args.no_cpu_baseline and ctx.mesh.world_size == 1:
-        dt, frac = cpu_fn(1)
+        # repeat the one-core sample until ~10 s of CPU work (at most 200 repeats)
+        dt = frac = 0.0
+        reps = 0
+        while reps < 200 and (reps == 0 or dt < 10.0):
+            d1, f1 = cpu_fn(1)
+            dt += d1
+            frac += f1
+            reps += 1
         cpu = {"value": frac / dt, "unit": W["unit"], "cores": 1, "kind": "port",
-               "sample": sample_desc, "seconds": dt}
+               "sample": f"{reps} x ({sample_desc})", "seconds": dt}
     line = {
         "metric": "sharded fwd+bwd step latency & samples/s",
         "value": value, "unit": W["unit"], "n_gpus": ctx.mesh.world_size, "steps": args.steps,
