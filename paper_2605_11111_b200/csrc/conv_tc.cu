@@ -361,7 +361,7 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
             const int w = wt * kTileW + m;
             for (int j = 0; j < q1 - q0; ++j) {
                 const uint32_t row = row_base + j, slot = row % NSLOT;
-                mbar_wait(&tfull[slot], (row / NSLOT) & 1);
+                mbar_wait_sleep(&tfull[slot], (row / NSLOT) & 1);
                 tc_fence_after();
                 const uint32_t col = lane_base + (NSLOT - 1 - slot) * N;
                 uint32_t v[N];

@@ -47,6 +47,24 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
         : "memory");
 }
 
+// wait with a nanosleep back-off between polls, for warps whose waits are
+// long and off the issue-critical path (so their polling leaves issue slots
+// to an MMA warp on the same SM sub-partition)
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "LAB_WAITS:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@P1 bra DONES;\n"
+        "nanosleep.u32 32;\n"
+        "bra LAB_WAITS;\n"
+        "DONES:\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
 // busy-poll wait (mbarrier.test_wait never suspends the thread)
 __device__ __forceinline__ void mbar_wait_spin(uint64_t *bar, uint32_t parity) {
     asm volatile(
