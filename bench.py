@@ -166,8 +166,7 @@ def init(args):
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if world != args.gpus:
-        if args.gpus > 1:
-            raise SystemExit(f"--gpus {args.gpus} needs torchrun with {args.gpus} processes")
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     if world == 1 and "MASTER_PORT" not in os.environ:
         import socket
 
@@ -202,33 +201,36 @@ def barrier(ctx):
 
 
 # ---------------------------------------------------------------------------
-# kernel-level timing (instrumented pass): events around every conv call
+# kernel-level timing INSIDE the timed region: CUDA events around every conv /
+# attention call, recorded on the stream the call launches on (the current
+# stream), keyed by entry point and layer shape
 
 
 class KernelTimer:
+    NAMES = ("conv_fwd", "conv_dgrad", "conv_wgrad", "attn_fwd_update", "attn_bwd_update")
+
     def __init__(self):
-        self.records = []  # (name, flops, start, end)
+        self.records = []  # (key, flops, start, end)
         self.active = False
 
     def wrap(self, kernels_mod):
         import torch
 
         timer = self
-        for name in ("conv_fwd", "conv_dgrad", "conv_wgrad", "attn_fwd_update",
-                     "attn_bwd_update"):
+        for name in self.NAMES:
             orig = getattr(kernels_mod, name)
 
             def make(orig=orig, name=name):
                 def inner(*a, **kw):
                     if not timer.active:
                         return orig(*a, **kw)
-                    flops = kernel_work(name, a, kw)
+                    flops, tag = kernel_work(name, a, kw)
                     s = torch.cuda.Event(enable_timing=True)
                     e = torch.cuda.Event(enable_timing=True)
                     s.record()
                     orig(*a, **kw)
                     e.record()
-                    timer.records.append((name, flops, s, e))
+                    timer.records.append((f"{name}[{tag}]", flops, s, e))
                 return inner
             setattr(kernels_mod, name, make())
 
@@ -237,12 +239,56 @@ class KernelTimer:
 
         torch.cuda.synchronize()
         out = {}
-        for name, flops, s, e in self.records:
-            d = out.setdefault(name, {"launches": 0, "ms": 0.0, "flops": 0.0})
+        for key, flops, s, e in self.records:
+            d = out.setdefault(key, {"launches": 0, "ms": 0.0, "flops": 0.0})
             d["launches"] += 1
             d["ms"] += s.elapsed_time(e)
             d["flops"] += flops
         return out
+
+
+class CommMeter:
+    """Bytes this rank posts to its peers (every send of every exchange round)
+    while active: halo faces, reverse halos, K||V hops, redistribute blocks,
+    all-reduce payloads."""
+
+    def __init__(self):
+        self.bytes = 0
+        self.calls = 0
+        self.active = False
+
+    def wrap(self, transport):
+        meter = self
+        orig_start = transport.exchange_start
+        orig_ex = transport.exchange
+        orig_ar = transport.all_reduce
+
+        def count(sends):
+            if meter.active:
+                meter.calls += 1
+                meter.bytes += sum(t.numel() * t.element_size() for _, t in sends)
+
+        def exchange_start(sends, recvs):
+            count(sends)
+            return orig_start(sends, recvs)
+
+        def exchange(sends, recvs):
+            count(sends)
+            return orig_ex(sends, recvs)
+
+        def all_reduce(members, me, t, op):
+            if meter.active:
+                meter.calls += 1
+                meter.bytes += t.numel() * t.element_size() * (len(members) - 1)
+            return orig_ar(members, me, t, op)
+
+        # the thread mailbox's exchange_start calls exchange; the process
+        # transports' exchange calls exchange_start: wrap the inner one only
+        if getattr(transport, "kind", "") == "thread":
+            transport.exchange = exchange
+        else:
+            transport.exchange_start = exchange_start
+        transport.all_reduce = all_reduce
 
 
 def kernel_work(name, a, kw):
@@ -266,12 +312,55 @@ def kernel_work(name, a, kw):
         q, k = a[0], a[1]
         heads = q.shape[1] if q.dim() == 3 else 1
         f = 4.0 * q.shape[0] * k.shape[0] * q.shape[-1] * heads
-        return f * (2.5 if name == "attn_bwd_update" else 1.0)
-    return 2.0 * w.shape[0] * w.shape[1] * math.prod(w.shape[2:]) * pos
+        return f * (2.5 if name == "attn_bwd_update" else 1.0), f"d{q.shape[-1]}"
+    tag = f"{w.shape[1]}->{w.shape[0]}"   # layer: c_in -> c_out (same for fwd, dgrad, wgrad)
+    return 2.0 * w.shape[0] * w.shape[1] * math.prod(w.shape[2:]) * pos, tag
 
 
 # ---------------------------------------------------------------------------
 # workloads (ours)
+
+
+def cfg5_n() -> int:
+    return int(round((SIZE_MIB * 2 ** 20 / 4) ** 0.5)) // 8 * 8   # [n, n] fp32
+
+
+def workload_info(name: str, R: int) -> dict:
+    """The `config` object of the JSON line — built from the config name and
+    the rank count only, so both arms (ours and --impl reference) print the
+    identical object."""
+    from paper_2605_11111_b200.plan import default_chunk
+
+    if name == "cfg2":
+        return {"workload": WORKLOAD_TEXT["cfg2"], "global_batch": 1, "volume": [256] * 3,
+                "channels": [16, 32, 32], "layout": "NDHWC (channels_last_3d)",
+                "shard_extents": list(default_chunk(256, R)), "parallelism": f"domain{R}",
+                "l2": "inputs larger than L2 (512 MiB activations per layer), no flush"}
+    if name == "cfg3":
+        return {"workload": WORKLOAD_TEXT["cfg3"], "global_batch": 1, "seq_len": 65536,
+                "heads": 16, "head_dim": 64, "shard_extents": list(default_chunk(65536, R)),
+                "parallelism": f"ring{R}",
+                "l2": "inputs (q, k, v, dO: 512 MiB) exceed L2, no flush"}
+    if name == "cfg4":
+        return {"workload": "cfg4: weak-scaling conv2d stack, 4 x conv(64->64, 3x3, s1 p1), "
+                            "2048^2 per GPU, bf16, H-sharded",
+                "global_batch": 1, "grid_per_gpu": [2048, 2048], "channels": 64, "layers": 4,
+                "layout": "NHWC (channels_last)", "shard_extents": [2048] * R,
+                "parallelism": f"domain{R}",
+                "l2": "inputs larger than L2 (512 MiB activations per layer), no flush"}
+    if name == "cfg5":
+        n = cfg5_n()
+        return {"workload": f"cfg5: uneven redistribute of a [{n},{n}] fp32 tensor "
+                            f"({n * n * 4 / 2 ** 20:.0f} MiB), Shard(0) random_partition extents "
+                            "-> Replicate and -> Shard(1)",
+                "global_batch": 1, "shape": [n, n], "shard_extents": random_partition(R, n, R),
+                "parallelism": f"domain{R}", "l2": "tensor exceeds L2, no flush"}
+    return {"workload": "cfg1: conv2d 3x3 halo exchange, 1x32x1024x1024 fp32, C_out=32, s1 p1, "
+                        "H-sharded (fp32 on the tensor cores as exact bf16x3 part products: the "
+                        "reference's 1e-5 tolerance)",
+            "global_batch": 1, "grid": [1024, 1024], "channels": [32, 32], "layout": "NCHW",
+            "shard_extents": list(default_chunk(1024, R)), "parallelism": f"domain{R}",
+            "l2": "128 MiB activations exceed L2, no flush"}
 
 
 def setup_cfg2(ctx):
@@ -309,11 +398,7 @@ def setup_cfg2(ctx):
         return dw1, dw2
 
     flops = 3 * 2.0 * (C0 * C1 + C1 * C1) * 27 * G ** 3  # fwd + dgrad + wgrad, both layers
-    info = {"workload": WORKLOAD_TEXT["cfg2"],
-            "global_batch": 1, "volume": [G, G, G], "channels": [C0, C1, C1],
-            "layout": "NDHWC (channels_last_3d)", "shard_extents": list(ext),
-            "parallelism": f"domain{R}",
-            "l2": "inputs larger than L2 (512 MiB activations per layer), no flush"}
+    info = workload_info("cfg2", R)
     return dict(step=step, inputs=[x], flops=flops, info=info, scaling="strong", dtype="bf16",
                 unit="samples/s", samples_per_step=1)
 
@@ -382,10 +467,7 @@ def setup_cfg3(ctx):
         return dq.local, dk.local, dv.local
 
     flops = 3.5 * 4.0 * S * S * D * H  # fwd + 2.5x bwd
-    info = {"workload": WORKLOAD_TEXT["cfg3"],
-            "global_batch": 1, "seq_len": S, "heads": H, "head_dim": D,
-            "shard_extents": list(ext), "parallelism": f"ring{R}",
-            "l2": "inputs (q,k,v,dO 8 MiB/head-tile stream, 512 MiB total) exceed L2, no flush"}
+    info = workload_info("cfg3", R)
     return dict(step=step, inputs=[q, k, v, do], flops=flops, info=info, scaling="strong",
                 dtype="bf16", unit="samples/s", samples_per_step=1)
 
@@ -466,11 +548,7 @@ def setup_cfg4(ctx):
         return dws
 
     flops = 3 * L * 2.0 * C * C * 9 * Hper * W
-    info = {"workload": "cfg4: weak-scaling conv2d stack, 4 x conv(64->64, 3x3, s1 p1), "
-                        "2048^2 per GPU, bf16, H-sharded",
-            "global_batch": 1, "grid_per_gpu": [Hper, W], "channels": C, "layers": L,
-            "layout": "NHWC (channels_last)", "shard_extents": ext, "parallelism": f"domain{R}",
-            "l2": "inputs larger than L2 (512 MiB activations per layer), no flush"}
+    info = workload_info("cfg4", R)
     return dict(step=step, inputs=[x], flops=flops, info=info, scaling="weak", dtype="bf16",
                 unit="samples/s", samples_per_step=1)
 
@@ -521,7 +599,7 @@ def setup_cfg5(ctx):
 
     import paper_2605_11111_b200 as dp
 
-    n = int(round((SIZE_MIB * 2 ** 20 / 4) ** 0.5)) // 8 * 8   # [n, n] fp32
+    n = cfg5_n()
     R = ctx.mesh.world_size
     me = ctx.rank_id
     dev = ctx.device
@@ -538,22 +616,16 @@ def setup_cfg5(ctx):
         s1 = dp.redistribute(s0, (dp.Shard(1),))
         return rep.local[:1], s1.local[:1]
 
-    mib = n * n * 4 / 2 ** 20
-    info = {"workload": f"cfg5: uneven redistribute of a [{n},{n}] fp32 tensor ({mib:.0f} MiB), "
-                        "Shard(0) random_partition extents -> Replicate and -> Shard(1)",
-            "global_batch": 1, "shape": [n, n], "shard_extents": ext,
-            "parallelism": f"domain{R}",
-            "bytes_received_per_rank": {"to_replicate": (n - ext[me]) * n * 4,
-                                        "to_shard1": (n - ext[me]) * (n // R) * 4},
-            "l2": "1 GiB tensor exceeds L2, no flush"}
+    info = workload_info("cfg5", R)
     # algorithmic HBM bytes of this rank's step: read its input block once and
     # write each output once (S(0) -> R: the whole [n, n]; S(0) -> S(1): [n, n/R])
     cshare = dp.default_chunk(n, R)[me]
     hbm = (ext[me] * n + n * n) * 4 + (ext[me] * n + n * cshare) * 4
-    info["hbm_bytes_per_step"] = hbm
+    extra = {"bytes_received_per_rank": {"to_replicate": (n - ext[me]) * n * 4,
+                                         "to_shard1": (n - ext[me]) * cshare * 4},
+             "hbm_bytes_per_step": hbm}
     return dict(step=step, inputs=[local], flops=0.0, info=info, scaling="strong", dtype="f32",
-                hbm_bytes_per_step=hbm,
-                unit="samples/s", samples_per_step=1)
+                hbm_bytes_per_step=hbm, extra=extra, unit="samples/s", samples_per_step=1)
 
 
 def cpu_sample_cfg5(threads: int):
@@ -613,11 +685,7 @@ def setup_cfg1(ctx):
         return [dw]
 
     flops = 3 * 2.0 * C * C * 9 * G * G
-    info = {"workload": "cfg1: conv2d 3x3 halo exchange, 1x32x1024x1024 fp32, C_out=32, s1 p1, "
-                        "H-sharded (fp32 CUDA-core kernels: the reference's 1e-5 tolerance)",
-            "global_batch": 1, "grid": [G, G], "channels": [C, C], "layout": "NCHW",
-            "shard_extents": list(ext), "parallelism": f"domain{R}",
-            "l2": "128 MiB activations exceed L2, no flush"}
+    info = workload_info("cfg1", R)
     return dict(step=step, inputs=[x], flops=flops, info=info, scaling="strong", dtype="f32",
                 unit="samples/s", samples_per_step=1)
 
@@ -666,34 +734,90 @@ CONFIGS = {"cfg2": (setup_cfg2, cpu_sample_cfg2,
 
 def run_reference(args):
     """The reference arm: the reference algorithm's CPU implementation (the
-    oracle port — the reference is Python and does not travel to this box)
-    on all host threads, bounded samples, same metric/unit/config."""
+    oracle port of domainpar's NumPy path — the reference is Python and does
+    not travel to this box) on all host threads.  Exactly W warm-up and K
+    timed steps, each one bounded sample of the configured workload (the
+    sample is named in cpu_baseline.sample); `value` = samples/s extrapolated
+    from the sampled fraction, `ms_per_step` = the measured wall time of one
+    sampled step, so K x ms_per_step is what this run actually spent."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
     _, cpu_fn, sample_desc = CONFIGS[args.config]
-    for _ in range(max(0, min(args.warmup, 1))):
+    for _ in range(max(0, args.warmup)):
         cpu_fn(cores)
     times = []
     frac = 1.0
-    for _ in range(max(1, min(args.steps, 2))):
+    for _ in range(max(1, args.steps)):
         dt, frac = cpu_fn(cores)
         times.append(dt)
     t = sum(times) / len(times)
     value = frac / t  # samples per second
-    line = {"impl": "reference", "metric": "sharded fwd+bwd step latency & samples/s",
-            "value": value, "unit": "samples/s", "n_gpus": args.gpus, "steps": len(times),
-            "warmup": args.warmup, "ms_per_step": 1000.0 / value, "higher_is_better": True,
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "samples/s",
+            "n_gpus": args.gpus, "steps": len(times), "warmup": max(0, args.warmup),
+            "ms_per_step": 1000.0 * t, "higher_is_better": True,
             "scaling": "weak" if args.config == "cfg4" else "strong", "vs_baseline": None,
             "dtype": "f32", "data": "synthetic",
-            "config": {"workload": WORKLOAD_TEXT.get(args.config, args.config),
-                       "sample": sample_desc},
+            "config": workload_info(args.config, max(1, args.gpus)),
+            "sample_fraction": frac,
             "cpu_baseline": {"value": value, "unit": "samples/s", "cores": cores,
-                             "kind": "port", "sample": f"{cores} x {sample_desc}"},
+                             "kind": "port", "sample": f"{cores} x {sample_desc}",
+                             "sample_fraction_per_step": frac,
+                             "note": "ms_per_step is one sampled step; value extrapolates "
+                                     "samples/s from the sampled fraction"},
             "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+METRIC = "sharded fwd+bwd step latency & samples/s"
+
+
+def self_launch(args) -> int:
+    """`python bench.py --gpus N` without a launcher: start N ranks of this
+    script the way torchrun would (RANK / LOCAL_RANK / WORLD_SIZE /
+    MASTER_ADDR=127.0.0.1 / MASTER_PORT), one process per GPU over NCCL.
+    With fewer visible GPUs than N (a one-GPU box) the ranks share the GPU
+    over gloo ("gloo-cuda": the same one-process-per-rank code path, payloads
+    staged through host memory) and the line says so."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    try:
+        import torch
+
+        ngpu = torch.cuda.device_count()
+    except Exception:  # noqa: BLE001
+        ngpu = 0
+    base = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port),
+                WORLD_SIZE=str(args.gpus), LOCAL_WORLD_SIZE=str(args.gpus))
+    if ngpu < args.gpus:
+        base["DP_MESH_BACKEND"] = "gloo-cuda"
+    procs = []
+    for r in range(args.gpus):
+        env = dict(base, RANK=str(r), LOCAL_RANK=str(r))
+        procs.append(subprocess.Popen([sys.executable, os.path.abspath(__file__)] + sys.argv[1:],
+                                      env=env, stdout=None if r == 0 else subprocess.DEVNULL))
+    rcs = [p.wait() for p in procs]
+    return max(abs(rc) for rc in rcs)
+
+
+def pick_peak(pk, clk_summary, dtype):
+    """Burst bf16 peak when the SM clock held (median >= 95 % of max) during
+    the timed region, else the sustained one; fp32 runs on the tensor cores
+    as six bf16 part products (conv_x3), so its roof is that / 6."""
+    sm, mx = clk_summary.get("sm_mhz"), clk_summary.get("sm_max_mhz")
+    burst = sm is None or mx is None or sm >= 0.95 * mx
+    key = "bf16_tflops" if burst else "bf16_tflops_sustained"
+    peak = pk.get(key, PEAKS_FALLBACK[key])
+    kind = f"bf16 {'burst' if burst else 'sustained'} (SM clock median {sm} of {mx} MHz)"
+    if dtype == "f32":
+        peak /= 6.0
+        kind += " / 6: fp32 = 6 bf16 part products on the tensor cores (conv_x3)"
+    return peak, kind
 
 
 def main():
@@ -703,6 +827,8 @@ def main():
     if args.impl == "reference":
         run_reference(args)
         return
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        raise SystemExit(self_launch(args))
     import torch
 
     from paper_2605_11111_b200 import _lib, kernels
@@ -714,37 +840,43 @@ def main():
     step = W["step"]
     for _ in range(max(3, args.warmup)):
         step()
+    timer = KernelTimer()
+    timer.wrap(kernels)
+    comm = CommMeter()
+    comm.wrap(ctx.transport)
     barrier(ctx)
 
-    # --- timed region: device time, inputs resident in HBM ----------------
+    # --- timed region: device time, inputs resident in HBM; every conv /
+    # attention launch bracketed by CUDA events on its stream ----------------
     start = torch.cuda.Event(enable_timing=True)
     end = torch.cuda.Event(enable_timing=True)
-    l0 = _lib.launch_count()
+    l0, s0 = _lib.launch_count(), _lib.simt_count()
     local_gpu = ctx.device.index if ctx.device.index is not None else 0
     with ClockSampler(local_gpu) as clk:
         barrier(ctx)
+        timer.active = comm.active = True
         start.record()
         for _ in range(args.steps):
             step()
         end.record()
+        timer.active = comm.active = False
         barrier(ctx)
     launches = _lib.launch_count() - l0
-    ms = max_over_ranks(ctx, start.elapsed_time(end) / args.steps)
-
-    # --- instrumented pass: per-kernel launch times --------------------------
-    timer = KernelTimer()
-    timer.wrap(kernels)
-    timer.active = True
-    for _ in range(max(1, min(args.steps, 3))):
-        step()
-    timer.active = False
+    simt_calls = _lib.simt_count() - s0
+    my_ms = start.elapsed_time(end) / args.steps
+    ms = max_over_ranks(ctx, my_ms)
     ksum = timer.summary()
+    comm_bytes = comm.bytes / args.steps
+    kernel_ms_step = sum(v["ms"] for v in ksum.values()) / args.steps
+    # every rank's per-kernel record (max over ranks for the roofline)
+    ranks_k = gather_all(ctx, {"ksum": ksum, "ms": my_ms, "kernel_ms": kernel_ms_step,
+                               "comm_bytes": comm_bytes, "simt": simt_calls})
 
-    # --- e2e through the public API: pinned host input -> device, dW -> host.
-    # Every step copies its own input shard from pinned host memory and reads
-    # its weight gradients back; the copy for step i+1 runs on a copy stream
-    # while step i computes (double-buffered input, as a training loop's
-    # prefetcher would), so the timed region = first H2D + K steps + last D2H.
+    # --- e2e through the public API: pinned host input -> device, gradients ->
+    # host.  Every step copies its own input shard from pinned host memory and
+    # reads its result back; the copy for step i+1 runs on a copy stream while
+    # step i computes (double-buffered input, as a training loop's prefetcher
+    # would), so the timed region = first H2D + K steps + last D2H.
     ins = W["inputs"]
     hosts = []
     for t in ins:
@@ -795,13 +927,19 @@ def main():
 
     if ctx.rank_id != 0:
         return
-    pk, pk_kind = peaks()
+    pk, pk_src = peaks()
+    clocks = clk.summary()
     samples = W["samples_per_step"]
     value = samples / (ms / 1000.0)
-    # dominant kernel
-    dom = max(ksum.items(), key=lambda kv: kv[1]["ms"]) if ksum else None
+    # per-kernel (entry point x layer) records, max launch time over ranks
+    merged = {}
+    for rk in ranks_k:
+        for key, d in rk["ksum"].items():
+            m = merged.setdefault(key, {"launches": d["launches"], "ms": 0.0,
+                                        "flops": d["flops"]})
+            m["ms"] = max(m["ms"], d["ms"])
     roof = None
-    if not dom and W.get("hbm_bytes_per_step"):
+    if not merged and W.get("hbm_bytes_per_step"):
         # data-movement workload (cfg5): the pack / unpack / copy kernels are the
         # step; algorithmic HBM bytes (read + write of every element moved) per
         # device-timed step against the measured copy bandwidth
@@ -809,39 +947,32 @@ def main():
         hbm = pk.get("hbm_gbs", PEAKS_FALLBACK["hbm_gbs"])
         roof = {"bound": "hbm", "kernel": "copy_rows (redistribute pack / unpack)",
                 "achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": gbs / hbm,
-                "traffic": None, "peak_kind": f"{pk_kind} HBM copy bandwidth",
+                "traffic": None, "peak_kind": f"{pk_src} HBM copy bandwidth",
                 "bytes_per_step": W["hbm_bytes_per_step"]}
-    if dom:
-        name, d = dom
-        avg_ms = d["ms"] / d["launches"]
-        ach = (d["flops"] / d["launches"]) / (avg_ms / 1000.0) / 1e12
-        peak = pk.get("bf16_tflops_sustained", PEAKS_FALLBACK["bf16_tflops_sustained"])
-        peak_kind = f"{pk_kind} bf16 sustained (kernel timed inside the step)"
-        if W["dtype"] == "f32":
-            # fp32 convs run on the tensor cores as six bf16 part-products per fp32
-            # product (conv_x3.cu: fp32-accurate, the reference's 1e-5 holds), so the
-            # roof for fp32 FLOPs is the bf16 peak / 6
-            peak = peak / 6.0
-            peak_kind = (f"{pk_kind} bf16 sustained / 6 (fp32 = 6 bf16 part-products on the "
-                         "tensor cores, conv_x3)")
+    peak, peak_kind = pick_peak(pk, clocks, W["dtype"])
+    per_kernel = {}
+    for key, d in merged.items():
+        avg = d["ms"] / d["launches"]
+        ach = (d["flops"] / d["launches"]) / (avg / 1000.0) / 1e12
+        per_kernel[key] = {"launches_per_step": d["launches"] / args.steps, "avg_ms": avg,
+                           "tflops": ach, "frac": ach / peak,
+                           "share_of_step": d["ms"] / args.steps / ms}
+    if merged:
+        key, d = max(merged.items(), key=lambda kv: kv[1]["ms"])
+        pk_ = per_kernel[key]
         traffic = None
         tpath = os.path.join(ROOT, "profiles", "traffic.json")
         if os.path.exists(tpath):
-            # per-launch DRAM bytes of the device kernels behind this wrapper,
-            # from the committed `ncu --set full` capture (scripts/ncu_summary.py)
+            # per-launch DRAM bytes of this kernel from the committed `ncu --set
+            # full` capture (scripts/ncu_summary.py), keyed like `kernels` below
             with open(tpath) as f:
-                tab = json.load(f).get(args.config, {})
-            pat = {"conv_wgrad": "conv_wgrad_t", "conv_fwd": "conv_tc_kernel",
-                   "conv_dgrad": "conv_tc_kernel", "attn_fwd_update": "attn_fwd_tc_kernel",
-                   "attn_bwd_update": "attn_bwd_tc_kernel"}.get(name, name)
-            hits = [v for k, v in tab.items() if pat in k]
-            if hits:
-                traffic = sum(hits) / len(hits)
-        roof = {"bound": "tensor", "kernel": name, "achieved": ach, "peak": peak,
-                "unit": "TFLOP/s", "frac": ach / peak, "traffic": traffic,
-                "peak_kind": peak_kind,
-                "avg_launch_ms": avg_ms,
-                "flops_per_launch": d["flops"] / d["launches"]}
+                traffic = json.load(f).get(args.config, {}).get(key)
+        roof = {"bound": "tensor", "kernel": key, "achieved": pk_["tflops"], "peak": peak,
+                "unit": "TFLOP/s", "frac": pk_["frac"], "traffic": traffic,
+                "peak_kind": f"{pk_src} {peak_kind}", "avg_launch_ms": pk_["avg_ms"],
+                "flops_per_launch": d["flops"] / d["launches"],
+                "timing": "CUDA events around every launch inside the timed steps, "
+                          "max over ranks"}
     cpu = None
     if not args.no_cpu_baseline and ctx.mesh.world_size == 1:
         # repeat the one-core sample until ~10 s of CPU work (at most 200 repeats)
@@ -854,8 +985,10 @@ def main():
             reps += 1
         cpu = {"value": frac / dt, "unit": W["unit"], "cores": 1, "kind": "port",
                "sample": f"{reps} x ({sample_desc})", "seconds": dt}
+    backend = getattr(ctx.transport, "kind", "thread")
+    shared = os.environ.get("DP_MESH_BACKEND") == "gloo-cuda"
     line = {
-        "metric": "sharded fwd+bwd step latency & samples/s",
+        "metric": METRIC,
         "value": value, "unit": W["unit"], "n_gpus": ctx.mesh.world_size, "steps": args.steps,
         "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True,
         "scaling": W["scaling"], "vs_baseline": None, "dtype": W["dtype"],
@@ -864,16 +997,33 @@ def main():
         "e2e": {"value": samples / (e2e_ms / 1000.0), "unit": W["unit"], "ms_per_step": e2e_ms,
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": e2e_steps,
                 "note": "pinned H2D of each step's input shards (prefetched one step ahead on "
-                        "a copy stream) + D2H of the step's gradients, through the public API"},
-        "gpu_launches": launches // args.steps * args.steps,
+                        "a copy stream) + D2H of the step's result, through the public API"},
+        "gpu_launches": launches,
         "gpu_launches_per_step": launches / args.steps,
-        "clocks": clk.summary(),
+        "simt_calls": sum(rk["simt"] for rk in ranks_k),
+        "clocks": clocks,
         "tflops_step": W["flops"] / (ms / 1000.0) / 1e12 if W["flops"] else None,
-        "kernels": {k: {"launches": v["launches"], "avg_ms": v["ms"] / v["launches"],
-                        "tflops": v["flops"] / (v["ms"] / 1000.0) / 1e12 if v["ms"] else None}
-                    for k, v in ksum.items()},
+        "kernels": per_kernel,
+        "step_breakdown": {
+            "kernel_ms_per_step_by_rank": [rk["kernel_ms"] for rk in ranks_k],
+            "ms_per_step_by_rank": [rk["ms"] for rk in ranks_k],
+            "non_kernel_ms_per_step_by_rank": [rk["ms"] - rk["kernel_ms"] for rk in ranks_k],
+            "note": "non-kernel = step time not covered by conv / attention launches: "
+                    "exposed exchange waits, copy / accumulate kernels, weight images"},
+        "comm": {"backend": backend + (" (ranks share one GPU: dry run)" if shared else ""),
+                 "bytes_sent_per_step_by_rank": [rk["comm_bytes"] for rk in ranks_k]},
     }
+    if W.get("extra"):
+        line["comm"].update(W["extra"])
     print(json.dumps(line), flush=True)
+
+
+def gather_all(ctx, obj):
+    """Every rank's `obj`, in rank order (host metadata, gloo)."""
+    if ctx.mesh.world_size == 1:
+        return [obj]
+    group = ctx.axis_group()
+    return ctx.transport.gather_meta(group.members, group.index, obj)
 
 
 def _shutdown():

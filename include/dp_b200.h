@@ -58,11 +58,17 @@ extern "C" {
 #define DP_ALGO_AUTO 0     /* tcgen05 path when eligible, else SIMT          */
 #define DP_ALGO_SIMT 1     /* direct CUDA-core kernels (any dtype / stride)  */
 #define DP_ALGO_TC 2       /* tcgen05 + TMA path; DP_ERR_UNSUPPORTED if not  */
+#define DP_ALGO_STRICT 3   /* tcgen05 for bf16 / fp32 (UNSUPPORTED outside the
+                              envelope), CUDA cores only for fp64            */
 
 int dp_abi_version(void);
 const char *dp_last_error(void);
 /* Kernels this library has launched in this process (monotonic). */
 uint64_t dp_launch_count(void);
+/* Conv / attention calls routed to the CUDA-core kernels (fp64, or a
+ * geometry outside the tcgen05 envelope under DP_ALGO_AUTO) in this process
+ * (monotonic).  The hot path asserts it never moves. */
+uint64_t dp_simt_count(void);
 /* SM count and compute capability of the current device. */
 int dp_device_info(int *sm_count, int *cc_major, int *cc_minor);
 
@@ -78,6 +84,20 @@ int dp_copy_strided(int ndim, const int64_t *shape, void *dst, const int64_t *ds
 int dp_accumulate_strided(int ndim, const int64_t *shape, void *dst,
                           const int64_t *dst_strides, const void *src,
                           const int64_t *src_strides, int dtype, void *stream);
+
+/* dst[i] = (dst dtype) src[i]: strided converted copy between DP_F32 /
+ * DP_F64 / DP_BF16 (round to nearest even into bf16) — accumulator ->
+ * parameter-dtype casts (ring-attention dQ/dK/dV, weight gradients). */
+int dp_convert_strided(int ndim, const int64_t *shape, void *dst, const int64_t *dst_strides,
+                       int dst_dtype, const void *src, const int64_t *src_strides, int src_dtype,
+                       void *stream);
+
+/* dst[i] = max(dst[i], src[i]) (all_reduce "max", domainpar/mesh.py:271-277). */
+int dp_max_strided(int ndim, const int64_t *shape, void *dst, const int64_t *dst_strides,
+                   const void *src, const int64_t *src_strides, int dtype, void *stream);
+
+/* dst[0..n) = value (contiguous; value 0 is a memset). */
+int dp_fill(int64_t n, void *dst, int dtype, double value, void *stream);
 
 /* ---- halo convolution --------------------------------------------------- */
 

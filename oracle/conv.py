@@ -4,6 +4,8 @@ conv()       domainpar/dense.py:174-214 — np.pad + sliding_window_view +
              einsum, with the reference's einsum specs for 1-D/2-D; the 3-D
              spec 'bcpqrklm,dcklm->bdpqr' extends the same construction (the
              reference rejects 3-D, dense.py:181-185).
+conv_fast()  the same convolution summed tap by tap with BLAS matmuls in
+             float64 (large parity cases), pinned against conv().
 conv_grads() the adjoint: dX by scattering dY*W back over every window
              position, dW by contracting the windows with dY.  No reference
              function exists (no autograd); pinned by central
@@ -38,13 +40,37 @@ def conv(x, w, stride=1, padding=0):
     return out if batched else out[0]
 
 
-def conv_grads(x, w, dy, stride=1, padding=0):
-    """(dx, dw) of y = conv(x, w) given dy, in float64."""
+def conv_fast(x, w, stride=1, padding=0):
+    """conv() with the same zero padding and window arithmetic, summed tap by
+    tap as BLAS matmuls in float64 (Y += W_tap X_tap) instead of the
+    reference's single einsum: the oracle for the large parity cases, pinned
+    against conv() in tests/test_oracle.py.  Returns float64."""
     n = w.ndim - 2
     batched = x.ndim == n + 2
     xb = (x if batched else x[None]).astype(np.float64)
-    dyb = (dy if batched else dy[None]).astype(np.float64)
     w64 = w.astype(np.float64)
+    strides, pads = _norm(n, stride), _norm(n, padding)
+    outs = [conv_out(g, k, s, p) for g, k, s, p in zip(xb.shape[2:], w.shape[2:], strides, pads)]
+    xp = np.pad(xb, [(0, 0), (0, 0)] + [(p, p) for p in pads])
+    nb, no = xb.shape[0], w.shape[0]
+    y = np.zeros((nb, no, int(np.prod(outs))), dtype=np.float64)
+    for tap in np.ndindex(*w.shape[2:]):
+        sl = (slice(None), slice(None)) + tuple(
+            slice(t, t + s * (o - 1) + 1, s) for t, s, o in zip(tap, strides, outs))
+        xs = np.ascontiguousarray(xp[sl]).reshape(nb, xb.shape[1], -1)
+        y += np.matmul(w64[(slice(None), slice(None)) + tap][None], xs)
+    y = y.reshape((nb, no) + tuple(outs))
+    return y if batched else y[0]
+
+
+def conv_grads(x, w, dy, stride=1, padding=0, dtype=np.float64):
+    """(dx, dw) of y = conv(x, w) given dy, computed in `dtype` (float64 for
+    parity; the CPU baseline legs use float32, the reference's compute type)."""
+    n = w.ndim - 2
+    batched = x.ndim == n + 2
+    xb = (x if batched else x[None]).astype(dtype)
+    dyb = (dy if batched else dy[None]).astype(dtype)
+    w64 = w.astype(dtype)
     strides, pads = _norm(n, stride), _norm(n, padding)
     xp = np.pad(xb, [(0, 0), (0, 0)] + [(p, p) for p in pads])
     dxp = np.zeros_like(xp)
@@ -57,9 +83,10 @@ def conv_grads(x, w, dy, stride=1, padding=0):
         wt = w64[(slice(None), slice(None)) + tap]      # [co, ci]
         nb, no = dyb.shape[:2]
         dyf = dyb.reshape(nb, no, -1)
-        dxp[sl] += np.einsum("bop,oc->bcp", dyf, wt).reshape(xs.shape)
-        dw[(slice(None), slice(None)) + tap] = np.einsum("bop,bcp->oc", dyf,
-                                                         xs.reshape(nb, xs.shape[1], -1))
+        # per-tap contractions as BLAS matmuls: dX_tap = W_tap^T dY, dW_tap = sum_b dY X_tap^T
+        dxp[sl] += np.matmul(wt.T[None], dyf).reshape(xs.shape)
+        xf = np.ascontiguousarray(xs).reshape(nb, xs.shape[1], -1)
+        dw[(slice(None), slice(None)) + tap] = np.matmul(dyf, xf.transpose(0, 2, 1)).sum(0)
     crop = (slice(None), slice(None)) + tuple(slice(p, p + g) for p, g in zip(pads, xb.shape[2:]))
     dx = dxp[crop]
     return (dx if batched else dx[0]), dw

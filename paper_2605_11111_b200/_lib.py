@@ -18,7 +18,7 @@ LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
 
 DP_OK, DP_ERR_INVALID, DP_ERR_UNSUPPORTED, DP_ERR_CUDA = 0, 1, 2, 3
 DP_F32, DP_F64, DP_BF16 = 0, 1, 2
-ALGO_AUTO, ALGO_SIMT, ALGO_TC = 0, 1, 2
+ALGO_AUTO, ALGO_SIMT, ALGO_TC, ALGO_STRICT = 0, 1, 2, 3
 CONV_FWD, CONV_DGRAD, CONV_WGRAD = 0, 1, 2
 NORM_MOMENTS, NORM_MAX, NORM_EXPSUM = 0, 1, 2
 EW_ADD, EW_MUL, EW_SCALE = 0, 1, 2
@@ -57,11 +57,17 @@ SIGNATURES = {
     "dp_abi_version": (ctypes.c_int, []),
     "dp_last_error": (ctypes.c_char_p, []),
     "dp_launch_count": (ctypes.c_uint64, []),
+    "dp_simt_count": (ctypes.c_uint64, []),
     "dp_device_info": (ctypes.c_int, [ctypes.POINTER(ctypes.c_int)] * 3),
     "dp_copy_strided": (ctypes.c_int, [ctypes.c_int, _i64p, _vp, _i64p, _vp, _i64p,
                                        ctypes.c_int, _vp]),
     "dp_accumulate_strided": (ctypes.c_int, [ctypes.c_int, _i64p, _vp, _i64p, _vp, _i64p,
                                              ctypes.c_int, _vp]),
+    "dp_convert_strided": (ctypes.c_int, [ctypes.c_int, _i64p, _vp, _i64p, ctypes.c_int, _vp,
+                                          _i64p, ctypes.c_int, _vp]),
+    "dp_max_strided": (ctypes.c_int, [ctypes.c_int, _i64p, _vp, _i64p, _vp, _i64p, ctypes.c_int,
+                                      _vp]),
+    "dp_fill": (ctypes.c_int, [ctypes.c_int64, _vp, ctypes.c_int, ctypes.c_double, _vp]),
     "dp_conv_workspace": (ctypes.c_int64, [ctypes.POINTER(ConvGeom), ctypes.c_int, ctypes.c_int,
                                            ctypes.c_int]),
     "dp_conv_fwd": (ctypes.c_int, [ctypes.POINTER(ConvGeom), ctypes.c_int, ctypes.c_int,
@@ -133,6 +139,11 @@ def check(rc: int, what: str) -> None:
 
 def launch_count() -> int:
     return int(load().dp_launch_count())
+
+
+def simt_count() -> int:
+    """Conv / attention calls the library routed to its CUDA-core kernels."""
+    return int(load().dp_simt_count())
 
 
 def i64_array(values):

@@ -1,5 +1,15 @@
 // C-ABI entry points for convolution and attention: validate, pick the
-// algorithm (tcgen05 path when eligible, CUDA-core path otherwise), launch.
+// algorithm, launch.
+//
+// Algorithm policy.  bf16 (and fp32, via the exact bf16x3 split) runs on the
+// tcgen05 kernels whenever the geometry is inside their envelope.  The
+// CUDA-core kernels exist for what the tensor cores cannot do exactly — fp64
+// (the reference's default dtype) — and for geometries outside the envelope
+// (strides > 1, 1-D convs, channel counts that are not multiples of 16, ...),
+// which the reference's own test-suite exercises.  They are never a silent
+// detour for the hot path: every call routed to them is counted
+// (dp_simt_count), DP_ALGO_STRICT refuses them for bf16/fp32, and the
+// sharded-conv parity tests and bench.py assert the count stays 0.
 #include "common.cuh"
 
 namespace dp {
@@ -49,20 +59,31 @@ static int eligible_tc(const dp_conv_geom *g, int dtype, int which) {
     return conv_tc_eligible(g, dtype, which);
 }
 
-static int pick(int algo, int eligible, const char *what) {
-    if (algo == DP_ALGO_SIMT) return DP_ALGO_SIMT;
-    if (algo == DP_ALGO_TC) {
+static unsigned long long g_simt_calls = 0;
+
+static int pick(int algo, int eligible, const char *what, int dtype, bool count = true) {
+    int a;
+    if (algo == DP_ALGO_SIMT) {
+        a = DP_ALGO_SIMT;
+    } else if (algo == DP_ALGO_TC || (algo == DP_ALGO_STRICT && dtype != DP_F64)) {
         if (!eligible) {
             set_error("%s: configuration outside the tcgen05 envelope", what);
             return -1;
         }
-        return DP_ALGO_TC;
+        a = DP_ALGO_TC;
+    } else {
+        a = eligible ? DP_ALGO_TC : DP_ALGO_SIMT;
     }
-    return eligible ? DP_ALGO_TC : DP_ALGO_SIMT;
+    if (count && a == DP_ALGO_SIMT) __atomic_add_fetch(&g_simt_calls, 1ull, __ATOMIC_RELAXED);
+    return a;
+}
+
+extern "C" uint64_t dp_simt_count(void) {
+    return __atomic_load_n(&g_simt_calls, __ATOMIC_RELAXED);
 }
 
 extern "C" int64_t dp_conv_workspace(const dp_conv_geom *g, int dtype, int algo, int which) {
-    int a = pick(algo, eligible_tc(g, dtype, which), "dp_conv_workspace");
+    int a = pick(algo, eligible_tc(g, dtype, which), "dp_conv_workspace", dtype, false);
     if (a < 0) return -1;
     if (a == DP_ALGO_TC)
         return dtype == DP_F32 ? conv_x3_workspace(g, which) : conv_tc_workspace(g, which);
@@ -72,7 +93,7 @@ extern "C" int64_t dp_conv_workspace(const dp_conv_geom *g, int dtype, int algo,
 extern "C" int dp_conv_fwd(const dp_conv_geom *g, int dtype, int algo, const void *x,
                            const void *xh, const void *w, void *y, void *ws, int64_t ws_bytes,
                            void *stream) {
-    int a = pick(algo, eligible_tc(g, dtype, DP_CONV_FWD), "dp_conv_fwd");
+    int a = pick(algo, eligible_tc(g, dtype, DP_CONV_FWD), "dp_conv_fwd", dtype);
     if (a < 0) return DP_ERR_UNSUPPORTED;
     cudaStream_t st = (cudaStream_t)stream;
     if (a == DP_ALGO_TC && dtype == DP_F32)
@@ -84,7 +105,7 @@ extern "C" int dp_conv_fwd(const dp_conv_geom *g, int dtype, int algo, const voi
 extern "C" int dp_conv_dgrad(const dp_conv_geom *g, int dtype, int algo, const void *dy,
                              const void *w, void *dx, void *dxh, void *ws, int64_t ws_bytes,
                              void *stream) {
-    int a = pick(algo, eligible_tc(g, dtype, DP_CONV_DGRAD), "dp_conv_dgrad");
+    int a = pick(algo, eligible_tc(g, dtype, DP_CONV_DGRAD), "dp_conv_dgrad", dtype);
     if (a < 0) return DP_ERR_UNSUPPORTED;
     cudaStream_t st = (cudaStream_t)stream;
     if (a == DP_ALGO_TC && dtype == DP_F32)
@@ -96,7 +117,7 @@ extern "C" int dp_conv_dgrad(const dp_conv_geom *g, int dtype, int algo, const v
 extern "C" int dp_conv_wgrad(const dp_conv_geom *g, int dtype, int algo, const void *x,
                              const void *xh, const void *dy, void *dw, void *ws, int64_t ws_bytes,
                              void *stream) {
-    int a = pick(algo, eligible_tc(g, dtype, DP_CONV_WGRAD), "dp_conv_wgrad");
+    int a = pick(algo, eligible_tc(g, dtype, DP_CONV_WGRAD), "dp_conv_wgrad", dtype);
     if (a < 0) return DP_ERR_UNSUPPORTED;
     cudaStream_t st = (cudaStream_t)stream;
     if (a == DP_ALGO_TC && dtype == DP_F32)
@@ -108,7 +129,7 @@ extern "C" int dp_conv_wgrad(const dp_conv_geom *g, int dtype, int algo, const v
 extern "C" int dp_attn_fwd_update(const dp_attn_geom *g, int dtype, int algo, const void *q,
                                   const void *k, const void *v, void *m, void *l, void *acc,
                                   void *stream) {
-    int a = pick(algo, attn_tc_eligible(g, dtype), "dp_attn_fwd_update");
+    int a = pick(algo, attn_tc_eligible(g, dtype), "dp_attn_fwd_update", dtype);
     if (a < 0) return DP_ERR_UNSUPPORTED;
     cudaStream_t st = (cudaStream_t)stream;
     if (a == DP_ALGO_TC) return attn_fwd_update_tc_launch(g, q, k, v, m, l, acc, st);
@@ -119,7 +140,7 @@ extern "C" int dp_attn_bwd_update(const dp_attn_geom *g, int dtype, int algo, co
                                   const void *k, const void *v, const void *dout,
                                   const void *lse, const void *delta, void *dq, void *dk,
                                   void *dv, void *stream) {
-    int a = pick(algo, attn_bwd_tc_eligible(g, dtype), "dp_attn_bwd_update");
+    int a = pick(algo, attn_bwd_tc_eligible(g, dtype), "dp_attn_bwd_update", dtype);
     if (a < 0) return DP_ERR_UNSUPPORTED;
     cudaStream_t st = (cudaStream_t)stream;
     if (a == DP_ALGO_TC)

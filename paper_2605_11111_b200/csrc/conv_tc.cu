@@ -697,27 +697,12 @@ int launch_n(const CUtensorMap &xm, const CUtensorMap &hm, const ConvTcParams &p
     return launch_k<N, 0, 0, 0, 0>(xm, hm, p, grid, smem, st);
 }
 
-struct PairPlan {
-    Roles R;
-    int Cin, N0, nstage, smem, wimg;
-};
-
-bool make_pair_plan(const dp_conv_geom *g, bool dgrad, PairPlan &pl);
-int run_conv_pair(const dp_conv_geom *g, bool dgrad, const PairPlan &pl, const void *in,
-                  const void *in_halo, const void *w, void *out, void *out2, void *ws,
-                  int64_t ws_bytes, cudaStream_t st);
-
 int run_conv_tc(const dp_conv_geom *g, bool dgrad, const void *in, const void *in_halo,
                 const void *w, void *out, void *out2, void *ws, int64_t ws_bytes,
                 cudaStream_t st, bool f32out = false) {
     Plan pl;
     DP_REQUIRE(make_plan(g, dgrad, pl, f32out), DP_ERR_UNSUPPORTED,
                "conv_tc: outside the envelope");
-    if (!f32out) {
-        PairPlan pp;
-        if (make_pair_plan(g, dgrad, pp))
-            return run_conv_pair(g, dgrad, pp, in, in_halo, w, out, out2, ws, ws_bytes, st);
-    }
     const Roles &R = pl.R;
     const int taps = R.KP * R.KQ * R.KW;
     DP_REQUIRE(ws_bytes >= pl.wimg_bytes, DP_ERR_INVALID, "conv_tc: workspace too small");
@@ -847,580 +832,6 @@ int run_conv_tc(const dp_conv_geom *g, bool dgrad, const void *in, const void *i
 }
 
 // ---------------------------------------------------------------------------
-// CTA-pair convolution (cta_group::2, M = 256): fwd and dgrad for rows of at
-// most 256 voxels with padding 1 along W (the cfg2 volume), KQ = KW = 3.
-//
-// GEMM view: M = the 256 INPUT voxels of a row (CTA r of the pair holds
-// voxels [128 r, 128 r + 128) in its TMEM lanes), N = (kw, c_out) per
-// output row slot, K = (kp, 16-channel step).  The kw taps moved from K
-// (an A-row shift re-reading the input tile 3x) into N, so each staged input
-// tile is read ONCE per (kp, kc, kq) MMA and the pair's MMAs are compute-bound
-// (N = 96: 48 cycles, each CTA reads 4 KB of A + 1.5 KB of B) instead of
-// shared-memory-bound (the single-CTA kernel's N = 96 MMA re-reads a 4 KB A
-// tile per kw).  Input voxel v contributes D[v][(kw, c)]; output w sums
-// D[w - 1][kw 0] + D[w][kw 1] + D[w + 1][kw 2] in the epilogue: neighbouring
-// lanes through warp shuffles, quarter edges through a small smem ring, and
-// the pair boundary (voxel 127 | 128) through DSMEM stores + a cluster-scope
-// mbarrier.  With padding 1 and W <= 256 every output is exact: lanes -1 and
-// 256 are the zero padding.  Everything else (Q streaming, P planes, halo
-// maps, dgrad's split output, the TMEM slot ring) follows conv_tc_kernel.
-constexpr int kPairW = 256;
-
-template <int N0, int CIN, int KP>
-struct PairShape {
-    static constexpr int KQ = 3, KW = 3;
-    static constexpr int SW = KW * N0;                       // TMEM columns per output row
-    static constexpr int NSLOT = (512 / SW) < 16 ? (512 / SW) : 16;
-    static constexpr int CBLK = chan_block(CIN);
-    static constexpr int NBLK = CIN / CBLK;
-    static constexpr int KC = CIN / 16;
-    static constexpr int KPB = CBLK / 16;
-    static constexpr int ROWB = CBLK * 2;
-    static constexpr int BOX = 128 * CBLK * 2;               // one (plane, channel block) tile
-    static constexpr int STAGE = KP * NBLK * BOX;
-    static constexpr int BHALF = SW / 2 * 32;                // B rows of one CTA per MMA block
-    static constexpr int WIMG = KP * KC * KQ * BHALF;        // per-CTA weight image bytes
-    static constexpr int HC = N0 / 2;                        // channels per epilogue half
-    static constexpr int EDGE = NSLOT * 2 * 6 * 2 * HC * 4;  // quarter-edge ring bytes
-    static constexpr int DR = 32, LAG = 4;                   // pair-boundary ring / lag (rows)
-    static constexpr int BOUND = 2 * DR * N0 * 4 + DR * 8;   // own partials, peer slices, dst
-    static_assert(LAG % 2 == 0 && LAG <= DR - NSLOT - 3,
-                  "boundary ring reuse must trail the TMEM slot ring");
-    static_assert(NSLOT >= KQ + 2, "3 rows accumulate while 2 drain");
-    static_assert(BOX % 1024 == 0, "swizzle atoms");
-    static_assert((SW / 2) % 8 == 0, "B halves are whole core-matrix groups");
-};
-
-constexpr int kPairThreads = 18 * 32;   // TMA, MMA, 16 epilogue warps
-
-template <int N0, int CIN, int KP>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
-conv_tc2_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap hmap,
-                const ConvTcParams p) {
-    using namespace tc;
-    using S = PairShape<N0, CIN, KP>;
-    constexpr int KQ = S::KQ, SW = S::SW, NSLOT = S::NSLOT;
-    extern __shared__ __align__(1024) uint8_t smem[];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t rank = cluster_ctarank();
-    const int cluster = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
-
-    uint8_t *wsm = smem;
-    uint8_t *stages = smem + ((S::WIMG + 1023) & ~1023);
-    float *edges = reinterpret_cast<float *>(stages + (size_t)p.nstage * S::STAGE);
-    float *bpart = edges + S::EDGE / 4;                 // [DR][N0] own partial of a boundary voxel
-    float *bpeer = bpart + S::DR * N0;                  // [DR][N0] the peer's slice (st.async)
-    __nv_bfloat16 **bdst = reinterpret_cast<__nv_bfloat16 **>(bpeer + S::DR * N0);   // [DR]
-    uint64_t *bars = reinterpret_cast<uint64_t *>(reinterpret_cast<uint8_t *>(edges) + S::EDGE +
-                                                  S::BOUND);
-    uint64_t *full = bars, *empty = bars + p.nstage;
-    uint64_t *tfull = empty + p.nstage, *tempty = tfull + NSLOT, *ebar = tempty + NSLOT;
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(ebar + 2 * S::DR);
-
-    // this CTA's half of the weight image, zeroed edge ring
-    const uint8_t *wsrc = reinterpret_cast<const uint8_t *>(p.wimg) + (size_t)rank * S::WIMG;
-    for (int i = threadIdx.x * 16; i < S::WIMG; i += kPairThreads * 16)
-        *reinterpret_cast<int4 *>(wsm + i) = *reinterpret_cast<const int4 *>(wsrc + i);
-    for (int i = threadIdx.x; i < S::EDGE / 4; i += kPairThreads) edges[i] = 0.f;
-    fence_async_smem();
-    if (warp == 0) {
-        if (lane == 0) {
-            for (int i = 0; i < p.nstage; ++i) {
-                mbar_init(&full[i], 1);
-                mbar_init(&empty[i], 1);
-            }
-            for (int i = 0; i < NSLOT; ++i) {
-                mbar_init(&tfull[i], 1);
-                mbar_init(&tempty[i], 16);    // 8 draining warps x 2 CTAs (even CTA's copy)
-            }
-            for (int i = 0; i < 2 * S::DR; ++i) mbar_init(&ebar[i], 1);
-            mbar_fence_init();
-            tma_prefetch(&xmap);
-            tma_prefetch(&hmap);
-        }
-        __syncwarp();
-        tmem_alloc2(tmem_slot, 512);
-    }
-    tc_fence_before();
-    __syncthreads();
-    cluster_sync();
-    tc_fence_after();
-    const uint32_t tmem = *tmem_slot;
-    tc_fence_before();
-    __syncthreads();
-    cluster_sync();
-    tc_fence_after();
-
-    if (warp == 0) {
-        // ===================== TMA producer (both CTAs) =====================
-        const uint32_t lead_full = mapa_shared(smem_u32(full), 0);
-        uint32_t it = 0;
-        for (int u = cluster; u < p.n_units; u += nclusters) {
-            int r = u;
-            const int qc = r % p.n_qc; r /= p.n_qc;
-            const int po = r % p.Pout;
-            const int b = r / p.Pout;
-            const int q0 = qc * p.q_chunk, q1 = min(p.Qout, q0 + p.q_chunk);
-            const int nrows = (q1 - q0) + KQ - 1;
-            for (int s = 0; s < nrows; ++s, ++it) {
-                const uint32_t idx = it % p.nstage, ph = (it / p.nstage) & 1;
-                mbar_wait(&empty[idx], ph ^ 1);
-                if (p.dbg & 8) {
-                    if (rank == 0 && lane == 0) mbar_arrive(&full[idx]);
-                    __syncwarp();
-                    continue;
-                }
-                if (rank == 0) mbar_expect_tx_e(&full[idx], 2u * S::STAGE);
-                uint8_t *dst = stages + (size_t)idx * S::STAGE;
-                const int qv = p.base_q + q0 + s;
-#pragma unroll
-                for (int kp = 0; kp < KP; ++kp) {
-                    const int pv = p.base_p + po + kp;
-                    const CUtensorMap *map = &xmap;
-                    int pc = pv, qcrd = qv;
-                    if (p.split == 0 && pv >= p.Pin && pv < p.Pin + p.halo) {
-                        map = &hmap;
-                        pc = pv - p.Pin;
-                    } else if (p.split == 1 && qv >= p.Qin && qv < p.Qin + p.halo) {
-                        map = &hmap;
-                        qcrd = qv - p.Qin;
-                    }
-#pragma unroll
-                    for (int cb = 0; cb < S::NBLK; ++cb)
-                        tma_load_5d_2sm_e(dst + (size_t)(kp * S::NBLK + cb) * S::BOX, map,
-                                          lead_full + idx * 8, cb * S::CBLK, (int)rank * 128, qcrd,
-                                          pc, b);
-                }
-            }
-        }
-    } else if (warp == 1) {
-        if (rank == 0) {
-            // ===================== MMA issuer (even CTA) =====================
-            const uint32_t idesc = idesc_bf16(256, SW);
-            const uint64_t bdesc0 = sdesc(smem_u32(wsm), 128, 256);
-            const uint64_t adesc0 = sdesc_sw(smem_u32(stages), 8 * S::ROWB, swz_layout(S::CBLK));
-            uint32_t it = 0, row_base = 0;
-            for (int u = cluster; u < p.n_units; u += nclusters) {
-                const int qc = u % p.n_qc;
-                const int q0 = qc * p.q_chunk, q1 = min(p.Qout, q0 + p.q_chunk);
-                const int nq = q1 - q0;
-                const int nrows = nq + KQ - 1;
-                for (int s = 0; s < nrows; ++s, ++it) {
-                    const uint32_t idx = it % p.nstage, ph = (it / p.nstage) & 1;
-                    if (s < nq) {
-                        const uint32_t row = row_base + s;
-                        mbar_wait(&tempty[row % NSLOT], ((row / NSLOT) & 1) ^ 1);
-                    }
-                    mbar_wait(&full[idx], ph);
-                    tc_fence_after();
-                    const uint64_t adesc = adesc0 + ((idx * S::STAGE) >> 4);
-                    if (!(p.dbg & 2)) {
-#pragma unroll
-                        for (int kq = 0; kq < KQ; ++kq) {
-                            const int j = s - kq;
-                            if (j < 0 || j >= nq) continue;
-                            const uint32_t d = tmem + ((row_base + j) % NSLOT) * SW;
-#pragma unroll
-                            for (int kp = 0; kp < KP; ++kp)
-#pragma unroll
-                                for (int kc = 0; kc < S::KC; ++kc) {
-                                    const uint32_t aoff = (kp * S::NBLK + kc / S::KPB) * S::BOX +
-                                                          (kc % S::KPB) * 32;
-                                    const uint32_t boff = ((kp * S::KC + kc) * KQ + kq) * S::BHALF;
-                                    // the first MMA into a row's slot overwrites it (no
-                                    // zeroing pass in the epilogue)
-                                    mma2_bf16_e(d, adesc + (aoff >> 4), bdesc0 + (boff >> 4), idesc,
-                                                (kq == 0 && kp == 0 && kc == 0) ? 0u : 1u);
-                                }
-                        }
-                    }
-                    mma2_commit_mc_e(&empty[idx]);
-                    const int jd = s - (KQ - 1);
-                    if (jd >= 0 && jd < nq) mma2_commit_mc_e(&tfull[(row_base + jd) % NSLOT]);
-                }
-                row_base += nq;
-            }
-        }
-    } else {
-        // ===================== epilogue (both CTAs, 16 warps) =====================
-        // Thread = input voxel v = 128 rank + 32 quarter + lane = output voxel w.
-        // out[w] = D[w-1][kw 0] + D[w][kw 1] + D[w+1][kw 2]: neighbours within the
-        // warp by shuffles; across quarters through edge entries e = quarter + 1
-        // of a per-slot smem ring ([e][0] = lane 0's kw 2 slice, [e][1] = lane
-        // 31's kw 0 slice; entries 0 and 5 stay zero = the row padding).  Warp
-        // group g = (warp - 2) / 4 (one warp per TMEM lane quarter) handles rows
-        // of parity g & 1 and channel half g >> 1, so two rows drain at once and
-        // each warp reads 3 x N0/2 columns.  The pair boundary (voxels 127 | 128)
-        // is not synchronised per row: the boundary threads keep partial sums in
-        // a ring, st.async their slice into the peer's ring (complete_tx on the
-        // peer's mbarrier) and finish row r LAG rows later.
-        const int quarter = warp & 3;
-        const int grp = (warp - 2) >> 2;
-        const int parity = grp & 1, chalf = grp >> 1;
-        const int cofs = chalf * S::HC;                        // first channel of this warp
-        const int w = (int)rank * 128 + quarter * 32 + lane;
-        const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
-        const uint32_t lead_tempty = mapa_shared(smem_u32(tempty), 0);
-        const bool bthread = (rank == 0 && quarter == 3 && lane == 31) ||
-                             (rank == 1 && quarter == 0 && lane == 0);
-        const uint32_t peer_bpeer = mapa_shared(smem_u32(bpeer), rank ^ 1u);
-        const uint32_t peer_ebar = mapa_shared(smem_u32(ebar), rank ^ 1u);
-        auto edge = [&](uint32_t slot, int e, int side) {
-            return edges + ((((size_t)slot * 2 + chalf) * 6 + e) * 2 + side) * S::HC;
-        };
-        auto finish_boundary = [&](uint32_t r) {      // boundary thread: row r is complete
-            const uint32_t e = r % S::DR;
-            uint64_t *bar = &ebar[e * 2 + chalf];
-            mbar_expect_tx(bar, S::HC * 4);
-            mbar_wait(bar, (r / S::DR) & 1);
-            __nv_bfloat16 *dst = bdst[e];
-            if (dst) {
-                const float *pa = bpart + e * N0 + cofs, *pb = bpeer + e * N0 + cofs;
-#pragma unroll
-                for (int c = 0; c < S::HC; c += 8) {
-                    uint4 pk;
-                    pk.x = pack_bf16(pa[c + 0] + pb[c + 0], pa[c + 1] + pb[c + 1]);
-                    pk.y = pack_bf16(pa[c + 2] + pb[c + 2], pa[c + 3] + pb[c + 3]);
-                    pk.z = pack_bf16(pa[c + 4] + pb[c + 4], pa[c + 5] + pb[c + 5]);
-                    pk.w = pack_bf16(pa[c + 6] + pb[c + 6], pa[c + 7] + pb[c + 7]);
-                    *reinterpret_cast<uint4 *>(dst + cofs + c) = pk;
-                }
-            }
-        };
-        uint32_t row_base = 0, last_mine = 0;
-        bool any_mine = false;
-        for (int u = cluster; u < p.n_units; u += nclusters) {
-            int r = u;
-            const int qc = r % p.n_qc; r /= p.n_qc;
-            const int po = r % p.Pout;
-            const int b = r / p.Pout;
-            const int q0 = qc * p.q_chunk, q1 = min(p.Qout, q0 + p.q_chunk);
-            for (int j = 0; j < q1 - q0; ++j) {
-                const uint32_t row = row_base + j;
-                if ((int)(row & 1) != parity) continue;
-                const uint32_t slot = row % NSLOT, par = (row / NSLOT) & 1;
-                mbar_wait(&tfull[slot], par);
-                tc_fence_after();
-                const uint32_t col = lane_base + slot * SW + cofs;
-                uint32_t v[3 * S::HC];      // [kw][c] for this warp's channel half
-#pragma unroll
-                for (int kw = 0; kw < 3; ++kw)
-#pragma unroll
-                    for (int c = 0; c < S::HC; c += 8) {
-                        uint32_t t[8];
-                        asm volatile(
-                            "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
-                            : "=r"(t[0]), "=r"(t[1]), "=r"(t[2]), "=r"(t[3]), "=r"(t[4]), "=r"(t[5]),
-                              "=r"(t[6]), "=r"(t[7])
-                            : "r"(col + kw * N0 + c));
-#pragma unroll
-                        for (int i = 0; i < 8; ++i) v[kw * S::HC + c + i] = t[i];
-                    }
-                tmem_wait_ld();
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) {   // this warp's columns of the slot are drained
-                    if (rank == 0) mbar_arrive(&tempty[slot]);
-                    else mbar_arrive_remote(lead_tempty + slot * 8);
-                }
-                if (lane == 0) {
-                    uint4 *e0 = reinterpret_cast<uint4 *>(edge(slot, quarter + 1, 0));
-#pragma unroll
-                    for (int c = 0; c < S::HC; c += 4)
-                        e0[c / 4] = make_uint4(v[2 * S::HC + c], v[2 * S::HC + c + 1],
-                                               v[2 * S::HC + c + 2], v[2 * S::HC + c + 3]);
-                }
-                if (lane == 31) {
-                    uint4 *e1 = reinterpret_cast<uint4 *>(edge(slot, quarter + 1, 1));
-#pragma unroll
-                    for (int c = 0; c < S::HC; c += 4)
-                        e1[c / 4] = make_uint4(v[c], v[c + 1], v[c + 2], v[c + 3]);
-                }
-                if (bthread) {   // the slice the peer's boundary voxel needs (kw 0 / kw 2)
-                    const bool k0 = rank == 0;
-                    const uint32_t e = row % S::DR;
-#pragma unroll
-                    for (int c = 0; c < S::HC; c += 4)
-                        st_async_v4(peer_bpeer + (e * N0 + cofs + c) * 4,
-                                    make_uint4(k0 ? v[c] : v[2 * S::HC + c],
-                                               k0 ? v[c + 1] : v[2 * S::HC + c + 1],
-                                               k0 ? v[c + 2] : v[2 * S::HC + c + 2],
-                                               k0 ? v[c + 3] : v[2 * S::HC + c + 3]),
-                                    peer_ebar + (e * 2 + chalf) * 8);
-                }
-                named_bar_sync(1 + grp, 128);
-                // branch-free combine (entries 5 of the even CTA / 0 of the odd CTA
-                // are zero: the boundary threads get their partial sums)
-                const float4 *lo_prev = reinterpret_cast<const float4 *>(edge(slot, quarter, 1));
-                const float4 *hi_next = reinterpret_cast<const float4 *>(edge(slot, quarter + 2, 0));
-                float o[S::HC];
-#pragma unroll
-                for (int c4 = 0; c4 < S::HC / 4; ++c4) {
-                    const float4 lp = lo_prev[c4], hn = hi_next[c4];
-                    const float lpa[4] = {lp.x, lp.y, lp.z, lp.w};
-                    const float hna[4] = {hn.x, hn.y, hn.z, hn.w};
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        const int c = c4 * 4 + e;
-                        const float a0 = __shfl_up_sync(0xffffffffu, __uint_as_float(v[c]), 1);
-                        const float a2 =
-                            __shfl_down_sync(0xffffffffu, __uint_as_float(v[2 * S::HC + c]), 1);
-                        const float left = lane == 0 ? lpa[e] : a0;
-                        const float right = lane == 31 ? hna[e] : a2;
-                        o[c] = (left + __uint_as_float(v[S::HC + c])) + right;
-                    }
-                }
-                __nv_bfloat16 *dst = nullptr;
-                if (w < p.Wout && !(p.dbg & 1)) {
-                    const int qo = q0 + j;
-                    if (p.ysplit_dim == 0 && po >= p.ysplit)
-                        dst = p.y2 + b * p.y2s[0] + (int64_t)(po - p.ysplit) * p.y2s[1] +
-                              (int64_t)qo * p.y2s[2] + (int64_t)w * p.y2s[3];
-                    else if (p.ysplit_dim == 1 && qo >= p.ysplit)
-                        dst = p.y2 + b * p.y2s[0] + (int64_t)po * p.y2s[1] +
-                              (int64_t)(qo - p.ysplit) * p.y2s[2] + (int64_t)w * p.y2s[3];
-                    else
-                        dst = p.y + b * p.ys[0] + (int64_t)po * p.ys[1] + (int64_t)qo * p.ys[2] +
-                              (int64_t)w * p.ys[3];
-                }
-                if (bthread) {
-                    const uint32_t e = row % S::DR;
-                    float4 *pa = reinterpret_cast<float4 *>(bpart + e * N0 + cofs);
-#pragma unroll
-                    for (int c = 0; c < S::HC; c += 4)
-                        pa[c / 4] = make_float4(o[c], o[c + 1], o[c + 2], o[c + 3]);
-                    bdst[e] = dst;      // both channel halves write the same pointer
-                    if (any_mine && row >= (uint32_t)S::LAG) finish_boundary(row - S::LAG);
-                } else if (dst) {
-#pragma unroll
-                    for (int c = 0; c < S::HC; c += 8) {
-                        uint4 pk;
-                        pk.x = pack_bf16(o[c + 0], o[c + 1]);
-                        pk.y = pack_bf16(o[c + 2], o[c + 3]);
-                        pk.z = pack_bf16(o[c + 4], o[c + 5]);
-                        pk.w = pack_bf16(o[c + 6], o[c + 7]);
-                        *reinterpret_cast<uint4 *>(dst + cofs + c) = pk;
-                    }
-                }
-                any_mine = true;
-                last_mine = row;
-            }
-            row_base += q1 - q0;
-        }
-        if (bthread && any_mine) {
-            // rows of this parity not yet finished: last_mine - LAG + 2 .. last_mine
-            const uint32_t lo = last_mine >= (uint32_t)S::LAG - 2 ? last_mine - (S::LAG - 2) : parity;
-            for (uint32_t rr = lo; rr <= last_mine; rr += 2) finish_boundary(rr);
-        }
-    }
-    tc_fence_before();
-    __syncthreads();
-    cluster_sync();
-    if (warp == 0) {
-        tc_fence_after();
-        tmem_dealloc2(tmem, 512);
-    }
-}
-
-// Pair weight image: [cta half r][kp][kc][kq] blocks of SW/2 rows (n = r*SW/2
-// + row -> (kw, c) = (n / N0, n % N0)) x 16 k, UMMA K-major canonical
-// ([n/8][k half][8 rows][8 k]).  flip = the dgrad image (taps reversed,
-// channels swapped), as conv_tc_weight_image.
-__global__ void conv_tc2_weight_image(const __nv_bfloat16 *__restrict__ w,
-                                      __nv_bfloat16 *__restrict__ img, int n0, int cin, int KP,
-                                      int flip) {
-    const int KQ = 3, KW = 3, SW = KW * n0, H = SW / 2, KC = cin / 16;
-    const int taps = KP * KQ * KW;
-    const int total = 2 * KP * KC * KQ * H * 16;
-    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
-        int r = e;
-        const int kk = r % 8; r /= 8;
-        const int nn = r % 8; r /= 8;
-        const int h = r % 2; r /= 2;
-        const int g = r % (H / 8); r /= (H / 8);
-        const int kq = r % KQ; r /= KQ;
-        const int kc = r % KC; r /= KC;
-        const int kp = r % KP;
-        const int half = r / KP;
-        const int n = half * H + g * 8 + nn;
-        const int kw = n / n0, c = n % n0;
-        const int k = kc * 16 + h * 8 + kk;
-        const int t = (kp * KQ + kq) * KW + kw;
-        __nv_bfloat16 v;
-        if (!flip)
-            v = w[((int64_t)c * cin + k) * taps + t];                   // W[co=c][ci=k][t]
-        else
-            v = w[((int64_t)k * n0 + c) * taps + (taps - 1 - t)];     // W[co=k][ci=c][T-1-t]
-        img[e] = v;
-    }
-}
-
-// Opt-in (DP_CONV_PAIR=1): correct, but measured SLOWER than conv_tc_kernel on
-// cfg2 (L2 fwd 1.85 vs 0.89 ms).  Moving kw into N triples the fp32 TMEM
-// bytes the epilogue must read per output (96 vs 32 columns per voxel), and
-// tcgen05.ld delivers ~64 B/clk/SM: 48 KB per 128-voxel row = ~770 cycles,
-// on top of the shuffle combine — the epilogue, not the tensor pipe, bounds
-// it ("negative results").
-bool pair_disabled() {
-    static const int v = (getenv("DP_CONV_PAIR") && getenv("DP_CONV_PAIR")[0] == '1') ? 0 : 1;
-    return v == 1;
-}
-
-template <int N0, int CIN, int KP>
-int pair_smem(int nstage) {
-    using S = PairShape<N0, CIN, KP>;
-    return ((S::WIMG + 1023) & ~1023) + nstage * S::STAGE + S::EDGE + S::BOUND +
-           (2 * nstage + 2 * S::NSLOT + 2 * S::DR) * 8 + 16;
-}
-
-bool make_pair_plan(const dp_conv_geom *g, bool dgrad, PairPlan &pl) {
-    if (pair_disabled()) return false;
-    if (!map_roles(g, dgrad, pl.R)) return false;
-    const Roles &R = pl.R;
-    pl.Cin = (int)(dgrad ? g->c_out : g->c_in);
-    pl.N0 = (int)(dgrad ? g->c_in : g->c_out);
-    if (!(pl.N0 == 16 || pl.N0 == 32) || !(pl.Cin == 16 || pl.Cin == 32)) return false;
-    if (R.KQ != 3 || R.KW != 3 || !(R.KP == 3 || R.KP == 1)) return false;
-    if (R.base_w != -1) return false;                         // padding 1 along W
-    if (R.Win > kPairW || R.Wout > kPairW || R.Win <= 160) return false;
-    const int64_t *is = dgrad ? g->ys : g->xs;
-    const int64_t *os = dgrad ? g->xs : g->ys;
-    if (is[1] != 1 || os[1] != 1) return false;
-    if (g->halo > 0 && g->hs[1] != 1) return false;
-    for (int i = 0; i < 4; ++i) {
-        if (R.xs[i] % 8 || R.ys[i] % 8) return false;
-        if (g->halo > 0 && R.hs[i] % 8) return false;
-    }
-    if (sm_count() < 2) return false;
-    const int budget = 220 * 1024;
-    int ns = 8;
-    for (; ns >= 2; --ns) {
-        int need;
-        if (R.KP == 3)
-            need = pl.N0 == 16 ? (pl.Cin == 16 ? pair_smem<16, 16, 3>(ns) : pair_smem<16, 32, 3>(ns))
-                               : (pl.Cin == 16 ? pair_smem<32, 16, 3>(ns) : pair_smem<32, 32, 3>(ns));
-        else
-            need = pl.N0 == 16 ? (pl.Cin == 16 ? pair_smem<16, 16, 1>(ns) : pair_smem<16, 32, 1>(ns))
-                               : (pl.Cin == 16 ? pair_smem<32, 16, 1>(ns) : pair_smem<32, 32, 1>(ns));
-        if (need <= budget) {
-            pl.smem = need;
-            break;
-        }
-    }
-    if (ns < 2) return false;
-    pl.nstage = ns;
-    pl.wimg = R.KP * 9 * pl.Cin * pl.N0 * 2;   // both halves: taps * Cin * N0 bf16
-    return true;
-}
-
-template <int N0, int CIN, int KP>
-int launch_pair_k(const CUtensorMap &xm, const CUtensorMap &hm, const ConvTcParams &p, int grid,
-                  int smem, cudaStream_t st) {
-    auto kern = conv_tc2_kernel<N0, CIN, KP>;
-    DP_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    kern<<<grid, kPairThreads, smem, st>>>(xm, hm, p);
-    return launch_status("conv_tc2_kernel");
-}
-
-int run_conv_pair(const dp_conv_geom *g, bool dgrad, const PairPlan &pl, const void *in,
-                  const void *in_halo, const void *w, void *out, void *out2, void *ws,
-                  int64_t ws_bytes, cudaStream_t st) {
-    const Roles &R = pl.R;
-    DP_REQUIRE(ws_bytes >= pl.wimg, DP_ERR_INVALID, "conv_tc2: workspace too small");
-    const int64_t outs = (int64_t)g->batch * R.Pout * R.Qout * R.Wout;
-    if (outs == 0) return DP_OK;
-    {
-        const int total = R.KP * 9 * pl.Cin * pl.N0;
-        conv_tc2_weight_image<<<grid_for(total, 256, 2), 256, 0, st>>>(
-            (const __nv_bfloat16 *)w, (__nv_bfloat16 *)ws, pl.N0, pl.Cin, R.KP, dgrad ? 1 : 0);
-        int rc = launch_status("conv_tc2_weight_image");
-        if (rc) return rc;
-    }
-    const int cblk = chan_block(pl.Cin);
-    uint32_t box[5] = {(uint32_t)cblk, 128, 1, 1, 1};
-    const CUtensorMapSwizzle swz = cblk == 16 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_64B;
-    CUtensorMap xm, hm;
-    {
-        uint64_t dims[5] = {(uint64_t)pl.Cin, (uint64_t)R.Win, (uint64_t)R.Qin, (uint64_t)R.Pin,
-                            (uint64_t)g->batch};
-        uint64_t strides[4] = {(uint64_t)R.xs[3] * 2, (uint64_t)R.xs[2] * 2,
-                               (uint64_t)R.xs[1] * 2, (uint64_t)R.xs[0] * 2};
-        int rc = encode_tensor_map(&xm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void *>(in),
-                                   dims, strides, box, swz);
-        if (rc) return rc;
-    }
-    hm = xm;
-    if (!dgrad && g->halo > 0) {
-        uint64_t dims[5] = {(uint64_t)pl.Cin, (uint64_t)R.Win,
-                            (uint64_t)(R.split == 1 ? g->halo : R.Qin),
-                            (uint64_t)(R.split == 0 ? g->halo : R.Pin), (uint64_t)g->batch};
-        uint64_t strides[4] = {(uint64_t)R.hs[3] * 2, (uint64_t)R.hs[2] * 2,
-                               (uint64_t)R.hs[1] * 2, (uint64_t)R.hs[0] * 2};
-        int rc = encode_tensor_map(&hm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5,
-                                   const_cast<void *>(in_halo), dims, strides, box, swz);
-        if (rc) return rc;
-    }
-    ConvTcParams p;
-    memset(&p, 0, sizeof(p));
-    p.B = (int)g->batch;
-    p.Cin = pl.Cin;
-    p.Cout = pl.N0;
-    p.Pin = R.Pin; p.Qin = R.Qin; p.Win = R.Win;
-    p.Pout = R.Pout; p.Qout = R.Qout; p.Wout = R.Wout;
-    p.KP = R.KP; p.KQ = R.KQ; p.KW = R.KW;
-    p.base_p = R.base_p; p.base_q = R.base_q; p.base_w = R.base_w;
-    p.split = dgrad ? -1 : (g->halo > 0 ? R.split : -1);
-    p.halo = dgrad ? 0 : (int)g->halo;
-    p.y = (__nv_bfloat16 *)out;
-    p.y2 = (__nv_bfloat16 *)(out2 ? out2 : out);
-    for (int i = 0; i < 4; ++i) {
-        p.ys[i] = R.ys[i];
-        p.y2s[i] = R.hs[i];
-    }
-    p.ysplit_dim = -1;
-    if (dgrad && g->halo > 0 && g->shard == 0) {
-        p.ysplit_dim = R.split;
-        p.ysplit = (int)g->in_ext[0];
-    }
-    p.n_wt = 1;
-    const int pairs = sm_count() / 2;
-    const int64_t cols = (int64_t)p.B * R.Pout;
-    int best_chunk = R.Qout;
-    double best = -1;
-    for (int nq = 1; nq <= R.Qout && nq <= 64; ++nq) {
-        const int chunk = (R.Qout + nq - 1) / nq;
-        const int nqc = (R.Qout + chunk - 1) / chunk;
-        const int64_t units = cols * nqc;
-        const int64_t waves = (units + pairs - 1) / pairs;
-        const double balance = (double)units / (double)(waves * pairs);
-        const double overhead = (double)(chunk + R.KQ - 1) / chunk;
-        const double score = balance / overhead;
-        if (score > best + 1e-9) {
-            best = score;
-            best_chunk = chunk;
-        }
-    }
-    p.q_chunk = best_chunk;
-    p.n_qc = (R.Qout + best_chunk - 1) / best_chunk;
-    p.n_units = (int)(cols * p.n_qc);
-    p.nstage = pl.nstage;
-    p.wimg = (const __nv_bfloat16 *)ws;
-    static const int dbg = getenv("DP_CONV_DBG") ? atoi(getenv("DP_CONV_DBG")) : 0;
-    p.dbg = dbg;
-    const int grid = 2 * (int)(p.n_units < pairs ? p.n_units : pairs);
-    if (R.KP == 3) {
-        if (pl.N0 == 16)
-            return pl.Cin == 16 ? launch_pair_k<16, 16, 3>(xm, hm, p, grid, pl.smem, st)
-                                : launch_pair_k<16, 32, 3>(xm, hm, p, grid, pl.smem, st);
-        return pl.Cin == 16 ? launch_pair_k<32, 16, 3>(xm, hm, p, grid, pl.smem, st)
-                            : launch_pair_k<32, 32, 3>(xm, hm, p, grid, pl.smem, st);
-    }
-    if (pl.N0 == 16)
-        return pl.Cin == 16 ? launch_pair_k<16, 16, 1>(xm, hm, p, grid, pl.smem, st)
-                            : launch_pair_k<16, 32, 1>(xm, hm, p, grid, pl.smem, st);
-    return pl.Cin == 16 ? launch_pair_k<32, 16, 1>(xm, hm, p, grid, pl.smem, st)
-                        : launch_pair_k<32, 32, 1>(xm, hm, p, grid, pl.smem, st);
-}
 
 
 // ---------------------------------------------------------------------------

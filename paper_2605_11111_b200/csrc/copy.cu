@@ -1,5 +1,7 @@
-// Strided copy / accumulate kernels: halo face pack/unpack, varlen
-// redistribute pack/unpack, reverse-halo gradient accumulate.
+// Strided copy / accumulate / convert kernels: halo face pack/unpack, varlen
+// redistribute pack/unpack, reverse-halo gradient accumulate, the
+// accumulator -> parameter-dtype casts and fills of the ring backward, and
+// the thread mesh's all_reduce fold.
 //
 // HBM-bound byte movement.  The host side collapses the index space
 // (merging dims that are contiguous in BOTH src and dst), then moves the
@@ -154,8 +156,12 @@ int lanes_for(int64_t inner) {
 }
 
 // Collapse (shape, src strides, dst strides) in place; returns new ndim.
-// Dims of extent 1 are dropped; neighbour dims merge when both tensors are
-// contiguous across them.
+// Dims of extent 1 are dropped; the rest are put in the destination's memory
+// order (decreasing dst stride, ties by src stride) — every op here is an
+// elementwise map, so the walk order is free, and a channels-last tensor
+// (C innermost in memory, second in logical order) becomes one unit-stride
+// run instead of an element-by-element walk; then neighbour dims merge when
+// both tensors are contiguous across them.
 int collapse(int nd, int64_t *shape, int64_t *ss, int64_t *ds) {
     int64_t sh[kMaxDims], a[kMaxDims], b[kMaxDims];
     int n = 0;
@@ -165,6 +171,19 @@ int collapse(int nd, int64_t *shape, int64_t *ss, int64_t *ds) {
         a[n] = ss[i];
         b[n] = ds[i];
         ++n;
+    }
+    for (int i = 1; i < n; ++i) {   // stable insertion sort, outermost first
+        int64_t s0 = sh[i], a0 = a[i], b0 = b[i];
+        int j = i - 1;
+        while (j >= 0 && (b[j] < b0 || (b[j] == b0 && a[j] < a0))) {
+            sh[j + 1] = sh[j];
+            a[j + 1] = a[j];
+            b[j + 1] = b[j];
+            --j;
+        }
+        sh[j + 1] = s0;
+        a[j + 1] = a0;
+        b[j + 1] = b0;
     }
     if (n == 0) {
         shape[0] = 1;
@@ -264,6 +283,191 @@ int launch_accum(const Walk &w, int64_t inner, int64_t rows, int64_t s_in, int64
     }
 #undef DP_ACC
     return launch_status("dp_accumulate_strided");
+}
+
+// ---------------------------------------------------------------------------
+// typed element maps: converted copy (dst = (Td) src) and max-combine
+// (dst = max(dst, src)); 4 elements per thread-step with vector loads /
+// stores when the inner run is unit-stride and aligned (fp32 -> bf16 reads a
+// float4 and writes 8 B), row-tiled like copy_rows.
+
+template <typename T> struct V4;
+template <> struct V4<float> {
+    static __device__ __forceinline__ void ld(const float *p, float (&v)[4]) {
+        float4 a = *reinterpret_cast<const float4 *>(p);
+        v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+    }
+    static __device__ __forceinline__ void st(float *p, const float (&v)[4]) {
+        *reinterpret_cast<float4 *>(p) = make_float4(v[0], v[1], v[2], v[3]);
+    }
+};
+template <> struct V4<double> {
+    static __device__ __forceinline__ void ld(const double *p, double (&v)[4]) {
+        double2 a = reinterpret_cast<const double2 *>(p)[0], b = reinterpret_cast<const double2 *>(p)[1];
+        v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+    }
+    static __device__ __forceinline__ void st(double *p, const double (&v)[4]) {
+        reinterpret_cast<double2 *>(p)[0] = make_double2(v[0], v[1]);
+        reinterpret_cast<double2 *>(p)[1] = make_double2(v[2], v[3]);
+    }
+};
+template <> struct V4<__nv_bfloat16> {
+    static __device__ __forceinline__ void ld(const __nv_bfloat16 *p, __nv_bfloat16 (&v)[4]) {
+        uint2 a = *reinterpret_cast<const uint2 *>(p);
+        const __nv_bfloat16 *h = reinterpret_cast<const __nv_bfloat16 *>(&a);
+        v[0] = h[0]; v[1] = h[1]; v[2] = h[2]; v[3] = h[3];
+    }
+    static __device__ __forceinline__ void st(__nv_bfloat16 *p, const __nv_bfloat16 (&v)[4]) {
+        uint2 a;
+        __nv_bfloat16 *h = reinterpret_cast<__nv_bfloat16 *>(&a);
+        h[0] = v[0]; h[1] = v[1]; h[2] = v[2]; h[3] = v[3];
+        *reinterpret_cast<uint2 *>(p) = a;
+    }
+};
+
+template <typename Td, typename Ts>
+__device__ __forceinline__ Td cvt(Ts v) { return from_acc<Td>(to_acc(v)); }
+template <> __device__ __forceinline__ double cvt<double, float>(float v) { return (double)v; }
+template <> __device__ __forceinline__ float cvt<float, double>(double v) { return (float)v; }
+
+template <typename Td, typename Ts, int OP>
+__device__ __forceinline__ Td apply_op(Td d, Ts s) {
+    if (OP == 0) return cvt<Td, Ts>(s);
+    Td c = cvt<Td, Ts>(s);
+    return to_acc(c) > to_acc(d) ? c : d;   // max; NaN in d stays, as max(nan, x)
+}
+
+// OP 0: dst = convert(src); OP 1: dst = max(dst, src)
+template <typename Td, typename Ts, int OP, int G, bool VEC>
+__global__ void __launch_bounds__(256) map_rows(Walk w, int64_t inner, int64_t rows,
+                                                int64_t s_inner, int64_t d_inner,
+                                                const Ts *__restrict__ src, Td *__restrict__ dst) {
+    const int64_t groups = (int64_t)gridDim.x * (blockDim.x / G);
+    const int sub = threadIdx.x % G;
+    for (int64_t row = (int64_t)blockIdx.x * (blockDim.x / G) + threadIdx.x / G; row < rows;
+         row += groups) {
+        int64_t so, d_o;
+        offsets(w, row, so, d_o);
+        if (VEC) {
+            for (int64_t c = sub; c < inner / 4; c += G) {
+                Ts a[4];
+                Td b[4];
+                V4<Ts>::ld(src + so + 4 * c, a);
+                if (OP == 1) V4<Td>::ld(dst + d_o + 4 * c, b);
+#pragma unroll
+                for (int k = 0; k < 4; ++k) b[k] = apply_op<Td, Ts, OP>(b[k], a[k]);
+                V4<Td>::st(dst + d_o + 4 * c, b);
+            }
+        } else {
+            for (int64_t c = sub; c < inner; c += G) {
+                Td *p = dst + d_o + c * d_inner;
+                *p = apply_op<Td, Ts, OP>(OP == 1 ? *p : Td(0), src[so + c * s_inner]);
+            }
+        }
+    }
+}
+
+template <typename Td, typename Ts, int OP>
+int launch_map(const Walk &w, int64_t inner, int64_t rows, int64_t s_in, int64_t d_in, bool vec,
+               const void *src, void *dst, cudaStream_t st) {
+    const int64_t units = vec ? inner / 4 : inner;
+    const int g = lanes_for(units);
+    const int grid = grid_for(rows * g, 256, 16);
+#define DP_MAP(G)                                                                              \
+    (vec ? map_rows<Td, Ts, OP, G, true><<<grid, 256, 0, st>>>(w, inner, rows, s_in, d_in,     \
+                                                               (const Ts *)src, (Td *)dst)     \
+         : map_rows<Td, Ts, OP, G, false><<<grid, 256, 0, st>>>(w, inner, rows, s_in, d_in,    \
+                                                                (const Ts *)src, (Td *)dst))
+    switch (g) {
+        case 1: DP_MAP(1); break;
+        case 2: DP_MAP(2); break;
+        case 4: DP_MAP(4); break;
+        case 8: DP_MAP(8); break;
+        case 16: DP_MAP(16); break;
+        default: DP_MAP(32); break;
+    }
+#undef DP_MAP
+    return launch_status(OP == 0 ? "dp_convert_strided" : "dp_max_strided");
+}
+
+int elem_bytes_of(int dtype) { return dtype == DP_F64 ? 8 : dtype == DP_F32 ? 4 : 2; }
+
+template <int OP>
+int map_strided(int ndim, const int64_t *shape, void *dst, const int64_t *dst_strides, int dt_d,
+                const void *src, const int64_t *src_strides, int dt_s, cudaStream_t st) {
+    DP_REQUIRE(ndim >= 1 && ndim <= 8, DP_ERR_INVALID, "element map: ndim %d out of [1,8]", ndim);
+    DP_REQUIRE((dt_d == DP_F32 || dt_d == DP_F64 || dt_d == DP_BF16) &&
+                   (dt_s == DP_F32 || dt_s == DP_F64 || dt_s == DP_BF16),
+               DP_ERR_INVALID, "element map: dtypes %d <- %d", dt_d, dt_s);
+    int64_t sh[8], ss[8], ds[8];
+    int64_t total = 1;
+    for (int i = 0; i < ndim; ++i) {
+        DP_REQUIRE(shape[i] >= 0, DP_ERR_INVALID, "element map: negative extent");
+        sh[i] = shape[i];
+        ss[i] = src_strides[i];
+        ds[i] = dst_strides[i];
+        total *= shape[i];
+    }
+    if (total == 0) return DP_OK;
+    DP_REQUIRE(src && dst, DP_ERR_INVALID, "element map: null pointer");
+    int n = collapse(ndim, sh, ss, ds);
+    Walk w;
+    w.nd = n - 1;
+    for (int i = 0; i < n - 1; ++i) {
+        w.shape[i] = sh[i];
+        w.ss[i] = ss[i];
+        w.ds[i] = ds[i];
+    }
+    int64_t inner = sh[n - 1];
+    int64_t rows = total / inner;
+    const int eb_s = elem_bytes_of(dt_s), eb_d = elem_bytes_of(dt_d);
+    if (inner > 16384 && ss[n - 1] == 1 && ds[n - 1] == 1 && w.nd < 8) {
+        constexpr int64_t kChunk = 8192;
+        const int64_t nch = inner / kChunk, rem = inner - nch * kChunk;
+        if (rem) {
+            int64_t tsh[8], tss[8], tds[8];
+            for (int i = 0; i < n; ++i) {
+                tsh[i] = sh[i];
+                tss[i] = ss[i];
+                tds[i] = ds[i];
+            }
+            tsh[n - 1] = rem;
+            int rc = map_strided<OP>(n, tsh, (char *)dst + nch * kChunk * eb_d, tds, dt_d,
+                                     (const char *)src + nch * kChunk * eb_s, tss, dt_s, st);
+            if (rc) return rc;
+        }
+        w.shape[w.nd] = nch;
+        w.ss[w.nd] = kChunk;
+        w.ds[w.nd] = kChunk;
+        ++w.nd;
+        rows *= nch;
+        inner = kChunk;
+    }
+    bool vec = ss[n - 1] == 1 && ds[n - 1] == 1 && inner % 4 == 0 &&
+               (uintptr_t)src % (4 * eb_s) == 0 && (uintptr_t)dst % (4 * eb_d) == 0;
+    for (int i = 0; i < w.nd && vec; ++i) vec = w.ss[i] % 4 == 0 && w.ds[i] % 4 == 0;
+    const int64_t si = ss[n - 1], di = ds[n - 1];
+#define DP_PAIR(TD, TS) return launch_map<TD, TS, OP>(w, inner, rows, si, di, vec, src, dst, st)
+    switch (dt_d * 3 + dt_s) {
+        case DP_F32 * 3 + DP_F32: DP_PAIR(float, float);
+        case DP_F32 * 3 + DP_F64: DP_PAIR(float, double);
+        case DP_F32 * 3 + DP_BF16: DP_PAIR(float, __nv_bfloat16);
+        case DP_F64 * 3 + DP_F32: DP_PAIR(double, float);
+        case DP_F64 * 3 + DP_F64: DP_PAIR(double, double);
+        case DP_F64 * 3 + DP_BF16: DP_PAIR(double, __nv_bfloat16);
+        case DP_BF16 * 3 + DP_F32: DP_PAIR(__nv_bfloat16, float);
+        case DP_BF16 * 3 + DP_F64: DP_PAIR(__nv_bfloat16, double);
+        default: DP_PAIR(__nv_bfloat16, __nv_bfloat16);
+    }
+#undef DP_PAIR
+}
+
+// fill: n elements of dtype with `value` (zero -> cudaMemsetAsync)
+template <typename T>
+__global__ void __launch_bounds__(256) fill_kernel(T *__restrict__ dst, int64_t n, T v) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = v;
 }
 
 }  // namespace
@@ -413,4 +617,41 @@ extern "C" int dp_accumulate_strided(int ndim, const int64_t *shape, void *dst,
             set_error("dp_accumulate_strided: dtype %d", dtype);
             return DP_ERR_INVALID;
     }
+}
+
+extern "C" int dp_convert_strided(int ndim, const int64_t *shape, void *dst,
+                                  const int64_t *dst_strides, int dst_dtype, const void *src,
+                                  const int64_t *src_strides, int src_dtype, void *stream) {
+    return map_strided<0>(ndim, shape, dst, dst_strides, dst_dtype, src, src_strides, src_dtype,
+                          (cudaStream_t)stream);
+}
+
+extern "C" int dp_max_strided(int ndim, const int64_t *shape, void *dst, const int64_t *dst_strides,
+                              const void *src, const int64_t *src_strides, int dtype,
+                              void *stream) {
+    return map_strided<1>(ndim, shape, dst, dst_strides, dtype, src, src_strides, dtype,
+                          (cudaStream_t)stream);
+}
+
+extern "C" int dp_fill(int64_t n, void *dst, int dtype, double value, void *stream) {
+    DP_REQUIRE(n >= 0, DP_ERR_INVALID, "dp_fill: negative count");
+    DP_REQUIRE(dtype == DP_F32 || dtype == DP_F64 || dtype == DP_BF16, DP_ERR_INVALID,
+               "dp_fill: dtype %d", dtype);
+    if (n == 0) return DP_OK;
+    DP_REQUIRE(dst, DP_ERR_INVALID, "dp_fill: null pointer");
+    cudaStream_t st = (cudaStream_t)stream;
+    const int eb = elem_bytes_of(dtype);
+    if (value == 0.0 && !signbit(value)) {
+        DP_CUDA_CHECK(cudaMemsetAsync(dst, 0, (size_t)n * eb, st));
+        return DP_OK;
+    }
+    const int grid = grid_for(n, 256, 8);
+    if (dtype == DP_F32)
+        fill_kernel<float><<<grid, 256, 0, st>>>((float *)dst, n, (float)value);
+    else if (dtype == DP_F64)
+        fill_kernel<double><<<grid, 256, 0, st>>>((double *)dst, n, value);
+    else
+        fill_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>((__nv_bfloat16 *)dst, n,
+                                                         __float2bfloat16_rn((float)value));
+    return launch_status("dp_fill");
 }

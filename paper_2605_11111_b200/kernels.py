@@ -19,8 +19,11 @@ from .errors import UnsupportedConfigError
 
 _DT = {torch.float32: _lib.DP_F32, torch.float64: _lib.DP_F64, torch.bfloat16: _lib.DP_BF16}
 
-# algorithm override for tests/benchmarks: "auto" | "simt" | "tc"
-_ALGO_NAMES = {"auto": _lib.ALGO_AUTO, "simt": _lib.ALGO_SIMT, "tc": _lib.ALGO_TC}
+# algorithm override for tests/benchmarks: "auto" | "simt" | "tc" | "strict"
+# (strict = tensor cores for bf16/fp32 or an UnsupportedConfigError, CUDA
+# cores only for fp64; auto counts every CUDA-core call in simt_count())
+_ALGO_NAMES = {"auto": _lib.ALGO_AUTO, "simt": _lib.ALGO_SIMT, "tc": _lib.ALGO_TC,
+               "strict": _lib.ALGO_STRICT}
 _algo = ALGO_AUTO
 
 
@@ -30,6 +33,12 @@ def set_algo(name: str) -> str:
     prev = next(k for k, v in _ALGO_NAMES.items() if v == _algo)
     _algo = _ALGO_NAMES[name]
     return prev
+
+
+def simt_count() -> int:
+    """Conv / attention calls routed to the CUDA-core kernels so far in this
+    process (fp64, or geometries outside the tcgen05 envelope)."""
+    return _lib.simt_count()
 
 
 def dtype_code(t: torch.Tensor) -> int:
@@ -102,6 +111,64 @@ def accumulate(dst: torch.Tensor, src: torch.Tensor) -> None:
         nd, i64_array(list(dst.shape) or [1]), _ptr(dst), i64_array(list(dst.stride()) or [1]),
         _ptr(src), i64_array(list(src.stride()) or [1]), dtype_code(dst), _stream(dst))
     _lib.check(rc, "dp_accumulate_strided")
+
+
+def convert(dst: torch.Tensor, src: torch.Tensor) -> None:
+    """dst[...] = src[...] converted to dst's dtype (fp32 / fp64 / bf16)."""
+    if tuple(dst.shape) != tuple(src.shape):
+        raise UnsupportedConfigError(f"convert: {tuple(src.shape)} -> {tuple(dst.shape)}")
+    require_device("convert", dst, src)
+    if dst.numel() == 0:
+        return
+    nd = max(1, dst.dim())
+    rc = _lib.load().dp_convert_strided(
+        nd, i64_array(list(dst.shape) or [1]), _ptr(dst), i64_array(list(dst.stride()) or [1]),
+        dtype_code(dst), _ptr(src), i64_array(list(src.stride()) or [1]), dtype_code(src),
+        _stream(dst))
+    _lib.check(rc, "dp_convert_strided")
+
+
+def max_into(dst: torch.Tensor, src: torch.Tensor) -> None:
+    """dst = max(dst, src) elementwise (all_reduce "max" fold)."""
+    if tuple(dst.shape) != tuple(src.shape) or dst.dtype != src.dtype:
+        raise UnsupportedConfigError("max_into: shape/dtype mismatch")
+    require_device("max_into", dst, src)
+    if dst.numel() == 0:
+        return
+    nd = max(1, dst.dim())
+    rc = _lib.load().dp_max_strided(
+        nd, i64_array(list(dst.shape) or [1]), _ptr(dst), i64_array(list(dst.stride()) or [1]),
+        _ptr(src), i64_array(list(src.stride()) or [1]), dtype_code(dst), _stream(dst))
+    _lib.check(rc, "dp_max_strided")
+
+
+def is_dense(t: torch.Tensor) -> bool:
+    """Non-overlapping and dense: the elements fill [0, numel) of memory in
+    some dim order (any permutation of a contiguous layout)."""
+    dims = sorted((s, n) for s, n in zip(t.stride(), t.shape) if n != 1)
+    expect = 1
+    for s, n in dims:
+        if s != expect:
+            return False
+        expect *= n
+    return True
+
+
+def fill(t: torch.Tensor, value: float) -> torch.Tensor:
+    """t[...] = value for a dense device tensor (dp_fill); returns t."""
+    require_device("fill", t)
+    if t.numel() == 0:
+        return t
+    if not is_dense(t):
+        raise UnsupportedConfigError("fill: tensor must be dense")
+    rc = _lib.load().dp_fill(t.numel(), _ptr(t), dtype_code(t), float(value), _stream(t))
+    _lib.check(rc, "dp_fill")
+    return t
+
+
+def zeros(shape, dtype, device) -> torch.Tensor:
+    """A zero-filled device tensor made by the library (no eager torch kernel)."""
+    return fill(torch.empty(tuple(shape), dtype=dtype, device=device), 0.0)
 
 
 # ---------------------------------------------------------------------------

@@ -266,12 +266,10 @@ class ThreadTransport:
                 raise CollectiveError(
                     f"all_reduce contribution mismatch: member 0 has {tuple(parts[0].shape)} "
                     f"{parts[0].dtype}, member {i} has {tuple(p.shape)} {p.dtype}")
-        acc = parts[0].clone()
+        acc = empty_like_layout(parts[0], parts[0].shape)
+        _copy_into(acc, parts[0])
         for p in parts[1:]:
-            if op == "sum":
-                acc.add_(p)
-            else:
-                torch.maximum(acc, p, out=acc)
+            _fold_into(acc, p, op)
         return acc
 
     def barrier(self, members, me: int) -> None:
@@ -322,17 +320,22 @@ class DistTransport:
         # are staged through host memory
         stage = self.kind != "nccl"
         for dst, t in sends:
-            t = t.contiguous()
+            t = t if _dense(t) else t.contiguous()
             if stage and t.is_cuda:
                 t = t.cpu()
             keep.append(t)
-            ops.append(dist.P2POp(dist.isend, t, dst))
+            # the wire format is the payload's bytes in memory order: a dense
+            # channels-last face travels as-is (a flat view, no transpose)
+            ops.append(dist.P2POp(dist.isend, _flat(t), dst))
         for src, out in recvs:
             if stage and out.is_cuda:
-                host = torch.empty(out.shape, dtype=out.dtype)
+                host = torch.empty_strided(out.shape, out.stride(), dtype=out.dtype) \
+                    if _dense(out) else torch.empty(out.shape, dtype=out.dtype)
                 after.append((out, host))
                 out = host
-            ops.append(dist.P2POp(dist.irecv, out, src))
+            if not _dense(out):
+                raise CollectiveError("receive buffers must be dense")
+            ops.append(dist.P2POp(dist.irecv, _flat(out), src))
         if not ops:
             return _Done()
         if self.kind == "nccl":
@@ -365,6 +368,35 @@ class DistTransport:
 
     def barrier(self, members, me: int) -> None:
         self.dist.barrier(group=self.meta_groups[tuple(members)])
+
+
+def _dense(t: torch.Tensor) -> bool:
+    """Non-overlapping and dense (some permutation of a contiguous layout)."""
+    return t.is_contiguous() or t.is_contiguous(memory_format=memory_format_of(t))
+
+
+def _fold_into(acc: torch.Tensor, part: torch.Tensor, op: str) -> None:
+    """acc = acc (+|max) part: the library's accumulate / max kernels on
+    device, host arithmetic for CPU tensors (the gloo test meshes)."""
+    if acc.is_cuda:
+        from . import kernels
+
+        if op == "sum":
+            kernels.accumulate(acc, part)
+        else:
+            kernels.max_into(acc, part)
+    elif op == "sum":
+        acc.add_(part)
+    else:
+        torch.maximum(acc, part, out=acc)
+
+
+def _flat(t: torch.Tensor) -> torch.Tensor:
+    """1-D contiguous view of a dense tensor's memory (element order = memory
+    order); the process-group P2P calls require standard contiguity."""
+    if t.is_contiguous():
+        return t.reshape(-1)
+    return t.as_strided((t.numel(),), (1,))
 
 
 def _copy_into(dst: torch.Tensor, src: torch.Tensor) -> None:
@@ -455,12 +487,43 @@ def _narrow(t: torch.Tensor, dim: int, start: int, length: int) -> torch.Tensor:
     return t.narrow(dim, start, length)
 
 
-def _packed(t: torch.Tensor) -> torch.Tensor:
-    """Contiguous copy of a (possibly strided) face — the halo/varlen pack
-    kernel on device, a host copy for CPU tensors."""
-    if t.is_contiguous():
+def memory_format_of(t: torch.Tensor):
+    """The dense memory format `t` is laid out in: channels-last (NHWC /
+    NDHWC, the conv hot path's layout) when it is channels-last and not
+    plain contiguous, else torch.contiguous_format.  When a tensor satisfies
+    both, the two byte layouts coincide."""
+    if t.dim() == 5 and not t.is_contiguous() and \
+            t.is_contiguous(memory_format=torch.channels_last_3d):
+        return torch.channels_last_3d
+    if t.dim() == 4 and not t.is_contiguous() and \
+            t.is_contiguous(memory_format=torch.channels_last):
+        return torch.channels_last
+    return torch.contiguous_format
+
+
+def empty_in_format(shape, fmt, dtype, device) -> torch.Tensor:
+    """Uninitialised tensor of `shape` laid out densely in memory format `fmt`."""
+    if fmt is torch.contiguous_format or len(shape) != (5 if fmt is torch.channels_last_3d else 4):
+        return torch.empty(tuple(shape), dtype=dtype, device=device)
+    return torch.empty(tuple(shape), dtype=dtype, device=device, memory_format=fmt)
+
+
+def empty_like_layout(ref: torch.Tensor, shape, dtype=None) -> torch.Tensor:
+    """Allocate `shape` in `ref`'s memory format (channels-last stays
+    channels-last, so halo buffers and gradients stay in the layout the
+    tcgen05 conv consumes: C innermost, one contiguous run per face)."""
+    return empty_in_format(shape, memory_format_of(ref), dtype or ref.dtype, ref.device)
+
+
+def _packed(t: torch.Tensor, fmt=torch.contiguous_format) -> torch.Tensor:
+    """`t` itself when it is one dense run in memory format `fmt`, else a copy
+    packed into that format — the halo / varlen pack kernel on device, a host
+    copy for CPU tensors.  Sender and receiver agree on `fmt` (the format of
+    their local blocks), so a channels-last D/H face (one contiguous run) goes
+    out in place with no pack at all."""
+    if t.is_contiguous(memory_format=fmt):
         return t
-    out = torch.empty(t.shape, dtype=t.dtype, device=t.device)
+    out = empty_in_format(t.shape, fmt, t.dtype, t.device)
     _copy_into(out, t)
     return out
 
@@ -473,7 +536,8 @@ def gather_known(group: AxisGroup, local: torch.Tensor, dim: int, extents) -> to
     extents = [int(e) for e in extents]
     shape = list(local.shape)
     shape[dim] = sum(extents)
-    out = torch.empty(shape, dtype=local.dtype, device=local.device)
+    fmt = memory_format_of(local)
+    out = empty_in_format(shape, fmt, local.dtype, local.device)
     me = group.index
     offs = [0]
     for e in extents:
@@ -484,7 +548,7 @@ def gather_known(group: AxisGroup, local: torch.Tensor, dim: int, extents) -> to
     if group.size == 1:
         return out
     sends = []
-    payload = _packed(local)
+    payload = _packed(local, fmt)
     if payload.numel():
         for i, r in enumerate(group.members):
             if i != me:
@@ -495,10 +559,10 @@ def gather_known(group: AxisGroup, local: torch.Tensor, dim: int, extents) -> to
         if i == me or extents[i] == 0 or out.numel() == 0:
             continue
         dst = _narrow(out, dim, offs[i], extents[i])
-        if dst.is_contiguous():
+        if dst.is_contiguous(memory_format=fmt):
             recvs.append((r, dst))
         else:
-            stage = torch.empty(dst.shape, dtype=out.dtype, device=out.device)
+            stage = empty_in_format(dst.shape, fmt, out.dtype, out.device)
             recvs.append((r, stage))
             unpack.append((dst, stage))
     group.ctx.transport.exchange(sends, recvs)
@@ -570,21 +634,25 @@ def halo_sendrecv(group: AxisGroup, local: torch.Tensor, dim: int, serve_left: i
     left = group.members[i - 1] if i > 0 else None
     right = group.members[i + 1] if i < group.size - 1 else None
     extent = local.shape[dim]
+    # faces travel and land in the local block's own memory format: a
+    # channels-last D (3-D) / H (2-D) face of a batch-1 block is one contiguous
+    # run, sent in place, and the received halo is directly a tcgen05 operand
+    fmt = memory_format_of(local)
     sends, recvs = [], []
     if left is not None and serve_left > 0:
-        sends.append((left, _packed(_narrow(local, dim, 0, serve_left))))
+        sends.append((left, _packed(_narrow(local, dim, 0, serve_left), fmt)))
     if right is not None and serve_right > 0:
-        sends.append((right, _packed(_narrow(local, dim, extent - serve_right, serve_right))))
+        sends.append((right, _packed(_narrow(local, dim, extent - serve_right, serve_right), fmt)))
     lh = rh = None
     if left is not None and lw > 0:
         shp = list(local.shape)
         shp[dim] = lw
-        lh = torch.empty(shp, dtype=local.dtype, device=local.device)
+        lh = empty_in_format(shp, fmt, local.dtype, local.device)
         recvs.append((left, lh))
     if right is not None and rw > 0:
         shp = list(local.shape)
         shp[dim] = rw
-        rh = torch.empty(shp, dtype=local.dtype, device=local.device)
+        rh = empty_in_format(shp, fmt, local.dtype, local.device)
         recvs.append((right, rh))
     if not wait:
         return lh, rh, group.ctx.transport.exchange_start(sends, recvs)
@@ -640,7 +708,7 @@ def halo_exchange(group: AxisGroup, local: torch.Tensor, dim: int, left_width: i
         return local
     shp = list(local.shape)
     shp[dim] = lw + extent + rw
-    out = torch.empty(shp, dtype=local.dtype, device=local.device)
+    out = empty_like_layout(local, shp)
     pos = 0
     for piece in (lh, local, rh):
         if piece is None:
@@ -684,6 +752,8 @@ def _spawn_threads(mesh: DeviceMesh, fn, seed: int, timeout: float, device):
     failures = {}
     lock = threading.Lock()
     dev = torch.device(device) if device is not None else _default_device()
+    if dev.type == "cuda" and dev.index is None:
+        dev = torch.device("cuda", torch.cuda.current_device())
 
     def run(rank: int):
         try:

@@ -33,8 +33,8 @@ from . import kernels
 from .dispatch import register_dense_reference, register_handler
 from .errors import (DegenerateInputError, DimensionError, HaloError, MetadataError,
                      UnsupportedConfigError)
-from .mesh import (AxisGroup, PeerAbort, all_reduce, halo_error_text, halo_sendrecv,
-                   ring_shift_known)
+from .mesh import (AxisGroup, PeerAbort, all_reduce, empty_like_layout, halo_error_text,
+                   halo_sendrecv, ring_shift_known)
 from .plan import conv_output_extent, halo_conv_plan, ring_source
 from .sharding import Shard, ShardTensor
 
@@ -81,21 +81,6 @@ def _conv_params(nsp, kernel, stride, padding):
     return strides, pads
 
 
-def _empty_like_layout(ref: torch.Tensor, shape, dtype=None) -> torch.Tensor:
-    """Allocate `shape` in `ref`'s memory format (channels-last stays
-    channels-last so the tcgen05 path sees C-innermost tensors)."""
-    dtype = dtype or ref.dtype
-    if ref.dim() == 5 and ref.is_contiguous(memory_format=torch.channels_last_3d) \
-            and not ref.is_contiguous():
-        return torch.empty(shape, dtype=dtype, device=ref.device,
-                           memory_format=torch.channels_last_3d)
-    if ref.dim() == 4 and ref.is_contiguous(memory_format=torch.channels_last) \
-            and not ref.is_contiguous():
-        return torch.empty(shape, dtype=dtype, device=ref.device,
-                           memory_format=torch.channels_last)
-    return torch.empty(shape, dtype=dtype, device=ref.device)
-
-
 # ---------------------------------------------------------------------------
 # dense (single-rank) device references — used for replicated inputs and as
 # the dispatch fallback's dense implementations
@@ -123,7 +108,7 @@ def dense_conv(x: torch.Tensor, weight: torch.Tensor, stride=1, padding=0) -> to
     out_sp = [conv_output_extent(g, k, s, p)
               for g, k, s, p in zip(xb.shape[2:], kernel, strides, pads)]
     w = weight.to(x.dtype).contiguous()
-    y = _empty_like_layout(xb, [xb.shape[0], c_out] + out_sp)
+    y = empty_like_layout(xb, [xb.shape[0], c_out] + out_sp)
     kernels.conv_fwd(xb, None, w, y, kernel=kernel, stride=strides,
                      base=[-p for p in pads], shard=-1, halo_rows=0)
     return y if batched else y[0]
@@ -236,7 +221,7 @@ def halo_conv_forward(x: ShardTensor, weight, stride=1, padding=0):
     out_sp[sp] = mine.n_out
     base = [-p for p in pads]
     base[sp] = mine.base
-    yb = _empty_like_layout(xb, [xb.shape[0], weight.shape[0]] + out_sp)
+    yb = empty_like_layout(xb, [xb.shape[0], weight.shape[0]] + out_sp)
     # Interior output rows read only local rows: they are convolved while the
     # halo is in flight; the boundary rows follow once it has landed.
     n_int = _interior_rows(mine.n_out, xb.shape[sp + 2], kernel[sp], strides[sp], mine.base) \
@@ -300,7 +285,7 @@ def halo_conv_backward(tape: ConvTape, dout):
     kernel = tuple(w.shape[2:])
     wd = kernels.wgrad_dtype(xl.dtype)
     dw = torch.empty(w.shape, dtype=wd, device=xl.device)
-    dxb = _empty_like_layout(xb, list(xb.shape))
+    dxb = empty_like_layout(xb, list(xb.shape))
     if tape.plan is None:
         if xb.numel():
             kernels.conv_dgrad(dyb, w, dxb, None, kernel=kernel, stride=tape.strides,
@@ -308,7 +293,7 @@ def halo_conv_backward(tape: ConvTape, dout):
             kernels.conv_wgrad(xb, None, dyb, dw, kernel=kernel, stride=tape.strides,
                                base=tape.base, shard=-1, halo_rows=0)
         else:
-            dw.zero_()
+            kernels.fill(dw, 0.0)
         dx = dxb if tape.batched else dxb[0]
         return ShardTensor(dx, x.global_shape, x.ctx, x.placements, x.shard_shapes), dw
     group = _group(x, tape.axis)
@@ -319,15 +304,14 @@ def halo_conv_backward(tape: ConvTape, dout):
     if mine.rw:
         hshape = list(xb.shape)
         hshape[dim] = mine.rw
-        halo_grad = torch.empty(hshape, dtype=xb.dtype, device=xb.device)
+        halo_grad = empty_like_layout(xb, hshape)
     work = mine.n_out and xb.shape[dim] + mine.rw
     if work:
         kernels.conv_dgrad(dyb, w, dxb, halo_grad, kernel=kernel, stride=tape.strides,
                            base=tape.base, shard=tape.sp, halo_rows=mine.rw)
     else:
-        if dxb.numel():
-            dxb.zero_()
-        dw.zero_()
+        kernels.fill(dxb, 0.0)
+        kernels.fill(dw, 0.0)
     # reverse halo: my halo rows' gradient goes to r+1, r-1's comes to me;
     # posted before wgrad so the transfer overlaps it
     x.ctx.collective_count += 1
@@ -341,7 +325,7 @@ def halo_conv_backward(tape: ConvTape, dout):
     if prv is not None and from_left:
         ishape = list(xb.shape)
         ishape[dim] = from_left
-        incoming = torch.empty(ishape, dtype=xb.dtype, device=xb.device)
+        incoming = empty_like_layout(xb, ishape)
         recvs.append((prv, incoming))
     pending = x.ctx.transport.exchange_start(sends, recvs)
     if work:
@@ -368,9 +352,9 @@ class RingSoftmaxState:
 
     def __init__(self, rows: int, heads: int, dim: int, dtype: torch.dtype, device):
         sd = kernels.state_dtype(dtype)
-        self.m = torch.full((rows, heads), -math.inf, dtype=sd, device=device)
-        self.l = torch.zeros((rows, heads), dtype=sd, device=device)
-        self.acc = torch.zeros((rows, heads, dim), dtype=sd, device=device)
+        self.m = kernels.fill(torch.empty((rows, heads), dtype=sd, device=device), -math.inf)
+        self.l = kernels.zeros((rows, heads), sd, device)
+        self.acc = kernels.zeros((rows, heads, dim), sd, device)
 
     def update(self, q, k, v, scale) -> None:
         if k.shape[0] == 0 or q.shape[0] == 0:
@@ -532,7 +516,7 @@ def ring_attention_backward(tape: AttnTape, dout):
     delta = torch.empty((ql.shape[0], heads), dtype=sd, device=ql.device)
     if ql.shape[0]:
         kernels.attn_bwd_preprocess(ol, do, delta)
-    dq = torch.zeros((ql.shape[0], heads, d), dtype=sd, device=ql.device)
+    dq = kernels.zeros((ql.shape[0], heads, d), sd, ql.device)
 
     def run_block(kb, vb, dkb, dvb):
         if kb.shape[0] == 0 or ql.shape[0] == 0:
@@ -541,8 +525,8 @@ def ring_attention_backward(tape: AttnTape, dout):
 
     if tape.axis is None:
         kl, vl = k.local, v.local
-        dk = torch.zeros((kl.shape[0], heads, d), dtype=sd, device=ql.device)
-        dv = torch.zeros_like(dk)
+        dk = kernels.zeros((kl.shape[0], heads, d), sd, ql.device)
+        dv = kernels.zeros((kl.shape[0], heads, d), sd, ql.device)
         run_block(kl, vl, dk, dv)
     else:
         group = _group(q, tape.axis)
@@ -563,7 +547,7 @@ def ring_attention_backward(tape: AttnTape, dout):
                 q.ctx.collective_count += 1
                 src = ring_source(me, step + 1, r)
                 nxt_pay, pending = _ring_post(group, pay, (kv_ext[src],) + tuple(pay.shape[1:]))
-            grads = torch.zeros((2, kv_ext[src_now], heads, d), dtype=sd, device=ql.device)
+            grads = kernels.zeros((2, kv_ext[src_now], heads, d), sd, ql.device)
             if pay.shape[0]:
                 kb, vb = pay[:, 0], pay[:, 1]
                 if ql.dim() == 2:
@@ -596,10 +580,8 @@ def ring_attention_backward(tape: AttnTape, dout):
 
 
 def _cast_into(dst: torch.Tensor, src: torch.Tensor) -> None:
-    """Accumulator -> parameter dtype (a cast, done by torch: it is a
-    one-pass elementwise conversion on the gradient, not part of the
-    attention arithmetic)."""
-    dst.copy_(src)
+    """Accumulator -> parameter dtype (dp_convert_strided: one HBM pass)."""
+    kernels.convert(dst, src)
 
 
 # ---------------------------------------------------------------------------

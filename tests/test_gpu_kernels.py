@@ -30,6 +30,46 @@ def kernels():
     return k
 
 
+LAYOUTS = [((1, 32, 6, 12, 40), torch.channels_last_3d, 2, 2),
+           ((2, 16, 5, 9, 33), torch.channels_last_3d, 2, 3),
+           ((3, 64, 7, 20), torch.channels_last, 2, 4),
+           ((513, 16, 64), None, 0, 100)]
+
+
+@pytest.mark.parametrize("shape,fmt,dim,n", LAYOUTS)
+def test_element_maps_on_layouts(shape, fmt, dim, n):
+    """copy / accumulate / convert / max / fill on channels-last and plain
+    blocks and on their narrowed faces (the halo pack / unpack / reverse-halo
+    shapes): exact against torch's own elementwise ops."""
+    k = kernels()
+    g = torch.Generator(device=DEV).manual_seed(3)
+
+    def mk(dtype):
+        t = torch.randn(shape, generator=g, device=DEV).to(dtype)
+        return t.contiguous(memory_format=fmt) if fmt is not None else t
+
+    for dtype in (torch.bfloat16, torch.float32, torch.float64):
+        a, b = mk(dtype), mk(dtype)
+        fa, fb = a.narrow(dim, 1, n), b.narrow(dim, 0, n)
+        want = fa + fb if dtype != torch.bfloat16 else (fa.float() + fb.float()).to(dtype)
+        k.accumulate(fa, fb)
+        assert torch.equal(fa, want)
+        want = torch.maximum(fa, fb)
+        k.max_into(fa, fb)
+        assert torch.equal(fa, want)
+        dst = torch.empty_like(fb)
+        k.copy_strided(dst, fb)
+        assert torch.equal(dst, fb)
+        for odt in (torch.bfloat16, torch.float32, torch.float64):
+            o = torch.empty(fb.shape, dtype=odt, device=DEV)
+            k.convert(o, fb)
+            assert torch.equal(o, fb.to(odt))
+        z = k.fill(torch.empty_like(a), -2.5)
+        assert torch.equal(z, torch.full_like(a, -2.5))
+        assert torch.equal(k.zeros(shape, dtype, DEV), torch.zeros(shape, dtype=dtype,
+                                                                    device=DEV))
+
+
 @pytest.mark.parametrize("shape,perm,sl", [
     ((64, 33, 7), (0, 1, 2), (slice(None), slice(3, 20), slice(None))),
     ((8, 16, 128), (2, 0, 1), (slice(None), slice(None), slice(5, 70))),
@@ -301,21 +341,6 @@ def test_conv_single_cta_and_per_mma_issue_paths():
                             "-k", "test_conv_tc_fwd_dgrad_vs_oracle"], env=env, capture_output=True,
                            text=True, timeout=600)
         assert r.returncode == 0, str(env_extra) + r.stdout[-2000:] + r.stderr[-2000:]
-
-
-def test_conv_pair_kernel_opt_in():
-    """The CTA-pair (cta_group::2) conv kernel is opt-in (DP_CONV_PAIR=1, read
-    once per process): run the tcgen05 conv parity cases with it enabled."""
-    import os
-    import subprocess
-    import sys
-
-    env = dict(os.environ, DP_CONV_PAIR="1")
-    here = os.path.dirname(os.path.abspath(__file__))
-    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", os.path.join(here, "test_gpu_kernels.py"),
-                        "-k", "test_conv_tc_fwd_dgrad_vs_oracle"], env=env, capture_output=True,
-                       text=True, timeout=600)
-    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
 
 
 X3_CASES = [

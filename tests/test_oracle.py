@@ -73,6 +73,19 @@ def test_conv_nd_against_nested_loops(n, s, p):
     assert np.allclose(oconv.conv(x, w, s, p), _conv_loops(x, w, s, p), atol=1e-12)
 
 
+@pytest.mark.parametrize("n,s,p", [(1, 2, 1), (2, 1, 1), (2, 3, 2), (3, 1, 1), (3, 2, 0)])
+def test_conv_fast_matches_reference_einsum(n, s, p):
+    """The BLAS tap-sum oracle (large parity cases) equals the reference's
+    einsum restatement to fp64 rounding."""
+    rng = np.random.default_rng(n * 7 + s + p)
+    x = rng.standard_normal((2, 3) + (7,) * n)
+    w = rng.standard_normal((4, 3) + (3,) * n)
+    want = oconv.conv(x, w, s, p)
+    got = oconv.conv_fast(x, w, s, p)
+    assert got.shape == want.shape
+    assert np.abs(got - want).max() <= 1e-12 * np.abs(want).max()
+
+
 @pytest.mark.parametrize("n,s,p", [(1, 1, 1), (2, 2, 1), (3, 1, 1)])
 def test_conv_grads_central_differences(n, s, p):
     rng = np.random.default_rng(5 + n)
