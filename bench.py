@@ -835,6 +835,7 @@ def main():
 
     kernels.set_algo(args.algo)
     ctx = init(args)
+    _OPEN.append(ctx)
     setup_fn, cpu_fn, sample_desc = CONFIGS[args.config]
     W = setup_fn(ctx)
     step = W["step"]
@@ -855,6 +856,8 @@ def main():
     with ClockSampler(local_gpu) as clk:
         barrier(ctx)
         timer.active = comm.active = True
+        if hasattr(ctx.transport, "timing"):
+            ctx.transport.timing = []   # NativeTransport: events around every NCCL round
         start.record()
         for _ in range(args.steps):
             step()
@@ -867,10 +870,17 @@ def main():
     ms = max_over_ranks(ctx, my_ms)
     ksum = timer.summary()
     comm_bytes = comm.bytes / args.steps
+    nccl_ms = nccl_bytes = None
+    if getattr(ctx.transport, "timing", None) is not None:
+        rounds = ctx.transport.timing
+        ctx.transport.timing = None
+        nccl_ms = sum(a.elapsed_time(b) for a, b, _ in rounds) / args.steps
+        nccl_bytes = sum(n for _, _, n in rounds) / args.steps
     kernel_ms_step = sum(v["ms"] for v in ksum.values()) / args.steps
     # every rank's per-kernel record (max over ranks for the roofline)
     ranks_k = gather_all(ctx, {"ksum": ksum, "ms": my_ms, "kernel_ms": kernel_ms_step,
-                               "comm_bytes": comm_bytes, "simt": simt_calls})
+                               "comm_bytes": comm_bytes, "simt": simt_calls,
+                               "nccl_ms": nccl_ms, "nccl_bytes": nccl_bytes})
 
     # --- e2e through the public API: pinned host input -> device, gradients ->
     # host.  Every step copies its own input shard from pinned host memory and
@@ -1013,6 +1023,16 @@ def main():
         "comm": {"backend": backend + (" (ranks share one GPU: dry run)" if shared else ""),
                  "bytes_sent_per_step_by_rank": [rk["comm_bytes"] for rk in ranks_k]},
     }
+    if any(rk["nccl_ms"] for rk in ranks_k):
+        # point-to-point rounds timed on the comm stream (CUDA events around
+        # each grouped NCCL round): bytes sent / round time per rank, against
+        # NVLink 5's 900 GB/s per direction
+        nv = []
+        for rk in ranks_k:
+            gbs = rk["nccl_bytes"] / (rk["nccl_ms"] / 1000.0) / 1e9 if rk["nccl_ms"] else None
+            nv.append({"ms_per_step": rk["nccl_ms"], "bytes_per_step": rk["nccl_bytes"],
+                       "gbs": gbs, "frac_of_nvlink": gbs / 900.0 if gbs else None})
+        line["comm"]["nvlink"] = nv
     if W.get("extra"):
         line["comm"].update(W["extra"])
     print(json.dumps(line), flush=True)
@@ -1026,7 +1046,17 @@ def gather_all(ctx, obj):
     return ctx.transport.gather_meta(group.members, group.index, obj)
 
 
+_OPEN = []
+
+
 def _shutdown():
+    for ctx in _OPEN:
+        close = getattr(ctx.transport, "close", None)
+        if close is not None:
+            try:
+                close()
+            except Exception:  # noqa: BLE001 - best effort at exit
+                pass
     try:
         import torch.distributed as dist
 

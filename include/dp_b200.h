@@ -48,6 +48,8 @@ extern "C" {
 #define DP_ERR_INVALID 1      /* bad argument (shape, stride, null pointer) */
 #define DP_ERR_UNSUPPORTED 2  /* configuration outside the kernel envelope  */
 #define DP_ERR_CUDA 3         /* CUDA runtime / launch failure              */
+#define DP_ERR_COMM 4         /* NCCL failure (synchronous or asynchronous) */
+#define DP_ERR_TIMEOUT 5      /* dp_comm_wait deadline passed (comm aborted) */
 
 /* element types */
 #define DP_F32 0
@@ -227,6 +229,65 @@ int dp_norm_apply(int kind, int64_t outer, int64_t n, int64_t inner, const void 
 #define DP_EW_SCALE 2
 int dp_elementwise(int op, int64_t n, const void *a, const void *b, double scalar, void *out,
                    int dtype, void *stream);
+
+/* ---- communicators and exchanges (NCCL over NVLink / NVSwitch) ------------
+ *
+ * Replace domainpar/mesh.py:252-403 (all_reduce, all_gather_varlen,
+ * ring_shift, halo_exchange, barrier over per-pair queues).  NCCL is loaded
+ * at run time (dlopen; dp_comm_load(NULL) = "libnccl.so.2", normally the copy
+ * the host process already has); without it these return DP_ERR_UNSUPPORTED
+ * and every other entry point still works.  A communicator is an opaque
+ * handle; one per mesh-axis line (dp_comm_split of the world communicator,
+ * color = line, key = position on the line).  Every exchange is ONE
+ * ncclGroupStart/End of byte sends / receives enqueued on `stream`: buffers
+ * are sent in their memory order (a dense channels-last face goes as-is).
+ * Byte counts of 0 post nothing.  The caller keeps buffers alive until the
+ * stream passes the exchange. */
+#define DP_NCCL_UNIQUE_ID_BYTES 128
+#define DP_REDUCE_SUM 0
+#define DP_REDUCE_MAX 1
+int dp_comm_load(const char *nccl_path);
+int dp_comm_version(int *version);
+/* rank 0 creates the id and ships it to the others out of band */
+int dp_comm_unique_id(void *id_out /* DP_NCCL_UNIQUE_ID_BYTES */);
+/* collective over `world` ranks; the current CUDA device is this rank's */
+int dp_comm_init(void **comm_out, int world, int rank, const void *unique_id);
+/* collective over the parent: ranks with the same color form one
+ * communicator ranked by key; color < 0 -> *comm_out = NULL */
+int dp_comm_split(void *parent, int color, int key, void **comm_out);
+int dp_comm_info(void *comm, int *rank, int *size);
+int dp_comm_destroy(void *comm);
+int dp_comm_abort(void *comm);
+/* generic grouped point-to-point: op i sends (is_recv[i] == 0) or receives
+ * bytes[i] bytes of bufs[i] to / from peers[i] */
+int dp_comm_exchange(void *comm, int n, const int *peers, const int *is_recv, void *const *bufs,
+                     const int64_t *bytes, void *stream);
+/* halo round (domainpar/mesh.py:318-386): send my first / last rows to the
+ * left / right neighbour, receive their faces; peer -1 = no neighbour */
+int dp_halo_sendrecv(void *comm, int left, int right, const void *send_left,
+                     int64_t send_left_bytes, const void *send_right, int64_t send_right_bytes,
+                     void *recv_left, int64_t recv_left_bytes, void *recv_right,
+                     int64_t recv_right_bytes, void *stream);
+/* ring hop (domainpar/mesh.py:305-315): send to rank+1, receive from rank-1 */
+int dp_ring_step(void *comm, const void *send, int64_t send_bytes, void *recv, int64_t recv_bytes,
+                 void *stream);
+/* varlen all-gather (domainpar/mesh.py:280-302): every rank's `local` lands
+ * at out + offsets[rank] (bytes[rank] bytes; this rank's own block is the
+ * caller's copy) */
+int dp_varlen_allgather(void *comm, const void *local, int64_t local_bytes, void *out,
+                        const int64_t *offsets, const int64_t *bytes, void *stream);
+/* variable-count all-to-all (Shard(i) -> Shard(j) redistribute): send[j] /
+ * recv[j] per peer j (entries for this rank are ignored) */
+int dp_varlen_alltoall(void *comm, const void *const *send, const int64_t *send_bytes,
+                       void *const *recv, const int64_t *recv_bytes, void *stream);
+/* recv = reduce(send) over the communicator, DP_REDUCE_SUM / _MAX
+ * (domainpar/mesh.py:252-277) */
+int dp_allreduce(void *comm, const void *send, void *recv, int64_t count, int dtype, int op,
+                 void *stream);
+/* watchdog: block until `stream` drains; an asynchronous NCCL error or the
+ * deadline (timeout_s > 0) aborts the communicator -> DP_ERR_COMM /
+ * DP_ERR_TIMEOUT */
+int dp_comm_wait(void *comm, void *stream, double timeout_s);
 
 #ifdef __cplusplus
 }

@@ -6,6 +6,10 @@ ring_members()  per-member outputs of domainpar/ops.py:217-279: member i
               folds K/V blocks in ring order (i, i-1, i-2, ...)
 sdpa_grads()  analytic gradients in fp64 (no reference function; pinned by
               finite differences in tests/test_oracle.py)
+head_slab()   one head's output / dq on a query-row slab and dk / dv on a
+              key slab at full sequence length, the same formulas restricted
+              (row statistics LSE / delta for every query computed in chunks):
+              full-size parity; pinned against sdpa / sdpa_grads.
 Multi-head inputs [S, H, d] are handled head by head (the reference is
 single-head [S, d]; its ViT pipeline loops heads, ops.py:590-600).
 """
@@ -100,3 +104,38 @@ def sdpa_grads(q, k, v, do):
     if q.ndim == 2:
         return dq[:, 0], dk[:, 0], dv[:, 0]
     return dq, dk, dv
+
+
+def head_slab(q, k, v, do, rows, keys, chunk=2048):
+    """One head ([S, d] arrays): (o[rows], dq[rows], dk[keys], dv[keys]) of
+    sdpa with dO, at any S.  Query rows need all keys (fp64, rows x S);
+    the key slab needs every query's LSE and delta = rowsum(dO * O), taken
+    chunk by chunk (scores of a chunk in fp32 BLAS, exp / sums in fp64)."""
+    S, d = q.shape
+    scale = 1.0 / math.sqrt(d)
+    q64, k64, v64, d64 = (t.astype(np.float64) for t in (q, k, v, do))
+    # query-row slab
+    p = softmax64(q64[rows] @ k64.T * scale)
+    o = p @ v64
+    dp = d64[rows] @ v64.T
+    delta = (d64[rows] * o).sum(axis=1, keepdims=True)
+    dq = (p * (dp - delta)) @ k64 * scale
+    # every query's lse and delta
+    q32, k32, v32 = (t.astype(np.float32) for t in (q, k, v))
+    lse = np.empty(S)
+    dl = np.empty(S)
+    for c0 in range(0, S, chunk):
+        s = (q32[c0:c0 + chunk] @ k32.T).astype(np.float64) * scale
+        mx = s.max(axis=1, keepdims=True)
+        e = np.exp(s - mx)
+        den = e.sum(axis=1, keepdims=True)
+        lse[c0:c0 + chunk] = (mx + np.log(den))[:, 0]
+        oc = (e / den).astype(np.float32) @ v32
+        dl[c0:c0 + chunk] = (d64[c0:c0 + chunk] * oc.astype(np.float64)).sum(axis=1)
+    # key slab
+    pk = np.exp(q64 @ k64[keys].T * scale - lse[:, None])        # [S, |keys|]
+    dpk = d64 @ v64[keys].T
+    dsk = pk * (dpk - dl[:, None])
+    dv = pk.T @ d64
+    dk = dsk.T @ q64 * scale
+    return o, dq, dk, dv

@@ -10,6 +10,9 @@ conv_grads() the adjoint: dX by scattering dY*W back over every window
              position, dW by contracting the windows with dY.  No reference
              function exists (no autograd); pinned by central
              finite differences in tests/test_oracle.py.
+stack_window() a box of the output of a stack of stride-1 same-padded convs
+             computed from the input box it depends on (zero padding only at
+             the global borders): full-size parity on slabs.
 halo_conv_members()  per-member outputs of the sharded algorithm
              (domainpar/ops.py:363-422) on the gathered input.
 """
@@ -129,3 +132,44 @@ def halo_conv_members(x, w, extents, shard_dim, stride=1, padding=0):
         lp[sp] = 0
         outs.append(conv(block, w, strides, tuple(lp)))
     return outs, [pl[1] - pl[0] for pl in plans]
+
+
+def transposed_flipped(w):
+    """Weights of the input-gradient convolution of a stride-1 conv:
+    wt[ci, co, t] = w[co, ci, k - 1 - t] (dX = conv(dY, wt, padding k-1-p))."""
+    n = w.ndim - 2
+    return np.ascontiguousarray(np.flip(w, axis=tuple(range(2, 2 + n))).swapaxes(0, 1))
+
+
+def stack_window(x, ws, lo, hi):
+    """Box [lo, hi) (per spatial dim) of the output of conv(...conv(x, ws[0])
+    ..., ws[-1]), every layer stride 1 with padding (k-1)/2, computed from
+    the input box it depends on: the global input is read (as float64) only
+    there, zero outside the volume; each intermediate is zeroed outside the
+    volume because that is the next layer's padding.  `x` is any array-like
+    with numpy slicing (a torch CPU tensor works).  Returns float64."""
+    n = ws[0].ndim - 2
+    G = tuple(int(g) for g in x.shape[-n:])
+    rad = [[(w.shape[2 + i] - 1) // 2 for i in range(n)] for w in ws]
+    a = [lo[i] - sum(r[i] for r in rad) for i in range(n)]
+    b = [hi[i] + sum(r[i] for r in rad) for i in range(n)]
+    lead = tuple(x.shape[:-n])
+    cur = np.zeros(lead + tuple(bb - aa for aa, bb in zip(a, b)))
+    src = tuple(slice(max(aa, 0), min(bb, g)) for aa, bb, g in zip(a, b, G))
+    dst = tuple(slice(s.start - aa, s.stop - aa) for s, aa in zip(src, a))
+    piece = x[(Ellipsis,) + src]
+    piece = piece.double().numpy() if hasattr(piece, "double") else np.asarray(piece)
+    cur[(Ellipsis,) + dst] = piece
+    for li, w in enumerate(ws):
+        cur = conv_fast(cur, np.asarray(w, dtype=np.float64), 1, 0)
+        a = [aa + r for aa, r in zip(a, rad[li])]
+        b = [bb - r for bb, r in zip(b, rad[li])]
+        if li + 1 < len(ws):
+            for i in range(n):
+                idx = np.arange(a[i], b[i])
+                bad = (idx < 0) | (idx >= G[i])
+                if bad.any():
+                    sl = [slice(None)] * cur.ndim
+                    sl[cur.ndim - n + i] = bad
+                    cur[tuple(sl)] = 0.0
+    return cur

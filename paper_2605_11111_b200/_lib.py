@@ -11,12 +11,15 @@ from __future__ import annotations
 import ctypes
 import os
 
-from .errors import DeviceError, UnsupportedConfigError
+from .errors import CollectiveError, DeviceError, UnsupportedConfigError
 
 LIB_NAME = "libdpb200.so"
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
 
-DP_OK, DP_ERR_INVALID, DP_ERR_UNSUPPORTED, DP_ERR_CUDA = 0, 1, 2, 3
+DP_OK, DP_ERR_INVALID, DP_ERR_UNSUPPORTED, DP_ERR_CUDA, DP_ERR_COMM, DP_ERR_TIMEOUT = \
+    0, 1, 2, 3, 4, 5
+REDUCE_SUM, REDUCE_MAX = 0, 1
+NCCL_UNIQUE_ID_BYTES = 128
 DP_F32, DP_F64, DP_BF16 = 0, 1, 2
 ALGO_AUTO, ALGO_SIMT, ALGO_TC, ALGO_STRICT = 0, 1, 2, 3
 CONV_FWD, CONV_DGRAD, CONV_WGRAD = 0, 1, 2
@@ -27,6 +30,8 @@ _i64 = ctypes.c_int64
 _i32 = ctypes.c_int32
 _vp = ctypes.c_void_p
 _i64p = ctypes.POINTER(ctypes.c_int64)
+_i32p = ctypes.POINTER(ctypes.c_int)
+_vpp = ctypes.POINTER(ctypes.c_void_p)
 
 
 class ConvGeom(ctypes.Structure):
@@ -94,6 +99,25 @@ SIGNATURES = {
                                      ctypes.c_double, ctypes.c_double, _vp]),
     "dp_elementwise": (ctypes.c_int, [ctypes.c_int, ctypes.c_int64, _vp, _vp, ctypes.c_double,
                                       _vp, ctypes.c_int, _vp]),
+    # communicators / exchanges (comm.cu)
+    "dp_comm_load": (ctypes.c_int, [ctypes.c_char_p]),
+    "dp_comm_version": (ctypes.c_int, [_i32p]),
+    "dp_comm_unique_id": (ctypes.c_int, [_vp]),
+    "dp_comm_init": (ctypes.c_int, [_vpp, ctypes.c_int, ctypes.c_int, _vp]),
+    "dp_comm_split": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, _vpp]),
+    "dp_comm_info": (ctypes.c_int, [_vp, _i32p, _i32p]),
+    "dp_comm_destroy": (ctypes.c_int, [_vp]),
+    "dp_comm_abort": (ctypes.c_int, [_vp]),
+    "dp_comm_exchange": (ctypes.c_int, [_vp, ctypes.c_int, _i32p, _i32p, _vpp, _i64p, _vp]),
+    "dp_halo_sendrecv": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, _vp, ctypes.c_int64, _vp,
+                                        ctypes.c_int64, _vp, ctypes.c_int64, _vp, ctypes.c_int64,
+                                        _vp]),
+    "dp_ring_step": (ctypes.c_int, [_vp, _vp, ctypes.c_int64, _vp, ctypes.c_int64, _vp]),
+    "dp_varlen_allgather": (ctypes.c_int, [_vp, _vp, ctypes.c_int64, _vp, _i64p, _i64p, _vp]),
+    "dp_varlen_alltoall": (ctypes.c_int, [_vp, _vpp, _i64p, _vpp, _i64p, _vp]),
+    "dp_allreduce": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int64, ctypes.c_int, ctypes.c_int,
+                                    _vp]),
+    "dp_comm_wait": (ctypes.c_int, [_vp, _vp, ctypes.c_double]),
 }
 
 _LIB = None
@@ -128,12 +152,16 @@ def available() -> bool:
 
 
 def check(rc: int, what: str) -> None:
-    """Map a DP_ERR_* code to the package's error types."""
+    """Map a DP_ERR_* code to the package's error types (NCCL failures and
+    watchdog timeouts are CollectiveErrors, as the reference's queue
+    timeouts, domainpar/mesh.py:196-206)."""
     if rc == DP_OK:
         return
     msg = load().dp_last_error().decode(errors="replace")
     if rc == DP_ERR_UNSUPPORTED:
         raise UnsupportedConfigError(f"{what}: {msg}")
+    if rc in (DP_ERR_COMM, DP_ERR_TIMEOUT):
+        raise CollectiveError(f"{what}: {msg}")
     raise DeviceError(f"{what} failed (code {rc}): {msg}")
 
 

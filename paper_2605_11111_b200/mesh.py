@@ -46,7 +46,7 @@ REDUCE_OPS = ("sum", "max")
 
 __all__ = [
     "DeviceMesh", "RankContext", "AxisGroup", "all_reduce", "all_gather_varlen",
-    "ring_shift", "halo_exchange", "barrier", "spawn_mesh", "init_mesh",
+    "ring_shift", "halo_exchange", "barrier", "spawn_mesh", "init_mesh", "NativeTransport",
     "TIMEOUT_ENV", "REDUCE_OPS",
 ]
 
@@ -368,6 +368,119 @@ class DistTransport:
 
     def barrier(self, members, me: int) -> None:
         self.dist.barrier(group=self.meta_groups[tuple(members)])
+
+
+class _NcclPending:
+    """Handle of one exchange round on the transport's comm stream: wait()
+    orders the caller's current stream after it (no host block)."""
+
+    def __init__(self, done, keep):
+        self.done = done
+        self.keep = keep
+
+    def wait(self) -> None:
+        if self.done is not None:
+            torch.cuda.current_stream().wait_event(self.done)
+        self.done = None
+        self.keep = []
+
+
+class NativeTransport(DistTransport):
+    """One process per GPU: the data plane is NCCL through libdpb200.so's C
+    ABI (comm.py / csrc/comm.cu) on a dedicated comm stream, the control
+    plane (rendezvous, unique-id broadcast, metadata, barriers) is gloo.
+
+    Communicators are created eagerly here — the world communicator for
+    every point-to-point round (halo faces, reverse halos, K||V hops,
+    redistribute blocks) and one ncclCommSplit per mesh axis for the
+    all-reduces — so no exchange round ever depends on a lazily created,
+    collective-on-first-use communicator: ranks with nothing to send in a
+    round simply post nothing.  Exchange rounds run on the comm stream after
+    an event from the caller's stream, and their handle's wait() makes the
+    caller's stream wait on the round's completion event, so compute
+    launched between post and wait overlaps the transfer.  `timing`, when a
+    list, collects (start, end, bytes) CUDA events per round (bench.py)."""
+
+    def __init__(self, mesh: DeviceMesh, rank: int, device, timeout: float):
+        super().__init__(mesh, rank, "gloo")
+        from . import comm
+
+        self.kind = "nccl"
+        self.timeout = timeout
+        self.device = torch.device(device)
+        box = [comm.unique_id() if rank == 0 else None]
+        self.dist.broadcast_object_list(box, src=0, group=self.world_meta)
+        self.world = comm.NcclComm.init(mesh.world_size, rank, box[0])
+        self.stream = torch.cuda.Stream(device=self.device)
+        self.timing = None
+        coords = mesh.coords_of(rank)
+        self.line_comms = {}
+        for axis in range(mesh.ndim):
+            line = mesh.line(coords, axis)
+            if mesh.ndim == 1:
+                self.line_comms[line] = self.world
+            else:
+                self.line_comms[line] = self.world.split(color=coords[1 - axis],
+                                                         key=coords[axis])
+
+    def exchange_start(self, sends, recvs):
+        ops, keep = [], []
+        for dst, t in sends:
+            t = t if _dense(t) else t.contiguous()
+            keep.append(t)
+            ops.append((dst, False, _flat(t)))
+        for src, out in recvs:
+            if not _dense(out):
+                raise CollectiveError("receive buffers must be dense")
+            keep.append(out)
+            ops.append((src, True, _flat(out)))
+        if not ops:
+            return _Done()
+        cur = torch.cuda.current_stream(self.device)
+        ready = torch.cuda.Event()
+        ready.record(cur)
+        self.stream.wait_event(ready)
+        t0 = t1 = None
+        if self.timing is not None:
+            t0 = torch.cuda.Event(enable_timing=True)
+            t1 = torch.cuda.Event(enable_timing=True)
+            t0.record(self.stream)
+        self.world.exchange(ops, self.stream)
+        done = torch.cuda.Event(enable_timing=False)
+        if t1 is not None:
+            t1.record(self.stream)
+            self.timing.append((t0, t1, sum(t.numel() * t.element_size() for _, r, t in ops
+                                              if not r)))
+        done.record(self.stream)
+        for t in keep:
+            if t.is_cuda:
+                t.record_stream(self.stream)
+        return _NcclPending(done, keep)
+
+    def exchange(self, sends, recvs) -> None:
+        self.exchange_start(sends, recvs).wait()
+
+    def all_reduce(self, members, me: int, t: torch.Tensor, op: str) -> torch.Tensor:
+        comm = self.line_comms[tuple(members)]
+        src = t if t.is_contiguous() else t.contiguous()
+        out = torch.empty_like(src)
+        comm.allreduce(src, out, op, torch.cuda.current_stream(self.device))
+        return out
+
+    def barrier(self, members, me: int) -> None:
+        # watchdog first: every posted round must drain (or raise
+        # CollectiveError on an NCCL error / the mesh timeout), then the host
+        # rendezvous of the reference's barrier
+        self.world.wait(self.stream, self.timeout)
+        self.world.wait(torch.cuda.current_stream(self.device), self.timeout)
+        super().barrier(members, me)
+
+    def close(self) -> None:
+        seen = set()
+        for c in list(self.line_comms.values()) + [self.world]:
+            if id(c) not in seen and c is not None:
+                seen.add(id(c))
+                c.destroy()
 
 
 def _dense(t: torch.Tensor) -> bool:
@@ -798,14 +911,17 @@ def _proc_main(rank, world, port, mesh_shape, names, fn, seed, timeout, backend,
         os.environ["MASTER_ADDR"] = "127.0.0.1"
         os.environ["MASTER_PORT"] = str(port)
         on_gpu = backend in ("nccl", "gloo-cuda")
-        pg_backend = "gloo" if backend == "gloo-cuda" else backend
+        native = backend == "nccl" and os.environ.get("DP_TRANSPORT", "native") != "torch"
+        pg_backend = "gloo" if (backend == "gloo-cuda" or native) else backend
         if on_gpu:
             torch.cuda.set_device(rank % torch.cuda.device_count())
         dist.init_process_group(pg_backend, rank=rank, world_size=world,
                                 timeout=datetime.timedelta(seconds=max(timeout, 1.0)))
         mesh = DeviceMesh(mesh_shape, names)
         dev = torch.device("cuda", torch.cuda.current_device()) if on_gpu else torch.device("cpu")
-        ctx = RankContext(mesh, rank, DistTransport(mesh, rank, pg_backend), seed=seed, device=dev)
+        tr = NativeTransport(mesh, rank, dev, timeout) if native else \
+            DistTransport(mesh, rank, pg_backend)
+        ctx = RankContext(mesh, rank, tr, seed=seed, device=dev)
         res = _to_host(fn(ctx))
         out_q.put((rank, "ok", pickle.dumps(res)))
     except BaseException as exc:  # noqa: BLE001
@@ -815,6 +931,9 @@ def _proc_main(rank, world, port, mesh_shape, names, fn, seed, timeout, backend,
             out_q.put((rank, "err", pickle.dumps(CollectiveError(f"{type(exc).__name__}: {exc}"))))
     finally:
         try:
+            close = getattr(getattr(locals().get("ctx"), "transport", None), "close", None)
+            if close is not None:
+                close()
             if dist.is_initialized():
                 dist.destroy_process_group()
         except Exception:
@@ -918,10 +1037,17 @@ def init_mesh(shape=None, axis_names=("domain",), *, seed: int = 0,
         local = local % torch.cuda.device_count()
     if backend == "nccl" or gpu_gloo:
         torch.cuda.set_device(local)
+    # DP_TRANSPORT=torch keeps torch.distributed's NCCL process groups as the
+    # data plane instead of the library's own communicators
+    native = backend == "nccl" and os.environ.get("DP_TRANSPORT", "native") != "torch"
     if not dist.is_initialized():
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ.setdefault("MASTER_PORT", "29533")
-        dist.init_process_group(backend, rank=rank, world_size=world,
+        dist.init_process_group("gloo" if native else backend, rank=rank, world_size=world,
                                 timeout=datetime.timedelta(seconds=_resolve_timeout(None) * 20))
     dev = torch.device("cuda", local) if (backend == "nccl" or gpu_gloo) else torch.device("cpu")
-    return RankContext(mesh, rank, DistTransport(mesh, rank, backend), seed=seed, device=dev)
+    if native:
+        tr = NativeTransport(mesh, rank, dev, _resolve_timeout(None))
+    else:
+        tr = DistTransport(mesh, rank, backend)
+    return RankContext(mesh, rank, tr, seed=seed, device=dev)

@@ -11,8 +11,10 @@ travel to the GPU box, so its outputs are committed here as small fixtures:
   redist_cases.npz  redistribute inputs and the reference's per-rank blocks
   layer_cases.npz   sharded_softmax / sharded_layer_norm (uneven shards),
                     ddp_allreduce_grads and vit_block_pipeline outputs
+  dispatch_cases.npz  the fallback path (gather -> dense -> default_chunk
+                    re-scatter) on sdpa / matmul: blocks, shapes, trace
 
-Run:  python tests/golden/make_golden.py [core|layers]   (needs /root/reference)
+Run:  python tests/golden/make_golden.py [core|layers|dispatch]   (needs /root/reference)
 """
 
 from __future__ import annotations
@@ -302,6 +304,60 @@ def make_layer_cases():
     return out
 
 
+DISPATCH_SPECS = [
+    # (op, q/a extents, k/v extents or None, dtype)
+    ("sdpa", (5, 0, 4, 3), (2, 6, 0, 4), "float64"),
+    ("sdpa", (3, 3, 3, 3), (4, 4, 2, 2), "float32"),
+    ("matmul", (4, 1, 0, 3), None, "float64"),
+]
+
+
+def make_dispatch_cases():
+    """The reference's GPU-less fallback path (dispatch.py:156-201) on ops
+    with no sharded handler: per-rank blocks, shard shapes, placements and
+    the trace record (level "fallback", collectives = gathers)."""
+    from domainpar.dispatch import dispatch_operation, trace_lines
+
+    out = {}
+    rng = np.random.default_rng(77)
+    for i, (op, ext, kext, dt) in enumerate(DISPATCH_SPECS):
+        R = len(ext)
+        if op == "sdpa":
+            S, d = sum(ext), 8
+            q = rng.standard_normal((S, d)).astype(dt)
+            k = rng.standard_normal((sum(kext), d)).astype(dt)
+            v = rng.standard_normal((sum(kext), d)).astype(dt)
+            ins = {"q": q, "k": k, "v": v}
+        else:
+            a = rng.standard_normal((sum(ext), 6)).astype(dt)
+            b = rng.standard_normal((6, 5)).astype(dt)
+            ins = {"a": a, "b": b}
+
+        def prog(ctx, op=op, ins=ins, ext=ext, kext=kext):
+            root = ctx.rank_id == 0
+            if op == "sdpa":
+                qs = scatter_global(ctx, ins["q"] if root else None, (Shard(0),), {0: ext})
+                ks = scatter_global(ctx, ins["k"] if root else None, (Shard(0),), {0: kext})
+                vs = scatter_global(ctx, ins["v"] if root else None, (Shard(0),), {0: kext})
+                res = dispatch_operation("sdpa", qs, ks, vs)
+            else:
+                sa = scatter_global(ctx, ins["a"] if root else None, (Shard(0),), {0: ext})
+                res = dispatch_operation("matmul", sa, replicated(ctx, ins["b"]))
+            return (res.local, {int(a): list(e) for a, e in res.shard_shapes.items()},
+                    [str(p) for p in res.placements], trace_lines(ctx)[-1])
+
+        res = spawn_mesh((R,), ("domain",), prog)
+        for n, arr in ins.items():
+            out[f"f{i}_{n}"] = arr
+        for r, (loc, shapes, pl, line) in enumerate(res):
+            out[f"f{i}_local{r}"] = loc
+        out[f"f{i}_meta"] = np.array(json.dumps({
+            "op": op, "ext": list(ext), "kext": None if kext is None else list(kext),
+            "shapes": res[0][1], "placements": res[0][2], "trace": res[0][3]}))
+    out["count"] = np.array(len(DISPATCH_SPECS))
+    return out
+
+
 def main():
     only = sys.argv[1] if len(sys.argv) > 1 else None
     if only in (None, "core"):
@@ -312,6 +368,8 @@ def main():
         np.savez_compressed(os.path.join(HERE, "redist_cases.npz"), **make_redist_cases())
     if only in (None, "layers"):
         np.savez_compressed(os.path.join(HERE, "layer_cases.npz"), **make_layer_cases())
+    if only in (None, "dispatch"):
+        np.savez_compressed(os.path.join(HERE, "dispatch_cases.npz"), **make_dispatch_cases())
     print("golden fixtures written to", HERE)
 
 

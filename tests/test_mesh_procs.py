@@ -113,3 +113,32 @@ def test_halo_plan_replicated_gloo():
     a, b = run_procs(_plan_prog)
     assert a == b
     assert a[0] == (3, 2)  # pkg/tests/test_acceptance.py:113-130
+
+
+def _cl_halo_prog(ctx):
+    """Channels-last blocks (the conv hot path's layout, batch 2 so a face is
+    NOT one contiguous run): faces are packed in the block's own format,
+    travel as bytes in memory order and land channels-last."""
+    from paper_2605_11111_b200.mesh import halo_sendrecv
+
+    ext = (5, 4)
+    g = torch.arange(2 * 3 * 9 * 4 * 6, dtype=torch.float32).reshape(2, 3, 9, 4, 6)
+    lo = sum(ext[:ctx.rank_id])
+    local = g[:, :, lo:lo + ext[ctx.rank_id]].contiguous(memory_format=torch.channels_last_3d)
+    grp = ctx.axis_group()
+    serve_left = 2 if ctx.rank_id == 1 else 0
+    rw = 2 if ctx.rank_id == 0 else 0
+    lh, rh = halo_sendrecv(grp, local, 2, serve_left, 0, 0, rw)
+    full = dp.full_tensor(dp.ShardTensor(local, tuple(g.shape), ctx, (dp.Shard(2),), {0: ext}))
+    return (rh, None if rh is None else rh.is_contiguous(memory_format=torch.channels_last_3d),
+            full, full.is_contiguous(memory_format=torch.channels_last_3d), g)
+
+
+def test_channels_last_faces_over_gloo():
+    res = run_procs(_cl_halo_prog)
+    rh, is_cl, full, full_cl, g = res[0]
+    assert is_cl and full_cl
+    assert torch.equal(rh, g[:, :, 5:7])
+    assert res[1][0] is None
+    for _, _, full, _, g in res:
+        assert torch.equal(full, g)

@@ -255,3 +255,41 @@ def test_ddp_mean_golden():
     g = d["ddp_grads"]
     assert rel_err(d["ddp_w"], g.sum(0) / 3) < 1e-15
     assert rel_err(d["ddp_b"], g[:, 0].sum(0) / 3) < 1e-15
+
+
+def test_stack_window_matches_full_stack():
+    """The windowed two-layer oracle (full-size conv parity on slabs) equals
+    the same box of the full computation, borders included, for the forward
+    and for the input gradient through transposed-flipped weights."""
+    rng = np.random.default_rng(11)
+    x = rng.standard_normal((1, 3, 9, 8, 10))
+    w1 = rng.standard_normal((4, 3, 3, 3, 3))
+    w2 = rng.standard_normal((2, 4, 3, 3, 3))
+    full = oconv.conv(oconv.conv(x, w1, 1, 1), w2, 1, 1)
+    for lo, hi in (((0, 0, 0), (3, 4, 5)), ((4, 2, 6), (9, 8, 10)), ((2, 3, 1), (6, 5, 7))):
+        got = oconv.stack_window(x, [w1, w2], lo, hi)
+        want = full[:, :, lo[0]:hi[0], lo[1]:hi[1], lo[2]:hi[2]]
+        assert np.abs(got - want).max() < 1e-10 * np.abs(want).max()
+    dy = rng.standard_normal(full.shape)
+    y1 = oconv.conv(x, w1, 1, 1)
+    dy1, _ = oconv.conv_grads(y1, w2, dy, 1, 1)
+    dx, _ = oconv.conv_grads(x, w1, dy1, 1, 1)
+    ws_t = [oconv.transposed_flipped(w2), oconv.transposed_flipped(w1)]
+    got = oconv.stack_window(dy, ws_t, (3, 0, 2), (9, 8, 7))
+    assert np.abs(got - dx[:, :, 3:9, 0:8, 2:7]).max() < 1e-10 * np.abs(dx).max()
+
+
+def test_head_slab_matches_dense_grads():
+    from oracle import attention as oatt
+
+    rng = np.random.default_rng(12)
+    S, d = 300, 16
+    q, k, v, do = (rng.standard_normal((S, d)) for _ in range(4))
+    o = oatt.sdpa(q, k, v)
+    dq, dk, dv = oatt.sdpa_grads(q, k, v, do)
+    rows, keys = slice(100, 164), slice(10, 60)
+    so, sdq, sdk, sdv = oatt.head_slab(q, k, v, do, rows, keys, chunk=64)
+    assert np.abs(so - o[rows]).max() < 1e-12
+    assert np.abs(sdq - dq[rows]).max() < 1e-12
+    assert np.abs(sdk - dk[keys]).max() < 1e-5     # row stats from fp32 score chunks
+    assert np.abs(sdv - dv[keys]).max() < 1e-5
