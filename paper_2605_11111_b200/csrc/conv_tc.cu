@@ -90,6 +90,20 @@ struct ConvTcParams {
 // its half of the B columns, its D rows); only the even CTA issues MMAs.  Per
 // CTA an N = 96 MMA then reads 4 KB of A + 1.5 KB of B (compute-bound, 48
 // cycles) instead of 4 KB + 3 KB (shared-memory-bound, 56 cycles).
+// TMEM accumulator ring.  NSLOT logical row slots of N columns, slot(r) =
+// NSLOT-1 - r mod NSLOT, plus (N <= 64) two EXTENSION slots after the ring:
+// the merged MMA of a top row near the ring's end writes the KQ-1 <= 2 rows
+// that wrapped past column (NSLOT-1)*N into the extension slots instead
+// (row slot L in {0, 1} -> column (NSLOT + L)*N), so EVERY interior stage is
+// one merged N = KQ*C_out MMA per (kp, kw, kc).  The epilogue adds the
+// extension slot into rows L in {0, 1} and zeroes both.  (Without the
+// extension 2 of every 16 rows fell back to per-kq MMAs with the full A
+// operand re-read per kq: +14 % stage time for N = 96, +21 % for N = 48.)
+__host__ __device__ constexpr bool ring_ext(int N) { return 512 / N >= 8; }
+__host__ __device__ constexpr int ring_slots(int N) {
+    return ring_ext(N) ? ((512 / N) < 18 ? (512 / N) : 18) - 2 : ((512 / N) < 16 ? (512 / N) : 16);
+}
+
 template <int N, int KP_, int KQ_, int KW_, int CIN_, bool PAIR = false>
 __global__ void __launch_bounds__(kThreads, 1)
 conv_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap hmap,
@@ -111,7 +125,10 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
     const int KC = CIN / 16;
     const int ROWB = CBLK * 2;               // bytes per voxel row of a box
     const int BOXB = box_bytes(CBLK, KW);
-    constexpr int NSLOT = (512 / N) < 16 ? (512 / N) : 16;
+    constexpr int NSLOT = ring_slots(N);
+    constexpr bool EXT = ring_ext(N);
+    constexpr int NPHYS = EXT ? NSLOT + 2 : NSLOT;
+    const bool wrap_ok = EXT && KQ <= 3;     // wrapped rows go to the extension slots
     const int BW = kTileW + KW - 1;
     const uint32_t stage_bytes = (uint32_t)(KP * NBLK * BOXB);
 
@@ -157,7 +174,7 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
         uint32_t z[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) z[i] = 0u;
-        for (int c = 0; c < NSLOT * N; c += 16) tmem_st16(lane_base + c, z);
+        for (int c = 0; c < NPHYS * N; c += 16) tmem_st16(lane_base + c, z);
         tmem_wait_st();
     }
     tc_fence_before();
@@ -251,7 +268,8 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
                 tc_fence_after();
                 const uint64_t adesc = adesc0 + ((idx * stage_bytes) >> 4);
                 const uint32_t top = row_base + s;  // row fed through kq = 0
-                const bool merged = s >= KQ - 1 && s < nq && (int)(top % NSLOT) >= KQ - 1;
+                const bool merged =
+                    s >= KQ - 1 && s < nq && (wrap_ok || (int)(top % NSLOT) >= KQ - 1);
                 if (p.dbg & 2) {
                 } else if (kStatic && KW_ == 3 && !(p.dbg & (16 | 32))) {
                     // the three kw taps of each (kp, kc) issued as one group (one elect;
@@ -376,6 +394,20 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
                 tmem_wait_ld();
 #pragma unroll
                 for (int c = 0; c < N; c += 16) tmem_st16(col + c, z);
+                if (wrap_ok && slot >= (uint32_t)(NSLOT - 2)) {
+                    // ring rows 0 / 1: the wrapped part of their sum sits in an extension slot
+                    const uint32_t ecol = lane_base + (uint32_t)(2 * NSLOT - 1 - slot) * N;
+#pragma unroll
+                    for (int c = 0; c < N; c += 16) {
+                        uint32_t t[16];
+                        tmem_ld16(ecol + c, t);
+                        tmem_wait_ld();
+#pragma unroll
+                        for (int i = 0; i < 16; ++i)
+                            v[c + i] = __float_as_uint(__uint_as_float(v[c + i]) + __uint_as_float(t[i]));
+                        tmem_st16(ecol + c, z);
+                    }
+                }
                 tmem_wait_st();
                 } else {
 #pragma unroll
@@ -600,7 +632,7 @@ bool make_plan(const dp_conv_geom *g, bool dgrad, Plan &pl, bool f32out = false)
     const Roles &R = pl.R;
     if (R.KW > 15 || R.KQ > 7 || R.KP > 7) return false;
     if (R.KQ * pl.N > 256) return false;                 // merged-tap MMA: N <= 256
-    if (R.KQ + 2 > ((512 / pl.N) < 16 ? (512 / pl.N) : 16)) return false;  // TMEM ring
+    if (R.KQ + 2 > ring_slots(pl.N)) return false;       // TMEM ring
     // channel stride 1 on input and output, 16-B aligned row strides
     const int64_t *is = dgrad ? g->ys : g->xs;
     const int64_t *os = dgrad ? g->xs : g->ys;
@@ -1091,9 +1123,9 @@ __global__ void wgrad_tc_reduce(const float *__restrict__ part, float *__restric
         const int kw = col / N, co = col % N;
         const int ci = row % Cin, kqkp = row / Cin;
         const int kp = kqkp % KP, kq = kqkp / KP;
-        float s = 0.f;
+        double s = 0.0;   // fixed order, fp64: deterministic and exact enough for any CTA count
         for (int c = 0; c < ctas; ++c) s += part[c * per_cta + o];
-        dw[(((co * Cin + ci) * KP + kp) * KQ + kq) * KW + kw] = s;
+        dw[(((co * Cin + ci) * KP + kp) * KQ + kq) * KW + kw] = (float)s;
     }
 }
 
@@ -1348,13 +1380,23 @@ struct TsShape {
     static_assert(BOXX % 1024 == 0, "X boxes must keep the swizzle atom alignment");
 };
 
-template <int CIN, int KP>
+// RF (row flush, the bf16x3 fp32 wgrad): the tensor core adds into its fp32
+// accumulator without round-to-nearest, and over a CTA's whole share of a
+// 1M-voxel reduction that bias reached 2.6e-5 of max|dW| on cfg1 (above the
+// reference's 1e-5).  With RF every output row accumulates into its own
+// fresh TMEM tile (double-buffered D), and the transposer warps add it into
+// per-thread fp32 registers (round-to-nearest FADD) right after staging the
+// next row's A: the tensor-core chain is one row (8 K steps), the register
+// chain the CTA's rows.
+template <int CIN, int KP, bool RF = false>
 __global__ void __launch_bounds__(kThreads, 1)
 conv_wgrad_ts_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap hmap,
                      const __grid_constant__ CUtensorMap dmap, const WgradTsParams p) {
     using namespace tc;
     using S = TsShape<CIN, KP>;
     constexpr int KQ = S::KQ, KW = S::KW;
+    constexpr int ACOL = RF ? (2 * S::NT + 31) / 32 * 32 : S::ACOL;   // first A column
+    static_assert(!RF || S::NT <= 96, "row-flush registers: NT <= 96");
     extern __shared__ __align__(1024) uint8_t smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int NXM = p.nx + KQ - 1;
@@ -1364,7 +1406,8 @@ conv_wgrad_ts_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_cons
     uint64_t *xfull = bars, *xempty = xfull + p.nx;
     uint64_t *dfull = xempty + p.nx, *dempty = dfull + p.nd;
     uint64_t *afull = dempty + p.nd, *aempty = afull + p.na, *done = aempty + p.na;
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(done + 1);
+    uint64_t *rfull = done + 1, *rempty = rfull + 2;              // RF: D tile hand-off
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(rempty + 2);
     if (warp == 0) {
         if (lane == 0) {
             for (int i = 0; i < p.nx; ++i) {
@@ -1380,6 +1423,10 @@ conv_wgrad_ts_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_cons
                 mbar_init(&aempty[i], 1);
             }
             mbar_init(done, 1);
+            for (int i = 0; i < 2; ++i) {
+                mbar_init(&rfull[i], 1);
+                mbar_init(&rempty[i], KW);
+            }
             mbar_fence_init();
             tma_prefetch(&xmap);
             tma_prefetch(&hmap);
@@ -1471,7 +1518,7 @@ conv_wgrad_ts_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_cons
         constexpr uint32_t bstep = (16 * S::CBX * 2) >> 4;   // one K step = 16 w' rows
         // ring slots / phases carried as counters (no integer division per row:
         // it costs MMA-warp issue time, cf. the fwd kernel)
-        uint32_t xidx = 0, xph = 0, aidx = 0, aph = 0;
+        uint32_t xidx = 0, xph = 0, aidx = 0, aph = 0, rrow = 0;
         bool fresh = true;
         for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
             int r = u / p.n_wt;
@@ -1488,9 +1535,16 @@ conv_wgrad_ts_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_cons
                 const uint32_t ca = aidx, caph = aph;
                 if (++aidx == (uint32_t)p.na) { aidx = 0; aph ^= 1u; }
                 mbar_wait(&afull[ca], caph);
+                uint32_t dcol = tmem;
+                if constexpr (RF) {   // this row's D tile must have been drained (row - 2)
+                    const uint32_t rb = rrow & 1u;
+                    mbar_wait(&rempty[rb], ((rrow >> 1) & 1u) ^ 1u);
+                    dcol += rb * S::NT;
+                    fresh = true;
+                }
                 tc_fence_after();
                 const uint64_t bx = b0 + ((xs * S::XSLOT) >> 4);
-                const uint32_t acol = tmem + S::ACOL + ca * S::ACOLS;
+                const uint32_t acol = tmem + ACOL + ca * S::ACOLS;
 #pragma unroll
                 for (int ks = 0; ks < kTsKT; ++ks) {
                     if (p.dbg & 2) break;
@@ -1499,12 +1553,16 @@ conv_wgrad_ts_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_cons
                     for (int c = 0; c < S::NCH; ++c) {
                         constexpr int last = S::NATOM - (S::NCH - 1) * S::APC;
                         const int atoms = c < S::NCH - 1 ? S::APC : last;
-                        mma_ts_e(tmem + c * S::APC * S::CBX, acol + ks * 8,
+                        mma_ts_e(dcol + c * S::APC * S::CBX, acol + ks * 8,
                                  bx + ((c * S::APC * S::BOXX) >> 4) + ks * bstep,
                                  idesc_bf16(128, atoms * S::CBX, 0, 1), acc);
                     }
                 }
                 fresh = false;
+                if constexpr (RF) {
+                    mma_commit_e(&rfull[rrow & 1u]);
+                    ++rrow;
+                }
                 mma_commit_e(&aempty[ca]);
                 mma_commit_e(&xempty[xs]);
                 uint32_t xn = xs + 1 == (uint32_t)p.nx ? 0u : xs + 1;
@@ -1531,7 +1589,33 @@ conv_wgrad_ts_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_cons
             const int mi = lane >> 3, ri = lane & 7;
             const int chunk = mi & 1;
             const int rbase = 8 * (mi >> 1) + ri + KW - 1 - kw;
-            uint32_t didx = 0, dph = 0, aidx = 0, aph = 0;
+            uint32_t didx = 0, dph = 0, aidx = 0, aph = 0, rrow = 0;
+            float racc[RF ? S::NT : 1];
+#pragma unroll
+            for (int i = 0; i < (RF ? S::NT : 1); ++i) racc[i] = 0.f;
+            // RF: add output row `row`'s D tile (this warp's lane quarter) into racc
+            auto drain = [&](uint32_t row) {
+                const uint32_t rb = row & 1u;
+                mbar_wait(&rfull[rb], (row >> 1) & 1u);
+                tc_fence_after();
+                const uint32_t src = tmem + ((uint32_t)(kw * 32) << 16) + rb * S::NT;
+#pragma unroll
+                for (int c0 = 0; c0 < S::NT; c0 += 48) {
+                    uint32_t v[3][16];
+#pragma unroll
+                    for (int t = 0; t < 3; ++t)
+                        if (c0 + 16 * t < S::NT) tmem_ld16(src + c0 + 16 * t, v[t]);
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int t = 0; t < 3; ++t)
+#pragma unroll
+                        for (int i = 0; i < 16; ++i)
+                            if (c0 + 16 * t < S::NT) racc[c0 + 16 * t + i] += __uint_as_float(v[t][i]);
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&rempty[rb]);
+            };
             for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
                 int r = u / p.n_wt;
                 const int qc = r % p.n_qc;
@@ -1543,7 +1627,7 @@ conv_wgrad_ts_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_cons
                     mbar_wait(&aempty[aidx], aph ^ 1);
                     tc_fence_after();
                     const uint32_t src = smem_u32(dring + (size_t)didx * kTsDSlot);
-                    const uint32_t dst = tmem + ((uint32_t)(32 * kw) << 16) + S::ACOL + aidx * S::ACOLS;
+                    const uint32_t dst = tmem + ((uint32_t)(32 * kw) << 16) + ACOL + aidx * S::ACOLS;
                     static_assert(kTsKT == 8, "one x16 store covers the 8 K steps of a tile");
 #pragma unroll
                     for (int h = 0; h < 2; ++h) {
@@ -1565,8 +1649,20 @@ conv_wgrad_ts_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_cons
                         mbar_arrive(&dempty[didx]);
                         mbar_arrive(&afull[aidx]);
                     }
+                    if constexpr (RF) {   // the previous row's MMAs overlap this row's A
+                        if (rrow > 0) drain(rrow - 1);
+                        ++rrow;
+                    }
                 }
             }
+            if constexpr (RF) {
+                if (rrow > 0) drain(rrow - 1);
+                float *dst = p.partial + ((size_t)blockIdx.x * 96 + kw * 32 + lane) * S::NT;
+#pragma unroll
+                for (int c = 0; c < S::NT; c += 4)
+                    *reinterpret_cast<float4 *>(dst + c) =
+                        make_float4(racc[c], racc[c + 1], racc[c + 2], racc[c + 3]);
+            } else {
             // epilogue: D rows (kw, co) of this warp's lane quarter -> per-CTA partial
             mbar_wait(done, 0);
             tc_fence_after();
@@ -1581,6 +1677,7 @@ conv_wgrad_ts_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_cons
                     *reinterpret_cast<float4 *>(dst + c + i) =
                         make_float4(__uint_as_float(v[i]), __uint_as_float(v[i + 1]),
                                     __uint_as_float(v[i + 2]), __uint_as_float(v[i + 3]));
+            }
             }
         }
     }
@@ -1604,15 +1701,16 @@ __global__ void wgrad_ts_reduce(const float *__restrict__ part, float *__restric
         const int kw = kwco / 32, co = kwco % 32;
         const int ci = col % Cin, kqkp = col / Cin;
         const int kp = kqkp % KP, kq = kqkp / KP;
-        float s = 0.f;
+        double s = 0.0;   // fixed order, fp64: deterministic and exact enough for any CTA count
         for (int c = 0; c < ctas; ++c) s += part[c * per_cta + o];
-        dw[(((co * Cin + ci) * KP + kp) * KQ + kq) * KW + kw] = s;
+        dw[(((co * Cin + ci) * KP + kp) * KQ + kq) * KW + kw] = (float)s;
     }
 }
 
 struct TsPlan {
     Roles R;
     int Cin, nt, xslot, nx, nd, na, smem, grid, q_chunk, n_qc, w_lo, n_wt;
+    bool rf;   // row flush (two-level fp32 accumulation, the bf16x3 fp32 wgrad)
     int64_t n_units;
 };
 
@@ -1625,7 +1723,7 @@ bool ts_disabled() {
     return v == 1;
 }
 
-bool make_tsplan(const dp_conv_geom *g, TsPlan &pl) {
+bool make_tsplan(const dp_conv_geom *g, TsPlan &pl, bool fp32 = false) {
     if (ts_disabled()) return false;
     if (!map_roles(g, false, pl.R)) return false;
     const Roles &R = pl.R;
@@ -1642,8 +1740,9 @@ bool make_tsplan(const dp_conv_geom *g, TsPlan &pl) {
     }
     const int cbx = chan_block(pl.Cin);
     pl.nt = 3 * R.KP * pl.Cin;
+    pl.rf = fp32 && pl.nt <= 96;
     pl.xslot = R.KP * (pl.Cin / cbx) * kTsWK * cbx * 2;
-    const int acol = (pl.nt + 31) / 32 * 32;
+    const int acol = ((pl.rf ? 2 : 1) * pl.nt + 31) / 32 * 32;
     pl.na = (512 - acol) / (kTsKT * 8);
     static const int na_cap = getenv("DP_WGRAD_NA") ? atoi(getenv("DP_WGRAD_NA")) : 4;
     if (pl.na > na_cap) pl.na = na_cap;
@@ -1688,10 +1787,10 @@ bool make_tsplan(const dp_conv_geom *g, TsPlan &pl) {
 
 int64_t ts_workspace(const TsPlan &pl) { return (int64_t)pl.grid * 96 * pl.nt * 4; }
 
-template <int CIN, int KP>
+template <int CIN, int KP, bool RF = false>
 int launch_ts_k(const CUtensorMap &xm, const CUtensorMap &hm, const CUtensorMap &dm,
                 const WgradTsParams &p, int grid, int smem, cudaStream_t st) {
-    auto kern = conv_wgrad_ts_kernel<CIN, KP>;
+    auto kern = conv_wgrad_ts_kernel<CIN, KP, RF>;
     DP_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     kern<<<grid, kThreads, smem, st>>>(xm, hm, dm, p);
     return launch_status("conv_wgrad_ts_kernel");
@@ -1762,6 +1861,9 @@ int run_wgrad_ts(const dp_conv_geom *g, const TsPlan &pl, const void *x, const v
     if (R.KP == 3)
         rc = pl.Cin == 16 ? launch_ts_k<16, 3>(xm, hm, dm, p, pl.grid, pl.smem, st)
                           : launch_ts_k<32, 3>(xm, hm, dm, p, pl.grid, pl.smem, st);
+    else if (pl.rf)
+        rc = pl.Cin == 16 ? launch_ts_k<16, 1, true>(xm, hm, dm, p, pl.grid, pl.smem, st)
+                          : launch_ts_k<32, 1, true>(xm, hm, dm, p, pl.grid, pl.smem, st);
     else
         rc = pl.Cin == 16   ? launch_ts_k<16, 1>(xm, hm, dm, p, pl.grid, pl.smem, st)
              : pl.Cin == 32 ? launch_ts_k<32, 1>(xm, hm, dm, p, pl.grid, pl.smem, st)
@@ -1824,12 +1926,12 @@ int64_t conv_tc_workspace(const dp_conv_geom *g, int which) {
 int conv_wgrad_x3_launch(const dp_conv_geom *g, const void *x, const void *xh, const void *dy,
                          void *dw, void *ws, int64_t ws_bytes, cudaStream_t st, int B) {
     TsPlan tp;
-    DP_REQUIRE(make_tsplan(g, tp), DP_ERR_UNSUPPORTED, "conv_wgrad_x3: outside the envelope");
+    DP_REQUIRE(make_tsplan(g, tp, true), DP_ERR_UNSUPPORTED, "conv_wgrad_x3: outside the envelope");
     return run_wgrad_ts(g, tp, x, xh, dy, (float *)dw, ws, ws_bytes, st, B);
 }
 int64_t conv_wgrad_x3_workspace(const dp_conv_geom *g) {
     TsPlan tp;
-    return make_tsplan(g, tp) ? ts_workspace(tp) : -1;
+    return make_tsplan(g, tp, true) ? ts_workspace(tp) : -1;
 }
 
 // bf16 tcgen05 conv with fp32 outputs (the bf16x3 fp32 path, conv_x3.cu)

@@ -72,7 +72,10 @@ FULL_METRICS = [
 ]
 
 
-def full(path, out, traffic=None, key=None):
+def full(path, out, traffic=None, key=None, names=None):
+    """names: the bench's kernel keys (e.g. conv_fwd[16->32]) of the captured
+    launches in capture order; traffic.json is then keyed by those, which is
+    what bench.py looks up for roofline.traffic."""
     raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
                          text=True, check=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
@@ -94,8 +97,9 @@ def full(path, out, traffic=None, key=None):
             v = float(r[idx[m]].replace(",", ""))
             u = units[idx[m]]
             return v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1)
-        tr.setdefault(name, []).append(to_bytes("dram__bytes_read.sum") +
-                                       to_bytes("dram__bytes_write.sum"))
+        label = names[len(lines) - 1] if names and len(lines) <= len(names) else name
+        tr.setdefault(label, []).append(to_bytes("dram__bytes_read.sum") +
+                                        to_bytes("dram__bytes_write.sum"))
     with open(out, "w") as f:
         f.write(f"# ncu --set full summary ({path})\n\n")
         for name, vals in lines:
@@ -109,6 +113,7 @@ def full(path, out, traffic=None, key=None):
             data = json.load(open(traffic))
         except OSError:
             data = {}
+        data[key] = {}
         for name, vals in tr.items():
             data.setdefault(key, {})[name] = sum(vals) / len(vals)
         json.dump(data, open(traffic, "w"), indent=1, sort_keys=True)
@@ -123,4 +128,7 @@ if __name__ == "__main__":
         if "--traffic" in sys.argv:
             i = sys.argv.index("--traffic")
             t, k = sys.argv[i + 1], sys.argv[i + 2]
-        full(sys.argv[2], sys.argv[3], t, k)
+        nm = None
+        if "--names" in sys.argv:
+            nm = sys.argv[sys.argv.index("--names") + 1].split(",")
+        full(sys.argv[2], sys.argv[3], t, k, nm)
