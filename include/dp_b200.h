@@ -124,6 +124,11 @@ typedef struct dp_conv_geom {
     int64_t xs[5];          /* element strides [b, c, s0, s1, s2] of the main block */
     int64_t hs[5];          /* ... of the halo block (ignored when halo == 0) */
     int64_t ys[5];          /* ... of the output */
+    int64_t out_org[3];     /* global index of the output's element 0 on each spatial dim
+                             * (fwd: y, dgrad: dx) — aligns the tcgen05 kernels'
+                             * accumulator ring to global rows so a sharded launch sums
+                             * every output in the same order as the unsharded one
+                             * (bitwise sharding invariance); 0 when unknown */
 } dp_conv_geom;
 
 /* Workspace bytes the conv entry point `which` (DP_CONV_FWD / _DGRAD /

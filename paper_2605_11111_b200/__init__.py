@@ -19,9 +19,10 @@ from .errors import (CollectiveError, DegenerateInputError, DeviceError, Dimensi
                      UnsupportedOperationError)
 from .mesh import (AxisGroup, DeviceMesh, RankContext, all_gather_varlen, all_reduce, barrier,
                    halo_exchange, init_mesh, ring_shift, spawn_mesh)
-from .ops import (AttnTape, ConvTape, RingSoftmaxState, dense_conv, halo_conv,
-                  halo_conv_backward, halo_conv_forward, ring_attention,
-                  ring_attention_backward, ring_attention_forward, sdpa_dense)
+from .ops import (AttnTape, ConvTape, HaloConv2, RingAttention, RingSoftmaxState, dense_conv,
+                  halo_conv, halo_conv_autograd, halo_conv_backward, halo_conv_forward,
+                  ring_attention, ring_attention_autograd, ring_attention_backward,
+                  ring_attention_forward, sdpa_dense)
 from .layers import (ELEMENTWISE_OPS, ActivationLedger, VitConfig, ddp_allreduce_grads,
                      dense_elementwise, dense_layer_norm, dense_linear, dense_matmul,
                      dense_softmax, image_to_sequence, make_vit_weights, sharded_elementwise,

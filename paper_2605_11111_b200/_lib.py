@@ -42,7 +42,7 @@ class ConvGeom(ctypes.Structure):
         ("batch", _i64), ("c_in", _i64), ("c_out", _i64),
         ("in_ext", _i64 * 3), ("halo", _i64), ("out_ext", _i64 * 3),
         ("kernel", _i32 * 3), ("stride", _i32 * 3), ("base", _i64 * 3),
-        ("xs", _i64 * 5), ("hs", _i64 * 5), ("ys", _i64 * 5),
+        ("xs", _i64 * 5), ("hs", _i64 * 5), ("ys", _i64 * 5), ("out_org", _i64 * 3),
     ]
 
 

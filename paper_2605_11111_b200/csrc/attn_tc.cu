@@ -124,7 +124,8 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
                    const __grid_constant__ CUtensorMap vmap, const FwdParams p) {
     using namespace tc;
     extern __shared__ __align__(1024) uint8_t smem[];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);   // warp-uniform for ptxas
+    const int lane = threadIdx.x & 31;
     const int qt = blockIdx.x % p.n_qt, h = blockIdx.x / p.n_qt;
     const int q0 = qt * kBM * kFwdTiles;
     const int nblk = (p.sk + kBN - 1) / kBN;
@@ -159,7 +160,7 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
             tma_prefetch(&vmap);
         }
         __syncwarp();
-        tmem_alloc(tmem_slot, 512);
+        tmem_alloc_ool(tmem_slot, 512);
     }
     tc_fence_before();
     __syncthreads();
@@ -458,7 +459,8 @@ attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
                    const __grid_constant__ CUtensorMap dqmap, const BwdParams p) {
     using namespace tc;
     extern __shared__ __align__(1024) uint8_t smem[];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);   // warp-uniform for ptxas
+    const int lane = threadIdx.x & 31;
     const int kt = blockIdx.x % p.n_kt, h = blockIdx.x / p.n_kt;
     const int k0 = kt * kBN;
     const int nq = (p.sq + kBM - 1) / kBM;
@@ -504,7 +506,7 @@ attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
             tma_prefetch(&dqmap);
         }
         __syncwarp();
-        tmem_alloc(tmem_slot, 512);
+        tmem_alloc_ool(tmem_slot, 512);
     }
     tc_fence_before();
     __syncthreads();

@@ -79,6 +79,7 @@ struct ConvTcParams {
     int dbg;                  // profiling ablations (DP_CONV_DBG): 1 no stores, 2 no MMA, 4 no TMA
     float *yf, *yf2;          // fp32 outputs (the bf16x3 fp32 path) instead of y / y2
     int64_t ycs, y2cs;        // their channel strides (elements)
+    int qorg;                 // global index of output row q = 0 (ring alignment)
 };
 
 // Template arguments KP_/KQ_/KW_/CIN_ = 0 select the runtime-shaped kernel;
@@ -110,8 +111,14 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
                const ConvTcParams p) {
     using namespace tc;
     extern __shared__ __align__(1024) uint8_t smem[];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t rank = PAIR ? cluster_ctarank() : 0u;
+    // warp index through a shuffle: ptxas then knows it is warp-uniform, the
+    // role branches stay on the uniform datapath and the MMA warp computes its
+    // descriptors in uniform registers (no per-MMA ELECT + R2UR.BROADCAST:
+    // ~15 -> ~4 instructions per tcgen05.mma, the issue rate that bounded
+    // the small-N stages)
+    const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
+    const int lane = threadIdx.x & 31;
+    const uint32_t rank = PAIR ? __shfl_sync(0xffffffffu, cluster_ctarank(), 0) : 0u;
     const int u0 = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;          // first unit
     const int ustep = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
     constexpr bool kStatic = KP_ > 0;
@@ -160,14 +167,14 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
             tma_prefetch(&hmap);
         }
         __syncwarp();
-        if constexpr (PAIR) tmem_alloc2(tmem_slot, 512);
-        else tmem_alloc(tmem_slot, 512);
+        if constexpr (PAIR) tmem_alloc2_ool(tmem_slot, 512);
+        else tmem_alloc_ool(tmem_slot, 512);
     }
     tc_fence_before();
     __syncthreads();
     if constexpr (PAIR) cluster_sync();
     tc_fence_after();
-    const uint32_t tmem = *tmem_slot;
+    const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);   // uniform for ptxas
     if (warp >= 2) {
         // every accumulator slot starts at zero (MMAs always accumulate)
         const uint32_t lane_base = tmem + ((uint32_t)((warp & 3) * 32) << 16);
@@ -257,6 +264,18 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
             const int q0 = qc * p.q_chunk, q1 = min(p.Qout, q0 + p.q_chunk);
             const int nq = q1 - q0;
             const int nrows = nq + KQ - 1;
+            if (wrap_ok) {
+                // ring slot of output row q = (global q) mod NSLOT: every row splits
+                // between ring and extension slot exactly as in any other launch
+                // (sharded or not), so the sums are bitwise sharding-invariant.
+                // Skipped slots pass through empty (tempty -> tfull, no MMA).
+                const uint32_t pad = (uint32_t)(((q0 + p.qorg - (int)(row_base % NSLOT)) % NSLOT +
+                                                 NSLOT) % NSLOT);
+                for (uint32_t d = 0; d < pad; ++d, ++row_base) {
+                    mbar_wait(&tempty[row_base % NSLOT], ((row_base / NSLOT) & 1) ^ 1);
+                    commit(&tfull[row_base % NSLOT]);
+                }
+            }
             for (int s = 0; s < nrows;
                  ++s, ++it, (++idx == (uint32_t)p.nstage ? (idx = 0u, ph ^= 1u) : 0u)) {
                 if (s < nq) {
@@ -280,10 +299,10 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
                     constexpr uint32_t BLK = PAIR ? KQS * N * 16 : KQS * N * 32;        // == blk
                     constexpr uint32_t DBM = (uint32_t)(KC_S * BLK) >> 4;                // kw step, merged
                     constexpr uint32_t DBQ = PAIR ? (uint32_t)(KC_S * KQS * N * 16) >> 4 : DBM;  // per-kq
-                    auto grp = [&](uint32_t d, uint64_t a, uint64_t b, uint32_t id, auto dbt) {
+                    const uint32_t ahi = (uint32_t)(adesc >> 32), alo = (uint32_t)adesc;
+                    auto grp = [&](uint32_t d, uint32_t aoff16, uint64_t b, uint32_t id, auto dbt) {
                         constexpr uint32_t DBV = decltype(dbt)::value;
-                        if constexpr (PAIR) mma2_bf16_x3<DA, DBV>(d, a, b, id);
-                        else mma_bf16_x3<DA, DBV>(d, a, b, id);
+                        mma_bf16_x3_lo<DA, DBV, PAIR>(d, alo + aoff16, ahi, b, id);
                     };
                     if (merged) {
                         const uint32_t d = tmem + (NSLOT - 1 - top % NSLOT) * N;
@@ -293,7 +312,7 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
                             for (int kc = 0; kc < KC_S; ++kc) {
                                 const uint32_t aoff = (kp * NB + kc / KPB_S) * BOXB + (kc % KPB_S) * 32;
                                 const uint32_t boff = ((kp * 3) * KC_S + kc) * BLK;
-                                grp(d, adesc + (aoff >> 4), bdesc0 + (boff >> 4), idesc_all,
+                                grp(d, aoff >> 4, bdesc0 + (boff >> 4), idesc_all,
                                     std::integral_constant<uint32_t, DBM>{});
                             }
                     } else {
@@ -302,7 +321,10 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
                             const int j = s - kq;
                             if (j < 0 || j >= nq) continue;
                             const uint32_t row = row_base + j;
-                            const uint32_t d = tmem + (NSLOT - 1 - row % NSLOT) * N;
+                            // the column the merged MMA of this top row would use (ring or
+                            // extension slot): identical sums whichever MMA form adds them
+                            const uint32_t d = tmem + (wrap_ok ? NSLOT - 1 - top % NSLOT + kq
+                                                               : NSLOT - 1 - row % NSLOT) * N;
 #pragma unroll
                             for (int kp = 0; kp < KP; ++kp)
 #pragma unroll
@@ -311,7 +333,7 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
                                     const uint32_t boff =
                                         PAIR ? kqblk0 + (((kp * 3) * KC_S + kc) * KQS + kq) * kqblk
                                              : ((kp * 3) * KC_S + kc) * BLK + kq * (N / 8) * 256;
-                                    grp(d, adesc + (aoff >> 4), bdesc0 + (boff >> 4), idesc_one,
+                                    grp(d, aoff >> 4, bdesc0 + (boff >> 4), idesc_one,
                                         std::integral_constant<uint32_t, DBQ>{});
                                 }
                         }
@@ -336,7 +358,10 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
                         const int j = s - kq;
                         if (j < 0 || j >= nq) continue;
                         const uint32_t row = row_base + j;
-                        const uint32_t d = tmem + (NSLOT - 1 - row % NSLOT) * N;
+                        // the column the merged MMA of this top row would use (ring or
+                            // extension slot): identical sums whichever MMA form adds them
+                            const uint32_t d = tmem + (wrap_ok ? NSLOT - 1 - top % NSLOT + kq
+                                                               : NSLOT - 1 - row % NSLOT) * N;
 #pragma unroll
                         for (int kp = 0; kp < KP; ++kp)
 #pragma unroll
@@ -377,6 +402,23 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
             const int b = r / p.Pout;
             const int q0 = qc * p.q_chunk, q1 = min(p.Qout, q0 + p.q_chunk);
             const int w = wt * kTileW + m;
+            if (wrap_ok) {   // the MMA warp's alignment rows: drain nothing, free the slot
+                const uint32_t pad = (uint32_t)(((q0 + p.qorg - (int)(row_base % NSLOT)) % NSLOT +
+                                                 NSLOT) % NSLOT);
+                for (uint32_t d = 0; d < pad; ++d, ++row_base) {
+                    const uint32_t slot = row_base % NSLOT;
+                    mbar_wait_sleep(&tfull[slot], (row_base / NSLOT) & 1);
+                    if constexpr (PAIR) {
+                        __syncwarp();
+                        if (lane == 0) {
+                            if (rank == 0) mbar_arrive(&tempty[slot]);
+                            else mbar_arrive_remote(lead_tempty + slot * 8);
+                        }
+                    } else {
+                        mbar_arrive(&tempty[slot]);
+                    }
+                }
+            }
             for (int j = 0; j < q1 - q0; ++j) {
                 const uint32_t row = row_base + j, slot = row % NSLOT;
                 mbar_wait_sleep(&tfull[slot], (row / NSLOT) & 1);
@@ -817,6 +859,10 @@ int run_conv_tc(const dp_conv_geom *g, bool dgrad, const void *in, const void *i
         p.ysplit_dim = R.split;                       // rows >= main extent -> dx_halo
         p.ysplit = R.split == 0 ? (int)g->in_ext[0] : (int)g->in_ext[0];
     }
+    {
+        const int64_t ns = ring_slots(pl.N), q = g->nsp == 3 ? g->out_org[1] : g->out_org[0];
+        p.qorg = (int)(((q % ns) + ns) % ns);
+    }
     p.n_wt = use_pair ? (n_wt_all + 1) / 2 : n_wt_all;   // PAIR: tile pairs
     // choose the Q chunk so the unit count balances well over the SMs (pairs)
     const int sms = use_pair ? sm_count() / 2 : sm_count();
@@ -930,7 +976,8 @@ conv_wgrad_tc_kernel(const __grid_constant__ CUtensorMap xmap,
                      const __grid_constant__ CUtensorMap dmap, const WgradTcParams p) {
     using namespace tc;
     extern __shared__ __align__(1024) uint8_t smem[];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);   // warp-uniform for ptxas
+    const int lane = threadIdx.x & 31;
     constexpr bool kStatic = KP_ > 0;
     const int KP = kStatic ? KP_ : p.KP;
     const int KQ = kStatic ? KQ_ : p.KQ;
@@ -965,7 +1012,7 @@ conv_wgrad_tc_kernel(const __grid_constant__ CUtensorMap xmap,
             tma_prefetch(&dmap);
         }
         __syncwarp();
-        tmem_alloc(tmem_slot, ncols);
+        tmem_alloc_ool(tmem_slot, ncols);
     }
     tc_fence_before();
     __syncthreads();
@@ -1398,7 +1445,8 @@ conv_wgrad_ts_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_cons
     constexpr int ACOL = RF ? (2 * S::NT + 31) / 32 * 32 : S::ACOL;   // first A column
     static_assert(!RF || S::NT <= 96, "row-flush registers: NT <= 96");
     extern __shared__ __align__(1024) uint8_t smem[];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);   // warp-uniform for ptxas
+    const int lane = threadIdx.x & 31;
     const int NXM = p.nx + KQ - 1;
     uint8_t *xring = smem;
     uint8_t *dring = smem + (size_t)NXM * S::XSLOT;
@@ -1433,7 +1481,7 @@ conv_wgrad_ts_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_cons
             tma_prefetch(&dmap);
         }
         __syncwarp();
-        tmem_alloc(tmem_slot, 512);
+        tmem_alloc_ool(tmem_slot, 512);
     }
     tc_fence_before();
     __syncthreads();

@@ -33,6 +33,13 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
                  "r"(bytes)
                  : "memory");
 }
+// 64-bit broadcast from lane 0 (makes the value provably warp-uniform for ptxas)
+__device__ __forceinline__ uint64_t ushfl64(uint64_t v) {
+    const uint32_t lo = __shfl_sync(0xffffffffu, (uint32_t)v, 0);
+    const uint32_t hi = __shfl_sync(0xffffffffu, (uint32_t)(v >> 32), 0);
+    return ((uint64_t)hi << 32) | lo;
+}
+
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
     asm volatile(
         "{\n"
@@ -351,6 +358,14 @@ __device__ __forceinline__ void tmem_alloc2(uint32_t *dst, uint32_t ncols) {
                  "r"(ncols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
 }
+// Out-of-line allocation: an inlined `.sync.aligned` tcgen05.alloc inside a
+// role branch makes ptxas treat the whole kernel as possibly non-converged,
+// and every tcgen05.mma then goes through an ELECT / R2UR.BROADCAST /
+// VOTEU sequence (~15 instructions per MMA on the single issuing warp).
+// Behind a call the MMA warp's descriptor math stays on the uniform datapath
+// (measured in SASS: 122 -> 23 R2UR, 51 -> 3 ELECT for 27 MMAs).
+static __device__ __noinline__ void tmem_alloc_ool(uint32_t *dst, uint32_t ncols) { tmem_alloc(dst, ncols); }
+static __device__ __noinline__ void tmem_alloc2_ool(uint32_t *dst, uint32_t ncols) { tmem_alloc2(dst, ncols); }
 __device__ __forceinline__ void tmem_dealloc2(uint32_t addr, uint32_t ncols) {
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(addr), "r"(ncols));
 }
@@ -389,6 +404,54 @@ __device__ __forceinline__ void mma2_bf16_x3(uint32_t d_tmem, uint64_t a, uint64
         "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a2, b2, %3, p;\n"
         "}\n" ::"r"(d_tmem),
         "l"(a), "l"(b), "r"(idesc), "n"(DA), "n"(2 * DA), "n"(DB), "n"(2 * DB));
+}
+// As mma2_bf16_x3 / mma_bf16_x3 with the A descriptor split into its low
+// word (start address + LBO: the only part a K step or kw tap moves) and its
+// constant high word: the per-MMA A arithmetic is one 32-bit add instead of
+// a 64-bit add pair, and the high word stays in one uniform register.
+template <uint32_t DA, uint32_t DB, bool PAIR>
+__device__ __forceinline__ void mma_bf16_x3_lo(uint32_t d_tmem, uint32_t alo, uint32_t ahi,
+                                               uint64_t b, uint32_t idesc) {
+    if constexpr (PAIR)
+        asm volatile(
+            "{\n"
+            ".reg .pred p, e;\n"
+            ".reg .b32 l1, l2;\n"
+            ".reg .b64 a0, a1, a2, b1, b2;\n"
+            "setp.eq.u32 p, 1, 1;\n"
+            "add.u32 l1, %1, %5;\n"
+            "add.u32 l2, %1, %6;\n"
+            "mov.b64 a0, {%1, %2};\n"
+            "mov.b64 a1, {l1, %2};\n"
+            "mov.b64 a2, {l2, %2};\n"
+            "add.s64 b1, %3, %7;\n"
+            "add.s64 b2, %3, %8;\n"
+            "elect.sync _|e, 0xffffffff;\n"
+            "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a0, %3, %4, p;\n"
+            "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a1, b1, %4, p;\n"
+            "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a2, b2, %4, p;\n"
+            "}\n" ::"r"(d_tmem),
+            "r"(alo), "r"(ahi), "l"(b), "r"(idesc), "n"(DA), "n"(2 * DA), "n"(DB), "n"(2 * DB));
+    else
+        asm volatile(
+            "{\n"
+            ".reg .pred p, e;\n"
+            ".reg .b32 l1, l2;\n"
+            ".reg .b64 a0, a1, a2, b1, b2;\n"
+            "setp.eq.u32 p, 1, 1;\n"
+            "add.u32 l1, %1, %5;\n"
+            "add.u32 l2, %1, %6;\n"
+            "mov.b64 a0, {%1, %2};\n"
+            "mov.b64 a1, {l1, %2};\n"
+            "mov.b64 a2, {l2, %2};\n"
+            "add.s64 b1, %3, %7;\n"
+            "add.s64 b2, %3, %8;\n"
+            "elect.sync _|e, 0xffffffff;\n"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a0, %3, %4, p;\n"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a1, b1, %4, p;\n"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a2, b2, %4, p;\n"
+            "}\n" ::"r"(d_tmem),
+            "r"(alo), "r"(ahi), "l"(b), "r"(idesc), "n"(DA), "n"(2 * DA), "n"(DB), "n"(2 * DB));
 }
 // cta_group::1 form of mma2_bf16_x3.
 template <uint32_t DA, uint32_t DB>

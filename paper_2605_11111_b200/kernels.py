@@ -181,10 +181,11 @@ def _pad5(vals, fill=0):
 
 
 def conv_geom(x: torch.Tensor, x_halo, y_shape, y_strides, c_out: int, kernel, stride, base,
-              shard: int, halo_rows: int) -> ConvGeom:
+              shard: int, halo_rows: int, out_org=None) -> ConvGeom:
     """Build dp_conv_geom for batched x [B, C, *sp] (main block), optional
     halo block (same dims, `halo_rows` on spatial dim `shard`), output
-    shape/strides [B, C_out, *out]."""
+    shape/strides [B, C_out, *out].  out_org: global index of the produced
+    tensor's element 0 per spatial dim (fwd: y, dgrad: dx)."""
     nsp = x.dim() - 2
     if not 1 <= nsp <= 3:
         raise UnsupportedConfigError(f"conv supports 1-3 spatial dims, got {nsp}")
@@ -208,6 +209,8 @@ def conv_geom(x: torch.Tensor, x_halo, y_shape, y_strides, c_out: int, kernel, s
         g.hs[i] = v
     for i, v in enumerate(_pad5(y_strides)):
         g.ys[i] = v
+    for i, v in enumerate(out_org or ()):
+        g.out_org[i] = int(v)
     return g
 
 
@@ -219,10 +222,10 @@ def _workspace(g, code, which, device):
     return ws, int(ws.numel())
 
 
-def conv_fwd(x, x_halo, w, y, *, kernel, stride, base, shard, halo_rows) -> None:
+def conv_fwd(x, x_halo, w, y, *, kernel, stride, base, shard, halo_rows, out_org=None) -> None:
     require_device("conv_fwd", x, x_halo, w, y)
     g = conv_geom(x, x_halo, y.shape, y.stride(), w.shape[0], kernel, stride, base, shard,
-                  halo_rows)
+                  halo_rows, out_org)
     code = dtype_code(x)
     ws, nb = _workspace(g, code, _lib.CONV_FWD, x.device)
     rc = _lib.load().dp_conv_fwd(ctypes.byref(g), code, _algo, _ptr(x), _ptr(x_halo), _ptr(w),
@@ -230,10 +233,11 @@ def conv_fwd(x, x_halo, w, y, *, kernel, stride, base, shard, halo_rows) -> None
     _lib.check(rc, "dp_conv_fwd")
 
 
-def conv_dgrad(dy, w, dx, dx_halo, *, kernel, stride, base, shard, halo_rows) -> None:
+def conv_dgrad(dy, w, dx, dx_halo, *, kernel, stride, base, shard, halo_rows,
+               out_org=None) -> None:
     require_device("conv_dgrad", dy, w, dx, dx_halo)
     g = conv_geom(dx, dx_halo, dy.shape, dy.stride(), w.shape[0], kernel, stride, base, shard,
-                  halo_rows)
+                  halo_rows, out_org)
     code = dtype_code(dy)
     ws, nb = _workspace(g, code, _lib.CONV_DGRAD, dy.device)
     rc = _lib.load().dp_conv_dgrad(ctypes.byref(g), code, _algo, _ptr(dy), _ptr(w), _ptr(dx),

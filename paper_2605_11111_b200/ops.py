@@ -18,8 +18,9 @@ tensor data is produced by the sm_100a kernels of libdpb200.so:
 
 Backward entry points are explicit (`halo_conv_backward`,
 `ring_attention_backward`) because collectives must run on the rank's own
-thread; `torch.autograd` wrappers (`HaloConv2`, `RingAttention`) are provided
-for the one-process-per-GPU mesh, where they call the same functions.
+thread; `torch.autograd` wrappers (`halo_conv_autograd` / `HaloConv2`,
+`ring_attention_autograd` / `RingAttention`) are provided for the
+one-process-per-GPU mesh, where they call the same functions.
 """
 
 from __future__ import annotations
@@ -41,7 +42,8 @@ from .sharding import Shard, ShardTensor
 __all__ = [
     "halo_conv", "halo_conv_forward", "halo_conv_backward", "ConvTape", "dense_conv",
     "ring_attention", "ring_attention_forward", "ring_attention_backward", "AttnTape",
-    "sdpa_dense", "RingSoftmaxState",
+    "sdpa_dense", "RingSoftmaxState", "HaloConv2", "halo_conv_autograd", "RingAttention",
+    "ring_attention_autograd",
 ]
 
 
@@ -222,22 +224,27 @@ def halo_conv_forward(x: ShardTensor, weight, stride=1, padding=0):
     base = [-p for p in pads]
     base[sp] = mine.base
     yb = empty_like_layout(xb, [xb.shape[0], weight.shape[0]] + out_sp)
+    org = [0] * nsp                       # global index of my output row 0
+    org[sp] = sum(plan.out_extents[:me])
     # Interior output rows read only local rows: they are convolved while the
     # halo is in flight; the boundary rows follow once it has landed.
     n_int = _interior_rows(mine.n_out, xb.shape[sp + 2], kernel[sp], strides[sp], mine.base) \
         if mine.rw else mine.n_out
     if yb.numel() and 0 < n_int < mine.n_out:
         kernels.conv_fwd(xb, None, w, yb.narrow(sp + 2, 0, n_int), kernel=kernel,
-                         stride=strides, base=base, shard=sp, halo_rows=0)
+                         stride=strides, base=base, shard=sp, halo_rows=0, out_org=org)
     pending.wait()
     if yb.numel() and n_int < mine.n_out:
         bb = list(base)
         bb[sp] = mine.base + n_int * strides[sp]
+        ob = list(org)
+        ob[sp] += n_int
         kernels.conv_fwd(xb, halo, w, yb.narrow(sp + 2, n_int, mine.n_out - n_int),
-                         kernel=kernel, stride=strides, base=bb, shard=sp, halo_rows=mine.rw)
+                         kernel=kernel, stride=strides, base=bb, shard=sp, halo_rows=mine.rw,
+                         out_org=ob)
     elif yb.numel() and n_int == mine.n_out:
         kernels.conv_fwd(xb, halo, w, yb, kernel=kernel, stride=strides, base=base, shard=sp,
-                         halo_rows=mine.rw)
+                         halo_rows=mine.rw, out_org=org)
     y = yb if batched else yb[0]
     out = ShardTensor(y, out_global, x.ctx, x.placements, {axis: plan.out_extents})
     tape = ConvTape(x, w, halo, plan, axis, d, sp, strides, pads, batched, tuple(base), out)
@@ -307,8 +314,10 @@ def halo_conv_backward(tape: ConvTape, dout):
         halo_grad = empty_like_layout(xb, hshape)
     work = mine.n_out and xb.shape[dim] + mine.rw
     if work:
+        org = [0] * (xb.dim() - 2)            # global index of my dx row 0
+        org[tape.sp] = sum(x.shard_shapes[tape.axis][:me])
         kernels.conv_dgrad(dyb, w, dxb, halo_grad, kernel=kernel, stride=tape.strides,
-                           base=tape.base, shard=tape.sp, halo_rows=mine.rw)
+                           base=tape.base, shard=tape.sp, halo_rows=mine.rw, out_org=org)
     else:
         kernels.fill(dxb, 0.0)
         kernels.fill(dw, 0.0)
@@ -607,14 +616,20 @@ class HaloConv2(torch.autograd.Function):
         return dx.local, dw.to(actx.wdtype), None, None, None
 
 
-def halo_conv_autograd(x: ShardTensor, weight: torch.Tensor, stride=1, padding=0) -> ShardTensor:
-    """halo_conv whose `.local` carries a grad_fn (process meshes only)."""
-    if x.ctx.transport.kind == "thread":
+def _need_process_mesh(ctx, what: str) -> None:
+    if ctx.transport.kind == "thread":
         raise UnsupportedConfigError(
-            "autograd through collectives needs one process per rank; use "
-            "halo_conv_forward/halo_conv_backward on a thread mesh")
-    y = HaloConv2.apply(x.local, weight, x, stride, padding)
+            f"autograd through collectives needs one process per rank; use "
+            f"{what}_forward/{what}_backward on a thread mesh")
+
+
+def halo_conv_autograd(x: ShardTensor, weight, stride=1, padding=0) -> ShardTensor:
+    """halo_conv whose `.local` carries a grad_fn (process meshes only).
+    `weight` is a plain tensor or a fully replicated ShardTensor (its local
+    tensor is the autograd leaf, as domainpar/ops.py:76-82 accepts both)."""
+    _need_process_mesh(x.ctx, "halo_conv")
     weight_p = _plain_weight(weight, "conv weight", x.local.device)
+    y = HaloConv2.apply(x.local, weight_p, x, stride, padding)
     nsp = weight_p.dim() - 2
     first = 2 if x.ndim == nsp + 2 else 1
     kernel = tuple(weight_p.shape[2:])
@@ -630,6 +645,35 @@ def halo_conv_autograd(x: ShardTensor, weight: torch.Tensor, stride=1, padding=0
                                   strides[sp], pads[sp])
             shapes[axis] = plan.out_extents
     return ShardTensor(y, out_global, x.ctx, x.placements, shapes)
+
+
+class RingAttention(torch.autograd.Function):
+    """torch.autograd bridge for ring_attention on a process mesh: forward =
+    ring_attention_forward, backward = ring_attention_backward (the (K, V,
+    dK, dV) ring plus the final hop home)."""
+
+    @staticmethod
+    def forward(actx, q_local, k_local, v_local, qst, kst, vst):
+        def st(t, like):
+            return ShardTensor(t.detach(), like.global_shape, like.ctx, like.placements,
+                               like.shard_shapes)
+
+        out, tape = ring_attention_forward(st(q_local, qst), st(k_local, kst), st(v_local, vst))
+        actx.tape = tape
+        return out.local
+
+    @staticmethod
+    def backward(actx, go):
+        dq, dk, dv = ring_attention_backward(actx.tape, go.contiguous())
+        return dq.local, dk.local, dv.local, None, None, None
+
+
+def ring_attention_autograd(q: ShardTensor, k: ShardTensor, v: ShardTensor) -> ShardTensor:
+    """ring_attention whose `.local` carries a grad_fn (process meshes only);
+    gradients flow to q.local, k.local and v.local."""
+    _need_process_mesh(q.ctx, "ring_attention")
+    y = RingAttention.apply(q.local, k.local, v.local, q, k, v)
+    return ShardTensor(y, q.global_shape, q.ctx, q.placements, q.shard_shapes)
 
 
 # ---------------------------------------------------------------------------

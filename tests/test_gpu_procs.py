@@ -111,3 +111,77 @@ def test_process_mesh_end_to_end_on_one_gpu():
         assert s1_shapes == {0: tuple(c)}
         assert torch.equal(back, torch.tensor(g))
         assert rel_err(ln.numpy(), olay.layer_norm(g, 0)) < 1e-5
+
+
+def _autograd_prog(ctx):
+    """halo_conv_autograd (replicated ShardTensor weight) and
+    ring_attention_autograd through torch.autograd on the process mesh."""
+    import paper_2605_11111_b200 as dp
+
+    x, w, dy, q, k, v, do, _ = _data()
+    dev = ctx.device
+    r = ctx.rank_id
+    cl = torch.channels_last_3d
+    ext = (9, 7)
+    lo = sum(ext[:r])
+    xl = torch.tensor(x[:, :, lo:lo + ext[r]]).to(torch.bfloat16).to(dev) \
+        .contiguous(memory_format=cl).requires_grad_(True)
+    st = dp.ShardTensor(xl, x.shape, ctx, (dp.Shard(2),), {0: ext})
+    wl = torch.tensor(w).to(torch.bfloat16).to(dev).requires_grad_(True)
+    wst = dp.ShardTensor(wl, w.shape, ctx, (dp.Replicate(),), {})
+    y = dp.halo_conv_autograd(st, wst, 1, 1)
+    oext = y.shard_shapes[0]
+    olo = sum(oext[:r])
+    dyl = torch.tensor(dy[:, :, olo:olo + oext[r]]).to(torch.bfloat16).to(dev) \
+        .contiguous(memory_format=cl)
+    y.local.backward(dyl)
+    dx = dp.ShardTensor(xl.grad, x.shape, ctx, (dp.Shard(2),), {0: ext}).full_tensor()
+    qe = (256, 256)
+    mk = lambda a: torch.tensor(a[r * 256:(r + 1) * 256]).to(torch.bfloat16).to(dev) \
+        .requires_grad_(True)  # noqa: E731
+    ql, kl, vl = mk(q), mk(k), mk(v)
+    qs, ks, vs = (dp.ShardTensor(t, q.shape, ctx, (dp.Shard(0),), {0: qe}) for t in (ql, kl, vl))
+    o = dp.ring_attention_autograd(qs, ks, vs)
+    o.local.backward(torch.tensor(do[r * 256:(r + 1) * 256]).to(torch.bfloat16).to(dev))
+    grads = [dp.ShardTensor(t.grad, q.shape, ctx, (dp.Shard(0),), {0: qe}).full_tensor()
+             for t in (ql, kl, vl)]
+    return (y.full_tensor(), dx, wl.grad.float().cpu(), o.full_tensor(), *grads)
+
+
+def test_autograd_wrappers_on_process_mesh():
+    import paper_2605_11111_b200 as dp
+
+    res = dp.spawn_mesh((2,), ("domain",), _autograd_prog, backend="gloo-cuda", timeout=120)
+    x, w, dy, q, k, v, do, _ = _data()
+    bf = lambda a: torch.tensor(a).to(torch.bfloat16).double().numpy()  # noqa: E731
+    xr, wr, dyr = bf(x), bf(w), bf(dy)
+    want_y = oconv.conv(xr, wr, 1, 1)
+    want_dx, want_dw = oconv.conv_grads(xr, wr, dyr, 1, 1)
+    qr, kr, vr, dor = bf(q), bf(k), bf(v), bf(do)
+    want = [oatt.sdpa(qr, kr, vr), *oatt.sdpa_grads(qr, kr, vr, dor)]
+    f = lambda t: t.float().numpy().astype(np.float64)  # noqa: E731
+    for y, dx, dw, o, dq, dk, dv in res:
+        assert rel_err(f(y), want_y) < 1e-2
+        assert rel_err(f(dx), want_dx) < 1e-2
+        assert rel_err(f(dw), want_dw) < 3e-2          # bf16 weight gradient (cast back)
+        assert rel_err(f(o), want[0]) < 1.5e-2
+        for got, exp in zip((dq, dk, dv), want[1:]):
+            assert rel_err(f(got), exp) < 2e-2
+
+
+def test_autograd_wrappers_refuse_thread_mesh():
+    import paper_2605_11111_b200 as dp
+
+    def prog(ctx):
+        xl = torch.zeros((1, 16, 4, 8, 16), dtype=torch.bfloat16, device=ctx.device)
+        st = dp.ShardTensor(xl, (1, 16, 4, 8, 16), ctx, (dp.Shard(2),), {0: (4,)})
+        with pytest.raises(dp.UnsupportedConfigError, match="one process per rank"):
+            dp.halo_conv_autograd(st, torch.zeros((16, 16, 3, 3, 3), dtype=torch.bfloat16,
+                                                  device=ctx.device), 1, 1)
+        q = dp.ShardTensor(torch.zeros((8, 64), dtype=torch.bfloat16, device=ctx.device),
+                           (8, 64), ctx, (dp.Shard(0),), {0: (8,)})
+        with pytest.raises(dp.UnsupportedConfigError, match="one process per rank"):
+            dp.ring_attention_autograd(q, q, q)
+        return True
+
+    assert dp.spawn_mesh((1,), ("domain",), prog)[0]
