@@ -35,7 +35,7 @@ from .dispatch import register_dense_reference, register_handler
 from .errors import (DegenerateInputError, DimensionError, HaloError, MetadataError,
                      UnsupportedConfigError)
 from .mesh import (AxisGroup, PeerAbort, all_reduce, empty_like_layout, halo_error_text,
-                   halo_sendrecv, ring_shift_known)
+                   halo_sendrecv, memory_format_of, ring_shift_known)
 from .plan import conv_output_extent, halo_conv_plan, ring_source
 from .sharding import Shard, ShardTensor
 
@@ -607,12 +607,12 @@ class HaloConv2(torch.autograd.Function):
         out, tape = halo_conv_forward(st, weight.detach(), stride, padding)
         actx.tape = tape
         actx.wdtype = weight.dtype
-        actx.out_meta = out
+        actx.out_fmt = memory_format_of(out.local)
         return out.local
 
     @staticmethod
     def backward(actx, gy):
-        dx, dw = halo_conv_backward(actx.tape, gy.contiguous(memory_format=torch.preserve_format))
+        dx, dw = halo_conv_backward(actx.tape, gy.contiguous(memory_format=actx.out_fmt))
         return dx.local, dw.to(actx.wdtype), None, None, None
 
 
