@@ -80,6 +80,7 @@ struct ConvTcParams {
     float *yf, *yf2;          // fp32 outputs (the bf16x3 fp32 path) instead of y / y2
     int64_t ycs, y2cs;        // their channel strides (elements)
     int qorg;                 // global index of output row q = 0 (ring alignment)
+    int cperm;                // bf16 output through the coalesced drain (permuted B columns)
 };
 
 // Template arguments KP_/KQ_/KW_/CIN_ = 0 select the runtime-shaped kernel;
@@ -393,7 +394,25 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
         uint32_t z[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) z[i] = 0u;
-        uint32_t row_base = 0;
+        // ring slot / phase of the next row to drain (division-free, as the MMA loop)
+        uint32_t eslot = 0, eph = 0;
+        auto next_row = [&]() {
+            if (++eslot == (uint32_t)NSLOT) { eslot = 0; eph ^= 1u; }
+        };
+        auto free_slot = [&](uint32_t slot) {
+            if constexpr (PAIR) {
+                __syncwarp();
+                if (lane == 0) {
+                    if (rank == 0) mbar_arrive(&tempty[slot]);
+                    else mbar_arrive_remote(lead_tempty + slot * 8);
+                }
+            } else {
+                mbar_arrive(&tempty[slot]);
+            }
+        };
+        // bf16 output through the coalesced drain (fp32 outputs / ablations take the
+        // per-lane path below); the halo output part must share the W stride
+        const bool fast = p.cperm && !(p.dbg & 8);
         for (int u = u0; u < p.n_units; u += ustep) {
             int r = u;
             const int wt = PAIR ? (r % p.n_wt) * 2 + (int)rank : r % p.n_wt; r /= p.n_wt;
@@ -403,25 +422,131 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
             const int q0 = qc * p.q_chunk, q1 = min(p.Qout, q0 + p.q_chunk);
             const int w = wt * kTileW + m;
             if (wrap_ok) {   // the MMA warp's alignment rows: drain nothing, free the slot
-                const uint32_t pad = (uint32_t)(((q0 + p.qorg - (int)(row_base % NSLOT)) % NSLOT +
-                                                 NSLOT) % NSLOT);
-                for (uint32_t d = 0; d < pad; ++d, ++row_base) {
-                    const uint32_t slot = row_base % NSLOT;
-                    mbar_wait_sleep(&tfull[slot], (row_base / NSLOT) & 1);
-                    if constexpr (PAIR) {
-                        __syncwarp();
-                        if (lane == 0) {
-                            if (rank == 0) mbar_arrive(&tempty[slot]);
-                            else mbar_arrive_remote(lead_tempty + slot * 8);
-                        }
-                    } else {
-                        mbar_arrive(&tempty[slot]);
-                    }
+                const uint32_t pad = (uint32_t)(((q0 + p.qorg - (int)eslot) % NSLOT + NSLOT) % NSLOT);
+                for (uint32_t d = 0; d < pad; ++d) {
+                    mbar_wait_sleep(&tfull[eslot], eph);
+                    free_slot(eslot);
+                    next_row();
                 }
             }
+            if (fast) {
+                // bf16 output, coalesced: 16x128b loads give thread t the columns
+                // 4 jj + t%4 of voxels 16 h + 8 g + t/4 of this warp's quarter; the B
+                // columns are permuted (conv_tc_weight_image*, cperm) so those are
+                // channels U (4 k + t%4) + i (jj = k U + i): each of the 4 threads of a
+                // voxel holds whole U-channel chunks, and one store instruction writes
+                // 8 voxels x 4 chunks = 8 contiguous runs of 4 U bf16 (512 B for N = 32)
+                // instead of 32 half-used sectors per instruction.  Addresses are set
+                // up once per unit: a row pointer advanced by the Q stride (switching
+                // to the halo output at the split row) + 4 per-voxel offsets.
+                constexpr int NJ = N / 4, U = (N % 32 == 0) ? 8 : 4;
+                __nv_bfloat16 *rowp;
+                int64_t rstep;
+                int jsw = 1 << 30;
+                __nv_bfloat16 *rowp2 = nullptr;
+                if (p.ysplit_dim == 0 && po >= p.ysplit) {
+                    rowp = p.y2 + b * p.y2s[0] + (int64_t)(po - p.ysplit) * p.y2s[1] +
+                           (int64_t)q0 * p.y2s[2];
+                    rstep = p.y2s[2];
+                } else {
+                    rowp = p.y + b * p.ys[0] + (int64_t)po * p.ys[1] + (int64_t)q0 * p.ys[2];
+                    rstep = p.ys[2];
+                    if (p.ysplit_dim == 1) {
+                        jsw = max(0, p.ysplit - q0);
+                        rowp2 = p.y2 + b * p.y2s[0] + (int64_t)po * p.y2s[1] +
+                                (int64_t)(q0 + jsw - p.ysplit) * p.y2s[2];
+                    }
+                }
+                int off[2][2];
+                bool ok[2][2];
+#pragma unroll
+                for (int h = 0; h < 2; ++h)
+#pragma unroll
+                    for (int g = 0; g < 2; ++g) {
+                        const int wv = wt * kTileW + quarter * 32 + 16 * h + 8 * g + (lane >> 2);
+                        ok[h][g] = wv < p.Wout && !(p.dbg & 1);
+                        off[h][g] = wv * (int)p.ys[3] + U * (lane & 3);
+                    }
+                for (int j = 0; j < q1 - q0; ++j) {
+                    const uint32_t slot = eslot;
+                    mbar_wait_sleep(&tfull[slot], eph);
+                    next_row();
+                    tc_fence_after();
+                    const uint32_t col = lane_base + (NSLOT - 1 - slot) * N;
+                    uint32_t v[2][2][NJ];
+#pragma unroll
+                    for (int h = 0; h < 2; ++h)
+#pragma unroll
+                        for (int c0 = 0; c0 < N; c0 += 16) {
+                            uint32_t t[8];
+                            tmem_ld16_16x128b(col + ((uint32_t)(16 * h) << 16) + c0, t);
+#pragma unroll
+                            for (int jj = 0; jj < 4; ++jj) {
+                                v[h][0][c0 / 4 + jj] = t[2 * jj];
+                                v[h][1][c0 / 4 + jj] = t[2 * jj + 1];
+                            }
+                        }
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int c = 0; c < N; c += 16) tmem_st16(col + c, z);
+                    if (wrap_ok && slot >= (uint32_t)(NSLOT - 2)) {
+                        const uint32_t ecol = lane_base + (uint32_t)(2 * NSLOT - 1 - slot) * N;
+#pragma unroll
+                        for (int h = 0; h < 2; ++h)
+#pragma unroll
+                            for (int c0 = 0; c0 < N; c0 += 16) {
+                                uint32_t t[8];
+                                tmem_ld16_16x128b(ecol + ((uint32_t)(16 * h) << 16) + c0, t);
+                                tmem_wait_ld();
+#pragma unroll
+                                for (int jj = 0; jj < 4; ++jj)
+#pragma unroll
+                                    for (int g = 0; g < 2; ++g)
+                                        v[h][g][c0 / 4 + jj] = __float_as_uint(
+                                            __uint_as_float(v[h][g][c0 / 4 + jj]) +
+                                            __uint_as_float(t[2 * jj + g]));
+                            }
+#pragma unroll
+                        for (int c = 0; c < N; c += 16) tmem_st16(ecol + c, z);
+                    }
+                    tmem_wait_st();
+                    tc_fence_before();
+                    free_slot(slot);
+                    if (j == jsw) {
+                        rowp = rowp2;
+                        rstep = p.y2s[2];
+                    }
+#pragma unroll
+                    for (int h = 0; h < 2; ++h)
+#pragma unroll
+                        for (int g = 0; g < 2; ++g) {
+                            __nv_bfloat16 *dst = rowp + off[h][g];
+#pragma unroll
+                            for (int k = 0; k < NJ / U; ++k) {
+                                const uint32_t *a = &v[h][g][k * U];
+                                if constexpr (U == 8) {
+                                    uint4 pk;
+                                    pk.x = pack_bf16(__uint_as_float(a[0]), __uint_as_float(a[1]));
+                                    pk.y = pack_bf16(__uint_as_float(a[2]), __uint_as_float(a[3]));
+                                    pk.z = pack_bf16(__uint_as_float(a[4]), __uint_as_float(a[5]));
+                                    pk.w = pack_bf16(__uint_as_float(a[6]), __uint_as_float(a[7]));
+                                    if (ok[h][g]) *reinterpret_cast<uint4 *>(dst + 4 * U * k) = pk;
+                                } else {
+                                    uint2 pk;
+                                    pk.x = pack_bf16(__uint_as_float(a[0]), __uint_as_float(a[1]));
+                                    pk.y = pack_bf16(__uint_as_float(a[2]), __uint_as_float(a[3]));
+                                    if (ok[h][g]) *reinterpret_cast<uint2 *>(dst + 4 * U * k) = pk;
+                                }
+                            }
+                        }
+                    rowp += rstep;
+                }
+                continue;
+            }
             for (int j = 0; j < q1 - q0; ++j) {
-                const uint32_t row = row_base + j, slot = row % NSLOT;
-                mbar_wait_sleep(&tfull[slot], (row / NSLOT) & 1);
+                const uint32_t slot = eslot;
+                mbar_wait_sleep(&tfull[slot], eph);
+                next_row();
                 tc_fence_after();
                 const uint32_t col = lane_base + (NSLOT - 1 - slot) * N;
                 uint32_t v[N];
@@ -508,7 +633,6 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
                     }
                 }
             }
-            row_base += q1 - q0;
         }
     }
     tc_fence_before();
@@ -521,13 +645,23 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
     }
 }
 
+// Output channel held by accumulator column `col` (0..N-1) when the bf16
+// epilogue's coalesced 16x128b drain is used: column 4 j + c (c = col % 4, the
+// lane-within-voxel of the fragment) carries channel U (4 (j / U) + c) + j % U,
+// U = 8 (N % 32 == 0) or 4, so thread c of a voxel owns whole U-channel chunks.
+__host__ __device__ __forceinline__ int epi_channel(int col, int N) {
+    const int U = (N % 32 == 0) ? 8 : 4;
+    const int j = col >> 2, c = col & 3;
+    return U * (4 * (j / U) + c) + j % U;
+}
+
 // Weight smem image.  One block per (kp, kw, 16-channel kc) with KQ*N rows
 // n = kq*N + c_out (the merged-tap MMA's B operand), UMMA K-major canonical:
 // [n/8 group][k half][8 rows][8 k] bf16 -> SBO 256 B, LBO 128 B.
 // flip=1 builds the dgrad weights W'[n=ci][k=co][t] = W[co][ci][taps-1-t].
 __global__ void conv_tc_weight_image(const __nv_bfloat16 *__restrict__ w,
                                      __nv_bfloat16 *__restrict__ img, int n_rows, int k_cols,
-                                     int KP, int KQ, int KW, int flip) {
+                                     int KP, int KQ, int KW, int flip, int cperm) {
     const int KC = k_cols / 16;
     const int taps = KP * KQ * KW;
     const int NB = KQ * n_rows;  // rows per block
@@ -542,7 +676,8 @@ __global__ void conv_tc_weight_image(const __nv_bfloat16 *__restrict__ w,
         const int kw = r % KW;
         const int kp = r / KW;
         const int nrow = g * 8 + nn;
-        const int kq = nrow / n_rows, n = nrow % n_rows;
+        const int kq = nrow / n_rows;
+        const int n = cperm ? epi_channel(nrow % n_rows, n_rows) : nrow % n_rows;
         const int k = kc * 16 + h * 8 + kk;
         const int t = (kp * KQ + kq) * KW + kw;
         __nv_bfloat16 v;
@@ -560,7 +695,7 @@ __global__ void conv_tc_weight_image(const __nv_bfloat16 *__restrict__ w,
 // conv_tc_weight_image; flip = the dgrad image.
 __global__ void conv_tc_weight_image_pair(const __nv_bfloat16 *__restrict__ w,
                                           __nv_bfloat16 *__restrict__ img, int n_rows, int k_cols,
-                                          int KP, int KQ, int KW, int flip) {
+                                          int KP, int KQ, int KW, int flip, int cperm) {
     const int KC = k_cols / 16;
     const int taps = KP * KQ * KW;
     const int MH = KQ * n_rows / 2, QH = n_rows / 2;          // rows per half block
@@ -599,6 +734,7 @@ __global__ void conv_tc_weight_image_pair(const __nv_bfloat16 *__restrict__ w,
         const int kc = bi % KC, kw = (bi / KC) % KW, kp = bi / (KC * KW);
         const int k = kc * 16 + h * 8 + kk;
         const int t = (kp * KQ + kq) * KW + kw;
+        if (cperm) c = epi_channel(c, n_rows);
         img[e] = !flip ? w[((int64_t)c * k_cols + k) * taps + t]
                        : w[((int64_t)k * n_rows + c) * taps + (taps - 1 - t)];
     }
@@ -789,17 +925,21 @@ int run_conv_tc(const dp_conv_geom *g, bool dgrad, const void *in, const void *i
     const bool use_pair = !pair_off && n_wt_all >= 2 && sm_count() >= 2 &&
                           pair_shape(pl.N, R.KP, R.KQ, R.KW, pl.Cin) &&
                           ws_bytes >= 2 * (int64_t)pl.wimg_bytes;
+    // bf16 outputs drain through the coalesced epilogue (permuted B columns) when
+    // the halo output part shares the main part's W stride
+    const bool split_out = dgrad && g->halo > 0 && g->shard == 0;
+    const int cperm = (!f32out && (!split_out || R.hs[3] == R.ys[3])) ? 1 : 0;
     // weight image
     {
         int total = taps * pl.Cin * pl.N;
         if (use_pair)
             conv_tc_weight_image_pair<<<grid_for(2 * total, 256, 2), 256, 0, st>>>(
                 (const __nv_bfloat16 *)w, (__nv_bfloat16 *)ws, pl.N, pl.Cin, R.KP, R.KQ, R.KW,
-                dgrad ? 1 : 0);
+                dgrad ? 1 : 0, cperm);
         else
             conv_tc_weight_image<<<grid_for(total, 256, 2), 256, 0, st>>>(
                 (const __nv_bfloat16 *)w, (__nv_bfloat16 *)ws, pl.N, pl.Cin, R.KP, R.KQ, R.KW,
-                dgrad ? 1 : 0);
+                dgrad ? 1 : 0, cperm);
         int rc = launch_status("conv_tc_weight_image");
         if (rc) return rc;
     }
@@ -853,6 +993,7 @@ int run_conv_tc(const dp_conv_geom *g, bool dgrad, const void *in, const void *i
         p.ys[i] = R.ys[i];
         p.y2s[i] = R.hs[i];
     }
+    p.cperm = cperm;
     p.ysplit_dim = -1;
     p.ysplit = 0;
     if (dgrad && g->halo > 0 && g->shard == 0) {

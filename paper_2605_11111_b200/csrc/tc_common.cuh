@@ -199,6 +199,15 @@ __device__ __forceinline__ void tmem_ld16(uint32_t addr, uint32_t (&r)[16]) {
           "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
         : "r"(addr));
 }
+// 16 lanes x 4 repetitions of 128 bits (16 consecutive fp32 columns): register
+// 2j + g <- lane (lane_base + lane_id / 4 + 8 g), column 4 j + lane_id % 4 (the
+// fragment the wgrad transposer's 16x128b stores use, conv_tc.cu).
+__device__ __forceinline__ void tmem_ld16_16x128b(uint32_t addr, uint32_t (&r)[8]) {
+    asm volatile("tcgen05.ld.sync.aligned.16x128b.x4.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
+                   "=r"(r[6]), "=r"(r[7])
+                 : "r"(addr));
+}
 __device__ __forceinline__ void tmem_st16(uint32_t addr, const uint32_t (&r)[16]) {
     asm volatile(
         "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
