@@ -6,23 +6,36 @@
 // loop on the host (K||V rotating over NVLink) is unchanged; the state
 // stays fp32 in HBM between ring steps.
 //
-// Forward CTA = one 128-row query tile of one head, looping over the block's
-// keys 128 at a time (warp-specialised, 192 threads):
-//   warp 0     TMA producer: Q once, K/V tiles into a 3-stage ring
-//   warp 1     MMA issuer:   S(j) = Q K_j^T into a double-buffered TMEM
-//              S (M=128, N=128, K=64), then O += P(j-1) V(j-1) (M=128, N=64,
-//              K=128) into the TMEM O accumulator — S(j+1) runs while the
-//              softmax warps work on S(j)
-//   warps 2-5  softmax: thread = query row; tcgen05.ld its S row, online
-//              max with lazy rescaling (O and l are rescaled only when the
-//              running max grows by more than 2^8, which keeps the state
-//              exact: any reference max gives the same acc/l), P = exp2(.)
-//              as bf16 into a swizzled smem tile (the A operand of P V);
-//              they also load acc into TMEM at the start and write the
-//              state back at the end.
-// Operand layouts: Q, K tiles land from TMA as [128 rows][64 d] with the
-// 128-B swizzle (K-major A/B of S = Q K^T); V lands the same way and is
-// read as the MN-major B operand of P V; P is written K-major SW128.
+// Forward (attn_fwd_tc_kernel): CTA = TWO 128-row query tiles of one head,
+// looping over the block's keys 128 at a time; 384 threads:
+//   warpgroup 0  warp 0 TMA producer (Q once, K/V tiles into a 4-stage
+//                ring), warp 1 MMA issuer: S_t(j) = Q_t K_j^T (SS, M=128,
+//                N=128, K=64) and O_t += P_t(j) V_j (TS: P from TMEM, V as
+//                the MN-major smem B operand, M=128, N=64, K=128) for both
+//                tiles t, ping-ponging between the two softmax warpgroups
+//   warpgroups 1-2  softmax of tile t (thread = query row = TMEM lane):
+//                tcgen05.ld its S row, online max with lazy rescaling (O and
+//                l rescaled only when the row max grows by > 2^8: exact, any
+//                reference max gives the same acc/l), P = exp2(.) written as
+//                packed bf16 pairs into its own TMEM columns (no smem round
+//                trip); one exp2 pair in four on the FMA pipe (cubic, POLY);
+//                they load acc into TMEM at the start and write the state
+//                (m, l, acc; LSE for the backward) back at the end.
+// TMEM per tile: S [128 t, +128), P [256 + 64 t, +64), O [384 + 64 t, +64);
+// P does not alias S, so S_t(j+1) is issued as soon as the softmax has read
+// S_t(j).  setmaxnreg splits registers 80 (warpgroup 0) / 208 (softmax).
+//
+// Backward (attn_bwd_tc_kernel): CTA = one 128-key tile (K, V resident, dK
+// and dV accumulated in TMEM) looping over 128-row query blocks (Q, dO in a
+// 3-stage TMA ring); 768 threads in six warpgroups: S^T = K Q^T and
+// dP^T = V dO^T into TMEM, 16 softmax warps write P^T as bf16 pairs into TMEM
+// (the TS A operand of dV += P^T dO) and dS^T = scale P^T o (dP^T - D) as a
+// swizzled smem tile (double-buffered) for dK += dS^T Q and dQ = dS K; dQ is
+// drained by 4 epilogue warps through swizzled fp32 smem and a TMA bulk
+// reduce-add into dq, and the same warps stage -LSE*log2e / scale*D rows into
+// a smem ring two blocks ahead.
+// Operand layouts: Q, K, V, dO tiles land from TMA as [128 rows][64 d] with
+// the 128-B swizzle.
 #include "tc_common.cuh"
 #include <cstdio>
 

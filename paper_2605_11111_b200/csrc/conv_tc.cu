@@ -106,7 +106,14 @@ __host__ __device__ constexpr int ring_slots(int N) {
     return ring_ext(N) ? ((512 / N) < 18 ? (512 / N) : 18) - 2 : ((512 / N) < 16 ? (512 / N) : 16);
 }
 
-template <int N, int KP_, int KQ_, int KW_, int CIN_, bool PAIR = false>
+// X3: the bf16x3 fp32 path.  The MMA contracts over CIN_ = 6 C channel blocks
+// [xh xh xh xm xm xl] (against W' = [wh wm wl wh wm wh], conv_x3.cu) but the
+// activation holds each part ONCE (3 C channels, [xh xm xl]): the producer
+// loads 3 part boxes of C channels per row, and K block b reads part
+// x3_part(b) — half the split writes and TMA bytes of a 6-block operand.
+__host__ __device__ constexpr int x3_part(int blk) { return blk < 3 ? 0 : blk < 5 ? 1 : 2; }
+
+template <int N, int KP_, int KQ_, int KW_, int CIN_, bool PAIR = false, bool X3 = false>
 __global__ void __launch_bounds__(kThreads, 1)
 conv_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap hmap,
                const ConvTcParams p) {
@@ -127,8 +134,9 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
     const int KQ = kStatic ? KQ_ : p.KQ;
     const int KW = kStatic ? KW_ : p.KW;
     const int CIN = kStatic ? CIN_ : p.Cin;
-    const int CBLK = chan_block(CIN);
-    const int NBLK = CIN / CBLK;
+    static_assert(!X3 || (KP_ > 0 && CIN_ % 96 == 0), "X3: static 6-block shapes only");
+    const int CBLK = X3 ? CIN / 6 : chan_block(CIN);
+    const int NBLK = X3 ? 3 : CIN / CBLK;
     const int KPB = CBLK / 16;               // 16-channel MMA steps per block row
     const int KC = CIN / 16;
     const int ROWB = CBLK * 2;               // bytes per voxel row of a box
@@ -291,11 +299,16 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
                 const bool merged =
                     s >= KQ - 1 && s < nq && (wrap_ok || (int)(top % NSLOT) >= KQ - 1);
                 if (p.dbg & 2) {
-                } else if (kStatic && KW_ == 3 && !(p.dbg & (16 | 32))) {
+                } else if (kStatic && KW_ == 3 && (X3 || !(p.dbg & (16 | 32)))) {
                     // the three kw taps of each (kp, kc) issued as one group (one elect;
                     // measured 4-7 % faster than one elect per MMA)
                     constexpr int CS = CIN_ > 0 ? CIN_ : 16, KQS = KQ_ > 0 ? KQ_ : 1;
-                    constexpr int CB = chan_block(CS), NB = CS / CB, KPB_S = CB / 16, KC_S = CS / 16;
+                    constexpr int CB = X3 ? CS / 6 : chan_block(CS), NB = X3 ? 3 : CS / CB;
+                    constexpr int KPB_S = CB / 16, KC_S = CS / 16;
+                    // K step kc -> stored 16-channel step (X3: part of its 6-block index)
+                    auto kstore = [](int kc) {
+                        return X3 ? x3_part(kc / KPB_S) * KPB_S + kc % KPB_S : kc;
+                    };
                     constexpr uint32_t DA = (uint32_t)(CB * 2) >> 4;                     // one voxel row
                     constexpr uint32_t BLK = PAIR ? KQS * N * 16 : KQS * N * 32;        // == blk
                     constexpr uint32_t DBM = (uint32_t)(KC_S * BLK) >> 4;                // kw step, merged
@@ -311,7 +324,7 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
                         for (int kp = 0; kp < KP; ++kp)
 #pragma unroll
                             for (int kc = 0; kc < KC_S; ++kc) {
-                                const uint32_t aoff = (kp * NB + kc / KPB_S) * BOXB + (kc % KPB_S) * 32;
+                                const uint32_t aoff = (kp * NB + kstore(kc) / KPB_S) * BOXB + (kstore(kc) % KPB_S) * 32;
                                 const uint32_t boff = ((kp * 3) * KC_S + kc) * BLK;
                                 grp(d, aoff >> 4, bdesc0 + (boff >> 4), idesc_all,
                                     std::integral_constant<uint32_t, DBM>{});
@@ -330,7 +343,7 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
                             for (int kp = 0; kp < KP; ++kp)
 #pragma unroll
                                 for (int kc = 0; kc < KC_S; ++kc) {
-                                    const uint32_t aoff = (kp * NB + kc / KPB_S) * BOXB + (kc % KPB_S) * 32;
+                                    const uint32_t aoff = (kp * NB + kstore(kc) / KPB_S) * BOXB + (kstore(kc) % KPB_S) * 32;
                                     const uint32_t boff =
                                         PAIR ? kqblk0 + (((kp * 3) * KC_S + kc) * KQS + kq) * kqblk
                                              : ((kp * 3) * KC_S + kc) * BLK + kq * (N / 8) * 256;
@@ -799,9 +812,10 @@ struct Plan {
     Roles R;
     int Cin, N;           // K channels, N channels of this conv
     int cblk, stage_bytes, wimg_bytes, nstage, smem;
+    bool x3;              // 6-block K over a 3-part activation (the bf16x3 path)
 };
 
-bool make_plan(const dp_conv_geom *g, bool dgrad, Plan &pl, bool f32out = false) {
+bool make_plan(const dp_conv_geom *g, bool dgrad, Plan &pl, bool f32out = false, bool x3 = false) {
     if (!map_roles(g, dgrad, pl.R)) return false;
     pl.Cin = (int)(dgrad ? g->c_out : g->c_in);
     pl.N = pick_n((int)(dgrad ? g->c_in : g->c_out));
@@ -822,8 +836,12 @@ bool make_plan(const dp_conv_geom *g, bool dgrad, Plan &pl, bool f32out = false)
         if (R.xs[i] % 8 || (!f32out && R.ys[i] % 8)) return false;
         if (g->halo > 0 && !(dgrad && f32out) && R.hs[i] % 8) return false;
     }
-    pl.cblk = chan_block(pl.Cin);
-    pl.stage_bytes = R.KP * (pl.Cin / pl.cblk) * box_bytes(pl.cblk, R.KW);
+    if (x3 && !(R.KP == 1 && R.KQ == 3 && R.KW == 3 && (pl.Cin == 96 || pl.Cin == 192) &&
+                (pl.N == 16 || pl.N == 32)))
+        return false;
+    pl.x3 = x3;
+    pl.cblk = x3 ? pl.Cin / 6 : chan_block(pl.Cin);       // X3: one box per stored part
+    pl.stage_bytes = R.KP * (x3 ? 3 : pl.Cin / pl.cblk) * box_bytes(pl.cblk, R.KW);
     pl.wimg_bytes = R.KP * R.KQ * R.KW * pl.Cin * pl.N * 2;
     const int budget = 220 * 1024;
     const int fixed = ((pl.wimg_bytes + 1023) & ~1023) + 1024;
@@ -838,20 +856,20 @@ bool make_plan(const dp_conv_geom *g, bool dgrad, Plan &pl, bool f32out = false)
     return true;
 }
 
-template <int N, int KP, int KQ, int KW, int CIN>
+template <int N, int KP, int KQ, int KW, int CIN, bool X3 = false>
 int launch_k(const CUtensorMap &xm, const CUtensorMap &hm, const ConvTcParams &p, int grid,
              int smem, cudaStream_t st) {
-    auto kern = conv_tc_kernel<N, KP, KQ, KW, CIN>;
+    auto kern = conv_tc_kernel<N, KP, KQ, KW, CIN, false, X3>;
     DP_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     kern<<<grid, kThreads, smem, st>>>(xm, hm, p);
     return launch_status("conv_tc_kernel");
 }
 
 // CTA-pair instantiation: (2, 1, 1) clusters, grid = 2 x clusters
-template <int N, int KP, int KQ, int KW, int CIN>
+template <int N, int KP, int KQ, int KW, int CIN, bool X3 = false>
 int launch_k_pair(const CUtensorMap &xm, const CUtensorMap &hm, const ConvTcParams &p, int grid,
                   int smem, cudaStream_t st) {
-    auto kern = conv_tc_kernel<N, KP, KQ, KW, CIN, true>;
+    auto kern = conv_tc_kernel<N, KP, KQ, KW, CIN, true, X3>;
     DP_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)grid);
@@ -909,9 +927,9 @@ int launch_n(const CUtensorMap &xm, const CUtensorMap &hm, const ConvTcParams &p
 
 int run_conv_tc(const dp_conv_geom *g, bool dgrad, const void *in, const void *in_halo,
                 const void *w, void *out, void *out2, void *ws, int64_t ws_bytes,
-                cudaStream_t st, bool f32out = false) {
+                cudaStream_t st, bool f32out = false, bool x3 = false) {
     Plan pl;
-    DP_REQUIRE(make_plan(g, dgrad, pl, f32out), DP_ERR_UNSUPPORTED,
+    DP_REQUIRE(make_plan(g, dgrad, pl, f32out, x3), DP_ERR_UNSUPPORTED,
                "conv_tc: outside the envelope");
     const Roles &R = pl.R;
     const int taps = R.KP * R.KQ * R.KW;
@@ -951,8 +969,8 @@ int run_conv_tc(const dp_conv_geom *g, bool dgrad, const void *in, const void *i
                                                    : CU_TENSOR_MAP_SWIZZLE_128B;
     CUtensorMap xm, hm;
     {
-        uint64_t dims[5] = {(uint64_t)pl.Cin, (uint64_t)R.Win, (uint64_t)R.Qin, (uint64_t)R.Pin,
-                            (uint64_t)g->batch};
+        uint64_t dims[5] = {(uint64_t)(x3 ? pl.Cin / 2 : pl.Cin), (uint64_t)R.Win, (uint64_t)R.Qin,
+                            (uint64_t)R.Pin, (uint64_t)g->batch};
         uint64_t strides[4] = {(uint64_t)R.xs[3] * 2, (uint64_t)R.xs[2] * 2,
                                (uint64_t)R.xs[1] * 2, (uint64_t)R.xs[0] * 2};
         int rc = encode_tensor_map(&xm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void *>(in),
@@ -961,7 +979,7 @@ int run_conv_tc(const dp_conv_geom *g, bool dgrad, const void *in, const void *i
     }
     hm = xm;
     if (!dgrad && g->halo > 0) {
-        uint64_t dims[5] = {(uint64_t)pl.Cin, (uint64_t)R.Win,
+        uint64_t dims[5] = {(uint64_t)(x3 ? pl.Cin / 2 : pl.Cin), (uint64_t)R.Win,
                             (uint64_t)(R.split == 1 ? g->halo : R.Qin),
                             (uint64_t)(R.split == 0 ? g->halo : R.Pin), (uint64_t)g->batch};
         uint64_t strides[4] = {(uint64_t)R.hs[3] * 2, (uint64_t)R.hs[2] * 2,
@@ -1038,6 +1056,21 @@ int run_conv_tc(const dp_conv_geom *g, bool dgrad, const void *in, const void *i
         p.dbg = dbg;
     }
     int grid = p.n_units < sms ? p.n_units : sms;
+    if (pl.x3) {   // N (output channels) and K (6 x the contracted channels) vary independently
+        const bool k96 = pl.Cin == 96;
+        if (use_pair) {
+            if (pl.N == 16)
+                return k96 ? launch_k_pair<16, 1, 3, 3, 96, true>(xm, hm, p, 2 * grid, pl.smem, st)
+                           : launch_k_pair<16, 1, 3, 3, 192, true>(xm, hm, p, 2 * grid, pl.smem, st);
+            return k96 ? launch_k_pair<32, 1, 3, 3, 96, true>(xm, hm, p, 2 * grid, pl.smem, st)
+                       : launch_k_pair<32, 1, 3, 3, 192, true>(xm, hm, p, 2 * grid, pl.smem, st);
+        }
+        if (pl.N == 16)
+            return k96 ? launch_k<16, 1, 3, 3, 96, true>(xm, hm, p, grid, pl.smem, st)
+                       : launch_k<16, 1, 3, 3, 192, true>(xm, hm, p, grid, pl.smem, st);
+        return k96 ? launch_k<32, 1, 3, 3, 96, true>(xm, hm, p, grid, pl.smem, st)
+                   : launch_k<32, 1, 3, 3, 192, true>(xm, hm, p, grid, pl.smem, st);
+    }
     if (use_pair)
         return pl.N == 16 ? launch_n_pair<16>(xm, hm, p, 2 * grid, pl.smem, st)
                           : launch_n_pair<32>(xm, hm, p, 2 * grid, pl.smem, st);
@@ -1879,20 +1912,48 @@ conv_wgrad_ts_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_cons
 }
 
 // dw[co][ci][kp][kq][kw] = sum_cta partial[cta][kw*32 + co][(kq*KP + kp)*Cin + ci]
-__global__ void wgrad_ts_reduce(const float *__restrict__ part, float *__restrict__ dw, int ctas,
-                                int KP, int Cin) {
+// Sum of the per-CTA partials [cta][96][NT] into dW.  A block covers 32
+// consecutive partial columns (coalesced 128-B reads) with 8 warps, warp g
+// summing CTAs g, g + 8, ... (four independent loads in flight per step),
+// then the 8 partial sums are added in a fixed order: deterministic, and
+// the loads no longer sit behind one serial 148-term dependency chain per
+// thread (was ~41 us per call, latency-bound).
+constexpr int kRedCols = 32, kRedGroups = 8;
+__global__ void __launch_bounds__(kRedCols * kRedGroups)
+wgrad_ts_reduce(const float *__restrict__ part, float *__restrict__ dw, int ctas, int KP, int Cin) {
+    __shared__ double red[kRedGroups][kRedCols + 1];
     const int KQ = 3, KW = 3;
     const int NT = KQ * KP * Cin;
     const int total = 96 * NT;            // partial layout order: coalesced reads
     const size_t per_cta = (size_t)total;
-    for (int o = blockIdx.x * blockDim.x + threadIdx.x; o < total; o += gridDim.x * blockDim.x) {
+    const int lo = threadIdx.x % kRedCols, g = threadIdx.x / kRedCols;
+    const int o = blockIdx.x * kRedCols + lo;
+    double s = 0.0;   // fp64: exact enough for any CTA count
+    if (o < total) {
+        int c = g;
+        for (; c + 3 * kRedGroups < ctas; c += 4 * kRedGroups) {
+            const float a0 = part[(size_t)c * per_cta + o];
+            const float a1 = part[(size_t)(c + kRedGroups) * per_cta + o];
+            const float a2 = part[(size_t)(c + 2 * kRedGroups) * per_cta + o];
+            const float a3 = part[(size_t)(c + 3 * kRedGroups) * per_cta + o];
+            s += (double)a0;
+            s += (double)a1;
+            s += (double)a2;
+            s += (double)a3;
+        }
+        for (; c < ctas; c += kRedGroups) s += (double)part[(size_t)c * per_cta + o];
+    }
+    red[g][lo] = s;
+    __syncthreads();
+    if (g == 0 && o < total) {
+        double t = 0.0;
+#pragma unroll
+        for (int k = 0; k < kRedGroups; ++k) t += red[k][lo];
         const int kwco = o / NT, col = o % NT;
         const int kw = kwco / 32, co = kwco % 32;
         const int ci = col % Cin, kqkp = col / Cin;
         const int kp = kqkp % KP, kq = kqkp / KP;
-        double s = 0.0;   // fixed order, fp64: deterministic and exact enough for any CTA count
-        for (int c = 0; c < ctas; ++c) s += part[c * per_cta + o];
-        dw[(((co * Cin + ci) * KP + kp) * KQ + kq) * KW + kw] = (float)s;
+        dw[(((co * Cin + ci) * KP + kp) * KQ + kq) * KW + kw] = (float)t;
     }
 }
 
@@ -2059,8 +2120,8 @@ int run_wgrad_ts(const dp_conv_geom *g, const TsPlan &pl, const void *x, const v
                             : launch_ts_k<64, 1>(xm, hm, dm, p, pl.grid, pl.smem, st);
     if (rc) return rc;
     const int total = 96 * 3 * R.KP * pl.Cin;
-    wgrad_ts_reduce<<<grid_for(total, 256, 4), 256, 0, st>>>((const float *)ws, dw, pl.grid, R.KP,
-                                                             pl.Cin);
+    wgrad_ts_reduce<<<(unsigned)((total + kRedCols - 1) / kRedCols), kRedCols * kRedGroups, 0, st>>>(
+        (const float *)ws, dw, pl.grid, R.KP, pl.Cin);
     return launch_status("wgrad_ts_reduce");
 }
 
@@ -2126,12 +2187,14 @@ int64_t conv_wgrad_x3_workspace(const dp_conv_geom *g) {
 // bf16 tcgen05 conv with fp32 outputs (the bf16x3 fp32 path, conv_x3.cu)
 int64_t conv_tc_f32out_workspace(const dp_conv_geom *g, bool dgrad) {
     Plan pl;
-    return make_plan(g, dgrad, pl, true) ? 2 * (int64_t)pl.wimg_bytes : -1;
+    return make_plan(g, dgrad, pl, true, true) ? 2 * (int64_t)pl.wimg_bytes : -1;
 }
+// g describes the 6-block MMA view (c_in or c_out = 6 C); the activation
+// operand holds the 3 parts once (3 C channels, strides in g)
 int conv_tc_f32out_launch(const dp_conv_geom *g, bool dgrad, const void *in, const void *in_halo,
                           const void *w, void *out, void *out2, void *ws, int64_t ws_bytes,
                           cudaStream_t st) {
-    return run_conv_tc(g, dgrad, in, in_halo, w, out, out2, ws, ws_bytes, st, true);
+    return run_conv_tc(g, dgrad, in, in_halo, w, out, out2, ws, ws_bytes, st, true, true);
 }
 
 int conv_fwd_tc_launch(const dp_conv_geom *g, const void *x, const void *xh, const void *w, void *y,

@@ -9,6 +9,8 @@
 // Those six terms become ONE bf16 convolution with fp32 accumulation in TMEM
 // by concatenating along the contraction:
 //   fwd    channels: X' = [xh xh xh xm xm xl] (6 C_in), W' = [wh wm wl wh wm wh]
+//          (X' is virtual: the operand stores [xh xm xl] once and the conv
+//          kernel's K block b reads part c_xpat[b] — conv_tc.cu X3)
 //   dgrad  channels: dY' = [dh dh dh dm dm dl] (6 C_out), W' split on c_out
 //   wgrad  batch:    pairs (xh dh, xm dh, xh dm, xl dh, xm dm, xh dl)
 // (wgrad contracts over positions, so the six pairings are six batch entries
@@ -53,7 +55,7 @@ __device__ __forceinline__ void split3(float x, __nv_bfloat16 (&pt)[3]) {
 }
 
 // fp32 activation [B][C][S0][S1] (any strides, 2-D) -> bf16 channels-last.
-// mode 0: channel blocks out[b][s0][s1][blk*C + c] = part_{pat[blk]};
+// mode 0: channel blocks out[b][s0][s1][blk*C + c] = part_{pat[blk]} (nblk blocks);
 // mode 1: batch blocks out[blk*B + b][s0][s1][c] = part_{pat[blk]}.
 // Tile: 32 channels x 64 positions along S1 through smem — coalesced fp32
 // reads along S1; then a thread splits 8 consecutive channels of one
@@ -107,7 +109,7 @@ x3_split_act(const float *__restrict__ x, int64_t B, int64_t C, int64_t S0, int6
         const int q = pat[blk];
         const uint4 v = make_uint4(pk[q][0], pk[q][1], pk[q][2], pk[q][3]);
         __nv_bfloat16 *dst =
-            mode == 0 ? out + ((b * S0 + i0) * S1 + i1) * (kParts * C) + blk * C + c0
+            mode == 0 ? out + ((b * S0 + i0) * S1 + i1) * (nblk * C) + blk * C + c0
                       : out + ((((int64_t)blk * B + b) * S0 + i0) * S1 + i1) * C + c0;
         *reinterpret_cast<uint4 *>(dst) = v;
     }
@@ -160,13 +162,15 @@ dp_conv_geom x3_geom(const dp_conv_geom *g, int which) {
     dp_conv_geom h = *g;
     const int64_t Hin = g->in_ext[0], Win = g->in_ext[1];
     const int64_t Hout = g->out_ext[0], Wout = g->out_ext[1];
+    // fwd / dgrad: the MMA contracts over 6 C channel blocks, the stored operand
+    // holds the 3 parts once (3 C channels; conv_tc.cu X3)
     if (which == DP_CONV_FWD) {
         h.c_in = kParts * g->c_in;
-        cl_strides(Hin, Win, h.c_in, h.xs);
-        cl_strides(g->halo, Win, h.c_in, h.hs);
+        cl_strides(Hin, Win, 3 * g->c_in, h.xs);
+        cl_strides(g->halo, Win, 3 * g->c_in, h.hs);
     } else if (which == DP_CONV_DGRAD) {
         h.c_out = kParts * g->c_out;
-        cl_strides(Hout, Wout, h.c_out, h.ys);
+        cl_strides(Hout, Wout, 3 * g->c_out, h.ys);
     } else {
         h.batch = kParts * g->batch;
         cl_strides(Hin, Win, g->c_in, h.xs);
@@ -190,11 +194,11 @@ X3Layout x3_layout(const dp_conv_geom *g, int which) {
     const int64_t taps = 9;
     int64_t off = 0;
     if (which == DP_CONV_FWD) {
-        L.act = off; off += align256(g->batch * Hin * Win * kParts * g->c_in * 2);
-        L.act_h = off; off += align256(g->batch * g->halo * Win * kParts * g->c_in * 2);
+        L.act = off; off += align256(g->batch * Hin * Win * 3 * g->c_in * 2);
+        L.act_h = off; off += align256(g->batch * g->halo * Win * 3 * g->c_in * 2);
         L.wimg = off; off += align256(g->c_out * kParts * g->c_in * taps * 2);
     } else if (which == DP_CONV_DGRAD) {
-        L.dy = off; off += align256(g->batch * Hout * Wout * kParts * g->c_out * 2);
+        L.dy = off; off += align256(g->batch * Hout * Wout * 3 * g->c_out * 2);
         L.wimg = off; off += align256(kParts * g->c_out * g->c_in * taps * 2);
     } else {
         const int64_t np = x3_wgrad_paired(g) ? 3 : kParts;   // parts once, or 6 pairings
@@ -254,11 +258,11 @@ int conv_x3_launch(const dp_conv_geom *g, int which, const void *a, const void *
         __nv_bfloat16 *xa = (__nv_bfloat16 *)(w8 + L.act), *xha = (__nv_bfloat16 *)(w8 + L.act_h);
         __nv_bfloat16 *wi = (__nv_bfloat16 *)(w8 + L.wimg);
         int64_t sx[4] = {g->xs[0], g->xs[1], g->xs[2], g->xs[3]};
-        if ((rc = launch_split((const float *)a, g->batch, g->c_in, Hin, Win, sx, xa, 0, 0, st)))
+        if ((rc = launch_split((const float *)a, g->batch, g->c_in, Hin, Win, sx, xa, 0, 1, st)))
             return rc;
         if (g->halo > 0) {
             int64_t sh[4] = {g->hs[0], g->hs[1], g->hs[2], g->hs[3]};
-            if ((rc = launch_split((const float *)ah, g->batch, g->c_in, g->halo, Win, sh, xha, 0, 0,
+            if ((rc = launch_split((const float *)ah, g->batch, g->c_in, g->halo, Win, sh, xha, 0, 1,
                                    st)))
                 return rc;
         }
@@ -272,7 +276,7 @@ int conv_x3_launch(const dp_conv_geom *g, int which, const void *a, const void *
     if (which == DP_CONV_DGRAD) {          // a = dy, b = w (fp32), out = dx, out2 = dx halo
         __nv_bfloat16 *da = (__nv_bfloat16 *)(w8 + L.dy), *wi = (__nv_bfloat16 *)(w8 + L.wimg);
         int64_t sd[4] = {g->ys[0], g->ys[1], g->ys[2], g->ys[3]};
-        if ((rc = launch_split((const float *)a, g->batch, g->c_out, Hout, Wout, sd, da, 0, 0, st)))
+        if ((rc = launch_split((const float *)a, g->batch, g->c_out, Hout, Wout, sd, da, 0, 1, st)))
             return rc;
         const int64_t nw = g->c_out * g->c_in * 9;
         x3_split_weight<<<grid_for(nw, 256, 2), 256, 0, st>>>((const float *)b, g->c_out, g->c_in, 9,
