@@ -207,7 +207,8 @@ def barrier(ctx):
 
 
 class KernelTimer:
-    NAMES = ("conv_fwd", "conv_dgrad", "conv_wgrad", "attn_fwd_update", "attn_bwd_update")
+    NAMES = ("conv_fwd", "conv_dgrad", "conv_wgrad", "attn_fwd_update", "attn_bwd_update",
+             "conv_fwd_x3", "conv_dgrad_x3", "conv_wgrad_x3", "x3_split")
 
     def __init__(self):
         self.records = []  # (key, flops, start, end)
@@ -228,9 +229,14 @@ class KernelTimer:
                     s = torch.cuda.Event(enable_timing=True)
                     e = torch.cuda.Event(enable_timing=True)
                     s.record()
-                    orig(*a, **kw)
+                    res = orig(*a, **kw)
                     e.record()
-                    timer.records.append((f"{name}[{tag}]", flops, s, e))
+                    base = name.replace("_x3", "")
+                    nbytes = 0
+                    if name == "x3_split":   # fp32 read + 3 bf16 parts written (HBM-bound)
+                        nbytes = a[0].numel() * (4 + 3 * 2)
+                    timer.records.append((f"{base}[{tag}]", flops, s, e, nbytes))
+                    return res
                 return inner
             setattr(kernels_mod, name, make())
 
@@ -239,11 +245,12 @@ class KernelTimer:
 
         torch.cuda.synchronize()
         out = {}
-        for key, flops, s, e in self.records:
-            d = out.setdefault(key, {"launches": 0, "ms": 0.0, "flops": 0.0})
+        for key, flops, s, e, nbytes in self.records:
+            d = out.setdefault(key, {"launches": 0, "ms": 0.0, "flops": 0.0, "bytes": 0})
             d["launches"] += 1
             d["ms"] += s.elapsed_time(e)
             d["flops"] += flops
+            d["bytes"] += nbytes
         return out
 
 
@@ -299,11 +306,22 @@ def kernel_work(name, a, kw):
     SURVEY 8(d))."""
     import math
 
+    if name == "x3_split":       # bf16x3 operand split: data movement, no FLOPs
+        return 0.0, "fp32->3xbf16"
     if name == "conv_fwd":
         x, _, w, y = a[:4]
         pos = y.shape[0] * math.prod(y.shape[2:])
+    elif name == "conv_fwd_x3":      # (x, x_halo, xp, xhp, w, y)
+        w, y = a[4], a[5]
+        pos = y.shape[0] * math.prod(y.shape[2:])
     elif name == "conv_dgrad":
         dy, w = a[0], a[1]
+        pos = dy.shape[0] * math.prod(dy.shape[2:])
+    elif name == "conv_dgrad_x3":    # (dy, dyp, w, dx, dx_halo)
+        dy, w = a[0], a[2]
+        pos = dy.shape[0] * math.prod(dy.shape[2:])
+    elif name == "conv_wgrad_x3":    # (x, x_halo, xp, xhp, dy, dyp, dw)
+        dy, w = a[4], a[6]
         pos = dy.shape[0] * math.prod(dy.shape[2:])
     elif name == "conv_wgrad":
         x, _, dy, w = a[0], a[1], a[2], a[3]
@@ -946,7 +964,7 @@ def main():
     for rk in ranks_k:
         for key, d in rk["ksum"].items():
             m = merged.setdefault(key, {"launches": d["launches"], "ms": 0.0,
-                                        "flops": d["flops"]})
+                                        "flops": d["flops"], "bytes": d.get("bytes", 0)})
             m["ms"] = max(m["ms"], d["ms"])
     roof = None
     if not merged and W.get("hbm_bytes_per_step"):
@@ -967,8 +985,13 @@ def main():
         per_kernel[key] = {"launches_per_step": d["launches"] / args.steps, "avg_ms": avg,
                            "tflops": ach, "frac": ach / peak,
                            "share_of_step": d["ms"] / args.steps / ms}
-    if merged:
-        key, d = max(merged.items(), key=lambda kv: kv[1]["ms"])
+        if d.get("bytes"):    # HBM-bound data movement (the bf16x3 operand split)
+            gbs = (d["bytes"] / d["launches"]) / (avg / 1000.0) / 1e9
+            hbm = pk.get("hbm_gbs", PEAKS_FALLBACK["hbm_gbs"])
+            per_kernel[key].update({"gbs": gbs, "frac": gbs / hbm, "bound": "hbm"})
+    tensor_keys = {k: v for k, v in merged.items() if not v.get("bytes")}
+    if tensor_keys:
+        key, d = max(tensor_keys.items(), key=lambda kv: kv[1]["ms"])
         pk_ = per_kernel[key]
         traffic = None
         tpath = os.path.join(ROOT, "profiles", "traffic.json")

@@ -23,6 +23,7 @@
  *                                                     trim/pad + dense.conv
  *   dp_conv_dgrad,         (no reference function)    conv backward, A9
  *   dp_conv_wgrad
+ *   dp_conv_x3_*           same, fp32 operands split once (bf16x3)
  *   dp_attn_fwd_update     domainpar/ops.py:199-211,272-275  scores +
  *                                                     RingSoftmaxState.update
  *   dp_attn_finalize       domainpar/ops.py:213-214,278   acc / l
@@ -161,6 +162,36 @@ int dp_conv_dgrad(const dp_conv_geom *g, int dtype, int algo, const void *dy, co
 int dp_conv_wgrad(const dp_conv_geom *g, int dtype, int algo, const void *x, const void *x_halo,
                   const void *dy, void *dw, void *workspace, int64_t workspace_bytes,
                   void *stream);
+
+/* ---- fp32 conv on the tensor cores with operands split once --------------- */
+/* The fp32 convs above run as bf16x3 (three exact bf16 parts per value,
+ * six part products, fp32 accumulation: the reference's 1e-5 tolerance,
+ * domainpar/verify.py:40) and split their fp32 operands inside each call.
+ * These entry points let the caller split an operand ONCE and reuse it: x
+ * (split in the forward) feeds the forward and the weight gradient, dy
+ * (split in the backward) feeds the data and the weight gradient — the
+ * tape of domainpar/ops.py:303-422's halo_conv keeps x's parts.  A split
+ * operand is [3][batch][s0][s1][c] bf16 channels-last (the parts as batch
+ * blocks); operand = DP_X3_X (x main block, strides g->xs), DP_X3_XHALO (the
+ * received halo rows, g->hs) or DP_X3_DY (g->ys).  Bytes: 0 for an empty
+ * operand, -1 outside the envelope (2-D 3x3, stride 1, c_in/c_out 16|32). */
+#define DP_X3_X 0
+#define DP_X3_XHALO 1
+#define DP_X3_DY 2
+int64_t dp_conv_x3_operand_bytes(const dp_conv_geom *g, int operand);
+int dp_conv_x3_split(const dp_conv_geom *g, int operand, const void *src, void *parts,
+                     void *stream);
+/* workspace of the *_parts calls (weight images, wgrad partials); -1 when
+ * the geometry is outside the bf16x3 path */
+int64_t dp_conv_x3_parts_workspace(const dp_conv_geom *g, int which);
+int dp_conv_x3_fwd_parts(const dp_conv_geom *g, const void *x_parts, const void *x_halo_parts,
+                         const void *w, void *y, void *workspace, int64_t workspace_bytes,
+                         void *stream);
+int dp_conv_x3_dgrad_parts(const dp_conv_geom *g, const void *dy_parts, const void *w, void *dx,
+                           void *dx_halo, void *workspace, int64_t workspace_bytes, void *stream);
+int dp_conv_x3_wgrad_parts(const dp_conv_geom *g, const void *x_parts, const void *x_halo_parts,
+                           const void *dy_parts, void *dw, void *workspace,
+                           int64_t workspace_bytes, void *stream);
 
 /* ---- ring attention blocks ------------------------------------------------ */
 

@@ -81,6 +81,15 @@ SIGNATURES = {
                                      _vp, _vp, _vp, _vp, _vp, ctypes.c_int64, _vp]),
     "dp_conv_wgrad": (ctypes.c_int, [ctypes.POINTER(ConvGeom), ctypes.c_int, ctypes.c_int,
                                      _vp, _vp, _vp, _vp, _vp, ctypes.c_int64, _vp]),
+    "dp_conv_x3_operand_bytes": (ctypes.c_int64, [ctypes.POINTER(ConvGeom), ctypes.c_int]),
+    "dp_conv_x3_split": (ctypes.c_int, [ctypes.POINTER(ConvGeom), ctypes.c_int, _vp, _vp, _vp]),
+    "dp_conv_x3_parts_workspace": (ctypes.c_int64, [ctypes.POINTER(ConvGeom), ctypes.c_int]),
+    "dp_conv_x3_fwd_parts": (ctypes.c_int, [ctypes.POINTER(ConvGeom), _vp, _vp, _vp, _vp, _vp,
+                                            ctypes.c_int64, _vp]),
+    "dp_conv_x3_dgrad_parts": (ctypes.c_int, [ctypes.POINTER(ConvGeom), _vp, _vp, _vp, _vp, _vp,
+                                              ctypes.c_int64, _vp]),
+    "dp_conv_x3_wgrad_parts": (ctypes.c_int, [ctypes.POINTER(ConvGeom), _vp, _vp, _vp, _vp, _vp,
+                                              ctypes.c_int64, _vp]),
     "dp_attn_fwd_update": (ctypes.c_int, [ctypes.POINTER(AttnGeom), ctypes.c_int, ctypes.c_int,
                                           _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "dp_attn_finalize": (ctypes.c_int, [ctypes.POINTER(AttnGeom), ctypes.c_int,

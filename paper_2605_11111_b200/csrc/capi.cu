@@ -48,6 +48,11 @@ int conv_x3_eligible(const dp_conv_geom *, int which);
 int64_t conv_x3_workspace(const dp_conv_geom *, int which);
 int conv_x3_launch(const dp_conv_geom *, int which, const void *, const void *, const void *, void *,
                    void *, void *, int64_t, cudaStream_t);
+int64_t conv_x3_parts_workspace(const dp_conv_geom *, int which);
+int64_t conv_x3_operand_bytes(const dp_conv_geom *, int operand);
+int conv_x3_split(const dp_conv_geom *, int operand, const void *, void *, cudaStream_t);
+int conv_x3_parts_launch(const dp_conv_geom *, int which, const void *, const void *, const void *,
+                         void *, void *, void *, int64_t, cudaStream_t);
 }  // namespace dp
 
 using namespace dp;
@@ -124,6 +129,36 @@ extern "C" int dp_conv_wgrad(const dp_conv_geom *g, int dtype, int algo, const v
         return conv_x3_launch(g, DP_CONV_WGRAD, x, xh, dy, dw, nullptr, ws, ws_bytes, st);
     if (a == DP_ALGO_TC) return conv_wgrad_tc_launch(g, x, xh, dy, dw, ws, ws_bytes, st);
     return conv_wgrad_simt_launch(g, dtype, x, xh, dy, dw, ws, ws_bytes, st);
+}
+
+// bf16x3 with caller-held split operands: tcgen05 only (no CUDA-core form)
+extern "C" int64_t dp_conv_x3_operand_bytes(const dp_conv_geom *g, int operand) {
+    return conv_x3_operand_bytes(g, operand);
+}
+extern "C" int dp_conv_x3_split(const dp_conv_geom *g, int operand, const void *src, void *parts,
+                                void *stream) {
+    return conv_x3_split(g, operand, src, parts, (cudaStream_t)stream);
+}
+extern "C" int64_t dp_conv_x3_parts_workspace(const dp_conv_geom *g, int which) {
+    return conv_x3_parts_workspace(g, which);
+}
+extern "C" int dp_conv_x3_fwd_parts(const dp_conv_geom *g, const void *xp, const void *xhp,
+                                    const void *w, void *y, void *ws, int64_t ws_bytes,
+                                    void *stream) {
+    return conv_x3_parts_launch(g, DP_CONV_FWD, xp, xhp, w, y, nullptr, ws, ws_bytes,
+                                (cudaStream_t)stream);
+}
+extern "C" int dp_conv_x3_dgrad_parts(const dp_conv_geom *g, const void *dyp, const void *w,
+                                      void *dx, void *dxh, void *ws, int64_t ws_bytes,
+                                      void *stream) {
+    return conv_x3_parts_launch(g, DP_CONV_DGRAD, dyp, nullptr, w, dx, dxh, ws, ws_bytes,
+                                (cudaStream_t)stream);
+}
+extern "C" int dp_conv_x3_wgrad_parts(const dp_conv_geom *g, const void *xp, const void *xhp,
+                                      const void *dyp, void *dw, void *ws, int64_t ws_bytes,
+                                      void *stream) {
+    return conv_x3_parts_launch(g, DP_CONV_WGRAD, xp, xhp, dyp, dw, nullptr, ws, ws_bytes,
+                                (cudaStream_t)stream);
 }
 
 extern "C" int dp_attn_fwd_update(const dp_attn_geom *g, int dtype, int algo, const void *q,

@@ -108,9 +108,11 @@ __host__ __device__ constexpr int ring_slots(int N) {
 
 // X3: the bf16x3 fp32 path.  The MMA contracts over CIN_ = 6 C channel blocks
 // [xh xh xh xm xm xl] (against W' = [wh wm wl wh wm wh], conv_x3.cu) but the
-// activation holds each part ONCE (3 C channels, [xh xm xl]): the producer
-// loads 3 part boxes of C channels per row, and K block b reads part
-// x3_part(b) — half the split writes and TMA bytes of a 6-block operand.
+// activation holds each part ONCE, as batch blocks [part][B][..][C] (the
+// layout the TS wgrad reads too, so one split serves fwd/dgrad and wgrad):
+// the producer loads the 3 part boxes of a row (batch coordinate
+// part * B + b), and K block b reads part x3_part(b) — half the split writes
+// and TMA bytes of a materialised 6-block operand.
 __host__ __device__ constexpr int x3_part(int blk) { return blk < 3 ? 0 : blk < 5 ? 1 : 2; }
 
 template <int N, int KP_, int KQ_, int KW_, int CIN_, bool PAIR = false, bool X3 = false>
@@ -237,10 +239,11 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
                     for (int cb = 0; cb < NBLK; ++cb) {
                         if constexpr (PAIR)
                             tma_load_5d_2sm_e(dst + (size_t)(kp * NBLK + cb) * BOXB, map,
-                                              lead_full + idx * 8, cb * CBLK, wc, qcrd, pc, b);
+                                              lead_full + idx * 8, X3 ? 0 : cb * CBLK, wc, qcrd,
+                                              pc, X3 ? cb * p.B + b : b);
                         else
                             tma_load_5d_e(dst + (size_t)(kp * NBLK + cb) * BOXB, map, &full[idx],
-                                          cb * CBLK, wc, qcrd, pc, b);
+                                          X3 ? 0 : cb * CBLK, wc, qcrd, pc, X3 ? cb * p.B + b : b);
                     }
                 }
             }
@@ -969,8 +972,8 @@ int run_conv_tc(const dp_conv_geom *g, bool dgrad, const void *in, const void *i
                                                    : CU_TENSOR_MAP_SWIZZLE_128B;
     CUtensorMap xm, hm;
     {
-        uint64_t dims[5] = {(uint64_t)(x3 ? pl.Cin / 2 : pl.Cin), (uint64_t)R.Win, (uint64_t)R.Qin,
-                            (uint64_t)R.Pin, (uint64_t)g->batch};
+        uint64_t dims[5] = {(uint64_t)(x3 ? pl.Cin / 6 : pl.Cin), (uint64_t)R.Win, (uint64_t)R.Qin,
+                            (uint64_t)R.Pin, (uint64_t)(x3 ? 3 : 1) * g->batch};
         uint64_t strides[4] = {(uint64_t)R.xs[3] * 2, (uint64_t)R.xs[2] * 2,
                                (uint64_t)R.xs[1] * 2, (uint64_t)R.xs[0] * 2};
         int rc = encode_tensor_map(&xm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void *>(in),
@@ -979,9 +982,10 @@ int run_conv_tc(const dp_conv_geom *g, bool dgrad, const void *in, const void *i
     }
     hm = xm;
     if (!dgrad && g->halo > 0) {
-        uint64_t dims[5] = {(uint64_t)(x3 ? pl.Cin / 2 : pl.Cin), (uint64_t)R.Win,
+        uint64_t dims[5] = {(uint64_t)(x3 ? pl.Cin / 6 : pl.Cin), (uint64_t)R.Win,
                             (uint64_t)(R.split == 1 ? g->halo : R.Qin),
-                            (uint64_t)(R.split == 0 ? g->halo : R.Pin), (uint64_t)g->batch};
+                            (uint64_t)(R.split == 0 ? g->halo : R.Pin),
+                            (uint64_t)(x3 ? 3 : 1) * g->batch};
         uint64_t strides[4] = {(uint64_t)R.hs[3] * 2, (uint64_t)R.hs[2] * 2,
                                (uint64_t)R.hs[1] * 2, (uint64_t)R.hs[0] * 2};
         int rc = encode_tensor_map(&hm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5,
@@ -2190,7 +2194,8 @@ int64_t conv_tc_f32out_workspace(const dp_conv_geom *g, bool dgrad) {
     return make_plan(g, dgrad, pl, true, true) ? 2 * (int64_t)pl.wimg_bytes : -1;
 }
 // g describes the 6-block MMA view (c_in or c_out = 6 C); the activation
-// operand holds the 3 parts once (3 C channels, strides in g)
+// operand holds the 3 parts once as batch blocks [3][B][..][C] (strides in g
+// are those of one [B][..][C] block)
 int conv_tc_f32out_launch(const dp_conv_geom *g, bool dgrad, const void *in, const void *in_halo,
                           const void *w, void *out, void *out2, void *ws, int64_t ws_bytes,
                           cudaStream_t st) {

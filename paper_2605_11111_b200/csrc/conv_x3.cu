@@ -9,8 +9,12 @@
 // Those six terms become ONE bf16 convolution with fp32 accumulation in TMEM
 // by concatenating along the contraction:
 //   fwd    channels: X' = [xh xh xh xm xm xl] (6 C_in), W' = [wh wm wl wh wm wh]
-//          (X' is virtual: the operand stores [xh xm xl] once and the conv
-//          kernel's K block b reads part c_xpat[b] — conv_tc.cu X3)
+//          (X' is virtual: the operand stores [xh xm xl] once, as batch
+//          blocks, and the conv kernel's K block b reads part c_xpat[b] —
+//          conv_tc.cu X3; the same split operands feed the wgrad, so the
+//          host splits x once in the forward and dy once in the backward:
+//          dp_conv_x3_split + dp_conv_x3_*_parts, ops.py keeps x's parts
+//          in the conv tape)
 //   dgrad  channels: dY' = [dh dh dh dm dm dl] (6 C_out), W' split on c_out
 //   wgrad  batch:    pairs (xh dh, xm dh, xh dm, xl dh, xm dm, xh dl)
 // (wgrad contracts over positions, so the six pairings are six batch entries
@@ -42,8 +46,6 @@ constexpr int kParts = 6;
 // part index (0 = hi, 1 = mid, 2 = lo) of each concatenated block
 __constant__ int c_xpat[kParts] = {0, 0, 0, 1, 1, 2};   // activations (fwd / dgrad input)
 __constant__ int c_wpat[kParts] = {0, 1, 2, 0, 1, 0};   // weights
-__constant__ int c_ppat[kParts] = {0, 1, 0, 2, 1, 0};   // wgrad X'' (6 blocks, SS fallback)
-__constant__ int c_dpat[kParts] = {0, 0, 1, 0, 1, 2};   // wgrad dY'' (6 blocks, SS fallback)
 __constant__ int c_ipat[kParts] = {0, 1, 2, 0, 0, 0};   // the 3 parts once (wgrad, paired
                                                         // in the kernel: conv_tc.cu kTsPair*)
 
@@ -66,7 +68,7 @@ x3_split_act(const float *__restrict__ x, int64_t B, int64_t C, int64_t S0, int6
              int mode, int which_pat) {
     __shared__ float tile[32][65];
     const int *pat = which_pat == 0 ? c_xpat : which_pat == 1 ? c_ipat
-                     : which_pat == 2 ? c_ppat : c_dpat;
+                     : c_xpat;
     const int nblk = which_pat == 1 ? 3 : kParts;
     const int64_t n1 = (S1 + 63) / 64, nc = (C + 31) / 32;
     int64_t t = blockIdx.x;
@@ -134,10 +136,6 @@ __global__ void x3_split_weight(const float *__restrict__ w, int64_t Co, int64_t
     }
 }
 
-struct X3Layout {
-    int64_t act, act_h, wimg, dy, dy_h, inner, total;   // byte offsets / sizes
-};
-
 int64_t align256(int64_t v) { return (v + 255) & ~int64_t(255); }
 
 // channels-last contiguous strides [b, c, s0, s1] of a [B][S0][S1][C] tensor
@@ -157,20 +155,21 @@ bool x3_shape_ok(const dp_conv_geom *g) {
     return true;
 }
 
-// geometry of the bf16 conv over the split operands
+// Geometry of the bf16 conv over the split operands.  Every split operand is
+// the 3 parts once as batch blocks [3][B][S0][S1][C] channels-last (strides
+// of one [B][..][C] block here); fwd / dgrad contract over the virtual 6 C
+// channel blocks (conv_tc.cu X3), wgrad pairs the parts as 6 batch entries.
 dp_conv_geom x3_geom(const dp_conv_geom *g, int which) {
     dp_conv_geom h = *g;
     const int64_t Hin = g->in_ext[0], Win = g->in_ext[1];
     const int64_t Hout = g->out_ext[0], Wout = g->out_ext[1];
-    // fwd / dgrad: the MMA contracts over 6 C channel blocks, the stored operand
-    // holds the 3 parts once (3 C channels; conv_tc.cu X3)
     if (which == DP_CONV_FWD) {
         h.c_in = kParts * g->c_in;
-        cl_strides(Hin, Win, 3 * g->c_in, h.xs);
-        cl_strides(g->halo, Win, 3 * g->c_in, h.hs);
+        cl_strides(Hin, Win, g->c_in, h.xs);
+        cl_strides(g->halo, Win, g->c_in, h.hs);
     } else if (which == DP_CONV_DGRAD) {
         h.c_out = kParts * g->c_out;
-        cl_strides(Hout, Wout, 3 * g->c_out, h.ys);
+        cl_strides(Hout, Wout, g->c_out, h.ys);
     } else {
         h.batch = kParts * g->batch;
         cl_strides(Hin, Win, g->c_in, h.xs);
@@ -187,33 +186,38 @@ bool x3_wgrad_paired(const dp_conv_geom *g) {
     return conv_wgrad_x3_workspace(&h) >= 0;
 }
 
-X3Layout x3_layout(const dp_conv_geom *g, int which) {
-    X3Layout L{};
-    const int64_t Hin = g->in_ext[0], Win = g->in_ext[1];
-    const int64_t Hout = g->out_ext[0], Wout = g->out_ext[1];
-    const int64_t taps = 9;
-    int64_t off = 0;
-    if (which == DP_CONV_FWD) {
-        L.act = off; off += align256(g->batch * Hin * Win * 3 * g->c_in * 2);
-        L.act_h = off; off += align256(g->batch * g->halo * Win * 3 * g->c_in * 2);
-        L.wimg = off; off += align256(g->c_out * kParts * g->c_in * taps * 2);
-    } else if (which == DP_CONV_DGRAD) {
-        L.dy = off; off += align256(g->batch * Hout * Wout * 3 * g->c_out * 2);
-        L.wimg = off; off += align256(kParts * g->c_out * g->c_in * taps * 2);
-    } else {
-        const int64_t np = x3_wgrad_paired(g) ? 3 : kParts;   // parts once, or 6 pairings
-        L.act = off; off += align256(np * g->batch * Hin * Win * g->c_in * 2);
-        L.act_h = off; off += align256(np * g->batch * g->halo * Win * g->c_in * 2);
-        L.dy = off; off += align256(np * g->batch * Hout * Wout * g->c_out * 2);
-    }
-    L.inner = off;
+// bytes of one split operand (DP_X3_X: x main block, DP_X3_XHALO: the
+// received x halo rows, DP_X3_DY: dy), 3 parts
+int64_t x3_operand_bytes(const dp_conv_geom *g, int operand) {
+    const int64_t Win = g->in_ext[1];
+    if (operand == DP_X3_X) return 3 * g->batch * g->in_ext[0] * Win * g->c_in * 2;
+    if (operand == DP_X3_XHALO) return 3 * g->batch * g->halo * Win * g->c_in * 2;
+    if (operand == DP_X3_DY) return 3 * g->batch * g->out_ext[0] * g->out_ext[1] * g->c_out * 2;
+    return -1;
+}
+
+// workspace of a launch over already-split operands: the weight image (fwd /
+// dgrad) + the tcgen05 kernel's own workspace
+int64_t x3_inner_bytes(const dp_conv_geom *g, int which, int64_t *wimg_bytes) {
     const dp_conv_geom h = x3_geom(g, which);
-    const int64_t in_ws = which != DP_CONV_WGRAD
-                              ? conv_tc_f32out_workspace(&h, which == DP_CONV_DGRAD)
-                              : (x3_wgrad_paired(g) ? conv_wgrad_x3_workspace(&h)
-                                                    : conv_tc_workspace(&h, DP_CONV_WGRAD));
-    L.total = in_ws < 0 ? -1 : off + align256(in_ws);
-    return L;
+    int64_t wimg = 0;
+    int64_t in_ws;
+    if (which == DP_CONV_WGRAD) {
+        if (x3_wgrad_paired(g)) {
+            in_ws = conv_wgrad_x3_workspace(&h);
+        } else {   // SS wgrad over the 6 pairings, materialised from the parts
+            in_ws = conv_tc_eligible(&h, DP_BF16, DP_CONV_WGRAD) ? conv_tc_workspace(&h, DP_CONV_WGRAD)
+                                                                 : -1;
+            wimg = 2 * align256(x3_operand_bytes(g, DP_X3_X)) +
+                   2 * align256(x3_operand_bytes(g, DP_X3_XHALO)) +
+                   2 * align256(x3_operand_bytes(g, DP_X3_DY));    // 6 blocks each
+        }
+    } else {
+        wimg = align256(kParts * g->c_out * g->c_in * 9 * 2);
+        in_ws = conv_tc_f32out_workspace(&h, which == DP_CONV_DGRAD);
+    }
+    if (wimg_bytes) *wimg_bytes = wimg;
+    return in_ws < 0 ? -1 : wimg + align256(in_ws);
 }
 
 int launch_split(const float *x, int64_t B, int64_t C, int64_t S0, int64_t S1, const int64_t *st,
@@ -226,17 +230,88 @@ int launch_split(const float *x, int64_t B, int64_t C, int64_t S0, int64_t S1, c
     return launch_status("x3_split_act");
 }
 
+// operand split: fp32 [B][C][S0][S1] (any strides) -> 3 bf16 parts as batch blocks
+int x3_split_operand(const dp_conv_geom *g, int operand, const void *src, void *parts,
+                     cudaStream_t st) {
+    const int64_t *s = operand == DP_X3_X ? g->xs : operand == DP_X3_XHALO ? g->hs : g->ys;
+    int64_t st4[4] = {s[0], s[1], s[2], s[3]};
+    const int64_t C = operand == DP_X3_DY ? g->c_out : g->c_in;
+    const int64_t S0 = operand == DP_X3_X ? g->in_ext[0]
+                       : operand == DP_X3_XHALO ? g->halo : g->out_ext[0];
+    const int64_t S1 = operand == DP_X3_DY ? g->out_ext[1] : g->in_ext[1];
+    return launch_split((const float *)src, g->batch, C, S0, S1, st4, (__nv_bfloat16 *)parts, 1, 1,
+                        st);
+}
+
+// fwd / dgrad / wgrad over split operands (a / ah / b as the `which` needs)
+int x3_run(const dp_conv_geom *g, int which, const void *a, const void *ah, const void *b,
+           void *out, void *out2, void *ws, int64_t ws_bytes, cudaStream_t st) {
+    int64_t wimg = 0;
+    const int64_t need = x3_inner_bytes(g, which, &wimg);
+    DP_REQUIRE(need >= 0, DP_ERR_UNSUPPORTED, "conv_x3: outside the envelope");
+    DP_REQUIRE(ws_bytes >= need, DP_ERR_INVALID, "conv_x3: workspace too small");
+    uint8_t *w8 = (uint8_t *)ws;
+    const dp_conv_geom h = x3_geom(g, which);
+    int rc;
+    if (which == DP_CONV_WGRAD && x3_wgrad_paired(g))  // a = x parts, ah = x halo parts, b = dy parts
+        return conv_wgrad_x3_launch(&h, a, g->halo > 0 ? ah : nullptr, b, out, ws, ws_bytes, st,
+                                    (int)g->batch);
+    if (which == DP_CONV_WGRAD) {
+        // the 6 pairings (X part c_ppat[k], dY part c_dpat[k]) as batch blocks
+        static const int ppat[kParts] = {0, 1, 0, 2, 1, 0}, dpat[kParts] = {0, 0, 1, 0, 1, 2};
+        const int64_t bx = x3_operand_bytes(g, DP_X3_X) / 3, bxh = x3_operand_bytes(g, DP_X3_XHALO) / 3,
+                      bd = x3_operand_bytes(g, DP_X3_DY) / 3;
+        uint8_t *x6 = w8, *xh6 = x6 + 2 * align256(3 * bx), *d6 = xh6 + 2 * align256(3 * bxh);
+        for (int k = 0; k < kParts; ++k) {
+            DP_CUDA_CHECK(cudaMemcpyAsync(x6 + k * bx, (const uint8_t *)a + ppat[k] * bx, bx,
+                                          cudaMemcpyDeviceToDevice, st));
+            if (g->halo > 0)
+                DP_CUDA_CHECK(cudaMemcpyAsync(xh6 + k * bxh, (const uint8_t *)ah + ppat[k] * bxh, bxh,
+                                              cudaMemcpyDeviceToDevice, st));
+            DP_CUDA_CHECK(cudaMemcpyAsync(d6 + k * bd, (const uint8_t *)b + dpat[k] * bd, bd,
+                                          cudaMemcpyDeviceToDevice, st));
+        }
+        return conv_wgrad_tc_launch(&h, x6, g->halo > 0 ? xh6 : nullptr, d6, out, w8 + wimg,
+                                    ws_bytes - wimg, st);
+    }
+    __nv_bfloat16 *wi = (__nv_bfloat16 *)w8;
+    const int64_t nw = g->c_out * g->c_in * 9;
+    x3_split_weight<<<grid_for(nw, 256, 2), 256, 0, st>>>((const float *)b, g->c_out, g->c_in, 9,
+                                                          wi, which == DP_CONV_DGRAD ? 1 : 0);
+    if ((rc = launch_status("x3_split_weight"))) return rc;
+    if (which == DP_CONV_FWD)     // a = x parts, ah = x halo parts, b = w (fp32), out = y
+        return conv_tc_f32out_launch(&h, false, a, g->halo > 0 ? ah : nullptr, wi, out, nullptr,
+                                     w8 + wimg, ws_bytes - wimg, st);
+    // dgrad: a = dy parts, b = w (fp32), out = dx, out2 = dx halo
+    return conv_tc_f32out_launch(&h, true, a, nullptr, wi, out, out2, w8 + wimg, ws_bytes - wimg,
+                                 st);
+}
+
+// operand layout of the one-call path: the split operands, then the inner workspace
+struct X3Layout {
+    int64_t a, ah, b, inner, total;
+};
+X3Layout x3_layout(const dp_conv_geom *g, int which) {
+    X3Layout L{};
+    int64_t off = 0;
+    if (which != DP_CONV_DGRAD) {
+        L.a = off; off += align256(x3_operand_bytes(g, DP_X3_X));
+        L.ah = off; off += align256(x3_operand_bytes(g, DP_X3_XHALO));
+    }
+    if (which != DP_CONV_FWD) {
+        L.b = off; off += align256(x3_operand_bytes(g, DP_X3_DY));
+    }
+    L.inner = off;
+    const int64_t in = x3_inner_bytes(g, which, nullptr);
+    L.total = in < 0 ? -1 : off + in;
+    return L;
+}
+
 }  // namespace
 
 int conv_x3_eligible(const dp_conv_geom *g, int which) {
     if (!g || !x3_shape_ok(g)) return 0;
-    if (which == DP_CONV_WGRAD) {
-        const dp_conv_geom h = x3_geom(g, which);
-        return (conv_wgrad_x3_workspace(&h) >= 0 || conv_tc_eligible(&h, DP_BF16, DP_CONV_WGRAD))
-                   ? 1 : 0;
-    }
-    const dp_conv_geom h = x3_geom(g, which);
-    return conv_tc_f32out_workspace(&h, which == DP_CONV_DGRAD) >= 0 ? 1 : 0;
+    return x3_inner_bytes(g, which, nullptr) >= 0 ? 1 : 0;
 }
 
 int64_t conv_x3_workspace(const dp_conv_geom *g, int which) {
@@ -244,69 +319,54 @@ int64_t conv_x3_workspace(const dp_conv_geom *g, int which) {
     return x3_layout(g, which).total;
 }
 
+int64_t conv_x3_parts_workspace(const dp_conv_geom *g, int which) {
+    if (!conv_x3_eligible(g, which)) return -1;
+    return x3_inner_bytes(g, which, nullptr);
+}
+
+int64_t conv_x3_operand_bytes(const dp_conv_geom *g, int operand) {
+    if (!g || !x3_shape_ok(g)) return -1;
+    return x3_operand_bytes(g, operand);
+}
+
+int conv_x3_split(const dp_conv_geom *g, int operand, const void *src, void *parts,
+                  cudaStream_t st) {
+    DP_REQUIRE(g && x3_shape_ok(g), DP_ERR_UNSUPPORTED, "conv_x3_split: outside the envelope");
+    DP_REQUIRE(operand == DP_X3_X || operand == DP_X3_XHALO || operand == DP_X3_DY, DP_ERR_INVALID,
+               "conv_x3_split: unknown operand %d", operand);
+    if (x3_operand_bytes(g, operand) == 0) return DP_OK;
+    DP_REQUIRE(src && parts, DP_ERR_INVALID, "conv_x3_split: null buffer");
+    return x3_split_operand(g, operand, src, parts, st);
+}
+
+int conv_x3_parts_launch(const dp_conv_geom *g, int which, const void *a, const void *ah,
+                         const void *b, void *out, void *out2, void *ws, int64_t ws_bytes,
+                         cudaStream_t st) {
+    DP_REQUIRE(conv_x3_eligible(g, which), DP_ERR_UNSUPPORTED, "conv_x3: outside the envelope");
+    return x3_run(g, which, a, ah, b, out, out2, ws, ws_bytes, st);
+}
+
+// one call: split the activation operands into the workspace, then run
 int conv_x3_launch(const dp_conv_geom *g, int which, const void *a, const void *ah, const void *b,
                    void *out, void *out2, void *ws, int64_t ws_bytes, cudaStream_t st) {
     DP_REQUIRE(conv_x3_eligible(g, which), DP_ERR_UNSUPPORTED, "conv_x3: outside the envelope");
     const X3Layout L = x3_layout(g, which);
     DP_REQUIRE(L.total >= 0 && ws_bytes >= L.total, DP_ERR_INVALID, "conv_x3: workspace too small");
     uint8_t *w8 = (uint8_t *)ws;
-    const dp_conv_geom h = x3_geom(g, which);
-    const int64_t Hin = g->in_ext[0], Win = g->in_ext[1];
-    const int64_t Hout = g->out_ext[0], Wout = g->out_ext[1];
     int rc;
-    if (which == DP_CONV_FWD) {            // a = x, ah = x halo, b = w (fp32), out = y
-        __nv_bfloat16 *xa = (__nv_bfloat16 *)(w8 + L.act), *xha = (__nv_bfloat16 *)(w8 + L.act_h);
-        __nv_bfloat16 *wi = (__nv_bfloat16 *)(w8 + L.wimg);
-        int64_t sx[4] = {g->xs[0], g->xs[1], g->xs[2], g->xs[3]};
-        if ((rc = launch_split((const float *)a, g->batch, g->c_in, Hin, Win, sx, xa, 0, 1, st)))
-            return rc;
-        if (g->halo > 0) {
-            int64_t sh[4] = {g->hs[0], g->hs[1], g->hs[2], g->hs[3]};
-            if ((rc = launch_split((const float *)ah, g->batch, g->c_in, g->halo, Win, sh, xha, 0, 1,
-                                   st)))
-                return rc;
-        }
-        const int64_t nw = g->c_out * g->c_in * 9;
-        x3_split_weight<<<grid_for(nw, 256, 2), 256, 0, st>>>((const float *)b, g->c_out, g->c_in, 9,
-                                                              wi, 0);
-        if ((rc = launch_status("x3_split_weight"))) return rc;
-        return conv_tc_f32out_launch(&h, false, xa, g->halo > 0 ? xha : nullptr, wi, out, nullptr,
-                                     w8 + L.inner, ws_bytes - L.inner, st);
+    if (which == DP_CONV_DGRAD) {          // a = dy, b = w
+        if ((rc = x3_split_operand(g, DP_X3_DY, a, w8 + L.b, st))) return rc;
+        return x3_run(g, which, w8 + L.b, nullptr, b, out, out2, w8 + L.inner, ws_bytes - L.inner,
+                      st);
     }
-    if (which == DP_CONV_DGRAD) {          // a = dy, b = w (fp32), out = dx, out2 = dx halo
-        __nv_bfloat16 *da = (__nv_bfloat16 *)(w8 + L.dy), *wi = (__nv_bfloat16 *)(w8 + L.wimg);
-        int64_t sd[4] = {g->ys[0], g->ys[1], g->ys[2], g->ys[3]};
-        if ((rc = launch_split((const float *)a, g->batch, g->c_out, Hout, Wout, sd, da, 0, 1, st)))
-            return rc;
-        const int64_t nw = g->c_out * g->c_in * 9;
-        x3_split_weight<<<grid_for(nw, 256, 2), 256, 0, st>>>((const float *)b, g->c_out, g->c_in, 9,
-                                                              wi, 1);
-        if ((rc = launch_status("x3_split_weight"))) return rc;
-        return conv_tc_f32out_launch(&h, true, da, nullptr, wi, out, out2, w8 + L.inner,
-                                     ws_bytes - L.inner, st);
-    }
-    // wgrad: a = x, ah = x halo, b = dy, out = dw (fp32)
-    __nv_bfloat16 *xa = (__nv_bfloat16 *)(w8 + L.act), *xha = (__nv_bfloat16 *)(w8 + L.act_h);
-    __nv_bfloat16 *da = (__nv_bfloat16 *)(w8 + L.dy);
-    const bool paired = x3_wgrad_paired(g);
-    const int px = paired ? 1 : 2, pd = paired ? 1 : 3;
-    int64_t sx[4] = {g->xs[0], g->xs[1], g->xs[2], g->xs[3]};
-    if ((rc = launch_split((const float *)a, g->batch, g->c_in, Hin, Win, sx, xa, 1, px, st)))
-        return rc;
-    if (g->halo > 0) {
-        int64_t sh[4] = {g->hs[0], g->hs[1], g->hs[2], g->hs[3]};
-        if ((rc = launch_split((const float *)ah, g->batch, g->c_in, g->halo, Win, sh, xha, 1, px,
-                               st)))
-            return rc;
-    }
-    int64_t sd[4] = {g->ys[0], g->ys[1], g->ys[2], g->ys[3]};
-    if ((rc = launch_split((const float *)b, g->batch, g->c_out, Hout, Wout, sd, da, 1, pd, st)))
-        return rc;
-    if (!paired)
-        return conv_wgrad_tc_launch(&h, xa, g->halo > 0 ? xha : nullptr, da, out, w8 + L.inner,
-                                    ws_bytes - L.inner, st);
-    return conv_wgrad_x3_launch(&h, xa, g->halo > 0 ? xha : nullptr, da, out, w8 + L.inner,
-                                ws_bytes - L.inner, st, (int)g->batch);
+    if ((rc = x3_split_operand(g, DP_X3_X, a, w8 + L.a, st))) return rc;
+    if (g->halo > 0 && (rc = x3_split_operand(g, DP_X3_XHALO, ah, w8 + L.ah, st))) return rc;
+    if (which == DP_CONV_FWD)              // b = w
+        return x3_run(g, which, w8 + L.a, w8 + L.ah, b, out, nullptr, w8 + L.inner,
+                      ws_bytes - L.inner, st);
+    if ((rc = x3_split_operand(g, DP_X3_DY, b, w8 + L.b, st))) return rc;   // wgrad: b = dy
+    return x3_run(g, which, w8 + L.a, w8 + L.ah, w8 + L.b, out, nullptr, w8 + L.inner,
+                  ws_bytes - L.inner, st);
 }
 
 }  // namespace dp

@@ -258,6 +258,81 @@ def conv_wgrad(x, x_halo, dy, dw, *, kernel, stride, base, shard, halo_rows) -> 
 
 
 # ---------------------------------------------------------------------------
+# fp32 conv with operands split once (bf16x3, include/dp_b200.h dp_conv_x3_*)
+
+X3_X, X3_XHALO, X3_DY = 0, 1, 2
+
+
+def x3_active(x, x_halo, y_shape, y_strides, c_out, *, kernel, stride, base, shard,
+              halo_rows) -> bool:
+    """True when fp32 convs of this geometry (fwd, dgrad AND wgrad) run on the
+    tensor cores as bf16x3 — then the caller splits x / dy once and uses the
+    *_parts entry points (the CUDA-core algorithm has no split form)."""
+    if x.dtype != torch.float32 or _algo == _lib.ALGO_SIMT:
+        return False
+    g = conv_geom(x, x_halo, y_shape, y_strides, c_out, kernel, stride, base, shard, halo_rows)
+    lib = _lib.load()
+    return all(lib.dp_conv_x3_parts_workspace(ctypes.byref(g), w) >= 0
+               for w in (_lib.CONV_FWD, _lib.CONV_DGRAD, _lib.CONV_WGRAD))
+
+
+def x3_split(t, operand, g) -> torch.Tensor:
+    """The 3 bf16 parts of fp32 operand `t` ([3][B][s0][s1][C] bf16) for geometry g."""
+    require_device("x3_split", t)
+    lib = _lib.load()
+    nbytes = lib.dp_conv_x3_operand_bytes(ctypes.byref(g), operand)
+    if nbytes < 0:
+        _lib.check(_lib.DP_ERR_UNSUPPORTED, "dp_conv_x3_operand_bytes")
+    parts = torch.empty(max(int(nbytes) // 2, 1), dtype=torch.bfloat16, device=t.device)
+    if nbytes:
+        _lib.check(lib.dp_conv_x3_split(ctypes.byref(g), operand, _ptr(t), _ptr(parts),
+                                        _stream(t)), "dp_conv_x3_split")
+    return parts
+
+
+def _x3_ws(g, which, device):
+    nbytes = _lib.load().dp_conv_x3_parts_workspace(ctypes.byref(g), which)
+    if nbytes < 0:
+        _lib.check(_lib.DP_ERR_UNSUPPORTED, "dp_conv_x3_parts_workspace")
+    ws = torch.empty(max(int(nbytes), 16), dtype=torch.uint8, device=device)
+    return ws, int(ws.numel())
+
+
+def conv_fwd_x3(x, x_halo, xp, xhp, w, y, *, kernel, stride, base, shard, halo_rows,
+                out_org=None) -> None:
+    """conv_fwd of fp32 x whose parts xp (and halo parts xhp) are already split."""
+    require_device("conv_fwd_x3", xp, w, y)
+    g = conv_geom(x, x_halo, y.shape, y.stride(), w.shape[0], kernel, stride, base, shard,
+                  halo_rows, out_org)
+    ws, nb = _x3_ws(g, _lib.CONV_FWD, y.device)
+    _lib.check(_lib.load().dp_conv_x3_fwd_parts(ctypes.byref(g), _ptr(xp), _ptr(xhp), _ptr(w),
+                                                _ptr(y), _ptr(ws), nb, _stream(y)),
+               "dp_conv_x3_fwd_parts")
+
+
+def conv_dgrad_x3(dy, dyp, w, dx, dx_halo, *, kernel, stride, base, shard, halo_rows,
+                  out_org=None) -> None:
+    require_device("conv_dgrad_x3", dyp, w, dx, dx_halo)
+    g = conv_geom(dx, dx_halo, dy.shape, dy.stride(), w.shape[0], kernel, stride, base, shard,
+                  halo_rows, out_org)
+    ws, nb = _x3_ws(g, _lib.CONV_DGRAD, dx.device)
+    _lib.check(_lib.load().dp_conv_x3_dgrad_parts(ctypes.byref(g), _ptr(dyp), _ptr(w), _ptr(dx),
+                                                  _ptr(dx_halo), _ptr(ws), nb, _stream(dx)),
+               "dp_conv_x3_dgrad_parts")
+
+
+def conv_wgrad_x3(x, x_halo, xp, xhp, dy, dyp, dw, *, kernel, stride, base, shard,
+                  halo_rows) -> None:
+    require_device("conv_wgrad_x3", xp, dyp, dw)
+    g = conv_geom(x, x_halo, dy.shape, dy.stride(), dw.shape[0], kernel, stride, base, shard,
+                  halo_rows)
+    ws, nb = _x3_ws(g, _lib.CONV_WGRAD, dw.device)
+    _lib.check(_lib.load().dp_conv_x3_wgrad_parts(ctypes.byref(g), _ptr(xp), _ptr(xhp), _ptr(dyp),
+                                                  _ptr(dw), _ptr(ws), nb, _stream(dw)),
+               "dp_conv_x3_wgrad_parts")
+
+
+# ---------------------------------------------------------------------------
 # attention
 
 

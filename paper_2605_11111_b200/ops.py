@@ -154,6 +154,8 @@ class ConvTape:
     batched: bool
     base: tuple                   # per spatial dim window start of output 0
     out: ShardTensor
+    xp: torch.Tensor | None = None   # fp32 on the tensor cores: x's bf16x3 parts (split
+    xhp: torch.Tensor | None = None  # once in the forward, reused by the weight gradient)
 
 
 def _validate_conv(x: ShardTensor, weight):
@@ -230,24 +232,41 @@ def halo_conv_forward(x: ShardTensor, weight, stride=1, padding=0):
     # halo is in flight; the boundary rows follow once it has landed.
     n_int = _interior_rows(mine.n_out, xb.shape[sp + 2], kernel[sp], strides[sp], mine.base) \
         if mine.rw else mine.n_out
+    # fp32 on the tensor cores (bf16x3): split x into its bf16 parts ONCE —
+    # both forward launches and the backward's weight gradient read them
+    xp = xhp = None
+    if yb.numel() and kernels.x3_active(xb, None, yb.shape, yb.stride(), weight.shape[0],
+                                        kernel=kernel, stride=strides, base=base, shard=sp,
+                                        halo_rows=0):
+        xp = kernels.x3_split(xb, kernels.X3_X, kernels.conv_geom(
+            xb, None, yb.shape, yb.stride(), weight.shape[0], kernel, strides, base, sp, 0))
+
+    def conv(xh, yv, bb, rows, ob):
+        if xp is None:
+            kernels.conv_fwd(xb, xh, w, yv, kernel=kernel, stride=strides, base=bb, shard=sp,
+                             halo_rows=rows, out_org=ob)
+        else:
+            kernels.conv_fwd_x3(xb, xh, xp, xhp if rows else None, w, yv, kernel=kernel,
+                                stride=strides, base=bb, shard=sp, halo_rows=rows, out_org=ob)
+
     if yb.numel() and 0 < n_int < mine.n_out:
-        kernels.conv_fwd(xb, None, w, yb.narrow(sp + 2, 0, n_int), kernel=kernel,
-                         stride=strides, base=base, shard=sp, halo_rows=0, out_org=org)
+        conv(None, yb.narrow(sp + 2, 0, n_int), base, 0, org)
     pending.wait()
+    if xp is not None and mine.rw:
+        xhp = kernels.x3_split(halo, kernels.X3_XHALO, kernels.conv_geom(
+            xb, halo, yb.shape, yb.stride(), weight.shape[0], kernel, strides, base, sp, mine.rw))
     if yb.numel() and n_int < mine.n_out:
         bb = list(base)
         bb[sp] = mine.base + n_int * strides[sp]
         ob = list(org)
         ob[sp] += n_int
-        kernels.conv_fwd(xb, halo, w, yb.narrow(sp + 2, n_int, mine.n_out - n_int),
-                         kernel=kernel, stride=strides, base=bb, shard=sp, halo_rows=mine.rw,
-                         out_org=ob)
+        conv(halo, yb.narrow(sp + 2, n_int, mine.n_out - n_int), bb, mine.rw, ob)
     elif yb.numel() and n_int == mine.n_out:
-        kernels.conv_fwd(xb, halo, w, yb, kernel=kernel, stride=strides, base=base, shard=sp,
-                         halo_rows=mine.rw, out_org=org)
+        conv(halo, yb, base, mine.rw, org)
     y = yb if batched else yb[0]
     out = ShardTensor(y, out_global, x.ctx, x.placements, {axis: plan.out_extents})
-    tape = ConvTape(x, w, halo, plan, axis, d, sp, strides, pads, batched, tuple(base), out)
+    tape = ConvTape(x, w, halo, plan, axis, d, sp, strides, pads, batched, tuple(base), out,
+                    xp, xhp)
     return out, tape
 
 
@@ -313,11 +332,21 @@ def halo_conv_backward(tape: ConvTape, dout):
         hshape[dim] = mine.rw
         halo_grad = empty_like_layout(xb, hshape)
     work = mine.n_out and xb.shape[dim] + mine.rw
+    dyp = None
     if work:
         org = [0] * (xb.dim() - 2)            # global index of my dx row 0
         org[tape.sp] = sum(x.shard_shapes[tape.axis][:me])
-        kernels.conv_dgrad(dyb, w, dxb, halo_grad, kernel=kernel, stride=tape.strides,
-                           base=tape.base, shard=tape.sp, halo_rows=mine.rw, out_org=org)
+        if tape.xp is not None:
+            # bf16x3: dy split once, for the data and the weight gradient
+            dyp = kernels.x3_split(dyb, kernels.X3_DY, kernels.conv_geom(
+                dxb, halo_grad, dyb.shape, dyb.stride(), w.shape[0], kernel, tape.strides,
+                tape.base, tape.sp, mine.rw))
+            kernels.conv_dgrad_x3(dyb, dyp, w, dxb, halo_grad, kernel=kernel,
+                                  stride=tape.strides, base=tape.base, shard=tape.sp,
+                                  halo_rows=mine.rw, out_org=org)
+        else:
+            kernels.conv_dgrad(dyb, w, dxb, halo_grad, kernel=kernel, stride=tape.strides,
+                               base=tape.base, shard=tape.sp, halo_rows=mine.rw, out_org=org)
     else:
         kernels.fill(dxb, 0.0)
         kernels.fill(dw, 0.0)
@@ -337,7 +366,11 @@ def halo_conv_backward(tape: ConvTape, dout):
         incoming = empty_like_layout(xb, ishape)
         recvs.append((prv, incoming))
     pending = x.ctx.transport.exchange_start(sends, recvs)
-    if work:
+    if work and dyp is not None:
+        kernels.conv_wgrad_x3(xb, tape.halo, tape.xp, tape.xhp, dyb, dyp, dw, kernel=kernel,
+                              stride=tape.strides, base=tape.base, shard=tape.sp,
+                              halo_rows=mine.rw)
+    elif work:
         kernels.conv_wgrad(xb, tape.halo, dyb, dw, kernel=kernel, stride=tape.strides,
                            base=tape.base, shard=tape.sp, halo_rows=mine.rw)
     pending.wait()
