@@ -392,3 +392,35 @@ def test_conv_fp32_bf16x3_vs_oracle(case):
         assert rel_err(to_np(dw), gw) < 1e-5
     finally:
         k.set_algo(prev)
+
+
+@pytest.mark.parametrize("shape,op", [((2, 32, 5, 256), 0), ((1, 16, 3, 384), 2),
+                                      ((2, 32, 4, 200), 0), ((1, 32, 2, 128), 1)])
+def test_x3_split_parts_bitexact(shape, op):
+    """dp_conv_x3_split: the 3 bf16 parts of every fp32 value, exactly
+    (x = xh + xm + xl, each the bf16 rounding of the remainder), laid out as
+    batch blocks [3][B][s0][s1][C] — float4 tile path (W % 128 == 0) and the
+    scalar tile path (W = 200)."""
+    k = kernels()
+    B, C, S0, S1 = shape
+    g = torch.Generator().manual_seed(sum(shape))
+    x = (torch.randn(shape, generator=g) * torch.logspace(-3, 3, S1)).to(DEV)
+    c_out = 32
+    if op == k.X3_DY:      # dy of a conv with C output channels: geometry over x of c_in = 32
+        xg = torch.empty((B, 32, S0, S1), device=DEV)
+        w_out = C
+        geom = k.conv_geom(xg, None, x.shape, x.stride(), w_out, (3, 3), (1, 1), (-1, -1), 0, 0)
+    elif op == k.X3_XHALO:
+        xg = torch.empty((B, C, 7, S1), device=DEV)
+        geom = k.conv_geom(xg, x, (B, c_out, 7, S1), (7 * S1 * c_out, 1, S1 * c_out, c_out),
+                           c_out, (3, 3), (1, 1), (0, -1), 0, S0)
+    else:
+        geom = k.conv_geom(x, None, (B, c_out, S0, S1), (S0 * S1 * c_out, 1, S1 * c_out, c_out),
+                           c_out, (3, 3), (1, 1), (-1, -1), 0, 0)
+    parts = k.x3_split(x, op, geom).view(3, B, S0, S1, C)
+    xh = x.to(torch.bfloat16)
+    r1 = x - xh.float()
+    xm = r1.to(torch.bfloat16)
+    xl = (r1 - xm.float()).to(torch.bfloat16)
+    want = torch.stack([t.permute(0, 2, 3, 1) for t in (xh, xm, xl)])
+    assert torch.equal(parts.view(torch.int16), want.contiguous().view(torch.int16))
