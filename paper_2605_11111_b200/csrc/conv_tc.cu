@@ -1123,6 +1123,7 @@ struct WgradTcParams {
     int n_wt, n_qc, q_chunk, n_units, n_mt, kt;  // kt = 16-voxel K steps per w' tile
     int nx, nd;                      // X ring slots (plus KQ-1 mirrors) / dY ring depth
     float *partial;                  // [grid][n_mt*128][KW*N]
+    int sdy;                         // dY staged ONCE per row (see wlayout)
 };
 
 struct WLayout {
@@ -1131,17 +1132,26 @@ struct WLayout {
     int xslot, dslot, tail;          // ring slot bytes, garbage tail after the mirrors
 };
 
+// sdy (single dY copy): the dY row is staged ONCE, as kt*16 + KW - 1 rows
+// starting at w' = w0 - (KW - 1), instead of KW copies each shifted by -kw.
+// The B operand N = (a, co), a = KW - 1 - kw, then reads MN swizzle atom a
+// at row a of that box: atoms overlap, one row (LBO = cbd * 2 bytes) apart —
+// the swizzle is a function of the absolute shared address (as for the
+// forward kernel's kw-shifted A), so each atom reads the rows TMA wrote.
+// Needs one channel block (cout <= 64) and a box of <= 256 rows.  Cuts the
+// dY TMA bytes and shared-memory writes KW-fold (cfg4: 768 -> 256 KB per
+// output row, which had pushed the kernel past the smem write + read budget).
 __host__ __device__ inline WLayout wlayout(int cin, int cout, int KP, int KQ, int KW, int kt,
-                                           int n_mt) {
+                                           int n_mt, int sdy = 0) {
     WLayout L;
     L.cbx = chan_block(cin);
     L.nbx = cin / L.cbx;
     L.boxx = (kt * 16 * L.cbx * 2 + 1023) / 1024 * 1024;
     L.cbd = chan_block(cout);
     L.nbd = cout / L.cbd;
-    L.boxd = (kt * 16 * L.cbd * 2 + 1023) / 1024 * 1024;
+    L.boxd = ((kt * 16 + (sdy ? KW - 1 : 0)) * L.cbd * 2 + 1023) / 1024 * 1024;
     L.xslot = KP * L.nbx * L.boxx;
-    L.dslot = KW * L.nbd * L.boxd;
+    L.dslot = (sdy ? 1 : KW) * L.nbd * L.boxd;
     const int over = (n_mt * 128 / L.cbx - KQ * KP * L.nbx) * L.boxx;
     L.tail = over > 0 ? over : 0;
     return L;
@@ -1162,7 +1172,7 @@ conv_wgrad_tc_kernel(const __grid_constant__ CUtensorMap xmap,
     const int KW = kStatic ? KW_ : p.KW;
     const int CIN = kStatic ? CIN_ : p.Cin;
     const int NMT = (KQ * KP * CIN + 127) / 128;
-    const WLayout L = wlayout(CIN, N, KP, KQ, KW, p.kt, NMT);
+    const WLayout L = wlayout(CIN, N, KP, KQ, KW, p.kt, NMT, p.sdy);
     const int NT = KW * N;  // MMA N
     const int NXM = p.nx + KQ - 1;   // physical X slots incl. mirrors
     uint8_t *xring = smem;
@@ -1202,7 +1212,8 @@ conv_wgrad_tc_kernel(const __grid_constant__ CUtensorMap xmap,
         // ===================== TMA producer (whole warp, elected issue) =====================
         uint32_t pxi = 0, pxph = 0, pdi = 0, pdph = 0;   // X / dY ring slots and phases
         const uint32_t xrow = (uint32_t)(KP * L.nbx * WK * L.cbx * 2);
-        const uint32_t dbytes = (uint32_t)(KW * L.nbd * WK * L.cbd * 2);
+        const uint32_t dbytes = p.sdy ? (uint32_t)((WK + KW - 1) * L.cbd * 2)
+                                      : (uint32_t)(KW * L.nbd * WK * L.cbd * 2);
         for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
             int r = u;
             const int wt = r % p.n_wt; r /= p.n_wt;
@@ -1247,10 +1258,13 @@ conv_wgrad_tc_kernel(const __grid_constant__ CUtensorMap xmap,
                     mbar_wait(&dempty[idx], ph ^ 1);
                     mbar_expect_tx_e(&dfull[idx], dbytes);
                     uint8_t *dst = dring + (size_t)idx * L.dslot;
-                    for (int kw = 0; kw < KW; ++kw)
-                        for (int cb = 0; cb < L.nbd; ++cb)
-                            tma_load_5d_e(dst + (size_t)(kw * L.nbd + cb) * L.boxd, &dmap,
-                                          &dfull[idx], cb * L.cbd, w0 - kw, q0 + s, po, b);
+                    if (p.sdy)
+                        tma_load_5d_e(dst, &dmap, &dfull[idx], 0, w0 - (KW - 1), q0 + s, po, b);
+                    else
+                        for (int kw = 0; kw < KW; ++kw)
+                            for (int cb = 0; cb < L.nbd; ++cb)
+                                tma_load_5d_e(dst + (size_t)(kw * L.nbd + cb) * L.boxd, &dmap,
+                                              &dfull[idx], cb * L.cbd, w0 - kw, q0 + s, po, b);
                 }
             }
         }
@@ -1258,7 +1272,8 @@ conv_wgrad_tc_kernel(const __grid_constant__ CUtensorMap xmap,
         // ===================== MMA issuer (whole warp, elected issue) =====================
         const uint32_t idesc = idesc_bf16(128, NT, 1, 1);
         const uint64_t a0 = sdesc_mn(smem_u32(xring), L.boxx, 8 * L.cbx * 2, swz_layout(L.cbx));
-        const uint64_t b0 = sdesc_mn(smem_u32(dring), L.boxd, 8 * L.cbd * 2, swz_layout(L.cbd));
+        const uint64_t b0 = sdesc_mn(smem_u32(dring), p.sdy ? L.cbd * 2 : L.boxd, 8 * L.cbd * 2,
+                                     swz_layout(L.cbd));
         const uint32_t astep = (16 * L.cbx * 2) >> 4;  // one K step = 16 w' rows
         const uint32_t bstep = (16 * L.cbd * 2) >> 4;
         const uint32_t mstep = (128 / L.cbx * L.boxx) >> 4;
@@ -1337,26 +1352,54 @@ conv_wgrad_tc_kernel(const __grid_constant__ CUtensorMap xmap,
     }
 }
 
-// dw[co][ci][kp][kq][kw] = sum_cta partial[cta][row][kw*N + co], row = (kq*KP + kp)*Cin + ci
-__global__ void wgrad_tc_reduce(const float *__restrict__ part, float *__restrict__ dw, int ctas,
-                                int n_mt, int KP, int KQ, int KW, int Cin, int N) {
+constexpr int kRedCols = 32, kRedGroups = 8;   // deterministic partial reductions
+
+// dw[co][ci][kp][kq][kw] = sum_cta partial[cta][row][a*N + co], row = (kq*KP + kp)*Cin + ci,
+// a = kw (a = KW-1-kw with the single dY copy).  Two-level fixed-order sum
+// as wgrad_ts_reduce (32 columns x 8 CTA groups per block).
+__global__ void __launch_bounds__(kRedCols * kRedGroups)
+wgrad_tc_reduce(const float *__restrict__ part, float *__restrict__ dw, int ctas, int n_mt, int KP,
+                int KQ, int KW, int Cin, int N, int sdy) {
+    __shared__ double red[kRedGroups][kRedCols + 1];
     const int NT = KW * N;
     const int total = KQ * KP * Cin * NT;          // real rows, partial layout order (coalesced)
     const size_t per_cta = (size_t)n_mt * 128 * NT;
-    for (int o = blockIdx.x * blockDim.x + threadIdx.x; o < total; o += gridDim.x * blockDim.x) {
+    const int lo = threadIdx.x % kRedCols, g = threadIdx.x / kRedCols;
+    const int o = blockIdx.x * kRedCols + lo;
+    double s = 0.0;
+    if (o < total) {
+        int c = g;
+        for (; c + 3 * kRedGroups < ctas; c += 4 * kRedGroups) {
+            const float a0 = part[(size_t)c * per_cta + o];
+            const float a1 = part[(size_t)(c + kRedGroups) * per_cta + o];
+            const float a2 = part[(size_t)(c + 2 * kRedGroups) * per_cta + o];
+            const float a3 = part[(size_t)(c + 3 * kRedGroups) * per_cta + o];
+            s += (double)a0;
+            s += (double)a1;
+            s += (double)a2;
+            s += (double)a3;
+        }
+        for (; c < ctas; c += kRedGroups) s += (double)part[(size_t)c * per_cta + o];
+    }
+    red[g][lo] = s;
+    __syncthreads();
+    if (g == 0 && o < total) {
+        double t = 0.0;
+#pragma unroll
+        for (int k = 0; k < kRedGroups; ++k) t += red[k][lo];
         const int row = o / NT, col = o % NT;
-        const int kw = col / N, co = col % N;
+        const int a = col / N, co = col % N;
+        const int kw = sdy ? KW - 1 - a : a;
         const int ci = row % Cin, kqkp = row / Cin;
         const int kp = kqkp % KP, kq = kqkp / KP;
-        double s = 0.0;   // fixed order, fp64: deterministic and exact enough for any CTA count
-        for (int c = 0; c < ctas; ++c) s += part[c * per_cta + o];
-        dw[(((co * Cin + ci) * KP + kp) * KQ + kq) * KW + kw] = (float)s;
+        dw[(((co * Cin + ci) * KP + kp) * KQ + kq) * KW + kw] = (float)t;
     }
 }
 
 struct WPlan {
     Roles R;
     int Cin, N, n_mt, kt, n_wt, nx, nd, smem, grid, q_chunk, n_qc;
+    int sdy;
     WLayout L;
     int64_t n_units;
 };
@@ -1384,8 +1427,11 @@ bool make_wplan(const dp_conv_geom *g, WPlan &pl) {
     // smem: X ring (KQ+1..KQ+2 slots, + KQ-1 mirrors + garbage tail), dY ring
     const int budget = 220 * 1024 - 512;
     pl.kt = 0;
+    static const bool sdy_off = getenv("DP_WGRAD_SDY") && getenv("DP_WGRAD_SDY")[0] == '0';
     for (int kt = kt0; kt >= 1 && !pl.kt; --kt) {
-        const WLayout L = wlayout(pl.Cin, pl.N, R.KP, R.KQ, R.KW, kt, pl.n_mt);
+        // one staged dY copy when the channels are one block and the box fits
+        pl.sdy = (!sdy_off && pl.N == chan_block(pl.N) && kt * 16 + R.KW - 1 <= 256) ? 1 : 0;
+        const WLayout L = wlayout(pl.Cin, pl.N, R.KP, R.KQ, R.KW, kt, pl.n_mt, pl.sdy);
         for (int nx = R.KQ + 2; nx >= R.KQ + 1; --nx) {
             const int nd = 3;
             const int need = (nx + R.KQ - 1) * L.xslot + L.tail + nd * L.dslot;
@@ -1493,7 +1539,7 @@ int run_wgrad_tc(const dp_conv_geom *g, const void *x, const void *xh, const voi
                             (uint64_t)g->batch};
         uint64_t strides[4] = {(uint64_t)R.ys[3] * 2, (uint64_t)R.ys[2] * 2,
                                (uint64_t)R.ys[1] * 2, (uint64_t)R.ys[0] * 2};
-        uint32_t dbox[5] = {(uint32_t)L.cbd, wk, 1, 1, 1};
+        uint32_t dbox[5] = {(uint32_t)L.cbd, wk + (pl.sdy ? (uint32_t)R.KW - 1 : 0u), 1, 1, 1};
         int rc = encode_tensor_map(&dm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void *>(dy),
                                    dims, strides, dbox, swz(L.cbd));
         if (rc) return rc;
@@ -1512,6 +1558,7 @@ int run_wgrad_tc(const dp_conv_geom *g, const void *x, const void *xh, const voi
     p.n_mt = pl.n_mt; p.kt = pl.kt;
     p.nx = pl.nx; p.nd = pl.nd;
     p.partial = (float *)ws;
+    p.sdy = pl.sdy;
     int rc;
     switch (pl.N) {
         case 16: rc = launch_wgrad_n<16>(xm, hm, dm, p, pl.grid, pl.smem, st); break;
@@ -1521,9 +1568,8 @@ int run_wgrad_tc(const dp_conv_geom *g, const void *x, const void *xh, const voi
     }
     if (rc) return rc;
     const int total = pl.N * pl.Cin * taps;
-    wgrad_tc_reduce<<<grid_for(total, 256, 4), 256, 0, st>>>((const float *)ws, dw, pl.grid,
-                                                             pl.n_mt, R.KP, R.KQ, R.KW, pl.Cin,
-                                                             pl.N);
+    wgrad_tc_reduce<<<(unsigned)((total + kRedCols - 1) / kRedCols), kRedCols * kRedGroups, 0, st>>>(
+        (const float *)ws, dw, pl.grid, pl.n_mt, R.KP, R.KQ, R.KW, pl.Cin, pl.N, pl.sdy);
     return launch_status("wgrad_tc_reduce");
 }
 
@@ -1922,7 +1968,6 @@ conv_wgrad_ts_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_cons
 // then the 8 partial sums are added in a fixed order: deterministic, and
 // the loads no longer sit behind one serial 148-term dependency chain per
 // thread (was ~41 us per call, latency-bound).
-constexpr int kRedCols = 32, kRedGroups = 8;
 __global__ void __launch_bounds__(kRedCols * kRedGroups)
 wgrad_ts_reduce(const float *__restrict__ part, float *__restrict__ dw, int ctas, int KP, int Cin) {
     __shared__ double red[kRedGroups][kRedCols + 1];
