@@ -18,7 +18,7 @@
 //                l rescaled only when the row max grows by > 2^8: exact, any
 //                reference max gives the same acc/l), P = exp2(.) written as
 //                packed bf16 pairs into its own TMEM columns (no smem round
-//                trip); one exp2 pair in four on the FMA pipe (cubic, POLY);
+//                trip); POLY exp2 pairs in eight on the FMA pipe (cubic);
 //                they load acc into TMEM at the start and write the state
 //                (m, l, acc; LSE for the backward) back at the end.
 // TMEM per tile: S [128 t, +128), P [256 + 64 t, +64), O [384 + 64 t, +64);
@@ -131,7 +131,7 @@ __device__ __forceinline__ float2 ex2_poly2(float2 x) {
     return r;
 }
 
-template <int POLY>  // pairs of every 4 computed on the FMA pipe instead of MUFU
+template <int POLY>  // exp2 pairs of every 8 computed on the FMA pipe instead of MUFU
 __global__ void __launch_bounds__(kFwdThreads, 1)
 attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap kmap,
                    const __grid_constant__ CUtensorMap vmap, const FwdParams p) {
@@ -341,7 +341,7 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
 #pragma unroll
                 for (int i = 0; i < 16; ++i) {
                     float2 x = ffma2(make_float2(s[c * 32 + 2 * i], s[c * 32 + 2 * i + 1]), c2, nm);
-                    if ((i & 3) < POLY) {
+                    if ((i & 7) < POLY) {
                         x = ex2_poly2(x);
                     } else {
                         x.x = ex2(x.x);
@@ -851,14 +851,15 @@ int attn_fwd_update_tc_launch(const dp_attn_geom *g, const void *q, const void *
     p.m = (float *)m;
     p.l = (float *)l;
     p.acc = (float *)acc;
-    static int poly = -1;  // DP_ATTN_POLY: exp2 pairs per 4 on the FMA pipe (tuning knob)
+    static int poly = -1;  // DP_ATTN_POLY: exp2 pairs per 8 on the FMA pipe (tuning knob)
     if (poly < 0) {
         const char *e = getenv("DP_ATTN_POLY");
-        poly = e ? atoi(e) : 1;
-        if (poly < 0 || poly > 2) poly = 1;
+        poly = e ? atoi(e) : 2;
+        if (poly < 0 || poly > 4) poly = 2;
     }
     auto kern = poly == 0 ? attn_fwd_tc_kernel<0> : poly == 1 ? attn_fwd_tc_kernel<1>
-                                                               : attn_fwd_tc_kernel<2>;
+              : poly == 2 ? attn_fwd_tc_kernel<2> : poly == 3 ? attn_fwd_tc_kernel<3>
+                                                  : attn_fwd_tc_kernel<4>;
     DP_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemFwd));
     const int64_t grid = (int64_t)p.n_qt * p.H;
     kern<<<(unsigned)grid, kFwdThreads, kSmemFwd, st>>>(qm, km, vm, p);
