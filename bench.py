@@ -94,6 +94,7 @@ class ClockSampler:
     def __init__(self, gpu: int):
         self.gpu = gpu
         self.samples = []   # (sm_mhz, reasons bitmask)
+        self.power = []     # board power draw, W
         self.max_mhz = None
         self._stop = threading.Event()
         self._nvml = None
@@ -119,6 +120,7 @@ class ClockSampler:
                 sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
                 rs = get_reasons(h) if get_reasons else 0
                 self.samples.append((sm, rs))
+                self.power.append(nv.nvmlDeviceGetPowerUsage(h) / 1000.0)   # W
             except Exception:  # noqa: BLE001 - sampling is best effort
                 pass
             self._stop.wait(0.01)
@@ -150,9 +152,18 @@ class ClockSampler:
                 if bit and rs & bit:
                     reasons.add(name)
         sms = sorted(sm for sm, _ in self.samples)
-        return {"sm_mhz": sms[len(sms) // 2], "sm_max_mhz": self.max_mhz,
-                "sm_min_mhz": sms[0], "reasons": sorted(reasons), "samples": len(sms),
-                "source": "nvml 10 ms"}
+        out = {"sm_mhz": sms[len(sms) // 2], "sm_max_mhz": self.max_mhz,
+               "sm_min_mhz": sms[0], "reasons": sorted(reasons), "samples": len(sms),
+               "source": "nvml 10 ms"}
+        if self.power:
+            pw = sorted(self.power)
+            out.update({"power_w_median": pw[len(pw) // 2], "power_w_max": pw[-1]})
+            try:
+                nv, h = self._nvml
+                out["power_limit_w"] = nv.nvmlDeviceGetEnforcedPowerLimit(h) / 1000.0
+            except Exception:  # noqa: BLE001
+                pass
+        return out
 
 
 # ---------------------------------------------------------------------------

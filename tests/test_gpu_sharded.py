@@ -76,6 +76,11 @@ CONV_SHARDED = [
     ((1, 64, 40, 72), (3, 3), 1, 1, 2, (10, 10, 10, 10), torch.bfloat16, True),
     ((1, 32, 33, 47), (3, 3), 1, 1, 2, (17, 16), torch.float32, False),
     ((2, 3, 16, 18), (3, 3), 2, 1, 3, (5, 6, 7), torch.float32, False),
+    # fp32 on the tensor cores with operands split once (bf16x3 parts in the tape):
+    # c_out 16 (the SS wgrad over materialised pairings) with an empty shard, and
+    # W = 256 (the float4 split path) over 3 uneven shards
+    ((1, 16, 20, 130), (3, 3), 1, 1, 2, (8, 0, 12), torch.float32, False),
+    ((1, 32, 12, 256), (3, 3), 1, 1, 2, (4, 5, 3), torch.float32, False),
     ((1, 4, 10, 12, 9), (3, 3, 3), 1, 1, 3, (4, 2, 6), torch.float64, False),
     ((1, 4, 10, 12, 9), (3, 3, 3), 1, 1, 4, (5, 4, 0), torch.float64, False),
 ]
