@@ -79,7 +79,7 @@ CONV_SHARDED = [
     # fp32 on the tensor cores with operands split once (bf16x3 parts in the tape):
     # c_out 16 (the SS wgrad over materialised pairings) with an empty shard, and
     # W = 256 (the float4 split path) over 3 uneven shards
-    ((1, 16, 20, 130), (3, 3), 1, 1, 2, (8, 0, 12), torch.float32, False),
+    ((1, 16, 20, 130), (3, 3), 1, 1, 2, (8, 12, 0), torch.float32, False),
     ((1, 32, 12, 256), (3, 3), 1, 1, 2, (4, 5, 3), torch.float32, False),
     ((1, 4, 10, 12, 9), (3, 3, 3), 1, 1, 3, (4, 2, 6), torch.float64, False),
     ((1, 4, 10, 12, 9), (3, 3, 3), 1, 1, 4, (5, 4, 0), torch.float64, False),
