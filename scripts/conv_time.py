@@ -18,7 +18,9 @@ dev = torch.device("cuda", 0)
 cl = torch.channels_last_3d
 x = torch.randn((1, ci, G, G, G), device=dev, dtype=torch.bfloat16).contiguous(memory_format=cl)
 w = (torch.randn((co, ci, 3, 3, 3), device=dev) * 0.05).to(torch.bfloat16)
-y = torch.empty((1, co, G, G, G), device=dev, dtype=torch.bfloat16, memory_format=cl)
+# random dY too: zero operands draw less tensor-core power and run faster than
+# the step's real activations
+y = torch.randn((1, co, G, G, G), device=dev, dtype=torch.bfloat16).contiguous(memory_format=cl)
 dw = torch.empty((co, ci, 3, 3, 3), device=dev, dtype=torch.float32)
 kw = dict(kernel=(3, 3, 3), stride=(1, 1, 1), base=[-1, -1, -1], shard=-1, halo_rows=0)
 
