@@ -2207,9 +2207,18 @@ int encode_tensor_map(CUtensorMap *map, CUtensorMapDataType dtype, int rank, voi
         fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
     }
     uint32_t estr[5] = {1, 1, 1, 1, 1};
+    // L2 sector promotion of the TMA reads (DP_TMA_PROMO = 0 / 64 / 128 / 256)
+    static int promo = -1;
+    if (promo < 0) {
+        const char *e = getenv("DP_TMA_PROMO");
+        promo = e ? atoi(e) : 128;
+    }
+    const CUtensorMapL2promotion pr = promo >= 256 ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B
+                                      : promo >= 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+                                      : promo >= 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+                                                    : CU_TENSOR_MAP_L2_PROMOTION_NONE;
     CUresult r = fn(map, dtype, rank, base, dims, strides_bytes, box, estr,
-                    CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle,
-                    CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle, pr, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     DP_REQUIRE(r == CUDA_SUCCESS, DP_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
     return DP_OK;
 }
