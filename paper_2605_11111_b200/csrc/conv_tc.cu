@@ -81,6 +81,7 @@ struct ConvTcParams {
     int64_t ycs, y2cs;        // their channel strides (elements)
     int qorg;                 // global index of output row q = 0 (ring alignment)
     int cperm;                // bf16 output through the coalesced drain (permuted B columns)
+    int Pu;                   // units along P: ceil(Pout / PPN)
 };
 
 // Template arguments KP_/KQ_/KW_/CIN_ = 0 select the runtime-shaped kernel;
@@ -101,9 +102,10 @@ struct ConvTcParams {
 // extension slot into rows L in {0, 1} and zeroes both.  (Without the
 // extension 2 of every 16 rows fell back to per-kq MMAs with the full A
 // operand re-read per kq: +14 % stage time for N = 96, +21 % for N = 48.)
-__host__ __device__ constexpr bool ring_ext(int N) { return 512 / N >= 8; }
-__host__ __device__ constexpr int ring_slots(int N) {
-    return ring_ext(N) ? ((512 / N) < 18 ? (512 / N) : 18) - 2 : ((512 / N) < 16 ? (512 / N) : 16);
+__host__ __device__ constexpr bool ring_ext(int N, int cols = 512) { return cols / N >= 8; }
+__host__ __device__ constexpr int ring_slots(int N, int cols = 512) {
+    return ring_ext(N, cols) ? ((cols / N) < 18 ? (cols / N) : 18) - 2
+                             : ((cols / N) < 16 ? (cols / N) : 16);
 }
 
 // X3: the bf16x3 fp32 path.  The MMA contracts over CIN_ = 6 C channel blocks
@@ -115,7 +117,15 @@ __host__ __device__ constexpr int ring_slots(int N) {
 // and TMA bytes of a materialised 6-block operand.
 __host__ __device__ constexpr int x3_part(int blk) { return blk < 3 ? 0 : blk < 5 ? 1 : 2; }
 
-template <int N, int KP_, int KQ_, int KW_, int CIN_, bool PAIR = false, bool X3 = false>
+// PPN = 2 (P-pair): a unit covers two adjacent output planes.  A stage holds
+// the KP + 1 input rows the two planes need (plane t reads boxes t .. t+KP-1),
+// each plane accumulates in its own TMEM ring (columns [t * 256, +256)), and
+// the epilogue drains both rows of a slot.  Every input row then crosses
+// L2 -> SMEM (KP + 1) / 2 times per plane instead of KP: the TMA input stream
+// the ablations price at ~0.1 ms per fwd / dgrad kernel.  The MMAs, their
+// order per plane and the ring / extension-slot mapping are those of PPN = 1.
+template <int N, int KP_, int KQ_, int KW_, int CIN_, bool PAIR = false, bool X3 = false,
+          int PPN = 1>
 __global__ void __launch_bounds__(kThreads, 1)
 conv_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap hmap,
                const ConvTcParams p) {
@@ -137,18 +147,21 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
     const int KW = kStatic ? KW_ : p.KW;
     const int CIN = kStatic ? CIN_ : p.Cin;
     static_assert(!X3 || (KP_ > 0 && CIN_ % 96 == 0), "X3: static 6-block shapes only");
+    static_assert(PPN == 1 || (KP_ > 0 && KW_ == 3 && !X3), "PPN = 2: static 3-tap shapes only");
+    constexpr int RCOLS = 512 / PPN;         // TMEM columns of one plane's ring
     const int CBLK = X3 ? CIN / 6 : chan_block(CIN);
     const int NBLK = X3 ? 3 : CIN / CBLK;
     const int KPB = CBLK / 16;               // 16-channel MMA steps per block row
     const int KC = CIN / 16;
     const int ROWB = CBLK * 2;               // bytes per voxel row of a box
     const int BOXB = box_bytes(CBLK, KW);
-    constexpr int NSLOT = ring_slots(N);
-    constexpr bool EXT = ring_ext(N);
+    constexpr int NSLOT = ring_slots(N, RCOLS);
+    constexpr bool EXT = ring_ext(N, RCOLS);
     constexpr int NPHYS = EXT ? NSLOT + 2 : NSLOT;
     const bool wrap_ok = EXT && KQ <= 3;     // wrapped rows go to the extension slots
     const int BW = kTileW + KW - 1;
-    const uint32_t stage_bytes = (uint32_t)(KP * NBLK * BOXB);
+    const int NROW = KP + PPN - 1;           // input rows (boxes per channel block) per stage
+    const uint32_t stage_bytes = (uint32_t)(NROW * NBLK * BOXB);
 
     uint8_t *wsm = smem;
     uint8_t *stages = smem + ((p.wimg_bytes + 1023) & ~1023);
@@ -192,7 +205,8 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
         uint32_t z[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) z[i] = 0u;
-        for (int c = 0; c < NPHYS * N; c += 16) tmem_st16(lane_base + c, z);
+        for (int t = 0; t < PPN; ++t)
+            for (int c = 0; c < NPHYS * N; c += 16) tmem_st16(lane_base + t * RCOLS + c, z);
         tmem_wait_st();
     }
     tc_fence_before();
@@ -208,8 +222,8 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
             int r = u;
             const int wt = PAIR ? (r % p.n_wt) * 2 + (int)rank : r % p.n_wt; r /= p.n_wt;
             const int qc = r % p.n_qc; r /= p.n_qc;
-            const int po = r % p.Pout;
-            const int b = r / p.Pout;
+            const int po = (r % p.Pu) * PPN;    // first output plane of the unit
+            const int b = r / p.Pu;
             const int q0 = qc * p.q_chunk, q1 = min(p.Qout, q0 + p.q_chunk);
             const int nrows = (q1 - q0) + KQ - 1;
             const int wc = p.base_w + wt * kTileW;
@@ -222,10 +236,10 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
                     continue;
                 }
                 if (!PAIR || rank == 0)
-                    mbar_expect_tx_e(&full[idx], (uint32_t)((PAIR ? 2 : 1) * KP * NBLK * BW * ROWB));
+                    mbar_expect_tx_e(&full[idx], (uint32_t)((PAIR ? 2 : 1) * NROW * NBLK * BW * ROWB));
                 uint8_t *dst = stages + (size_t)idx * stage_bytes;
                 const int qv = p.base_q + q0 + s;
-                for (int kp = 0; kp < KP; ++kp) {
+                for (int kp = 0; kp < NROW; ++kp) {   // input rows po + 0 .. po + NROW - 1
                     const int pv = p.base_p + po + kp;
                     const CUtensorMap *map = &xmap;
                     int pc = pv, qcrd = qv;
@@ -302,7 +316,7 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
                 const bool merged =
                     s >= KQ - 1 && s < nq && (wrap_ok || (int)(top % NSLOT) >= KQ - 1);
                 if (p.dbg & 2) {
-                } else if (kStatic && KW_ == 3 && (X3 || !(p.dbg & (16 | 32)))) {
+                } else if (kStatic && KW_ == 3 && (X3 || PPN > 1 || !(p.dbg & (16 | 32)))) {
                     // the three kw taps of each (kp, kc) issued as one group (one elect;
                     // measured 4-7 % faster than one elect per MMA)
                     constexpr int CS = CIN_ > 0 ? CIN_ : 16, KQS = KQ_ > 0 ? KQ_ : 1;
@@ -321,13 +335,16 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
                         constexpr uint32_t DBV = decltype(dbt)::value;
                         mma_bf16_x3_lo<DA, DBV, PAIR>(d, alo + aoff16, ahi, b, id);
                     };
+                    // plane t of the unit: its own ring, input boxes t .. t + KP - 1
+#pragma unroll
+                    for (int t = 0; t < PPN; ++t) {
                     if (merged) {
-                        const uint32_t d = tmem + (NSLOT - 1 - top % NSLOT) * N;
+                        const uint32_t d = tmem + t * RCOLS + (NSLOT - 1 - top % NSLOT) * N;
 #pragma unroll
                         for (int kp = 0; kp < KP; ++kp)
 #pragma unroll
                             for (int kc = 0; kc < KC_S; ++kc) {
-                                const uint32_t aoff = (kp * NB + kstore(kc) / KPB_S) * BOXB + (kstore(kc) % KPB_S) * 32;
+                                const uint32_t aoff = ((t + kp) * NB + kstore(kc) / KPB_S) * BOXB + (kstore(kc) % KPB_S) * 32;
                                 const uint32_t boff = ((kp * 3) * KC_S + kc) * BLK;
                                 grp(d, aoff >> 4, bdesc0 + (boff >> 4), idesc_all,
                                     std::integral_constant<uint32_t, DBM>{});
@@ -340,13 +357,14 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
                             const uint32_t row = row_base + j;
                             // the column the merged MMA of this top row would use (ring or
                             // extension slot): identical sums whichever MMA form adds them
-                            const uint32_t d = tmem + (wrap_ok ? NSLOT - 1 - top % NSLOT + kq
-                                                               : NSLOT - 1 - row % NSLOT) * N;
+                            const uint32_t d = tmem + t * RCOLS +
+                                               (wrap_ok ? NSLOT - 1 - top % NSLOT + kq
+                                                        : NSLOT - 1 - row % NSLOT) * N;
 #pragma unroll
                             for (int kp = 0; kp < KP; ++kp)
 #pragma unroll
                                 for (int kc = 0; kc < KC_S; ++kc) {
-                                    const uint32_t aoff = (kp * NB + kstore(kc) / KPB_S) * BOXB + (kstore(kc) % KPB_S) * 32;
+                                    const uint32_t aoff = ((t + kp) * NB + kstore(kc) / KPB_S) * BOXB + (kstore(kc) % KPB_S) * 32;
                                     const uint32_t boff =
                                         PAIR ? kqblk0 + (((kp * 3) * KC_S + kc) * KQS + kq) * kqblk
                                              : ((kp * 3) * KC_S + kc) * BLK + kq * (N / 8) * 256;
@@ -355,6 +373,7 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
                                 }
                         }
                     }
+                    }   // planes t
                 } else if (merged) {
                     const uint32_t d = tmem + (NSLOT - 1 - top % NSLOT) * N;
 #pragma unroll
@@ -428,13 +447,13 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
         };
         // bf16 output through the coalesced drain (fp32 outputs / ablations take the
         // per-lane path below); the halo output part must share the W stride
-        const bool fast = p.cperm && !(p.dbg & 8);
+        const bool fast = p.cperm && (PPN > 1 || !(p.dbg & 8));   // PPN = 2: always
         for (int u = u0; u < p.n_units; u += ustep) {
             int r = u;
             const int wt = PAIR ? (r % p.n_wt) * 2 + (int)rank : r % p.n_wt; r /= p.n_wt;
             const int qc = r % p.n_qc; r /= p.n_qc;
-            const int po = r % p.Pout;
-            const int b = r / p.Pout;
+            const int po = (r % p.Pu) * PPN;    // first output plane of the unit
+            const int b = r / p.Pu;
             const int q0 = qc * p.q_chunk, q1 = min(p.Qout, q0 + p.q_chunk);
             const int w = wt * kTileW + m;
             if (wrap_ok) {   // the MMA warp's alignment rows: drain nothing, free the slot
@@ -456,21 +475,30 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
                 // up once per unit: a row pointer advanced by the Q stride (switching
                 // to the halo output at the split row) + 4 per-voxel offsets.
                 constexpr int NJ = N / 4, U = (N % 32 == 0) ? 8 : 4;
-                __nv_bfloat16 *rowp;
-                int64_t rstep;
-                int jsw = 1 << 30;
-                __nv_bfloat16 *rowp2 = nullptr;
-                if (p.ysplit_dim == 0 && po >= p.ysplit) {
-                    rowp = p.y2 + b * p.y2s[0] + (int64_t)(po - p.ysplit) * p.y2s[1] +
-                           (int64_t)q0 * p.y2s[2];
-                    rstep = p.y2s[2];
-                } else {
-                    rowp = p.y + b * p.ys[0] + (int64_t)po * p.ys[1] + (int64_t)q0 * p.ys[2];
-                    rstep = p.ys[2];
-                    if (p.ysplit_dim == 1) {
-                        jsw = max(0, p.ysplit - q0);
-                        rowp2 = p.y2 + b * p.y2s[0] + (int64_t)po * p.y2s[1] +
-                                (int64_t)(q0 + jsw - p.ysplit) * p.y2s[2];
+                // per plane of the unit: row pointer, Q step, split row (Q-split halo
+                // output), and whether the plane exists (an odd P extent's last pair)
+                __nv_bfloat16 *rowp[PPN], *rowp2[PPN];
+                int64_t rstep[PPN];
+                int jsw[PPN];
+                bool pok[PPN];
+#pragma unroll
+                for (int t = 0; t < PPN; ++t) {
+                    const int pl = po + t;
+                    pok[t] = pl < p.Pout;
+                    jsw[t] = 1 << 30;
+                    rowp2[t] = nullptr;
+                    if (p.ysplit_dim == 0 && pl >= p.ysplit) {
+                        rowp[t] = p.y2 + b * p.y2s[0] + (int64_t)(pl - p.ysplit) * p.y2s[1] +
+                                  (int64_t)q0 * p.y2s[2];
+                        rstep[t] = p.y2s[2];
+                    } else {
+                        rowp[t] = p.y + b * p.ys[0] + (int64_t)pl * p.ys[1] + (int64_t)q0 * p.ys[2];
+                        rstep[t] = p.ys[2];
+                        if (p.ysplit_dim == 1) {
+                            jsw[t] = max(0, p.ysplit - q0);
+                            rowp2[t] = p.y2 + b * p.y2s[0] + (int64_t)pl * p.y2s[1] +
+                                       (int64_t)(q0 + jsw[t] - p.ysplit) * p.y2s[2];
+                        }
                     }
                 }
                 int off[2][2];
@@ -488,74 +516,82 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
                     mbar_wait_sleep(&tfull[slot], eph);
                     next_row();
                     tc_fence_after();
-                    const uint32_t col = lane_base + (NSLOT - 1 - slot) * N;
-                    uint32_t v[2][2][NJ];
+                    uint32_t v[PPN][2][2][NJ];
 #pragma unroll
-                    for (int h = 0; h < 2; ++h)
-#pragma unroll
-                        for (int c0 = 0; c0 < N; c0 += 16) {
-                            uint32_t t[8];
-                            tmem_ld16_16x128b(col + ((uint32_t)(16 * h) << 16) + c0, t);
-#pragma unroll
-                            for (int jj = 0; jj < 4; ++jj) {
-                                v[h][0][c0 / 4 + jj] = t[2 * jj];
-                                v[h][1][c0 / 4 + jj] = t[2 * jj + 1];
-                            }
-                        }
-                    tmem_wait_ld();
-#pragma unroll
-                    for (int c = 0; c < N; c += 16) tmem_st16(col + c, z);
-                    if (wrap_ok && slot >= (uint32_t)(NSLOT - 2)) {
-                        const uint32_t ecol = lane_base + (uint32_t)(2 * NSLOT - 1 - slot) * N;
+                    for (int t = 0; t < PPN; ++t) {
+                        const uint32_t col = lane_base + t * RCOLS + (NSLOT - 1 - slot) * N;
 #pragma unroll
                         for (int h = 0; h < 2; ++h)
 #pragma unroll
                             for (int c0 = 0; c0 < N; c0 += 16) {
-                                uint32_t t[8];
-                                tmem_ld16_16x128b(ecol + ((uint32_t)(16 * h) << 16) + c0, t);
-                                tmem_wait_ld();
+                                uint32_t tt[8];
+                                tmem_ld16_16x128b(col + ((uint32_t)(16 * h) << 16) + c0, tt);
 #pragma unroll
-                                for (int jj = 0; jj < 4; ++jj)
-#pragma unroll
-                                    for (int g = 0; g < 2; ++g)
-                                        v[h][g][c0 / 4 + jj] = __float_as_uint(
-                                            __uint_as_float(v[h][g][c0 / 4 + jj]) +
-                                            __uint_as_float(t[2 * jj + g]));
+                                for (int jj = 0; jj < 4; ++jj) {
+                                    v[t][h][0][c0 / 4 + jj] = tt[2 * jj];
+                                    v[t][h][1][c0 / 4 + jj] = tt[2 * jj + 1];
+                                }
                             }
+                        tmem_wait_ld();
 #pragma unroll
-                        for (int c = 0; c < N; c += 16) tmem_st16(ecol + c, z);
+                        for (int c = 0; c < N; c += 16) tmem_st16(col + c, z);
+                        if (wrap_ok && slot >= (uint32_t)(NSLOT - 2)) {
+                            const uint32_t ecol =
+                                lane_base + t * RCOLS + (uint32_t)(2 * NSLOT - 1 - slot) * N;
+#pragma unroll
+                            for (int h = 0; h < 2; ++h)
+#pragma unroll
+                                for (int c0 = 0; c0 < N; c0 += 16) {
+                                    uint32_t tt[8];
+                                    tmem_ld16_16x128b(ecol + ((uint32_t)(16 * h) << 16) + c0, tt);
+                                    tmem_wait_ld();
+#pragma unroll
+                                    for (int jj = 0; jj < 4; ++jj)
+#pragma unroll
+                                        for (int g = 0; g < 2; ++g)
+                                            v[t][h][g][c0 / 4 + jj] = __float_as_uint(
+                                                __uint_as_float(v[t][h][g][c0 / 4 + jj]) +
+                                                __uint_as_float(tt[2 * jj + g]));
+                                }
+#pragma unroll
+                            for (int c = 0; c < N; c += 16) tmem_st16(ecol + c, z);
+                        }
                     }
                     tmem_wait_st();
                     tc_fence_before();
                     free_slot(slot);
-                    if (j == jsw) {
-                        rowp = rowp2;
-                        rstep = p.y2s[2];
-                    }
 #pragma unroll
-                    for (int h = 0; h < 2; ++h)
+                    for (int t = 0; t < PPN; ++t) {
+                        if (j == jsw[t]) {
+                            rowp[t] = rowp2[t];
+                            rstep[t] = p.y2s[2];
+                        }
+                        if (!pok[t]) continue;
 #pragma unroll
-                        for (int g = 0; g < 2; ++g) {
-                            __nv_bfloat16 *dst = rowp + off[h][g];
+                        for (int h = 0; h < 2; ++h)
 #pragma unroll
-                            for (int k = 0; k < NJ / U; ++k) {
-                                const uint32_t *a = &v[h][g][k * U];
-                                if constexpr (U == 8) {
-                                    uint4 pk;
-                                    pk.x = pack_bf16(__uint_as_float(a[0]), __uint_as_float(a[1]));
-                                    pk.y = pack_bf16(__uint_as_float(a[2]), __uint_as_float(a[3]));
-                                    pk.z = pack_bf16(__uint_as_float(a[4]), __uint_as_float(a[5]));
-                                    pk.w = pack_bf16(__uint_as_float(a[6]), __uint_as_float(a[7]));
-                                    if (ok[h][g]) *reinterpret_cast<uint4 *>(dst + 4 * U * k) = pk;
-                                } else {
-                                    uint2 pk;
-                                    pk.x = pack_bf16(__uint_as_float(a[0]), __uint_as_float(a[1]));
-                                    pk.y = pack_bf16(__uint_as_float(a[2]), __uint_as_float(a[3]));
-                                    if (ok[h][g]) *reinterpret_cast<uint2 *>(dst + 4 * U * k) = pk;
+                            for (int g = 0; g < 2; ++g) {
+                                __nv_bfloat16 *dst = rowp[t] + off[h][g];
+#pragma unroll
+                                for (int k = 0; k < NJ / U; ++k) {
+                                    const uint32_t *a = &v[t][h][g][k * U];
+                                    if constexpr (U == 8) {
+                                        uint4 pk;
+                                        pk.x = pack_bf16(__uint_as_float(a[0]), __uint_as_float(a[1]));
+                                        pk.y = pack_bf16(__uint_as_float(a[2]), __uint_as_float(a[3]));
+                                        pk.z = pack_bf16(__uint_as_float(a[4]), __uint_as_float(a[5]));
+                                        pk.w = pack_bf16(__uint_as_float(a[6]), __uint_as_float(a[7]));
+                                        if (ok[h][g]) *reinterpret_cast<uint4 *>(dst + 4 * U * k) = pk;
+                                    } else {
+                                        uint2 pk;
+                                        pk.x = pack_bf16(__uint_as_float(a[0]), __uint_as_float(a[1]));
+                                        pk.y = pack_bf16(__uint_as_float(a[2]), __uint_as_float(a[3]));
+                                        if (ok[h][g]) *reinterpret_cast<uint2 *>(dst + 4 * U * k) = pk;
+                                    }
                                 }
                             }
-                        }
-                    rowp += rstep;
+                        rowp[t] += rstep[t];
+                    }
                 }
                 continue;
             }
@@ -816,9 +852,11 @@ struct Plan {
     int Cin, N;           // K channels, N channels of this conv
     int cblk, stage_bytes, wimg_bytes, nstage, smem;
     bool x3;              // 6-block K over a 3-part activation (the bf16x3 path)
+    int ppn;              // output planes per unit (2: P-pair, two TMEM rings)
 };
 
-bool make_plan(const dp_conv_geom *g, bool dgrad, Plan &pl, bool f32out = false, bool x3 = false) {
+bool make_plan(const dp_conv_geom *g, bool dgrad, Plan &pl, bool f32out = false, bool x3 = false,
+               bool allow_pp = true) {
     if (!map_roles(g, dgrad, pl.R)) return false;
     pl.Cin = (int)(dgrad ? g->c_out : g->c_in);
     pl.N = pick_n((int)(dgrad ? g->c_in : g->c_out));
@@ -844,7 +882,13 @@ bool make_plan(const dp_conv_geom *g, bool dgrad, Plan &pl, bool f32out = false,
         return false;
     pl.x3 = x3;
     pl.cblk = x3 ? pl.Cin / 6 : chan_block(pl.Cin);       // X3: one box per stored part
-    pl.stage_bytes = R.KP * (x3 ? 3 : pl.Cin / pl.cblk) * box_bytes(pl.cblk, R.KW);
+    // P-pair units for the hot 3-D shapes with a bf16 output: each input row then
+    // crosses L2 -> SMEM twice per two planes instead of three times per plane
+    static const bool pp_off = getenv("DP_CONV_PP") && getenv("DP_CONV_PP")[0] == '0';
+    pl.ppn = (allow_pp && !pp_off && !x3 && !f32out && R.nsp == 3 && R.KP == 3 && R.KQ == 3 && R.KW == 3 &&
+              (pl.Cin == 16 || pl.Cin == 32) && (pl.N == 16 || pl.N == 32) && R.Pout >= 2 &&
+              R.KQ + 2 <= ring_slots(pl.N, 256)) ? 2 : 1;
+    pl.stage_bytes = (R.KP + pl.ppn - 1) * (x3 ? 3 : pl.Cin / pl.cblk) * box_bytes(pl.cblk, R.KW);
     pl.wimg_bytes = R.KP * R.KQ * R.KW * pl.Cin * pl.N * 2;
     const int budget = 220 * 1024;
     const int fixed = ((pl.wimg_bytes + 1023) & ~1023) + 1024;
@@ -859,20 +903,20 @@ bool make_plan(const dp_conv_geom *g, bool dgrad, Plan &pl, bool f32out = false,
     return true;
 }
 
-template <int N, int KP, int KQ, int KW, int CIN, bool X3 = false>
+template <int N, int KP, int KQ, int KW, int CIN, bool X3 = false, int PPN = 1>
 int launch_k(const CUtensorMap &xm, const CUtensorMap &hm, const ConvTcParams &p, int grid,
              int smem, cudaStream_t st) {
-    auto kern = conv_tc_kernel<N, KP, KQ, KW, CIN, false, X3>;
+    auto kern = conv_tc_kernel<N, KP, KQ, KW, CIN, false, X3, PPN>;
     DP_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     kern<<<grid, kThreads, smem, st>>>(xm, hm, p);
     return launch_status("conv_tc_kernel");
 }
 
 // CTA-pair instantiation: (2, 1, 1) clusters, grid = 2 x clusters
-template <int N, int KP, int KQ, int KW, int CIN, bool X3 = false>
+template <int N, int KP, int KQ, int KW, int CIN, bool X3 = false, int PPN = 1>
 int launch_k_pair(const CUtensorMap &xm, const CUtensorMap &hm, const ConvTcParams &p, int grid,
                   int smem, cudaStream_t st) {
-    auto kern = conv_tc_kernel<N, KP, KQ, KW, CIN, true, X3>;
+    auto kern = conv_tc_kernel<N, KP, KQ, KW, CIN, true, X3, PPN>;
     DP_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)grid);
@@ -950,6 +994,9 @@ int run_conv_tc(const dp_conv_geom *g, bool dgrad, const void *in, const void *i
     // the halo output part shares the main part's W stride
     const bool split_out = dgrad && g->halo > 0 && g->shard == 0;
     const int cperm = (!f32out && (!split_out || R.hs[3] == R.ys[3])) ? 1 : 0;
+    if (pl.ppn > 1 && !cperm)   // P-pair units drain through the coalesced epilogue only
+        DP_REQUIRE(make_plan(g, dgrad, pl, f32out, x3, false), DP_ERR_UNSUPPORTED,
+                   "conv_tc: outside the envelope");
     // weight image
     {
         int total = taps * pl.Cin * pl.N;
@@ -1023,13 +1070,14 @@ int run_conv_tc(const dp_conv_geom *g, bool dgrad, const void *in, const void *i
         p.ysplit = R.split == 0 ? (int)g->in_ext[0] : (int)g->in_ext[0];
     }
     {
-        const int64_t ns = ring_slots(pl.N), q = g->nsp == 3 ? g->out_org[1] : g->out_org[0];
+        const int64_t ns = ring_slots(pl.N, 512 / pl.ppn), q = g->nsp == 3 ? g->out_org[1] : g->out_org[0];
         p.qorg = (int)(((q % ns) + ns) % ns);
     }
     p.n_wt = use_pair ? (n_wt_all + 1) / 2 : n_wt_all;   // PAIR: tile pairs
     // choose the Q chunk so the unit count balances well over the SMs (pairs)
     const int sms = use_pair ? sm_count() / 2 : sm_count();
-    const int64_t cols = (int64_t)p.B * R.Pout * p.n_wt;
+    p.Pu = (R.Pout + pl.ppn - 1) / pl.ppn;
+    const int64_t cols = (int64_t)p.B * p.Pu * p.n_wt;
     int best_chunk = R.Qout;
     double best = -1;
     for (int nq = 1; nq <= R.Qout && nq <= 64; ++nq) {
@@ -1060,6 +1108,21 @@ int run_conv_tc(const dp_conv_geom *g, bool dgrad, const void *in, const void *i
         p.dbg = dbg;
     }
     int grid = p.n_units < sms ? p.n_units : sms;
+    if (pl.ppn == 2) {   // P-pair units (3-D 3x3x3, bf16 out, C 16 / 32)
+        const bool c16 = pl.Cin == 16;
+        if (use_pair) {
+            if (pl.N == 16)
+                return c16 ? launch_k_pair<16, 3, 3, 3, 16, false, 2>(xm, hm, p, 2 * grid, pl.smem, st)
+                           : launch_k_pair<16, 3, 3, 3, 32, false, 2>(xm, hm, p, 2 * grid, pl.smem, st);
+            return c16 ? launch_k_pair<32, 3, 3, 3, 16, false, 2>(xm, hm, p, 2 * grid, pl.smem, st)
+                       : launch_k_pair<32, 3, 3, 3, 32, false, 2>(xm, hm, p, 2 * grid, pl.smem, st);
+        }
+        if (pl.N == 16)
+            return c16 ? launch_k<16, 3, 3, 3, 16, false, 2>(xm, hm, p, grid, pl.smem, st)
+                       : launch_k<16, 3, 3, 3, 32, false, 2>(xm, hm, p, grid, pl.smem, st);
+        return c16 ? launch_k<32, 3, 3, 3, 16, false, 2>(xm, hm, p, grid, pl.smem, st)
+                   : launch_k<32, 3, 3, 3, 32, false, 2>(xm, hm, p, grid, pl.smem, st);
+    }
     if (pl.x3) {   // N (output channels) and K (6 x the contracted channels) vary independently
         const bool k96 = pl.Cin == 96;
         if (use_pair) {
