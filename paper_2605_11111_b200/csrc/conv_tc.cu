@@ -2124,7 +2124,9 @@ bool make_tsplan(const dp_conv_geom *g, TsPlan &pl, bool fp32 = false) {
     static const int nd = getenv("DP_WGRAD_ND") ? atoi(getenv("DP_WGRAD_ND")) : 4;
     pl.nd = nd;
     pl.nx = (budget - pl.nd * kTsDSlot) / pl.xslot - (3 - 1);
-    if (pl.nx > 8) pl.nx = 8;
+    // X ring depth: the KQ-1 mirrored slots cost 2/nx extra X loads (L1 wgrad 0.504 -> 0.494 ms at 12)
+    static const int nx_cap = getenv("DP_WGRAD_NX") ? atoi(getenv("DP_WGRAD_NX")) : 12;
+    if (pl.nx > nx_cap) pl.nx = nx_cap;
     if (pl.nx < 4) return false;
     pl.smem = (pl.nx + 2) * pl.xslot + pl.nd * kTsDSlot + 512;
     // useful w' columns: X real there (padding columns contribute zero)
