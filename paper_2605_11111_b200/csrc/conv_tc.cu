@@ -1652,8 +1652,9 @@ int run_wgrad_tc(const dp_conv_geom *g, const void *x, const void *xh, const voi
 // staged dY row (rows w' - kw, re-ordered {0,1,4,5,..} / {2,3,6,7,..} so the
 // transposed fragment IS the tcgen05 16x256b fragment) and one
 // tcgen05.st.16x256b.  Lanes 96..127 are junk rows (never reduced).
-// X rows come through the same mirrored TMA ring as the SS kernel (the KQ
-// rows j..j+2 of output row j are adjacent boxes, one uniform-LBO operand).
+// X rows come through a TMA ring like the SS kernel's (the KQ rows j..j+2 of
+// output row j are adjacent slots, one uniform-LBO operand; a row whose KQ
+// slots wrap past the ring end issues its B as two MMAs — no mirrored slots).
 // Only the w' range where X is real is visited (the zero padding columns
 // contribute nothing), so 256-wide rows are exactly two 128-voxel tiles.
 constexpr int kTsCo = 32, kTsKT = 8, kTsWK = kTsKT * 16;
@@ -1735,7 +1736,11 @@ conv_wgrad_ts_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_cons
     extern __shared__ __align__(1024) uint8_t smem[];
     const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);   // warp-uniform for ptxas
     const int lane = threadIdx.x & 31;
-    const int NXM = p.nx + KQ - 1;
+    // X ring: nx slots, no mirrored copies — an output row whose KQ input rows
+    // wrap past the last slot issues its B operand as two MMAs (before / after
+    // the wrap) instead of reading mirrored slots (those cost 2 / nx extra X
+    // loads: 40 % of the X stream for the L2 shape's 5-slot ring)
+    const int NXM = p.nx;
     uint8_t *xring = smem;
     uint8_t *dring = smem + (size_t)NXM * S::XSLOT;
     uint64_t *bars = reinterpret_cast<uint64_t *>(dring + (size_t)p.nd * kTsDSlot);
@@ -1800,13 +1805,12 @@ conv_wgrad_ts_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_cons
                 {
                     const uint32_t idx = pxi, ph = pxph;
                     if (++pxi == (uint32_t)p.nx) { pxi = 0; pxph ^= 1u; }
-                    const bool mirror = (int)idx < KQ - 1;
                     mbar_wait(&xempty[idx], ph ^ 1);
                     if (p.dbg & 4) {
                         if (lane == 0) mbar_arrive(&xfull[idx]);
                         __syncwarp();
                     } else {
-                    mbar_expect_tx_e(&xfull[idx], mirror ? 2 * xrow : xrow);
+                    mbar_expect_tx_e(&xfull[idx], xrow);
                     const int qv = p.base_q + q0 + s;
 #pragma unroll
                     for (int kp = 0; kp < KP; ++kp) {
@@ -1825,9 +1829,6 @@ conv_wgrad_ts_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_cons
                             const size_t off = (size_t)(kp * S::NBX + cb) * S::BOXX;
                             tma_load_5d_e(xring + (size_t)idx * S::XSLOT + off, map, &xfull[idx],
                                           cb * S::CBX, p.base_w + w0, qcrd, pc, bx);
-                            if (mirror)
-                                tma_load_5d_e(xring + (size_t)(p.nx + idx) * S::XSLOT + off, map,
-                                              &xfull[idx], cb * S::CBX, p.base_w + w0, qcrd, pc, bx);
                         }
                     }
                     }
@@ -1885,6 +1886,7 @@ conv_wgrad_ts_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_cons
                 tc_fence_after();
                 const uint64_t bx = b0 + ((xs * S::XSLOT) >> 4);
                 const uint32_t acol = tmem + ACOL + ca * S::ACOLS;
+                if (xs + KQ - 1 < (uint32_t)p.nx) {   // the KQ rows are adjacent slots
 #pragma unroll
                 for (int ks = 0; ks < kTsKT; ++ks) {
                     if (p.dbg & 2) break;
@@ -1896,6 +1898,18 @@ conv_wgrad_ts_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_cons
                         mma_ts_e(dcol + c * S::APC * S::CBX, acol + ks * 8,
                                  bx + ((c * S::APC * S::BOXX) >> 4) + ks * bstep,
                                  idesc_bf16(128, atoms * S::CBX, 0, 1), acc);
+                    }
+                }
+                } else {   // wrap: atoms of slots xs .. nx-1, then of slots 0 ..
+                    const int aw = (int)(p.nx - xs) * KP * S::NBX;
+                    const uint32_t id1 = idesc_bf16(128, aw * S::CBX, 0, 1);
+                    const uint32_t id2 = idesc_bf16(128, (S::NATOM - aw) * S::CBX, 0, 1);
+#pragma unroll
+                    for (int ks = 0; ks < kTsKT; ++ks) {
+                        if (p.dbg & 2) break;
+                        const uint32_t acc = (fresh && ks == 0) ? 0u : 1u;
+                        mma_ts_e(dcol, acol + ks * 8, bx + ks * bstep, id1, acc);
+                        mma_ts_e(dcol + aw * S::CBX, acol + ks * 8, b0 + ks * bstep, id2, acc);
                     }
                 }
                 fresh = false;
@@ -2123,12 +2137,12 @@ bool make_tsplan(const dp_conv_geom *g, TsPlan &pl, bool fp32 = false) {
     const int budget = 220 * 1024 - 512;
     static const int nd = getenv("DP_WGRAD_ND") ? atoi(getenv("DP_WGRAD_ND")) : 4;
     pl.nd = nd;
-    pl.nx = (budget - pl.nd * kTsDSlot) / pl.xslot - (3 - 1);
-    // X ring depth: the KQ-1 mirrored slots cost 2/nx extra X loads (L1 wgrad 0.504 -> 0.494 ms at 12)
+    pl.nx = (budget - pl.nd * kTsDSlot) / pl.xslot;
+    // X ring depth (L1 wgrad 0.504 -> 0.494 ms at 12, measured with mirrored slots)
     static const int nx_cap = getenv("DP_WGRAD_NX") ? atoi(getenv("DP_WGRAD_NX")) : 12;
     if (pl.nx > nx_cap) pl.nx = nx_cap;
     if (pl.nx < 4) return false;
-    pl.smem = (pl.nx + 2) * pl.xslot + pl.nd * kTsDSlot + 512;
+    pl.smem = pl.nx * pl.xslot + pl.nd * kTsDSlot + 512;
     // useful w' columns: X real there (padding columns contribute zero)
     const int wr = R.Wout + 3 - 1;
     pl.w_lo = R.base_w < 0 ? -R.base_w : 0;
