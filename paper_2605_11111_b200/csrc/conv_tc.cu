@@ -936,8 +936,10 @@ int launch_k_pair(const CUtensorMap &xm, const CUtensorMap &hm, const ConvTcPara
 
 // shapes with a CTA-pair instantiation (the hot, statically unrolled ones)
 bool pair_shape(int N, int KP, int KQ, int KW, int Cin) {
-    if (!(N == 16 || N == 32)) return false;
     const bool k333 = KP == 3 && KQ == 3 && KW == 3, k133 = KP == 1 && KQ == 3 && KW == 3;
+    static const bool p64_off = getenv("DP_CONV_PAIR64") && getenv("DP_CONV_PAIR64")[0] == '0';
+    if (N == 64) return !p64_off && k133 && Cin == 64;   // cfg4's 2-D 64 -> 64 layers
+    if (!(N == 16 || N == 32)) return false;
     return (k333 && (Cin == 16 || Cin == 32)) ||
            (k133 && (Cin == 32 || Cin == 64 || Cin == 96 || Cin == 192));
 }
@@ -1140,7 +1142,8 @@ int run_conv_tc(const dp_conv_geom *g, bool dgrad, const void *in, const void *i
     }
     if (use_pair)
         return pl.N == 16 ? launch_n_pair<16>(xm, hm, p, 2 * grid, pl.smem, st)
-                          : launch_n_pair<32>(xm, hm, p, 2 * grid, pl.smem, st);
+               : pl.N == 32 ? launch_n_pair<32>(xm, hm, p, 2 * grid, pl.smem, st)
+                            : launch_k_pair<64, 1, 3, 3, 64>(xm, hm, p, 2 * grid, pl.smem, st);
     switch (pl.N) {
         case 16: return launch_n<16>(xm, hm, p, grid, pl.smem, st);
         case 32: return launch_n<32>(xm, hm, p, grid, pl.smem, st);

@@ -207,6 +207,12 @@ TC_CASES = [
     (2, 1, 32, 32, (6, 256), 3, 1, 0),
     (3, 2, 16, 16, (3, 3, 181), 3, 1, 1),
     (2, 2, 16, 32, (5, 170), 3, 1, 3),
+    # 64 -> 64 2-D rows of 200..256 voxels: the N = 64 CTA-pair fwd / dgrad (cfg4's layers)
+    (2, 1, 64, 64, (6, 256), 3, 1, 2),
+    (2, 2, 64, 64, (5, 200), 3, 1, 0),
+    # 3-D odd output-plane counts with a halo: the P-pair units' last, half-empty pair
+    (3, 1, 16, 32, (5, 4, 256), 3, 1, 2),
+    (3, 1, 32, 16, (3, 6, 140), 3, 1, 1),
 ]
 
 
