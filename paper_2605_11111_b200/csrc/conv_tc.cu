@@ -124,19 +124,9 @@ __host__ __device__ constexpr int x3_part(int blk) { return blk < 3 ? 0 : blk < 
 // L2 -> SMEM (KP + 1) / 2 times per plane instead of KP: the TMA input stream
 // the ablations price at ~0.1 ms per fwd / dgrad kernel.  The MMAs, their
 // order per plane and the ring / extension-slot mapping are those of PPN = 1.
-// TSA (the 3-D 32 -> 16 dgrad, P-pair, single CTA): the A operand comes from
-// TMEM.  SS MMAs of N = KQ * 16 = 48 read 4 KB of A per 16-channel step from
-// shared memory against 24 cycles of math (operand-bound at ~0.55); here eight
-// stager warps (two groups, alternate boxes) load each staged input row's three
-// kw-shifted copies with conflict-free swizzled 16-B loads and tcgen05.st them
-// into a TMEM A ring (48 columns per box), and
-// the MMA warp issues TS MMAs that read only B from shared memory.  The
-// stagers also release the shared-memory stage (the tensor core never reads
-// it).  Two 128-column accumulator rings (6 + 2 extension slots of N = 16)
-// leave 256 columns for 5 A boxes.
 template <int N, int KP_, int KQ_, int KW_, int CIN_, bool PAIR = false, bool X3 = false,
-          int PPN = 1, int TSA = 0>
-__global__ void __launch_bounds__(TSA == 1 ? kThreads + 256 : kThreads, 1)
+          int PPN = 1>
+__global__ void __launch_bounds__(kThreads, 1)
 conv_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap hmap,
                const ConvTcParams p) {
     using namespace tc;
@@ -158,11 +148,7 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
     const int CIN = kStatic ? CIN_ : p.Cin;
     static_assert(!X3 || (KP_ > 0 && CIN_ % 96 == 0), "X3: static 6-block shapes only");
     static_assert(PPN == 1 || (KP_ > 0 && KW_ == 3 && !X3), "PPN = 2: static 3-tap shapes only");
-    static_assert(TSA == 0 || ((TSA == 1 || !PAIR) && PPN == 2 && N == 16 && CIN_ == 32 && KQ_ == 3),
-                  "TSA: the single-CTA P-pair 32 -> 16 shape");
-    constexpr int NTHR = TSA == 1 ? kThreads + 256 : kThreads;
-    constexpr int RCOLS = TSA ? 128 : 512 / PPN;   // TMEM columns of one plane's ring
-    constexpr int TS_ACOL = 256, TS_NA = 5, TS_ABOX = 48;   // TSA: A ring (kw x 16 columns per box)
+    constexpr int RCOLS = 512 / PPN;         // TMEM columns of one plane's ring
     const int CBLK = X3 ? CIN / 6 : chan_block(CIN);
     const int NBLK = X3 ? 3 : CIN / CBLK;
     const int KPB = CBLK / 16;               // 16-channel MMA steps per block row
@@ -182,30 +168,24 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
     uint64_t *bars = reinterpret_cast<uint64_t *>(stages + (size_t)p.nstage * stage_bytes);
     uint64_t *full = bars, *empty = bars + p.nstage;
     uint64_t *tfull = empty + p.nstage, *tempty = tfull + NSLOT;
-    uint64_t *afull = tempty + NSLOT, *aempty = afull + TS_NA;   // TSA: A ring hand-off
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(TSA ? aempty + TS_NA : tempty + NSLOT);
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + NSLOT);
 
     // weights: global image -> smem once per CTA (generic proxy), then fence
     // (PAIR: this CTA's half of the B columns, image [rank][...])
     const uint8_t *wsrc = reinterpret_cast<const uint8_t *>(p.wimg) + (size_t)rank * p.wimg_bytes;
-    for (int i = threadIdx.x * 16; i < p.wimg_bytes; i += NTHR * 16)
+    for (int i = threadIdx.x * 16; i < p.wimg_bytes; i += kThreads * 16)
         *reinterpret_cast<int4 *>(wsm + i) = *reinterpret_cast<const int4 *>(wsrc + i);
     fence_async_smem();
     if (warp == 0) {
         if (lane == 0) {
             for (int i = 0; i < p.nstage; ++i) {
                 mbar_init(&full[i], 1);
-                mbar_init(&empty[i], TSA == 1 ? 8 : 1);  // TSA 1: released by the 8 stager warps
+                mbar_init(&empty[i], 1);
             }
             for (int i = 0; i < NSLOT; ++i) {
                 mbar_init(&tfull[i], 1);
                 mbar_init(&tempty[i], PAIR ? 8 : 128);   // PAIR: one arrival per warp x 2 CTAs
             }
-            if constexpr (TSA)
-                for (int i = 0; i < TS_NA; ++i) {
-                    mbar_init(&afull[i], PAIR ? 8 : 4);   // one group x (2) CTAs
-                    mbar_init(&aempty[i], 1);
-                }
             mbar_fence_init();
             tma_prefetch(&xmap);
             tma_prefetch(&hmap);
@@ -219,7 +199,7 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
     if constexpr (PAIR) cluster_sync();
     tc_fence_after();
     const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);   // uniform for ptxas
-    if (warp >= 2 && warp < 6) {
+    if (warp >= 2) {
         // every accumulator slot starts at zero (MMAs always accumulate)
         const uint32_t lane_base = tmem + ((uint32_t)((warp & 3) * 32) << 16);
         uint32_t z[16];
@@ -255,10 +235,8 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
                     __syncwarp();
                     continue;
                 }
-                // (TSA: each CTA's stagers read their own stage -> per-CTA barriers)
-                if (TSA || !PAIR || rank == 0)
-                    mbar_expect_tx_e(&full[idx],
-                                     (uint32_t)((PAIR && !TSA ? 2 : 1) * NROW * NBLK * BW * ROWB));
+                if (!PAIR || rank == 0)
+                    mbar_expect_tx_e(&full[idx], (uint32_t)((PAIR ? 2 : 1) * NROW * NBLK * BW * ROWB));
                 uint8_t *dst = stages + (size_t)idx * stage_bytes;
                 const int qv = p.base_q + q0 + s;
                 for (int kp = 0; kp < NROW; ++kp) {   // input rows po + 0 .. po + NROW - 1
@@ -273,7 +251,7 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
                         qcrd = qv - p.Qin;
                     }
                     for (int cb = 0; cb < NBLK; ++cb) {
-                        if constexpr (PAIR && TSA == 0)
+                        if constexpr (PAIR)
                             tma_load_5d_2sm_e(dst + (size_t)(kp * NBLK + cb) * BOXB, map,
                                               lead_full + idx * 8, X3 ? 0 : cb * CBLK, wc, qcrd,
                                               pc, X3 ? cb * p.B + b : b);
@@ -281,172 +259,6 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
                             tma_load_5d_e(dst + (size_t)(kp * NBLK + cb) * BOXB, map, &full[idx],
                                           X3 ? 0 : cb * CBLK, wc, qcrd, pc, X3 ? cb * p.B + b : b);
                     }
-                }
-            }
-        }
-    } else if (TSA && warp == 1 && (!PAIR || rank == 0)) {
-        // ============ MMA issuer, TS form: A from the TMEM ring, B from smem ============
-        if constexpr (TSA) {
-            constexpr int KC_S = CIN_ / 16;
-            const uint32_t idesc_one = idesc_bf16(PAIR ? 256 : 128, N);
-            const uint32_t idesc_all = idesc_bf16(PAIR ? 256 : 128, N * KQ_);
-            // B blocks as the SS kernels (PAIR: this CTA's halves, merged then per-kq)
-            constexpr uint32_t BLK = PAIR ? KQ_ * N * 16 : KQ_ * N * 32;   // (kp, kw, kc) block
-            constexpr uint32_t DB = (uint32_t)(KC_S * BLK) >> 4;           // kw step, merged
-            constexpr uint32_t KQB0 = (uint32_t)(KP_ * 3 * KC_S) * BLK, KQB = N * 16;
-            constexpr uint32_t DBQ = PAIR ? (uint32_t)(KC_S * KQ_ * N * 16) >> 4 : DB;   // per-kq
-            auto commit = [&](uint64_t *bar) {
-                if constexpr (PAIR) mma2_commit_mc_e(bar);
-                else mma_commit_e(bar);
-            };
-            const uint64_t bdesc0 = sdesc(smem_u32(wsm), 128, 256);
-            const uint64_t adesc0 = sdesc_sw(smem_u32(stages), 8 * 64, swz_layout(32));   // TSA 2
-            uint32_t row_base = 0, aslot = 0, aph = 0, idx = 0, ph = 0;
-            for (int u = u0; u < p.n_units; u += ustep) {
-                int r = u / p.n_wt;
-                const int qc = r % p.n_qc;
-                const int q0 = qc * p.q_chunk, q1 = min(p.Qout, q0 + p.q_chunk);
-                const int nq = q1 - q0;
-                const int nrows = nq + KQ - 1;
-                {   // ring alignment rows (as the SS issuer)
-                    const uint32_t pad = (uint32_t)(((q0 + p.qorg - (int)(row_base % NSLOT)) % NSLOT +
-                                                     NSLOT) % NSLOT);
-                    for (uint32_t d = 0; d < pad; ++d, ++row_base) {
-                        mbar_wait(&tempty[row_base % NSLOT], ((row_base / NSLOT) & 1) ^ 1);
-                        commit(&tfull[row_base % NSLOT]);
-                    }
-                }
-                for (int s = 0; s < nrows; ++s) {
-                    if (s < nq) {
-                        const uint32_t row = row_base + s;
-                        mbar_wait(&tempty[row % NSLOT], ((row / NSLOT) & 1) ^ 1);
-                    }
-                    const uint32_t top = row_base + s;
-                    const bool merged = s >= KQ - 1 && s < nq;
-                    // box k of the stage feeds plane t with tap kp = k - t; per accumulator
-                    // the order (kp, kc, kw) is the SS kernels'
-#pragma unroll
-                    if constexpr (TSA == 2) {
-                        mbar_wait(&full[idx], ph);
-                        tc_fence_after();
-                    }
-                    for (int k = 0; k < KP_ + 1; ++k) {
-                        const uint32_t abox = tmem + TS_ACOL + aslot * TS_ABOX;
-                        if constexpr (TSA == 2) {
-                            // the box's 3 taps x 2 K steps: smem -> TMEM in the tensor pipe
-                            tmem_cp_box3x2<64>(abox, adesc0 + ((idx * stage_bytes + k * BOXB) >> 4));
-                        } else {
-                            mbar_wait(&afull[aslot], aph);
-                            tc_fence_after();
-                        }
-#pragma unroll
-                        for (int t = 0; t < 2; ++t) {
-                            const int kp = k - t;
-                            if (kp < 0 || kp >= KP_) continue;
-                            if (merged) {
-                                const uint32_t d = tmem + t * RCOLS + (NSLOT - 1 - top % NSLOT) * N;
-#pragma unroll
-                                for (int kc = 0; kc < KC_S; ++kc)
-                                    mma_ts_x3<16, DB, PAIR>(d, abox + kc * 8,
-                                                            bdesc0 + ((((kp * 3) * KC_S + kc) * BLK) >> 4),
-                                                            idesc_all);
-                            } else {
-#pragma unroll
-                                for (int kq = 0; kq < KQ_; ++kq) {
-                                    const int j = s - kq;
-                                    if (j < 0 || j >= nq) continue;
-                                    const uint32_t d =
-                                        tmem + t * RCOLS + (NSLOT - 1 - top % NSLOT + kq) * N;
-#pragma unroll
-                                    for (int kc = 0; kc < KC_S; ++kc)
-                                        mma_ts_x3<16, DBQ, PAIR>(
-                                            d, abox + kc * 8,
-                                            bdesc0 + ((PAIR ? KQB0 + (((kp * 3) * KC_S + kc) * KQ_ + kq) * KQB
-                                                            : ((kp * 3) * KC_S + kc) * BLK + kq * (N / 8) * 256) >> 4),
-                                            idesc_one);
-                                }
-                            }
-                        }
-                        if constexpr (TSA == 1) commit(&aempty[aslot]);
-                        if (++aslot == (uint32_t)TS_NA) { aslot = 0; aph ^= 1u; }
-                    }
-                    if constexpr (TSA == 2) {
-                        mma_commit_e(&empty[idx]);
-                        if (++idx == (uint32_t)p.nstage) { idx = 0; ph ^= 1u; }
-                    }
-                    const int jd = s - (KQ - 1);
-                    if (jd >= 0 && jd < nq) commit(&tfull[(row_base + jd) % NSLOT]);
-                }
-                row_base += nq;
-            }
-        }
-    } else if (TSA == 1 && warp >= 6) {
-        // ============ A stagers (TSA): smem box -> 3 kw-shifted TMEM copies ============
-        // two warpgroups (two independent load -> tcgen05.st -> wait chains: TMEM
-        // stores are latency-bound per warp); group g stages boxes g, g + 2 of
-        // every stage
-        if constexpr (TSA == 1) {
-            const int quarter = warp & 3;
-            const int grp = (warp - 6) >> 2;
-            const uint32_t abase = tmem + ((uint32_t)(quarter * 32) << 16) + TS_ACOL;
-            constexpr uint32_t BOXS = box_bytes(32, 3);
-            constexpr int NBOX = KP_ + 1;
-            // SWIZZLE_64B: 16-B chunk c of voxel v (64-B rows) sits at
-            // v * 64 + 16 (c ^ ((v >> 1) & 3)); 8 consecutive voxels hit 8 distinct
-            // chunks of a 128-B line, so the loads are conflict-free
-            const uint32_t v0 = (uint32_t)(quarter * 32 + lane);
-            const uint32_t lead_afull = PAIR ? mapa_shared(smem_u32(afull), 0) : 0u;
-            uint32_t idx = 0, ph = 0, sslot = 0, sph = 0;   // A slot / phase of box 0 of the stage
-            for (int u = u0; u < p.n_units; u += ustep) {
-                int r = u / p.n_wt;
-                const int qc = r % p.n_qc;
-                const int q0 = qc * p.q_chunk, q1 = min(p.Qout, q0 + p.q_chunk);
-                const int nrows = (q1 - q0) + KQ - 1;
-                for (int s = 0; s < nrows; ++s) {
-                    mbar_wait(&full[idx], ph);
-                    const uint32_t sb = smem_u32(stages) + idx * stage_bytes;
-                    // tap kw: lane t takes voxel t + kw, read straight from the swizzled
-                    // box (three conflict-free 16-B loads per chunk; shuffling one load
-                    // measured slower: the SHFL work, not shared-memory bandwidth, bound
-                    // the stager).  The next box's loads are issued before the stores.
-                    uint32_t v[2][3][16];
-                    auto load = [&](int k, uint32_t (&vv)[3][16]) {
-                        const uint32_t bx = sb + (uint32_t)k * BOXS;
-#pragma unroll
-                        for (int kw = 0; kw < 3; ++kw) {
-                            const uint32_t vx = v0 + kw;
-#pragma unroll
-                            for (int c = 0; c < 4; ++c)
-                                lds128(bx + vx * 64 + 16 * (c ^ ((vx >> 1) & 3)), &vv[kw][4 * c]);
-                        }
-                    };
-                    load(grp, v[0]);
-#pragma unroll
-                    for (int kk = 0; kk < NBOX / 2; ++kk) {
-                        const int k = grp + 2 * kk;
-                        if (kk + 1 < NBOX / 2) load(k + 2, v[(kk + 1) & 1]);
-                        uint32_t aslot = sslot + (uint32_t)k, aph = sph;
-                        if (aslot >= (uint32_t)TS_NA) { aslot -= TS_NA; aph ^= 1u; }
-                        mbar_wait(&aempty[aslot], aph ^ 1);
-                        tc_fence_after();
-                        const uint32_t dst = abase + aslot * TS_ABOX;
-                        if (!(p.dbg & 128)) {
-#pragma unroll
-                            for (int kw = 0; kw < 3; ++kw) tmem_st16(dst + kw * 16, v[kk & 1][kw]);
-                            tmem_wait_st();
-                        }
-                        tc_fence_before();
-                        __syncwarp();
-                        if (lane == 0) {
-                            if (!PAIR || rank == 0) mbar_arrive(&afull[aslot]);
-                            else mbar_arrive_remote(lead_afull + aslot * 8);
-                        }
-                    }
-                    sslot += NBOX;
-                    if (sslot >= (uint32_t)TS_NA) { sslot -= TS_NA; sph ^= 1u; }
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(&empty[idx]);   // the stage's rows are in TMEM
-                    if (++idx == (uint32_t)p.nstage) { idx = 0; ph ^= 1u; }
                 }
             }
         }
@@ -608,7 +420,7 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
             }
             row_base += nq;
         }
-    } else if (warp >= 2 && warp < 6) {
+    } else if (warp >= 2) {
         // ===================== epilogue =====================
         const int quarter = warp & 3;
         const int m = quarter * 32 + lane;  // TMEM lane = voxel within the tile
@@ -1041,8 +853,6 @@ struct Plan {
     int cblk, stage_bytes, wimg_bytes, nstage, smem;
     bool x3;              // 6-block K over a 3-part activation (the bf16x3 path)
     int ppn;              // output planes per unit (2: P-pair, two TMEM rings)
-    int tsa;              // TS form (A in TMEM) for the P-pair 32 -> 16 shape: 1 stager
-                          // warps, 2 tcgen05.cp
 };
 
 bool make_plan(const dp_conv_geom *g, bool dgrad, Plan &pl, bool f32out = false, bool x3 = false,
@@ -1078,11 +888,6 @@ bool make_plan(const dp_conv_geom *g, bool dgrad, Plan &pl, bool f32out = false,
     pl.ppn = (allow_pp && !pp_off && !x3 && !f32out && R.nsp == 3 && R.KP == 3 && R.KQ == 3 && R.KW == 3 &&
               (pl.Cin == 16 || pl.Cin == 32) && (pl.N == 16 || pl.N == 32) && R.Pout >= 2 &&
               R.KQ + 2 <= ring_slots(pl.N, 256)) ? 2 : 1;
-    // TS form (A operand in TMEM) for the operand-bound N = 16 shape (the 3-D
-    // dgrad of a 16 -> 32 layer); DP_CONV_TSA=0 keeps the SS CTA-pair kernel
-    static const int tsa_mode = getenv("DP_CONV_TSA") ? atoi(getenv("DP_CONV_TSA")) : 0;
-    pl.tsa = (pl.ppn == 2 && pl.N == 16 && pl.Cin == 32 && R.KQ + 2 <= ring_slots(pl.N, 128))
-                 ? tsa_mode : 0;
     pl.stage_bytes = (R.KP + pl.ppn - 1) * (x3 ? 3 : pl.Cin / pl.cblk) * box_bytes(pl.cblk, R.KW);
     pl.wimg_bytes = R.KP * R.KQ * R.KW * pl.Cin * pl.N * 2;
     const int budget = 220 * 1024;
@@ -1098,24 +903,24 @@ bool make_plan(const dp_conv_geom *g, bool dgrad, Plan &pl, bool f32out = false,
     return true;
 }
 
-template <int N, int KP, int KQ, int KW, int CIN, bool X3 = false, int PPN = 1, int TSA = 0>
+template <int N, int KP, int KQ, int KW, int CIN, bool X3 = false, int PPN = 1>
 int launch_k(const CUtensorMap &xm, const CUtensorMap &hm, const ConvTcParams &p, int grid,
              int smem, cudaStream_t st) {
-    auto kern = conv_tc_kernel<N, KP, KQ, KW, CIN, false, X3, PPN, TSA>;
+    auto kern = conv_tc_kernel<N, KP, KQ, KW, CIN, false, X3, PPN>;
     DP_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    kern<<<grid, TSA == 1 ? kThreads + 256 : kThreads, smem, st>>>(xm, hm, p);
+    kern<<<grid, kThreads, smem, st>>>(xm, hm, p);
     return launch_status("conv_tc_kernel");
 }
 
 // CTA-pair instantiation: (2, 1, 1) clusters, grid = 2 x clusters
-template <int N, int KP, int KQ, int KW, int CIN, bool X3 = false, int PPN = 1, int TSA = 0>
+template <int N, int KP, int KQ, int KW, int CIN, bool X3 = false, int PPN = 1>
 int launch_k_pair(const CUtensorMap &xm, const CUtensorMap &hm, const ConvTcParams &p, int grid,
                   int smem, cudaStream_t st) {
-    auto kern = conv_tc_kernel<N, KP, KQ, KW, CIN, true, X3, PPN, TSA>;
+    auto kern = conv_tc_kernel<N, KP, KQ, KW, CIN, true, X3, PPN>;
     DP_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)grid);
-    cfg.blockDim = dim3(TSA == 1 ? kThreads + 256 : kThreads);
+    cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = (size_t)smem;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
@@ -1184,7 +989,7 @@ int run_conv_tc(const dp_conv_geom *g, bool dgrad, const void *in, const void *i
     // instantiation, there are >= 2 tiles and the workspace holds both images
     const int n_wt_all = (R.Wout + kTileW - 1) / kTileW;
     static const bool pair_off = getenv("DP_CONV_2CTA") && getenv("DP_CONV_2CTA")[0] == '0';
-    const bool use_pair = !pair_off && pl.tsa != 2 && n_wt_all >= 2 && sm_count() >= 2 &&
+    const bool use_pair = !pair_off && n_wt_all >= 2 && sm_count() >= 2 &&
                           pair_shape(pl.N, R.KP, R.KQ, R.KW, pl.Cin) &&
                           ws_bytes >= 2 * (int64_t)pl.wimg_bytes;
     // bf16 outputs drain through the coalesced epilogue (permuted B columns) when
@@ -1267,7 +1072,7 @@ int run_conv_tc(const dp_conv_geom *g, bool dgrad, const void *in, const void *i
         p.ysplit = R.split == 0 ? (int)g->in_ext[0] : (int)g->in_ext[0];
     }
     {
-        const int64_t ns = ring_slots(pl.N, pl.tsa ? 128 : 512 / pl.ppn), q = g->nsp == 3 ? g->out_org[1] : g->out_org[0];
+        const int64_t ns = ring_slots(pl.N, 512 / pl.ppn), q = g->nsp == 3 ? g->out_org[1] : g->out_org[0];
         p.qorg = (int)(((q % ns) + ns) % ns);
     }
     p.n_wt = use_pair ? (n_wt_all + 1) / 2 : n_wt_all;   // PAIR: tile pairs
@@ -1310,16 +1115,13 @@ int run_conv_tc(const dp_conv_geom *g, bool dgrad, const void *in, const void *i
         if (use_pair) {
             if (pl.N == 16)
                 return c16 ? launch_k_pair<16, 3, 3, 3, 16, false, 2>(xm, hm, p, 2 * grid, pl.smem, st)
-                       : pl.tsa ? launch_k_pair<16, 3, 3, 3, 32, false, 2, 1>(xm, hm, p, 2 * grid, pl.smem, st)
-                                : launch_k_pair<16, 3, 3, 3, 32, false, 2>(xm, hm, p, 2 * grid, pl.smem, st);
+                           : launch_k_pair<16, 3, 3, 3, 32, false, 2>(xm, hm, p, 2 * grid, pl.smem, st);
             return c16 ? launch_k_pair<32, 3, 3, 3, 16, false, 2>(xm, hm, p, 2 * grid, pl.smem, st)
                        : launch_k_pair<32, 3, 3, 3, 32, false, 2>(xm, hm, p, 2 * grid, pl.smem, st);
         }
         if (pl.N == 16)
             return c16 ? launch_k<16, 3, 3, 3, 16, false, 2>(xm, hm, p, grid, pl.smem, st)
-                   : pl.tsa == 2 ? launch_k<16, 3, 3, 3, 32, false, 2, 2>(xm, hm, p, grid, pl.smem, st)
-                   : pl.tsa ? launch_k<16, 3, 3, 3, 32, false, 2, 1>(xm, hm, p, grid, pl.smem, st)
-                            : launch_k<16, 3, 3, 3, 32, false, 2>(xm, hm, p, grid, pl.smem, st);
+                       : launch_k<16, 3, 3, 3, 32, false, 2>(xm, hm, p, grid, pl.smem, st);
         return c16 ? launch_k<32, 3, 3, 3, 16, false, 2>(xm, hm, p, grid, pl.smem, st)
                    : launch_k<32, 3, 3, 3, 32, false, 2>(xm, hm, p, grid, pl.smem, st);
     }

@@ -217,11 +217,6 @@ __device__ __forceinline__ void tmem_st16(uint32_t addr, const uint32_t (&r)[16]
         "r"(r[15])
         : "memory");
 }
-__device__ __forceinline__ void lds128(uint32_t addr, uint32_t *r) {
-    asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
-                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
-                 : "r"(addr));
-}
 __device__ __forceinline__ void tmem_wait_st() {
     asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
@@ -466,73 +461,6 @@ __device__ __forceinline__ void mma_bf16_x3_lo(uint32_t d_tmem, uint32_t alo, ui
             "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a2, b2, %4, p;\n"
             "}\n" ::"r"(d_tmem),
             "r"(alo), "r"(ahi), "l"(b), "r"(idesc), "n"(DA), "n"(2 * DA), "n"(DB), "n"(2 * DB));
-}
-// Three TS MMAs (A in TMEM) into one accumulator under ONE elect: A columns
-// a, a + DA, a + 2 DA, B descriptors b, b + DB, b + 2 DB (the kw taps of the
-// TS conv kernel).
-template <uint32_t DA, uint32_t DB, bool PAIR = false>
-__device__ __forceinline__ void mma_ts_x3(uint32_t d_tmem, uint32_t a_tmem, uint64_t b,
-                                          uint32_t idesc) {
-    if constexpr (PAIR)   // cta_group::2: each CTA's 128 A rows from its own TMEM
-    asm volatile(
-        "{\n"
-        ".reg .pred p, e;\n"
-        ".reg .b32 a1, a2;\n"
-        ".reg .b64 b1, b2;\n"
-        "setp.eq.u32 p, 1, 1;\n"
-        "add.u32 a1, %1, %4;\n"
-        "add.u32 a2, %1, %5;\n"
-        "add.s64 b1, %2, %6;\n"
-        "add.s64 b2, %2, %7;\n"
-        "elect.sync _|e, 0xffffffff;\n"
-        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n"
-        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [a1], b1, %3, p;\n"
-        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [a2], b2, %3, p;\n"
-        "}\n" ::"r"(d_tmem),
-        "r"(a_tmem), "l"(b), "r"(idesc), "n"(DA), "n"(2 * DA), "n"(DB), "n"(2 * DB));
-    else
-    asm volatile(
-        "{\n"
-        ".reg .pred p, e;\n"
-        ".reg .b32 a1, a2;\n"
-        ".reg .b64 b1, b2;\n"
-        "setp.eq.u32 p, 1, 1;\n"
-        "add.u32 a1, %1, %4;\n"
-        "add.u32 a2, %1, %5;\n"
-        "add.s64 b1, %2, %6;\n"
-        "add.s64 b2, %2, %7;\n"
-        "elect.sync _|e, 0xffffffff;\n"
-        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n"
-        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a1], b1, %3, p;\n"
-        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a2], b2, %3, p;\n"
-        "}\n" ::"r"(d_tmem),
-        "r"(a_tmem), "l"(b), "r"(idesc), "n"(DA), "n"(2 * DA), "n"(DB), "n"(2 * DB));
-}
-// Six tcgen05.cp (shared memory -> TMEM, 128 rows x 256 bits each) under ONE
-// elect: TMEM columns t + 16 kw + 8 kc <- the K-major swizzled A tile at
-// descriptor start + (kw * ROWB + kc * 32) bytes (the SS kernels' A operand of
-// tap kw, K step kc).  Executed in issue order with the MMAs that read them.
-template <uint32_t ROWB>
-__device__ __forceinline__ void tmem_cp_box3x2(uint32_t t, uint64_t desc) {
-    asm volatile(
-        "{\n"
-        ".reg .pred e;\n"
-        ".reg .b64 d1, d2, d3, d4, d5;\n"
-        "add.s64 d1, %1, %2;\n"
-        "add.s64 d2, %1, %3;\n"
-        "add.s64 d3, %1, %4;\n"
-        "add.s64 d4, %1, %5;\n"
-        "add.s64 d5, %1, %6;\n"
-        "elect.sync _|e, 0xffffffff;\n"
-        "@e tcgen05.cp.cta_group::1.128x256b [%0], %1;\n"
-        "@e tcgen05.cp.cta_group::1.128x256b [%0+8], d1;\n"
-        "@e tcgen05.cp.cta_group::1.128x256b [%0+16], d2;\n"
-        "@e tcgen05.cp.cta_group::1.128x256b [%0+24], d3;\n"
-        "@e tcgen05.cp.cta_group::1.128x256b [%0+32], d4;\n"
-        "@e tcgen05.cp.cta_group::1.128x256b [%0+40], d5;\n"
-        "}\n" ::"r"(t),
-        "l"(desc), "n"(2), "n"(ROWB >> 4), "n"((ROWB >> 4) + 2), "n"(2 * (ROWB >> 4)),
-        "n"(2 * (ROWB >> 4) + 2));
 }
 // cta_group::1 form of mma2_bf16_x3.
 template <uint32_t DA, uint32_t DB>
