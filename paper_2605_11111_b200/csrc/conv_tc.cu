@@ -1727,7 +1727,14 @@ struct TsShape {
 // per-thread fp32 registers (round-to-nearest FADD) right after staging the
 // next row's A: the tensor-core chain is one row (8 K steps), the register
 // chain the CTA's rows.
-template <int CIN, int KP, bool RF = false>
+//
+// G3 (the 2-D bf16x3 fp32 wgrad, grouped): a unit runs ALL 6 part pairings
+// of its rows — an X ring slot holds the 3 X part boxes of a row, each dY part
+// is staged and transposed ONCE per row (3 A entries), and the MMA warp issues
+// the 6 pairings' K steps into the same D tile (every pairing adds into the
+// same dW columns; each MMA's B spans one X part's KQ rows at the slot stride).
+// Half the transposes and TMA bytes of running the pairings as batch entries.
+template <int CIN, int KP, bool RF = false, bool G3 = false>
 __global__ void __launch_bounds__(kThreads, 1)
 conv_wgrad_ts_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap hmap,
                      const __grid_constant__ CUtensorMap dmap, const WgradTsParams p) {
@@ -1736,6 +1743,9 @@ conv_wgrad_ts_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_cons
     constexpr int KQ = S::KQ, KW = S::KW;
     constexpr int ACOL = RF ? (2 * S::NT + 31) / 32 * 32 : S::ACOL;   // first A column
     static_assert(!RF || S::NT <= 96, "row-flush registers: NT <= 96");
+    static_assert(!G3 || (KP == 1 && RF), "G3: the 2-D bf16x3 wgrad");
+    constexpr int NXP = G3 ? 3 : 1;            // X / dY parts per row (G3)
+    constexpr int XS = NXP * S::XSLOT;         // X ring slot bytes
     extern __shared__ __align__(1024) uint8_t smem[];
     const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);   // warp-uniform for ptxas
     const int lane = threadIdx.x & 31;
@@ -1745,7 +1755,7 @@ conv_wgrad_ts_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_cons
     // loads: 40 % of the X stream for the L2 shape's 5-slot ring)
     const int NXM = p.nx;
     uint8_t *xring = smem;
-    uint8_t *dring = smem + (size_t)NXM * S::XSLOT;
+    uint8_t *dring = smem + (size_t)NXM * XS;
     uint64_t *bars = reinterpret_cast<uint64_t *>(dring + (size_t)p.nd * kTsDSlot);
     uint64_t *xfull = bars, *xempty = xfull + p.nx;
     uint64_t *dfull = xempty + p.nx, *dempty = dfull + p.nd;
@@ -1796,7 +1806,7 @@ conv_wgrad_ts_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_cons
             const int po = r % p.Pout;
             const int b = r / p.Pout;
             int bx = b, bd = b;
-            if (p.pairB > 0) {
+            if (p.pairB > 0 && !G3) {
                 const int kk = b / p.pairB, bb = b % p.pairB;
                 bx = (int)((kTsPairX >> (2 * kk)) & 3u) * p.pairB + bb;
                 bd = (int)((kTsPairD >> (2 * kk)) & 3u) * p.pairB + bb;
@@ -1813,7 +1823,7 @@ conv_wgrad_ts_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_cons
                         if (lane == 0) mbar_arrive(&xfull[idx]);
                         __syncwarp();
                     } else {
-                    mbar_expect_tx_e(&xfull[idx], xrow);
+                    mbar_expect_tx_e(&xfull[idx], xrow * NXP);
                     const int qv = p.base_q + q0 + s;
 #pragma unroll
                     for (int kp = 0; kp < KP; ++kp) {
@@ -1828,15 +1838,19 @@ conv_wgrad_ts_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_cons
                             qcrd = qv - p.Qin;
                         }
 #pragma unroll
+                        for (int xp = 0; xp < NXP; ++xp)
+#pragma unroll
                         for (int cb = 0; cb < S::NBX; ++cb) {
-                            const size_t off = (size_t)(kp * S::NBX + cb) * S::BOXX;
-                            tma_load_5d_e(xring + (size_t)idx * S::XSLOT + off, map, &xfull[idx],
-                                          cb * S::CBX, p.base_w + w0, qcrd, pc, bx);
+                            const size_t off = (size_t)xp * S::XSLOT + (size_t)(kp * S::NBX + cb) * S::BOXX;
+                            tma_load_5d_e(xring + (size_t)idx * XS + off, map, &xfull[idx],
+                                          cb * S::CBX, p.base_w + w0, qcrd, pc,
+                                          G3 ? xp * p.pairB + b : bx);
                         }
                     }
                     }
                 }
                 if (s < nq) {  // dY row q0 + s: two 16-channel halves, w' in [w0 - 2, w0 + 128)
+                    for (int dp = 0; dp < NXP; ++dp) {   // G3: the 3 dY parts, one ring entry each
                     const uint32_t idx = pdi, ph = pdph;
                     if (++pdi == (uint32_t)p.nd) { pdi = 0; pdph ^= 1u; }
                     mbar_wait(&dempty[idx], ph ^ 1);
@@ -1847,14 +1861,18 @@ conv_wgrad_ts_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_cons
                     }
                     mbar_expect_tx_e(&dfull[idx], dbytes);
                     uint8_t *dst = dring + (size_t)idx * kTsDSlot;
-                    tma_load_5d_e(dst, &dmap, &dfull[idx], 0, w0 - (KW - 1), q0 + s, po, bd);
-                    tma_load_5d_e(dst + kTsDHalf, &dmap, &dfull[idx], 16, w0 - (KW - 1), q0 + s, po, bd);
+                    const int bdp = G3 ? dp * p.pairB + b : bd;
+                    tma_load_5d_e(dst, &dmap, &dfull[idx], 0, w0 - (KW - 1), q0 + s, po, bdp);
+                    tma_load_5d_e(dst + kTsDHalf, &dmap, &dfull[idx], 16, w0 - (KW - 1), q0 + s, po, bdp);
+                    }
                 }
             }
         }
     } else if (warp == 1) {
         // ===================== MMA issuer =====================
-        const uint64_t b0 = sdesc_mn(smem_u32(xring), S::BOXX, 8 * S::CBX * 2, swz_layout(S::CBX));
+        // B atoms: (kq, kp, cb) boxes at one stride (G3: one X part's KQ rows, slot stride)
+        const uint64_t b0 = sdesc_mn(smem_u32(xring), G3 ? XS : S::BOXX, 8 * S::CBX * 2,
+                                     swz_layout(S::CBX));
         constexpr uint32_t bstep = (16 * S::CBX * 2) >> 4;   // one K step = 16 w' rows
         // ring slots / phases carried as counters (no integer division per row:
         // it costs MMA-warp issue time, cf. the fwd kernel)
@@ -1872,9 +1890,14 @@ conv_wgrad_ts_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_cons
                 mbar_wait(&xfull[cx], cph);
                 const int j = s - (KQ - 1);
                 if (j < 0) continue;
-                const uint32_t ca = aidx, caph = aph;
-                if (++aidx == (uint32_t)p.na) { aidx = 0; aph ^= 1u; }
-                mbar_wait(&afull[ca], caph);
+                uint32_t cas[NXP];   // this row's A entries (G3: one per dY part)
+#pragma unroll
+                for (int dp = 0; dp < NXP; ++dp) {
+                    cas[dp] = aidx;
+                    mbar_wait(&afull[aidx], aph);
+                    if (++aidx == (uint32_t)p.na) { aidx = 0; aph ^= 1u; }
+                }
+                const uint32_t ca = cas[0];
                 uint32_t dcol = tmem;
                 if constexpr (RF) {   // group g = rrow / rf_rows uses D tile g & 1; a new
                                       // group's tile must have been drained (group g - 2)
@@ -1887,9 +1910,32 @@ conv_wgrad_ts_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_cons
                     dcol += rb * S::NT;
                 }
                 tc_fence_after();
-                const uint64_t bx = b0 + ((xs * S::XSLOT) >> 4);
+                const uint64_t bx = b0 + ((xs * XS) >> 4);
                 const uint32_t acol = tmem + ACOL + ca * S::ACOLS;
-                if (xs + KQ - 1 < (uint32_t)p.nx) {   // the KQ rows are adjacent slots
+                if constexpr (G3) {
+                    // the 6 pairings (X part kTsPairX[k], dY part kTsPairD[k]) into one D
+                    const bool wrap = xs + KQ - 1 >= (uint32_t)p.nx;
+                    const int aw = wrap ? (int)(p.nx - xs) : KQ;
+                    const uint32_t id1 = idesc_bf16(128, aw * S::CBX, 0, 1);
+                    const uint32_t id2 = idesc_bf16(128, (KQ - aw) * S::CBX, 0, 1);
+                    // smallest products first (lo / mid pairings, then hi x hi): the tensor
+                    // core's accumulator adds truncate, so the small terms go in while the
+                    // tile's running sum is still small
+#pragma unroll
+                    for (int k = 5; k >= 0; --k) {
+                        const uint32_t xp = (kTsPairX >> (2 * k)) & 3u, dp = (kTsPairD >> (2 * k)) & 3u;
+                        const uint32_t ak = tmem + ACOL + cas[dp] * S::ACOLS;
+                        const uint64_t bk = bx + ((xp * S::XSLOT) >> 4);
+                        const uint64_t bk0 = b0 + ((xp * S::XSLOT) >> 4);
+#pragma unroll
+                        for (int ks = 0; ks < kTsKT; ++ks) {
+                            if (p.dbg & 2) break;
+                            const uint32_t acc = (fresh && k == 5 && ks == 0) ? 0u : 1u;
+                            mma_ts_e(dcol, ak + ks * 8, bk + ks * bstep, id1, acc);
+                            if (wrap) mma_ts_e(dcol + aw * S::CBX, ak + ks * 8, bk0 + ks * bstep, id2, acc);
+                        }
+                    }
+                } else if (xs + KQ - 1 < (uint32_t)p.nx) {   // the KQ rows are adjacent slots
 #pragma unroll
                 for (int ks = 0; ks < kTsKT; ++ks) {
                     if (p.dbg & 2) break;
@@ -1921,7 +1967,8 @@ conv_wgrad_ts_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_cons
                         mma_commit_e(&rfull[((rrow >> p.rf_shift)) & 1u]);
                     ++rrow;
                 }
-                mma_commit_e(&aempty[ca]);
+#pragma unroll
+                for (int dp = 0; dp < NXP; ++dp) mma_commit_e(&aempty[cas[dp]]);
                 mma_commit_e(&xempty[xs]);
                 uint32_t xn = xs + 1 == (uint32_t)p.nx ? 0u : xs + 1;
                 if (j == nq - 1)
@@ -1982,7 +2029,8 @@ conv_wgrad_ts_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_cons
                 int r = u / p.n_wt;
                 const int qc = r % p.n_qc;
                 const int q0 = qc * p.q_chunk, q1 = min(p.Qout, q0 + p.q_chunk);
-                for (int s = 0; s < q1 - q0; ++s,
+                for (int s = 0; s < q1 - q0; ++s) {
+                    for (int dp = 0; dp < NXP; ++dp,   // G3: the row's 3 dY parts
                          (++didx == (uint32_t)p.nd ? (didx = 0u, dph ^= 1u) : 0u),
                          (++aidx == (uint32_t)p.na ? (aidx = 0u, aph ^= 1u) : 0u)) {
                     mbar_wait(&dfull[didx], dph);
@@ -2011,6 +2059,7 @@ conv_wgrad_ts_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_cons
                         mbar_arrive(&dempty[didx]);
                         mbar_arrive(&afull[aidx]);
                     }
+                    }   // parts
                     if constexpr (RF) {   // the previous group's MMAs overlap this row's A
                         if (rrow > 0 && (rrow & ((1u << p.rf_shift) - 1u)) == 0)
                             drain(rrow / (1u << p.rf_shift) - 1u);
@@ -2113,7 +2162,8 @@ bool ts_disabled() {
     return v == 1;
 }
 
-bool make_tsplan(const dp_conv_geom *g, TsPlan &pl, bool fp32 = false) {
+// g3: the grouped bf16x3 wgrad (all 6 part pairings per unit, conv_wgrad_ts_kernel G3)
+bool make_tsplan(const dp_conv_geom *g, TsPlan &pl, bool fp32 = false, bool g3 = false) {
     if (ts_disabled()) return false;
     if (!map_roles(g, false, pl.R)) return false;
     const Roles &R = pl.R;
@@ -2131,15 +2181,16 @@ bool make_tsplan(const dp_conv_geom *g, TsPlan &pl, bool fp32 = false) {
     const int cbx = chan_block(pl.Cin);
     pl.nt = 3 * R.KP * pl.Cin;
     pl.rf = fp32 && pl.nt <= 96;
-    pl.xslot = R.KP * (pl.Cin / cbx) * kTsWK * cbx * 2;
+    if (g3 && !(pl.rf && R.KP == 1 && pl.Cin == 32)) return false;
+    pl.xslot = R.KP * (pl.Cin / cbx) * kTsWK * cbx * 2 * (g3 ? 3 : 1);
     const int acol = ((pl.rf ? 2 : 1) * pl.nt + 31) / 32 * 32;
     pl.na = (512 - acol) / (kTsKT * 8);
     static const int na_cap = getenv("DP_WGRAD_NA") ? atoi(getenv("DP_WGRAD_NA")) : 4;
-    if (pl.na > na_cap) pl.na = na_cap;
-    if (pl.na < 2) return false;
+    if (!g3 && pl.na > na_cap) pl.na = na_cap;   // G3: 3 A entries per row, take them all
+    if (pl.na < (g3 ? 3 : 2)) return false;
     const int budget = 220 * 1024 - 512;
     static const int nd = getenv("DP_WGRAD_ND") ? atoi(getenv("DP_WGRAD_ND")) : 4;
-    pl.nd = nd;
+    pl.nd = g3 ? 6 : nd;                          // G3: two rows of 3 dY parts
     pl.nx = (budget - pl.nd * kTsDSlot) / pl.xslot;
     // X ring depth (L1 wgrad 0.504 -> 0.494 ms at 12, measured with mirrored slots)
     static const int nx_cap = getenv("DP_WGRAD_NX") ? atoi(getenv("DP_WGRAD_NX")) : 12;
@@ -2179,10 +2230,10 @@ bool make_tsplan(const dp_conv_geom *g, TsPlan &pl, bool fp32 = false) {
 
 int64_t ts_workspace(const TsPlan &pl) { return (int64_t)pl.grid * 96 * pl.nt * 4; }
 
-template <int CIN, int KP, bool RF = false>
+template <int CIN, int KP, bool RF = false, bool G3 = false>
 int launch_ts_k(const CUtensorMap &xm, const CUtensorMap &hm, const CUtensorMap &dm,
                 const WgradTsParams &p, int grid, int smem, cudaStream_t st) {
-    auto kern = conv_wgrad_ts_kernel<CIN, KP, RF>;
+    auto kern = conv_wgrad_ts_kernel<CIN, KP, RF, G3>;
     DP_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     kern<<<grid, kThreads, smem, st>>>(xm, hm, dm, p);
     return launch_status("conv_wgrad_ts_kernel");
@@ -2190,7 +2241,7 @@ int launch_ts_k(const CUtensorMap &xm, const CUtensorMap &hm, const CUtensorMap 
 
 int run_wgrad_ts(const dp_conv_geom *g, const TsPlan &pl, const void *x, const void *xh,
                  const void *dy, float *dw, void *ws, int64_t ws_bytes, cudaStream_t st,
-                 int pairB = 0) {
+                 int pairB = 0, bool g3 = false) {
     const uint64_t nb = pairB > 0 ? (uint64_t)3 * pairB : (uint64_t)g->batch;   // tensor batch
     const Roles &R = pl.R;
     DP_REQUIRE(ws_bytes >= ts_workspace(pl), DP_ERR_INVALID, "conv_wgrad_ts: workspace too small");
@@ -2251,13 +2302,19 @@ int run_wgrad_ts(const dp_conv_geom *g, const TsPlan &pl, const void *x, const v
     // nearest register add (DP_WGRAD_RF_ROWS, a power of two; measured on the
     // full cfg1 grid vs fp64: 1 row 3.9e-7, 4 rows 5.9e-7, 8 rows 1.1e-6 of
     // max|dW| — the reference's bound is 1e-5 — and 0.178 -> 0.162 ms)
-    static const int rf_rows = getenv("DP_WGRAD_RF_ROWS") ? atoi(getenv("DP_WGRAD_RF_ROWS")) : 4;
+    // G3 (all 6 pairings in one tile, small products first): one row per group —
+    // 2.0e-7 of max|dW| on cfg1 at 0.1375 ms, vs 2.9e-6 at 0.134 ms with 4 rows
+    // (and 5.9e-7 / 0.152 ms for the pairings as batch entries with 4 rows)
+    static const int rf_env = getenv("DP_WGRAD_RF_ROWS") ? atoi(getenv("DP_WGRAD_RF_ROWS")) : 0;
+    const int rf_rows = rf_env > 0 ? rf_env : (g3 ? 1 : 4);
     p.rf_shift = 0;
     while ((2 << p.rf_shift) <= rf_rows && p.rf_shift < 5) ++p.rf_shift;
     static const int dbg = getenv("DP_CONV_DBG") ? atoi(getenv("DP_CONV_DBG")) : 0;
     p.dbg = dbg;
     int rc;
-    if (R.KP == 3)
+    if (g3)
+        rc = launch_ts_k<32, 1, true, true>(xm, hm, dm, p, pl.grid, pl.smem, st);
+    else if (R.KP == 3)
         rc = pl.Cin == 16 ? launch_ts_k<16, 3>(xm, hm, dm, p, pl.grid, pl.smem, st)
                           : launch_ts_k<32, 3>(xm, hm, dm, p, pl.grid, pl.smem, st);
     else if (pl.rf)
@@ -2331,15 +2388,34 @@ int64_t conv_tc_workspace(const dp_conv_geom *g, int which) {
 
 // bf16x3 fp32 wgrad (conv_x3.cu): x / dy hold 3 parts each as batch blocks
 // [3B]; the 6 pairings run as batch entries of g (g->batch = 6B)
+// The grouped form (G3: units over the B real batch entries, each running all
+// 6 pairings) when the shape has it; DP_WGRAD_G3=0 keeps the pairings as
+// batch entries.
+bool x3_g3_plan(const dp_conv_geom *g, int B, dp_conv_geom &g1, TsPlan &tp) {
+    static const bool off = getenv("DP_WGRAD_G3") && getenv("DP_WGRAD_G3")[0] == '0';
+    if (off || B <= 0 || g->batch != 6 * (int64_t)B) return false;
+    g1 = *g;
+    g1.batch = B;
+    return make_tsplan(&g1, tp, true, true);
+}
 int conv_wgrad_x3_launch(const dp_conv_geom *g, const void *x, const void *xh, const void *dy,
                          void *dw, void *ws, int64_t ws_bytes, cudaStream_t st, int B) {
     TsPlan tp;
+    dp_conv_geom g1;
+    if (x3_g3_plan(g, B, g1, tp))
+        return run_wgrad_ts(&g1, tp, x, xh, dy, (float *)dw, ws, ws_bytes, st, B, true);
     DP_REQUIRE(make_tsplan(g, tp, true), DP_ERR_UNSUPPORTED, "conv_wgrad_x3: outside the envelope");
     return run_wgrad_ts(g, tp, x, xh, dy, (float *)dw, ws, ws_bytes, st, B);
 }
 int64_t conv_wgrad_x3_workspace(const dp_conv_geom *g) {
     TsPlan tp;
-    return make_tsplan(g, tp, true) ? ts_workspace(tp) : -1;
+    if (!make_tsplan(g, tp, true)) return -1;
+    int64_t ws = ts_workspace(tp);
+    dp_conv_geom g1;
+    TsPlan t3;
+    if (g->batch % 6 == 0 && x3_g3_plan(g, (int)(g->batch / 6), g1, t3) && ts_workspace(t3) > ws)
+        ws = ts_workspace(t3);
+    return ws;
 }
 
 // bf16 tcgen05 conv with fp32 outputs (the bf16x3 fp32 path, conv_x3.cu)

@@ -20,4 +20,4 @@ xp, dyp = k.x3_split(x, k.X3_X, g), k.x3_split(dy, k.X3_DY, g)
 k.conv_wgrad_x3(x, None, xp, None, dy, dyp, dw, **kw)
 ref = torch.nn.grad.conv2d_weight(x.double(), (32, 32, 3, 3), dy.double(), padding=1)
 err = ((dw.double() - ref).abs().max() / ref.abs().max()).item()
-print(f"rf_rows={os.environ.get('DP_WGRAD_RF_ROWS', '4')}: dW rel err {err:.2e}")
+print(f"rf_rows={os.environ.get('DP_WGRAD_RF_ROWS', 'default')}: dW rel err {err:.2e}")
