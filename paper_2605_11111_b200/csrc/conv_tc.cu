@@ -125,7 +125,7 @@ __host__ __device__ constexpr int x3_part(int blk) { return blk < 3 ? 0 : blk < 
 // the ablations price at ~0.1 ms per fwd / dgrad kernel.  The MMAs, their
 // order per plane and the ring / extension-slot mapping are those of PPN = 1.
 template <int N, int KP_, int KQ_, int KW_, int CIN_, bool PAIR = false, bool X3 = false,
-          int PPN = 1, bool PM = false>
+          int PPN = 1>
 __global__ void __launch_bounds__(kThreads, 1)
 conv_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap hmap,
                const ConvTcParams p) {
@@ -148,9 +148,6 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
     const int CIN = kStatic ? CIN_ : p.Cin;
     static_assert(!X3 || (KP_ > 0 && CIN_ % 96 == 0), "X3: static 6-block shapes only");
     static_assert(PPN == 1 || (KP_ > 0 && KW_ == 3 && !X3), "PPN = 2: static 3-tap shapes only");
-    static_assert(!PM || (PAIR && PPN == 1 && !X3 && N == 32 && KP_ == 4 && KW_ == 3),
-                  "PM: the plane-merged CTA-pair form of a 16-channel 3x3x3 conv only");
-    constexpr int PSTEP = PM ? 2 : PPN;      // output planes per unit
     constexpr int RCOLS = 512 / PPN;         // TMEM columns of one plane's ring
     const int CBLK = X3 ? CIN / 6 : chan_block(CIN);
     const int NBLK = X3 ? 3 : CIN / CBLK;
@@ -225,7 +222,7 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
             int r = u;
             const int wt = PAIR ? (r % p.n_wt) * 2 + (int)rank : r % p.n_wt; r /= p.n_wt;
             const int qc = r % p.n_qc; r /= p.n_qc;
-            const int po = (r % p.Pu) * PSTEP;  // first output plane of the unit
+            const int po = (r % p.Pu) * PPN;    // first output plane of the unit
             const int b = r / p.Pu;
             const int q0 = qc * p.q_chunk, q1 = min(p.Qout, q0 + p.q_chunk);
             const int nrows = (q1 - q0) + KQ - 1;
@@ -450,12 +447,12 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
         };
         // bf16 output through the coalesced drain (fp32 outputs / ablations take the
         // per-lane path below); the halo output part must share the W stride
-        const bool fast = p.cperm && (PPN > 1 || PM || !(p.dbg & 8));   // PPN = 2 / PM: always
+        const bool fast = p.cperm && (PPN > 1 || !(p.dbg & 8));   // PPN = 2: always
         for (int u = u0; u < p.n_units; u += ustep) {
             int r = u;
             const int wt = PAIR ? (r % p.n_wt) * 2 + (int)rank : r % p.n_wt; r /= p.n_wt;
             const int qc = r % p.n_qc; r /= p.n_qc;
-            const int po = (r % p.Pu) * PSTEP;  // first output plane of the unit
+            const int po = (r % p.Pu) * PPN;    // first output plane of the unit
             const int b = r / p.Pu;
             const int q0 = qc * p.q_chunk, q1 = min(p.Qout, q0 + p.q_chunk);
             const int w = wt * kTileW + m;
@@ -479,18 +476,14 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
                 // to the halo output at the split row) + 4 per-voxel offsets.
                 constexpr int NJ = N / 4, U = (N % 32 == 0) ? 8 : 4;
                 // per plane of the unit: row pointer, Q step, split row (Q-split halo
-                // output), and whether the plane exists (an odd P extent's last pair).
-                // PM: accumulator column (virtual channel) 16 tp + c is plane po + tp's
-                // channel c; with U = 8 thread t%4 of a voxel owns virtual channels
-                // 8 (t%4) .. +7, i.e. threads 0-1 store plane po, threads 2-3 plane po + 1
-                const int tl = PM ? (lane & 3) >> 1 : 0;
+                // output), and whether the plane exists (an odd P extent's last pair)
                 __nv_bfloat16 *rowp[PPN], *rowp2[PPN];
                 int64_t rstep[PPN];
                 int jsw[PPN];
                 bool pok[PPN];
 #pragma unroll
                 for (int t = 0; t < PPN; ++t) {
-                    const int pl = po + t + tl;
+                    const int pl = po + t;
                     pok[t] = pl < p.Pout;
                     jsw[t] = 1 << 30;
                     rowp2[t] = nullptr;
@@ -516,7 +509,7 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__
                     for (int g = 0; g < 2; ++g) {
                         const int wv = wt * kTileW + quarter * 32 + 16 * h + 8 * g + (lane >> 2);
                         ok[h][g] = wv < p.Wout && !(p.dbg & 1);
-                        off[h][g] = wv * (int)p.ys[3] + U * (lane & 3) - (N / 2) * tl;
+                        off[h][g] = wv * (int)p.ys[3] + U * (lane & 3);
                     }
                 for (int j = 0; j < q1 - q0; ++j) {
                     const uint32_t slot = eslot;
@@ -752,17 +745,11 @@ __global__ void conv_tc_weight_image(const __nv_bfloat16 *__restrict__ w,
 // (kp, kw, kc): rows n = r*KQ*N/2 + nn of the KQ*N merged rows (n = kq*N + c);
 // per-kq block (kp, kw, kc, kq): rows c = r*N/2 + nn.  Canonical K-major as
 // conv_tc_weight_image; flip = the dgrad image.
-//
-// pm = 1: the plane-merged image (PM kernels).  n_rows / KP are the VIRTUAL
-// extents 2 N / KP + 1: virtual channel 16 tp + c at input box kp' carries
-// W[c][..][kp' - tp] (zero where kp' - tp is outside [0, KP)), so one MMA
-// over box kp' feeds both output planes of the unit.
 __global__ void conv_tc_weight_image_pair(const __nv_bfloat16 *__restrict__ w,
                                           __nv_bfloat16 *__restrict__ img, int n_rows, int k_cols,
-                                          int KP, int KQ, int KW, int flip, int cperm, int pm) {
+                                          int KP, int KQ, int KW, int flip, int cperm) {
     const int KC = k_cols / 16;
-    const int nr = pm ? n_rows / 2 : n_rows;                  // real output channels
-    const int taps = (pm ? KP - 1 : KP) * KQ * KW;            // real taps
+    const int taps = KP * KQ * KW;
     const int MH = KQ * n_rows / 2, QH = n_rows / 2;          // rows per half block
     const int nblk = KP * KW * KC;
     const int per_cta = nblk * (MH + KQ * QH) * 16;           // elements
@@ -796,21 +783,12 @@ __global__ void conv_tc_weight_image_pair(const __nv_bfloat16 *__restrict__ w,
         } else {
             c = r * QH + nn;
         }
-        const int kc = bi % KC, kw = (bi / KC) % KW;
-        int kp = bi / (KC * KW);
+        const int kc = bi % KC, kw = (bi / KC) % KW, kp = bi / (KC * KW);
         const int k = kc * 16 + h * 8 + kk;
-        if (cperm) c = epi_channel(c, n_rows);
-        if (pm) {
-            kp -= c / nr;
-            c %= nr;
-            if (kp < 0 || kp >= KP - 1) {
-                img[e] = __float2bfloat16(0.f);
-                continue;
-            }
-        }
         const int t = (kp * KQ + kq) * KW + kw;
+        if (cperm) c = epi_channel(c, n_rows);
         img[e] = !flip ? w[((int64_t)c * k_cols + k) * taps + t]
-                       : w[((int64_t)k * nr + c) * taps + (taps - 1 - t)];
+                       : w[((int64_t)k * n_rows + c) * taps + (taps - 1 - t)];
     }
 }
 
@@ -875,12 +853,10 @@ struct Plan {
     int cblk, stage_bytes, wimg_bytes, nstage, smem;
     bool x3;              // 6-block K over a 3-part activation (the bf16x3 path)
     int ppn;              // output planes per unit (2: P-pair, two TMEM rings)
-    bool pm;              // P-pair planes merged into the MMA N (PM kernels): one ring of
-                          // 2 N virtual channels, KP + 1 virtual kp taps, CTA pairs only
 };
 
 bool make_plan(const dp_conv_geom *g, bool dgrad, Plan &pl, bool f32out = false, bool x3 = false,
-               bool allow_pp = true, bool allow_pm = true) {
+               bool allow_pp = true) {
     if (!map_roles(g, dgrad, pl.R)) return false;
     pl.Cin = (int)(dgrad ? g->c_out : g->c_in);
     pl.N = pick_n((int)(dgrad ? g->c_in : g->c_out));
@@ -912,17 +888,8 @@ bool make_plan(const dp_conv_geom *g, bool dgrad, Plan &pl, bool f32out = false,
     pl.ppn = (allow_pp && !pp_off && !x3 && !f32out && R.nsp == 3 && R.KP == 3 && R.KQ == 3 && R.KW == 3 &&
               (pl.Cin == 16 || pl.Cin == 32) && (pl.N == 16 || pl.N == 32) && R.Pout >= 2 &&
               R.KQ + 2 <= ring_slots(pl.N, 256)) ? 2 : 1;
-    // Plane-merged P-pair (PM) for 16 output channels: the two planes' KQ-tap
-    // accumulators interleave in ONE ring of 32 virtual channels, so each
-    // (input box, kw, 16-channel) step is ONE N = 96 MMA feeding both planes
-    // (zero weights where a box is outside a plane's KP taps) instead of two
-    // N = 48 MMAs: an N = 48 SS MMA is shared-memory-bound (the 4-KB A read,
-    // 32 cycles, against 24 of compute), N = 96 is compute-bound (48 cycles)
-    // and reads A once for both planes.  CTA pairs only (run_conv_tc re-plans).
-    static const bool pm_off = getenv("DP_CONV_PM") && getenv("DP_CONV_PM")[0] == '0';
-    pl.pm = allow_pm && !pm_off && pl.ppn == 2 && pl.N == 16;
     pl.stage_bytes = (R.KP + pl.ppn - 1) * (x3 ? 3 : pl.Cin / pl.cblk) * box_bytes(pl.cblk, R.KW);
-    pl.wimg_bytes = (pl.pm ? (R.KP + 1) * 2 : R.KP) * R.KQ * R.KW * pl.Cin * pl.N * 2;
+    pl.wimg_bytes = R.KP * R.KQ * R.KW * pl.Cin * pl.N * 2;
     const int budget = 220 * 1024;
     const int fixed = ((pl.wimg_bytes + 1023) & ~1023) + 1024;
     int ns = (budget - fixed) / pl.stage_bytes;
@@ -946,10 +913,10 @@ int launch_k(const CUtensorMap &xm, const CUtensorMap &hm, const ConvTcParams &p
 }
 
 // CTA-pair instantiation: (2, 1, 1) clusters, grid = 2 x clusters
-template <int N, int KP, int KQ, int KW, int CIN, bool X3 = false, int PPN = 1, bool PM = false>
+template <int N, int KP, int KQ, int KW, int CIN, bool X3 = false, int PPN = 1>
 int launch_k_pair(const CUtensorMap &xm, const CUtensorMap &hm, const ConvTcParams &p, int grid,
                   int smem, cudaStream_t st) {
-    auto kern = conv_tc_kernel<N, KP, KQ, KW, CIN, true, X3, PPN, PM>;
+    auto kern = conv_tc_kernel<N, KP, KQ, KW, CIN, true, X3, PPN>;
     DP_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)grid);
@@ -1014,6 +981,7 @@ int run_conv_tc(const dp_conv_geom *g, bool dgrad, const void *in, const void *i
     DP_REQUIRE(make_plan(g, dgrad, pl, f32out, x3), DP_ERR_UNSUPPORTED,
                "conv_tc: outside the envelope");
     const Roles &R = pl.R;
+    const int taps = R.KP * R.KQ * R.KW;
     DP_REQUIRE(ws_bytes >= pl.wimg_bytes, DP_ERR_INVALID, "conv_tc: workspace too small");
     int64_t outs = (int64_t)g->batch * R.Pout * R.Qout * R.Wout;
     if (outs == 0) return DP_OK;
@@ -1031,18 +999,13 @@ int run_conv_tc(const dp_conv_geom *g, bool dgrad, const void *in, const void *i
     if (pl.ppn > 1 && !cperm)   // P-pair units drain through the coalesced epilogue only
         DP_REQUIRE(make_plan(g, dgrad, pl, f32out, x3, false), DP_ERR_UNSUPPORTED,
                    "conv_tc: outside the envelope");
-    if (pl.pm && !use_pair)     // the plane-merged form exists as a CTA-pair kernel only
-        DP_REQUIRE(make_plan(g, dgrad, pl, f32out, x3, true, false), DP_ERR_UNSUPPORTED,
-                   "conv_tc: outside the envelope");
-    const int NV = pl.pm ? 2 * pl.N : pl.N;        // accumulator columns per output row
-    const int KPV = pl.pm ? R.KP + 1 : R.KP;        // weight-image kp taps
     // weight image
     {
-        int total = KPV * R.KQ * R.KW * pl.Cin * NV;
+        int total = taps * pl.Cin * pl.N;
         if (use_pair)
             conv_tc_weight_image_pair<<<grid_for(2 * total, 256, 2), 256, 0, st>>>(
-                (const __nv_bfloat16 *)w, (__nv_bfloat16 *)ws, NV, pl.Cin, KPV, R.KQ, R.KW,
-                dgrad ? 1 : 0, cperm, pl.pm ? 1 : 0);
+                (const __nv_bfloat16 *)w, (__nv_bfloat16 *)ws, pl.N, pl.Cin, R.KP, R.KQ, R.KW,
+                dgrad ? 1 : 0, cperm);
         else
             conv_tc_weight_image<<<grid_for(total, 256, 2), 256, 0, st>>>(
                 (const __nv_bfloat16 *)w, (__nv_bfloat16 *)ws, pl.N, pl.Cin, R.KP, R.KQ, R.KW,
@@ -1109,7 +1072,7 @@ int run_conv_tc(const dp_conv_geom *g, bool dgrad, const void *in, const void *i
         p.ysplit = R.split == 0 ? (int)g->in_ext[0] : (int)g->in_ext[0];
     }
     {
-        const int64_t ns = pl.pm ? ring_slots(NV, 512) : ring_slots(pl.N, 512 / pl.ppn), q = g->nsp == 3 ? g->out_org[1] : g->out_org[0];
+        const int64_t ns = ring_slots(pl.N, 512 / pl.ppn), q = g->nsp == 3 ? g->out_org[1] : g->out_org[0];
         p.qorg = (int)(((q % ns) + ns) % ns);
     }
     p.n_wt = use_pair ? (n_wt_all + 1) / 2 : n_wt_all;   // PAIR: tile pairs
@@ -1147,9 +1110,6 @@ int run_conv_tc(const dp_conv_geom *g, bool dgrad, const void *in, const void *i
         p.dbg = dbg;
     }
     int grid = p.n_units < sms ? p.n_units : sms;
-    if (pl.pm)   // plane-merged P-pair: 32 virtual channels, 4 virtual kp taps
-        return pl.Cin == 16 ? launch_k_pair<32, 4, 3, 3, 16, false, 1, true>(xm, hm, p, 2 * grid, pl.smem, st)
-                            : launch_k_pair<32, 4, 3, 3, 32, false, 1, true>(xm, hm, p, 2 * grid, pl.smem, st);
     if (pl.ppn == 2) {   // P-pair units (3-D 3x3x3, bf16 out, C 16 / 32)
         const bool c16 = pl.Cin == 16;
         if (use_pair) {

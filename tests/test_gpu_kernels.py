@@ -333,69 +333,20 @@ def test_attention_tc_fwd_bwd_vs_oracle(case, payload):
 
 def test_conv_single_cta_and_per_mma_issue_paths():
     """The non-default conv issue paths stay correct: single-CTA MMAs
-    (DP_CONV_2CTA=0), one elect per MMA instead of the grouped kw taps
-    (DP_CONV_DBG=32) and the two-ring P-pair form of the 16-channel shapes
-    (DP_CONV_PM=0), each over the tcgen05 conv parity cases."""
+    (DP_CONV_2CTA=0) and one elect per MMA instead of the grouped kw taps
+    (DP_CONV_DBG=32), each over the tcgen05 conv parity cases."""
     import os
     import subprocess
     import sys
 
     here = os.path.dirname(os.path.abspath(__file__))
-    for env_extra in ({"DP_CONV_2CTA": "0"}, {"DP_CONV_DBG": "32"}, {"DP_CONV_PM": "0"}):
+    for env_extra in ({"DP_CONV_2CTA": "0"}, {"DP_CONV_DBG": "32"}):
         env = dict(os.environ, **env_extra)
         r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x",
                             os.path.join(here, "test_gpu_kernels.py"),
                             "-k", "test_conv_tc_fwd_dgrad_vs_oracle"], env=env, capture_output=True,
                            text=True, timeout=600)
         assert r.returncode == 0, str(env_extra) + r.stdout[-2000:] + r.stderr[-2000:]
-
-
-_PM_SCRIPT = r"""
-import hashlib, sys, torch
-sys.path.insert(0, sys.argv[1])
-from paper_2605_11111_b200 import kernels as k
-k.set_algo("tc")
-cl = torch.channels_last_3d
-g = torch.Generator(device="cuda").manual_seed(7)
-outs = []
-for (P, Q, W, halo) in ((40, 24, 256, 0), (9, 5, 300, 2)):
-    dy = torch.randn((1, 32, P, Q, W), device="cuda", generator=g).to(torch.bfloat16).contiguous(memory_format=cl)
-    w = (torch.randn((32, 16, 3, 3, 3), device="cuda", generator=g) * 0.1).to(torch.bfloat16)
-    # halo: a sharded rank at the global start, dY rows [0, main + halo - 1)
-    dx = torch.empty((1, 16, P + 1 - halo if halo else P, Q, W), device="cuda",
-                     dtype=torch.bfloat16).contiguous(memory_format=cl)
-    dxh = torch.empty((1, 16, halo, Q, W), device="cuda", dtype=torch.bfloat16).contiguous(memory_format=cl) if halo else None
-    k.conv_dgrad(dy, w, dx, dxh, kernel=(3, 3, 3), stride=(1, 1, 1), base=[-1, -1, -1],
-                 shard=0 if halo else -1, halo_rows=halo)
-    # 32 -> 16 forward too (C_out = 16 takes the same plane-merged kernel)
-    x = torch.randn((1, 32, P, Q, W), device="cuda", generator=g).to(torch.bfloat16).contiguous(memory_format=cl)
-    y = torch.empty((1, 16, P, Q, W), device="cuda", dtype=torch.bfloat16).contiguous(memory_format=cl)
-    k.conv_fwd(x, None, w.transpose(0, 1).contiguous(), y, kernel=(3, 3, 3), stride=(1, 1, 1),
-               base=[-1, -1, -1], shard=-1, halo_rows=0)
-    outs += [dx, y] + ([dxh] if halo else [])
-torch.cuda.synchronize()
-print(hashlib.sha256(b"".join(t.cpu().view(torch.int16).numpy().tobytes() for t in outs)).hexdigest())
-"""
-
-
-def test_conv_plane_merged_bitwise_vs_two_rings():
-    """The plane-merged P-pair kernel (one N = 96 MMA feeding both planes of a
-    16-channel conv, zero weights where a box is outside a plane's taps) gives
-    bitwise the sums of the two-ring P-pair kernel (DP_CONV_PM=0): same MMA
-    order per plane, the extra terms are exact zeros."""
-    import os
-    import subprocess
-    import sys
-
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    digests = []
-    for pm in ("1", "0"):
-        env = dict(os.environ, DP_CONV_PM=pm)
-        r = subprocess.run([sys.executable, "-c", _PM_SCRIPT, root], env=env, capture_output=True,
-                           text=True, timeout=600)
-        assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
-        digests.append(r.stdout.strip().splitlines()[-1])
-    assert digests[0] == digests[1]
 
 
 X3_CASES = [
