@@ -915,7 +915,9 @@ def main():
     # host.  Every step copies its own input shard from pinned host memory and
     # reads its result back; the copy for step i+1 runs on a copy stream while
     # step i computes (double-buffered input, as a training loop's prefetcher
-    # would), so the timed region = first H2D + K steps + last D2H.
+    # would), and step i's result drains to host on a third stream while step
+    # i+1 computes (PCIe is full duplex: the H2D prefetch and the D2H drain run
+    # at once), so the timed region = first H2D + K steps + last D2H.
     ins = W["inputs"]
     hosts = []
     for t in ins:
@@ -929,6 +931,7 @@ def main():
     d2h = sum(o.numel() * o.element_size() for o in outs)
     h2d = sum(t.numel() * t.element_size() for t in ins)
     copy_stream = torch.cuda.Stream(device=ctx.device)
+    d2h_stream = torch.cuda.Stream(device=ctx.device)
     compute = torch.cuda.current_stream()
     e2e_steps = max(1, args.steps)
     barrier(ctx)
@@ -958,8 +961,12 @@ def main():
         compute.wait_event(ready[cur])
         outs = step(bufs[cur])
         free[cur].record(compute)
-        for h, o in zip(host_out, outs):
-            h.copy_(o, non_blocking=True)
+        d2h_stream.wait_stream(compute)
+        with torch.cuda.stream(d2h_stream):
+            for h, o in zip(host_out, outs):
+                o.record_stream(d2h_stream)   # the allocator keeps o until its D2H is done
+                h.copy_(o, non_blocking=True)
+    compute.wait_stream(d2h_stream)
     e_end.record(compute)
     barrier(ctx)
     e2e_ms = max_over_ranks(ctx, e_start.elapsed_time(e_end) / e2e_steps)
@@ -1041,7 +1048,8 @@ def main():
         "e2e": {"value": samples / (e2e_ms / 1000.0), "unit": W["unit"], "ms_per_step": e2e_ms,
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": e2e_steps,
                 "note": "pinned H2D of each step's input shards (prefetched one step ahead on "
-                        "a copy stream) + D2H of the step's result, through the public API"},
+                        "a copy stream) + D2H of the step's result (drained on a second copy "
+                        "stream under the next step), through the public API"},
         "gpu_launches": launches,
         "gpu_launches_per_step": launches / args.steps,
         "simt_calls": sum(rk["simt"] for rk in ranks_k),
