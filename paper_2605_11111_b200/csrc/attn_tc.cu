@@ -466,12 +466,6 @@ __device__ __forceinline__ void named_bar(int id, int n) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
-// MC: (2,1,1) clusters over adjacent key tiles of one head (n_kt even).  Both
-// CTAs walk the same query blocks, so each stage's Q and dO tiles are loaded
-// ONCE per pair: CTA 0 multicasts Q, CTA 1 multicasts dO into both CTAs' ring
-// slot; a slot is refilled only when both CTAs' dK MMAs released it (each
-// commit arrives on both CTAs' qd_empty).  Halves the Q/dO L2 -> SM stream.
-template <bool MC>
 __global__ void __launch_bounds__(kBwdThreads, 1)
 attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap kmap,
                    const __grid_constant__ CUtensorMap vmap, const __grid_constant__ CUtensorMap dmap,
@@ -502,7 +496,7 @@ attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
             mbar_init(kv_full, 1);
             for (int i = 0; i < kQDStages; ++i) {
                 mbar_init(&qd_full[i], 1);
-                mbar_init(&qd_empty[i], MC ? 2 : 1);   // MC: both CTAs' consumers
+                mbar_init(&qd_empty[i], 1);
             }
             for (int i = 0; i < 2; ++i) {
                 mbar_init(&p_full[i], 512);
@@ -529,7 +523,6 @@ attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
     }
     tc_fence_before();
     __syncthreads();
-    if constexpr (MC) cluster_sync();   // the peer's barriers are initialised before any multicast
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
@@ -553,21 +546,8 @@ attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
             }
             mbar_expect_tx_e(&qd_full[st], 2 * kTileBytes);
             uint8_t *dst = smem + kB_QD + st * 2 * kTileBytes;
-            if constexpr (MC) {   // rank 0 sends Q, rank 1 dO, each to both CTAs
-                if (cluster_ctarank() == 0)
-                    tma_load_3d_mc_e(dst, &qmap, &qd_full[st], 0, h, i * kBM, 3);
-                else
-                    tma_load_3d_mc_e(dst + kTileBytes, &dmap, &qd_full[st], 0, h, i * kBM, 3);
-            } else {
-                tma_load_3d_e(dst, &qmap, &qd_full[st], 0, h, i * kBM);
-                tma_load_3d_e(dst + kTileBytes, &dmap, &qd_full[st], 0, h, i * kBM);
-            }
-        }
-        if constexpr (MC) {
-            // every release of this CTA's slots by the PEER's MMAs has landed
-            // before either CTA may exit (commits arrive asynchronously)
-            for (int i = nq; i < nq + kQDStages; ++i)
-                if (i >= kQDStages) mbar_wait(&qd_empty[i % kQDStages], ((i / kQDStages) & 1) ^ 1);
+            tma_load_3d_e(dst, &qmap, &qd_full[st], 0, h, i * kBM);
+            tma_load_3d_e(dst + kTileBytes, &dmap, &qd_full[st], 0, h, i * kBM);
         }
     } else if (warp == 1) {
         // ===================== MMA issuer =====================
@@ -607,8 +587,7 @@ attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
                 const uint32_t bb = (k * 16 * 128) >> 4;
                 mma_bf16_e(tmem + kColDK, dst_k + a, q_mn + bb, id_g, (j > 0 || k > 0) ? 1u : 0u);
             }
-            if constexpr (MC) mma_commit_mc_e(&qd_empty[qs], 3);   // both CTAs' slot
-            else mma_commit_e(&qd_empty[qs]);       // Q / dO(j) no longer read (dQ uses dS, K)
+            mma_commit_e(&qd_empty[qs]);            // Q / dO(j) no longer read (dQ uses dS, K)
             BWD_TRACE(j, 8);
             if (j >= 1) mbar_wait(dq_empty, (j - 1) & 1);   // dQ(j-1) drained from TMEM
             BWD_TRACE(j, 2);
@@ -827,7 +806,6 @@ attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_consta
     }
     tc_fence_before();
     __syncthreads();
-    if constexpr (MC) cluster_sync();
     if (warp == 0) {
         tc_fence_after();
         tmem_dealloc(tmem, 512);
@@ -939,30 +917,10 @@ int attn_bwd_update_tc_launch(const dp_attn_geom *g, const void *q, const void *
     if (want_trace && !trace) DP_CUDA_CHECK(cudaMalloc(&trace, 64 * 16 * 8));
     if (trace) DP_CUDA_CHECK(cudaMemsetAsync(trace, 0, 64 * 16 * 8, st));
     p.trace = trace;
+    DP_CUDA_CHECK(cudaFuncSetAttribute(attn_bwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       kSmemBwd));
     const int64_t grid = (int64_t)p.n_kt * p.H;
-    // Q/dO multicast over key-tile pairs when the tiles pair up within each head
-    static const bool mc_off = getenv("DP_ATTN_MC") && getenv("DP_ATTN_MC")[0] == '0';
-    if (!mc_off && p.n_kt % 2 == 0 && !trace && !(p.dbg & 16)) {
-        DP_CUDA_CHECK(cudaFuncSetAttribute(attn_bwd_tc_kernel<true>,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBwd));
-        cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3((unsigned)grid);
-        cfg.blockDim = dim3(kBwdThreads);
-        cfg.dynamicSmemBytes = (size_t)kSmemBwd;
-        cfg.stream = st;
-        cudaLaunchAttribute attr[1];
-        attr[0].id = cudaLaunchAttributeClusterDimension;
-        attr[0].val.clusterDim.x = 2;
-        attr[0].val.clusterDim.y = 1;
-        attr[0].val.clusterDim.z = 1;
-        cfg.attrs = attr;
-        cfg.numAttrs = 1;
-        DP_CUDA_CHECK(cudaLaunchKernelEx(&cfg, attn_bwd_tc_kernel<true>, qm, km, vm, dm, dqm, p));
-        return launch_status("attn_bwd_tc_kernel<mc>");
-    }
-    DP_CUDA_CHECK(cudaFuncSetAttribute(attn_bwd_tc_kernel<false>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBwd));
-    attn_bwd_tc_kernel<false><<<(unsigned)grid, kBwdThreads, kSmemBwd, st>>>(qm, km, vm, dm, dqm, p);
+    attn_bwd_tc_kernel<<<(unsigned)grid, kBwdThreads, kSmemBwd, st>>>(qm, km, vm, dm, dqm, p);
     if (trace) {  // debug: CTA 0's per-block event clocks relative to block 20's s_full
         unsigned long long hbuf[64 * 16];
         DP_CUDA_CHECK(cudaStreamSynchronize(st));

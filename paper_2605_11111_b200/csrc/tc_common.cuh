@@ -493,32 +493,6 @@ __device__ __forceinline__ void mma2_commit_mc_e(uint64_t *bar) {
         "}\n" ::"r"(smem_u32(bar))
         : "memory");
 }
-// TMA load multicast to the CTAs in `mask`: the box lands at the same offset
-// in each destination CTA's shared memory and completes tx on each one's
-// barrier at the same offset.
-__device__ __forceinline__ void tma_load_3d_mc_e(void *dst, const CUtensorMap *map, uint64_t *bar,
-                                                 int c0, int c1, int c2, uint16_t mask) {
-    asm volatile(
-        "{\n"
-        ".reg .pred e;\n"
-        "elect.sync _|e, 0xffffffff;\n"
-        "@e cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-        ".multicast::cluster [%0], [%1, {%2, %3, %4}], [%5], %6;\n"
-        "}\n" ::"r"(smem_u32(dst)),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)),
-        "h"(mask)
-        : "memory");
-}
-// cta_group::1 commit arriving on `bar` (same offset) in every CTA of `mask`
-__device__ __forceinline__ void mma_commit_mc_e(uint64_t *bar, uint16_t mask) {
-    asm volatile(
-        "{\n"
-        ".reg .pred e;\n"
-        "elect.sync _|e, 0xffffffff;\n"
-        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n"
-        "}\n" ::"r"(smem_u32(bar)), "h"(mask)
-        : "memory");
-}
 // TMA load into this CTA's smem whose complete_tx lands on the EVEN CTA's
 // barrier at the same offset (both CTAs of a pair feed one MMA).
 __device__ __forceinline__ void tma_load_5d_2sm_e(void *dst, const CUtensorMap *map,
