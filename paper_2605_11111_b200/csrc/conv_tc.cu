@@ -1342,6 +1342,9 @@ conv_wgrad_tc_kernel(const __grid_constant__ CUtensorMap xmap,
                                      swz_layout(L.cbd));
         const uint32_t astep = (16 * L.cbx * 2) >> 4;  // one K step = 16 w' rows
         const uint32_t bstep = (16 * L.cbd * 2) >> 4;
+        // the static shapes' steps as constants (grouped issue below)
+        constexpr uint32_t AS8 = (16 * chan_block(CIN_ > 0 ? CIN_ : 16) * 2) >> 4;
+        constexpr uint32_t BS8 = (16 * chan_block(N) * 2) >> 4;
         const uint32_t mstep = (128 / L.cbx * L.boxx) >> 4;
         // X / dY ring slots and phases carried as counters (no integer division
         // per row); the K-step loop is unrolled to its 16-step maximum with an
@@ -1372,6 +1375,11 @@ conv_wgrad_tc_kernel(const __grid_constant__ CUtensorMap xmap,
                     const uint32_t bit = 1u << mt;
                     uint32_t acc = (fresh & bit) ? 0u : 1u;
                     fresh &= ~bit;
+                    if (kStatic && p.kt == 8 && astep == AS8 && bstep == BS8) {
+                        // one elect for the tile's 8 K steps (static shapes, 128-w' tiles)
+                        mma_bf16_x8<AS8, BS8>(d, ax + mt * mstep, bd, idesc, acc);
+                        continue;
+                    }
 #pragma unroll
                     for (int ks = 0; ks < 16; ++ks) {
                         if (ks >= p.kt) break;
@@ -1927,28 +1935,33 @@ conv_wgrad_ts_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_cons
                         const uint32_t ak = tmem + ACOL + cas[dp] * S::ACOLS;
                         const uint64_t bk = bx + ((xp * S::XSLOT) >> 4);
                         const uint64_t bk0 = b0 + ((xp * S::XSLOT) >> 4);
+                        if (!wrap) {   // the pairing's 8 K steps under one elect
+                            static_assert(kTsKT == 8, "mma_ts_x8 covers one 128-w' tile");
+                            if (!(p.dbg & 2))
+                                mma_ts_x8<bstep>(dcol, ak, bk, id1, (fresh && k == 5) ? 0u : 1u);
+                            continue;
+                        }
 #pragma unroll
                         for (int ks = 0; ks < kTsKT; ++ks) {
                             if (p.dbg & 2) break;
                             const uint32_t acc = (fresh && k == 5 && ks == 0) ? 0u : 1u;
                             mma_ts_e(dcol, ak + ks * 8, bk + ks * bstep, id1, acc);
-                            if (wrap) mma_ts_e(dcol + aw * S::CBX, ak + ks * 8, bk0 + ks * bstep, id2, acc);
+                            mma_ts_e(dcol + aw * S::CBX, ak + ks * 8, bk0 + ks * bstep, id2, acc);
                         }
                     }
                 } else if (xs + KQ - 1 < (uint32_t)p.nx) {   // the KQ rows are adjacent slots
-#pragma unroll
-                for (int ks = 0; ks < kTsKT; ++ks) {
-                    if (p.dbg & 2) break;
-                    const uint32_t acc = (fresh && ks == 0) ? 0u : 1u;
+                    // per N chunk, its 8 K steps under one elect (the chunks write disjoint
+                    // D columns, so chunk-outer order gives the same sums)
+                    static_assert(kTsKT == 8, "mma_ts_x8 covers one 128-w' tile");
 #pragma unroll
                     for (int c = 0; c < S::NCH; ++c) {
+                        if (p.dbg & 2) break;
                         constexpr int last = S::NATOM - (S::NCH - 1) * S::APC;
                         const int atoms = c < S::NCH - 1 ? S::APC : last;
-                        mma_ts_e(dcol + c * S::APC * S::CBX, acol + ks * 8,
-                                 bx + ((c * S::APC * S::BOXX) >> 4) + ks * bstep,
-                                 idesc_bf16(128, atoms * S::CBX, 0, 1), acc);
+                        mma_ts_x8<bstep>(dcol + c * S::APC * S::CBX, acol,
+                                         bx + ((c * S::APC * S::BOXX) >> 4),
+                                         idesc_bf16(128, atoms * S::CBX, 0, 1), fresh ? 0u : 1u);
                     }
-                }
                 } else {   // wrap: atoms of slots xs .. nx-1, then of slots 0 ..
                     const int aw = (int)(p.nx - xs) * KP * S::NBX;
                     const uint32_t id1 = idesc_bf16(128, aw * S::CBX, 0, 1);

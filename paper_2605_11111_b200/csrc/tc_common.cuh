@@ -304,6 +304,85 @@ __device__ __forceinline__ void mma_ts_e(uint32_t d_tmem, uint32_t a_tmem, uint6
         "r"(a_tmem), "l"(b), "r"(idesc), "r"(accumulate));
 }
 
+// Eight TS MMAs over consecutive K steps (A advances 8 TMEM columns, B one
+// descriptor step BSTEP per step) under ONE elect: at N <= 96 (48-cycle MMAs)
+// the per-MMA elect / predicate / uniform-register setup of mma_ts_e is
+// comparable to the MMA itself.  acc0 applies to the first MMA only.
+template <uint32_t BSTEP>
+__device__ __forceinline__ void mma_ts_x8(uint32_t d_tmem, uint32_t a_tmem, uint64_t b,
+                                          uint32_t idesc, uint32_t acc0) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p, q, e;\n"
+        ".reg .b32 a1, a2, a3, a4, a5, a6, a7;\n"
+        ".reg .b64 b1, b2, b3, b4, b5, b6, b7;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "setp.eq.u32 q, 1, 1;\n"
+        "add.u32 a1, %1, 8;\n"
+        "add.u32 a2, %1, 16;\n"
+        "add.u32 a3, %1, 24;\n"
+        "add.u32 a4, %1, 32;\n"
+        "add.u32 a5, %1, 40;\n"
+        "add.u32 a6, %1, 48;\n"
+        "add.u32 a7, %1, 56;\n"
+        "add.s64 b1, %2, %5;\n"
+        "add.s64 b2, %2, %6;\n"
+        "add.s64 b3, %2, %7;\n"
+        "add.s64 b4, %2, %8;\n"
+        "add.s64 b5, %2, %9;\n"
+        "add.s64 b6, %2, %10;\n"
+        "add.s64 b7, %2, %11;\n"
+        "elect.sync _|e, 0xffffffff;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a1], b1, %3, q;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a2], b2, %3, q;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a3], b3, %3, q;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a4], b4, %3, q;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a5], b5, %3, q;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a6], b6, %3, q;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a7], b7, %3, q;\n"
+        "}\n" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc0), "n"(1 * BSTEP), "n"(2 * BSTEP), "n"(3 * BSTEP), "n"(4 * BSTEP), "n"(5 * BSTEP), "n"(6 * BSTEP), "n"(7 * BSTEP));
+}
+
+// SS form of mma_ts_x8: A and B descriptors advance ASTEP / BSTEP per K step.
+template <uint32_t ASTEP, uint32_t BSTEP>
+__device__ __forceinline__ void mma_bf16_x8(uint32_t d_tmem, uint64_t a, uint64_t b,
+                                            uint32_t idesc, uint32_t acc0) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p, q, e;\n"
+        ".reg .b64 a1, a2, a3, a4, a5, a6, a7, b1, b2, b3, b4, b5, b6, b7;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "setp.eq.u32 q, 1, 1;\n"
+        "add.s64 a1, %1, %5;\n"
+        "add.s64 a2, %1, %6;\n"
+        "add.s64 a3, %1, %7;\n"
+        "add.s64 a4, %1, %8;\n"
+        "add.s64 a5, %1, %9;\n"
+        "add.s64 a6, %1, %10;\n"
+        "add.s64 a7, %1, %11;\n"
+        "add.s64 b1, %2, %12;\n"
+        "add.s64 b2, %2, %13;\n"
+        "add.s64 b3, %2, %14;\n"
+        "add.s64 b4, %2, %15;\n"
+        "add.s64 b5, %2, %16;\n"
+        "add.s64 b6, %2, %17;\n"
+        "add.s64 b7, %2, %18;\n"
+        "elect.sync _|e, 0xffffffff;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a1, b1, %3, q;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a2, b2, %3, q;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a3, b3, %3, q;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a4, b4, %3, q;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a5, b5, %3, q;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a6, b6, %3, q;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a7, b7, %3, q;\n"
+        "}\n" ::"r"(d_tmem),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc0), "n"(1 * ASTEP), "n"(2 * ASTEP), "n"(3 * ASTEP), "n"(4 * ASTEP), "n"(5 * ASTEP), "n"(6 * ASTEP), "n"(7 * ASTEP),
+        "n"(1 * BSTEP), "n"(2 * BSTEP), "n"(3 * BSTEP), "n"(4 * BSTEP), "n"(5 * BSTEP), "n"(6 * BSTEP), "n"(7 * BSTEP));
+}
+
 __device__ __forceinline__ void named_bar_sync(int id, int n) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
