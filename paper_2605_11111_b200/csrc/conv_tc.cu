@@ -1869,7 +1869,8 @@ conv_wgrad_ts_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_cons
                     }
                     mbar_expect_tx_e(&dfull[idx], dbytes);
                     uint8_t *dst = dring + (size_t)idx * kTsDSlot;
-                    const int bdp = G3 ? dp * p.pairB + b : bd;
+                    // G3: parts in the order the MMA warp first reads them (lo, mid, hi)
+                    const int bdp = G3 ? (NXP - 1 - dp) * p.pairB + b : bd;
                     tma_load_5d_e(dst, &dmap, &dfull[idx], 0, w0 - (KW - 1), q0 + s, po, bdp);
                     tma_load_5d_e(dst + kTsDHalf, &dmap, &dfull[idx], 16, w0 - (KW - 1), q0 + s, po, bdp);
                     }
@@ -1898,11 +1899,17 @@ conv_wgrad_ts_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_cons
                 mbar_wait(&xfull[cx], cph);
                 const int j = s - (KQ - 1);
                 if (j < 0) continue;
-                uint32_t cas[NXP];   // this row's A entries (G3: one per dY part)
+                // this row's A entries (G3: one per dY part, staged lo, mid, hi — the
+                // order the pairings first read them — each waited for just before its
+                // first pairing and released after its last, so with 5 entries for 3
+                // parts a row's first MMAs never wait for the previous row to finish)
+                uint32_t cas[NXP], caph[NXP];
 #pragma unroll
-                for (int dp = 0; dp < NXP; ++dp) {
-                    cas[dp] = aidx;
-                    mbar_wait(&afull[aidx], aph);
+                for (int i = 0; i < NXP; ++i) {
+                    const int dpi = G3 ? NXP - 1 - i : i;
+                    cas[dpi] = aidx;
+                    caph[dpi] = aph;
+                    if (!G3) mbar_wait(&afull[aidx], aph);
                     if (++aidx == (uint32_t)p.na) { aidx = 0; aph ^= 1u; }
                 }
                 const uint32_t ca = cas[0];
@@ -1939,10 +1946,17 @@ conv_wgrad_ts_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_cons
                         // the ring (2 of every nx rows) as two such groups over disjoint D
                         // columns (slots xs .. nx-1, then 0 ..)
                         static_assert(kTsKT == 8, "mma_ts_x8 covers one 128-w' tile");
-                        if (p.dbg & 2) continue;
-                        const uint32_t acc0 = (fresh && k == 5) ? 0u : 1u;
-                        mma_ts_x8<bstep>(dcol, ak, bk, id1, acc0);
-                        if (wrap) mma_ts_x8<bstep>(dcol + aw * S::CBX, ak, bk0, id2, acc0);
+                        if (k == 5 || k == 4 || k == 3) {   // first read of dY part dp
+                            mbar_wait(&afull[cas[dp]], caph[dp]);
+                            tc_fence_after();
+                        }
+                        if (!(p.dbg & 2)) {
+                            const uint32_t acc0 = (fresh && k == 5) ? 0u : 1u;
+                            mma_ts_x8<bstep>(dcol, ak, bk, id1, acc0);
+                            if (wrap) mma_ts_x8<bstep>(dcol + aw * S::CBX, ak, bk0, id2, acc0);
+                        }
+                        if (k == 5 || k == 2 || k == 0)     // last read of dY part dp
+                            mma_commit_e(&aempty[cas[dp]]);
                     }
                 } else if (xs + KQ - 1 < (uint32_t)p.nx) {   // the KQ rows are adjacent slots
                     // per N chunk, its 8 K steps under one elect (the chunks write disjoint
@@ -1975,8 +1989,7 @@ conv_wgrad_ts_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_cons
                         mma_commit_e(&rfull[((rrow >> p.rf_shift)) & 1u]);
                     ++rrow;
                 }
-#pragma unroll
-                for (int dp = 0; dp < NXP; ++dp) mma_commit_e(&aempty[cas[dp]]);
+                if constexpr (!G3) mma_commit_e(&aempty[cas[0]]);   // (G3: released per part)
                 mma_commit_e(&xempty[xs]);
                 uint32_t xn = xs + 1 == (uint32_t)p.nx ? 0u : xs + 1;
                 if (j == nq - 1)
